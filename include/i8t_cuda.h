@@ -1,0 +1,209 @@
+/*
+ * i8t_cuda.h -- C-ABI of the B200-native (sm_100a) INT8 training hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (`namespace i8t`, /root/reference/proj/core/include/i8t/).  Every entry
+ * point below names the reference interface it replaces (file:line).  The C++
+ * shim in include/i8t/*.hpp re-exports the reference signatures on top of it
+ * (host tensors, same exception types); the PyTorch layer in
+ * paper_1912_12607_b200/ calls it through ctypes with device pointers.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers unless a name says `host`.
+ *  - Every call is asynchronous on the context's CUDA stream and returns an
+ *    i8t_status for argument errors detected on the host.  Data-dependent
+ *    errors (non-finite input: the reference's std::domain_error) are latched
+ *    in a device error word and reported by i8t_ctx_check(), which
+ *    synchronises the stream.
+ *  - No CPU fallback exists: if the CUDA library cannot run, calls fail.
+ *  - Layouts: activations/gradients are NHWC int8 ("channels-last"), with an
+ *    optional padded channel stride; weights are KRSC int8 (forward) and CRSK
+ *    int8 (backward-data); float outputs are NHWC (or KRSC for weights).
+ *    Conversions to the reference's NCHW/KCRS order are provided.
+ *  - The per-tensor quantisation scale is s = clip / 127.0f, computed on the
+ *    device from a device-resident clip (QuantParams::from_clip,
+ *    quantize.cpp:11-14).
+ */
+#ifndef I8T_CUDA_H
+#define I8T_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define I8T_ABI_VERSION 1
+
+typedef enum i8t_status {
+  I8T_OK = 0,
+  I8T_EINVAL = 1,      /* std::invalid_argument in the reference */
+  I8T_EDOMAIN = 2,     /* std::domain_error (non-finite input) */
+  I8T_ECUDA = 3,       /* CUDA runtime / launch failure */
+  I8T_EUNSUPPORTED = 4 /* shape outside the kernels' envelope */
+} i8t_status;
+
+typedef struct i8t_ctx i8t_ctx;
+
+/* Convolution geometry.  Replaces ConvGeometry (conv.hpp:14-28) and extends
+ * it: separate stride/pad per dimension and floor-mode output size (the
+ * reference demands exact division, conv.cpp:15-17). */
+typedef struct i8t_conv_geom {
+  int64_t n, c, h, w;       /* input (N,C,H,W) */
+  int64_t k, kh, kw;        /* filters (K,C,kh,kw); depthwise: k == c, (C,1,kh,kw) */
+  int64_t stride_h, stride_w, pad_h, pad_w;
+  int32_t depthwise;
+  int32_t floor_mode;       /* 0: reference validation (exact division) */
+} i8t_conv_geom;
+
+/* Device-resident DSGC/DCLR state of one quantised layer.  Replaces
+ * ClipState (clip.hpp:12-18) + the per-step measurements of QuantState
+ * (layers.hpp:28-38).  Allocate with i8t_dsgc_state_size() bytes of device
+ * memory, zero it, then call i8t_dsgc_init(). */
+typedef struct i8t_dsgc_view {
+  float clip;               /* gradient clip; 0 = uninitialised */
+  float scale;              /* scale of the last quantised gradient */
+  float max_abs;            /* max |g| of the last gradient */
+  uint32_t flags;           /* bit0 non-finite input, bit1 zero gradient */
+  double last_dc;           /* ClipState::last_dc */
+  double lr_scale;          /* phi(d_c), QuantState::lr_scale */
+  double eps_norm;          /* ||g - g_hat||, QuantState::eps_norm */
+  double ghat_sqnorm;       /* ||g_hat||^2, QuantState::ghat_sqnorm */
+  int64_t iter_of_last_update;
+  int64_t period;
+} i8t_dsgc_view;
+
+/* ------------------------------------------------------------ context */
+int i8t_abi_version(void);
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int i8t_ctx_create(void* stream, i8t_ctx** out);
+int i8t_ctx_set_stream(i8t_ctx* ctx, void* stream);
+int i8t_ctx_destroy(i8t_ctx* ctx);
+/* Synchronise the stream; report and clear any latched device error. */
+int i8t_ctx_check(i8t_ctx* ctx);
+const char* i8t_last_error(void);
+/* Number of kernels this library launched (for bench accounting). */
+uint64_t i8t_launch_count(void);
+
+/* ------------------------------------------------------------ LCG stream */
+/* The gradient stream of LcgStream (quantize.hpp:32-50) lives in device memory
+ * as one uint32 state; stochastic quantisers read it and advance it by the
+ * number of draws, exactly like the reference's caller-owned stream. */
+int i8t_lcg_jump_host(uint32_t state, uint64_t k, uint32_t* out);
+
+/* ------------------------------------------------------------ quantisers */
+/* quantize(x, from_clip(*clip), kNearest) (quantize.cpp:33-43) over a flat
+ * tensor; optionally fuses max_abs(x) into *amax (device float, running max
+ * when accumulate_amax != 0, i.e. QuantState::pending_amax, layers.cpp:101). */
+int i8t_quantize_nearest(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, int8_t* q, float* amax,
+                         int accumulate_amax);
+/* Same quantiser, writing rows of `cols` values into a padded row stride
+ * ld_q >= cols (zero pad).  x is [rows, cols] contiguous (NHWC activations). */
+int i8t_quantize_nearest_rows(i8t_ctx* ctx, const float* x, int64_t rows, int64_t cols, const float* clip,
+                              int8_t* q, int64_t ld_q, float* amax, int accumulate_amax);
+/* NCHW float -> NHWC int8 with padded channel stride c_pad (drop-in path). */
+int i8t_quantize_nearest_nchw_to_nhwc(i8t_ctx* ctx, const float* x, int64_t n, int64_t c, int64_t hw,
+                                      const float* clip, int8_t* q, int64_t c_pad, float* amax,
+                                      int accumulate_amax);
+/* Weights KCRS float (or KRSC when src_krsc != 0) -> nearest int8 in two
+ * layouts: KRSC rows [K][ld_krsc] (channel stride c_pad, zero padded) for the
+ * forward conv and CRSK rows [C][ld_crsk] (K stride k_pad) for backward-data.
+ * Either output may be NULL.  Replaces quantize(W) (layers.cpp:108). */
+int i8t_quantize_weight(i8t_ctx* ctx, const float* w, int src_krsc, int64_t k, int64_t c, int64_t kh, int64_t kw,
+                        const float* clip, int8_t* q_krsc, int64_t c_pad, int64_t ld_krsc, int8_t* q_crsk,
+                        int64_t k_pad, int64_t ld_crsk, float* amax);
+/* quantize(x, p, kStochastic, stream) (quantize.cpp:33-43) on a flat tensor,
+ * draws in row-major order from the device LCG state, which is advanced by n. */
+int i8t_quantize_stochastic(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, uint32_t* lcg_state,
+                            int8_t* q);
+/* quantize_partitioned (quantize.cpp:45-79): chunk k seeded base_seed + k. */
+int i8t_quantize_partitioned(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, uint32_t base_seed,
+                             int partitions, int8_t* q);
+/* dequantize (quantize.cpp:81-87). */
+int i8t_dequantize(i8t_ctx* ctx, const int8_t* q, int64_t n, const float* clip, float* out);
+/* Layout helpers for the drop-in path. */
+int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, int64_t hw, int64_t ld_src,
+                         float* dst);
+int i8t_nchw_to_nhwc_i8(i8t_ctx* ctx, const int8_t* src, int64_t n, int64_t c, int64_t hw, int8_t* dst,
+                        int64_t c_pad);
+int i8t_kcrs_to_krsc_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, int64_t kh, int64_t kw, int8_t* dst,
+                        int64_t c_pad, int64_t ld);
+int i8t_kcrs_to_crsk_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, int64_t kh, int64_t kw, int8_t* dst,
+                        int64_t k_pad, int64_t ld);
+
+/* ------------------------------------------------------------ reductions */
+/* max_abs / sq_l2_norm / dot / has_nonfinite (tensor.cpp:72-101); results
+ * written to device scalars.  Sums are double, deterministic for a given n. */
+int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out);
+int i8t_sq_l2_norm(i8t_ctx* ctx, const float* x, int64_t n, double* out);
+int i8t_dot(i8t_ctx* ctx, const float* a, const float* b, int64_t n, double* out);
+int i8t_has_nonfinite(i8t_ctx* ctx, const float* x, int64_t n, int32_t* out);
+
+/* ------------------------------------------------------------ DSGC / DCLR */
+/* cosine_distance (clip.cpp:8-22). */
+int i8t_cosine_distance(i8t_ctx* ctx, const float* g, const float* h, int64_t n, double* out);
+/* measure_dc (clip.cpp:24-28) at a host clip value. */
+int i8t_measure_dc(i8t_ctx* ctx, const float* g, int64_t n, float clip, double* out);
+/* search_clip (clip.cpp:30-78); result {clip, dc} in device memory. */
+int i8t_search_clip(i8t_ctx* ctx, const float* g, int64_t n, int grid, int rounds, float prev_clip,
+                    float* clip_out, double* dc_out);
+int64_t i8t_dsgc_state_size(void);
+int i8t_dsgc_init(i8t_ctx* ctx, void* state, int64_t period);
+int i8t_dsgc_read(i8t_ctx* ctx, const void* state, i8t_dsgc_view* host_out);
+int i8t_dsgc_write(i8t_ctx* ctx, void* state, const i8t_dsgc_view* host_in);
+/* maybe_update (clip.cpp:80-93) on a device state.  `due` is decided on the
+ * host from (iter, iter_of_last_update, period, clip > 0): pass the host
+ * mirror; i8t_dsgc_read() gives it back. */
+int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64_t iter, int grid, int rounds,
+                     int due);
+/* quantize_gradient (layers.cpp:19-59): Periodic-Update DSGC, phi(d_c) with
+ * (alpha, beta, form), zero-gradient skip, stochastic quantisation from the
+ * device LCG state and the eps/g_hat statistics, fused into one pass over g
+ * on non-search iterations.  g is [rows = N*H*W, cols = C] NHWC (or flat:
+ * rows = 1 ... use hw = rows, c = 1) with the reference's NCHW draw order:
+ * element (n, c, hw) consumes draw index (n*C + c)*HW + hw.
+ * q is written NHWC with channel stride ld_q. */
+int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t c, int64_t hw,
+                          int64_t iter, int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled,
+                          double alpha, double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q);
+/* scale_factor (lr_scale.cpp:8-20), host scalar helper. */
+int i8t_scale_factor(double dc, double alpha, double beta, int form, double* out);
+
+/* ------------------------------------------------------------ convolutions */
+/* Forward: z = float(double(s_a)*double(s_w)*acc), conv2d_q (conv.cpp:108-145).
+ *   a   : NHWC int8, channel stride c_pad (multiple of 4, >= c)
+ *   w   : KRSC int8 rows, row stride ld_w (multiple of 16, >= kh*kw*c_pad)
+ *   z   : NHWC float [N*P*Q][K] (may be NULL); acc: int32 same shape (may be NULL) */
+int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t c_pad, const int8_t* w,
+                 int64_t ld_w, const float* clip_a, const float* clip_w, float* z, int32_t* acc);
+/* Backward-data (conv.cpp:197-203): ga = float(double(s_g)*double(s_w)*acc).
+ *   gz  : NHWC int8 [N*P*Q][k_pad]; wt: CRSK int8 rows (stride ld_wt)
+ *   ga  : NHWC float [N*H*W][C] (may be NULL); acc int32 (may be NULL) */
+int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                   int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc);
+/* Backward-weight (conv.cpp:186-195), int64 accumulation (no depth bound):
+ *   acc : int64 workspace [kh*kw*c_pad][K] (zeroed by the call)
+ *   gw  : float weights, KCRS when out_kcrs != 0 else KRSC (may be NULL) */
+int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a,
+                   int64_t c_pad, const float* clip_g, const float* clip_a, int64_t* acc, float* gw, int out_kcrs);
+/* Depthwise (conv.cpp:115-131, :159-184): a, gz NHWC int8 with channel
+ * stride c_pad; w (C, kh*kw) int8.  Outputs NHWC float / (C, kh*kw) float. */
+int i8t_conv_dw_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t c_pad, const int8_t* w,
+                    const float* clip_a, const float* clip_w, float* z, int32_t* acc);
+int i8t_conv_dw_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t c_pad, const int8_t* w,
+                      const float* clip_g, const float* clip_w, float* ga, int32_t* acc);
+int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, const int8_t* a, int64_t c_pad,
+                      const float* clip_g, const float* clip_a, int64_t* acc, float* gw);
+/* gemm_i8 (gemm.cpp:18-40): C[m][n] = A[m][k] . B[k][n] exact int32
+ * (row-major int8 operands; runs on the tcgen05 path as a 1x1 convolution). */
+int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64_t k, int64_t n, int32_t* c);
+
+/* ------------------------------------------------------------ optimiser */
+/* SGD step of Trainer::train_step (train.cpp:97-117), momentum 0:
+ *   w[i] -= float(lr * g[i]),  lr = base_lr * (phi ? state.lr_scale : 1). */
+int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double base_lr, const void* state);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* I8T_CUDA_H */

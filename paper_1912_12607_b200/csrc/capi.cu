@@ -1,0 +1,123 @@
+// capi.cu -- context, error reporting and scratch management behind i8t_cuda.h.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "internal.cuh"
+
+namespace i8t_dev {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+int set_error(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(I8T_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return I8T_OK;
+}
+
+double* ensure_partials(Ctx* c, size_t doubles) {
+  if (doubles <= c->partials_cap) return c->d_partials;
+  // growth is rare (first use of a larger reduction); keep ordering on the stream
+  cudaStreamSynchronize(c->stream);
+  if (c->d_partials) cudaFree(c->d_partials);
+  c->d_partials = nullptr;
+  size_t cap = doubles < 4096 ? 4096 : doubles * 2;
+  if (cudaMalloc(&c->d_partials, cap * sizeof(double)) != cudaSuccess) {
+    c->partials_cap = 0;
+    return nullptr;
+  }
+  c->partials_cap = cap;
+  return c->d_partials;
+}
+
+void* ensure_scratch(Ctx* c, size_t bytes) {
+  if (bytes <= c->scratch_cap) return c->d_scratch;
+  cudaStreamSynchronize(c->stream);
+  if (c->d_scratch) cudaFree(c->d_scratch);
+  c->d_scratch = nullptr;
+  size_t cap = bytes < 65536 ? 65536 : bytes * 2;
+  if (cudaMalloc(&c->d_scratch, cap) != cudaSuccess) {
+    c->scratch_cap = 0;
+    return nullptr;
+  }
+  cudaMemset(c->d_scratch, 0, cap);
+  c->scratch_cap = cap;
+  return c->d_scratch;
+}
+
+}  // namespace i8t_dev
+
+using namespace i8t_dev;
+
+extern "C" {
+
+int i8t_abi_version(void) { return I8T_ABI_VERSION; }
+
+const char* i8t_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t i8t_launch_count(void) { return g_launches.load(); }
+
+int i8t_ctx_create(void* stream, i8t_ctx** out) {
+  if (!out) return set_error(I8T_EINVAL, "ctx_create: null output");
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    return set_error(I8T_ECUDA, "ctx_create: no CUDA device (this library has no CPU fallback)");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  if (prop.major != 10) return set_error(I8T_EUNSUPPORTED, "ctx_create: requires an sm_100 (B200) device");
+  Ctx* c = new Ctx();
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) {
+    delete c;
+    return set_error(I8T_ECUDA, "ctx_create: cudaMalloc failed");
+  }
+  cudaMemset(c->d_err, 0, sizeof(int));
+  cudaDeviceSynchronize();
+  *out = reinterpret_cast<i8t_ctx*>(c);
+  return cuda_check("ctx_create");
+}
+
+int i8t_ctx_set_stream(i8t_ctx* ctx, void* stream) {
+  if (!ctx) return set_error(I8T_EINVAL, "ctx_set_stream: null ctx");
+  reinterpret_cast<Ctx*>(ctx)->stream = reinterpret_cast<cudaStream_t>(stream);
+  return I8T_OK;
+}
+
+int i8t_ctx_destroy(i8t_ctx* ctx) {
+  if (!ctx) return I8T_OK;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  cudaStreamSynchronize(c->stream);
+  if (c->d_err) cudaFree(c->d_err);
+  if (c->d_partials) cudaFree(c->d_partials);
+  if (c->d_scratch) cudaFree(c->d_scratch);
+  if (c->d_tab) cudaFree(c->d_tab);
+  delete c;
+  return I8T_OK;
+}
+
+int i8t_ctx_check(i8t_ctx* ctx) {
+  if (!ctx) return set_error(I8T_EINVAL, "ctx_check: null ctx");
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_error(I8T_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
+  int h = 0;
+  cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaMemset(c->d_err, 0, sizeof(int));
+  if (h & ERR_NONFINITE) return set_error(I8T_EDOMAIN, "quantize: non-finite input element");
+  if (h) return set_error(I8T_ECUDA, "device error word set");
+  return cuda_check("ctx_check");
+}
+
+}  // extern "C"

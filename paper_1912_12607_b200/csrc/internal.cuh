@@ -1,0 +1,80 @@
+// internal.cuh -- shared declarations of the sm_100a kernels behind i8t_cuda.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/i8t_cuda.h"
+
+namespace i8t_dev {
+
+constexpr uint32_t LCG_A = 1664525u;
+constexpr uint32_t LCG_C = 1013904223u;
+
+// affine map x -> a*x + c (mod 2^32); composition of LCG steps.
+struct Affine {
+  uint32_t a, c;
+};
+
+__host__ __device__ inline Affine lcg_jump_map(uint64_t k) {
+  uint32_t mul = 1u, add = 0u, am = LCG_A, cm = LCG_C;
+  while (k) {
+    if (k & 1u) {
+      mul = am * mul;
+      add = am * add + cm;
+    }
+    cm = am * cm + cm;
+    am = am * am;
+    k >>= 1u;
+  }
+  return {mul, add};
+}
+
+// error bits latched in the context's device error word
+enum : int { ERR_NONFINITE = 1, ERR_INTERNAL = 2 };
+
+// Device-side DSGC state (public view first, search scratch after).
+struct DsgcState {
+  i8t_dsgc_view v;
+  // --- search scratch (clip.cpp:30-78)
+  float m;            // max_abs(g) of the search
+  float best_clip;
+  double best_dc;
+  double sq_g;        // sum g^2
+  double lo, hi, x1, x2, f1, f2;
+  int32_t active;     // search in progress and not short-circuited
+  int32_t ncand;      // candidates in cand[]
+  int32_t phase;      // 0 grid, 1 golden-init, 2.. rounds
+  int32_t grid_done;  // grid candidates consumed so far
+  float cand[32];
+  float prev_clip;
+  int32_t pad_;
+};
+
+// Context: stream, error word, scratch.
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  int* d_err = nullptr;                // latched error bits
+  double* d_partials = nullptr;        // per-block reduction partials
+  size_t partials_cap = 0;             // in doubles
+  void* d_scratch = nullptr;           // misc scratch (tables, temp states)
+  size_t scratch_cap = 0;
+  // cached NCHW-draw-order LCG tables for the gradient quantiser
+  int64_t tab_n = -1, tab_c = -1, tab_hw = -1;
+  Affine* d_tab = nullptr;
+  size_t tab_cap = 0;
+};
+
+// partial buffer layout helpers
+constexpr int RED_THREADS = 256;
+int red_blocks(int64_t n);
+
+double* ensure_partials(Ctx* c, size_t doubles);
+void* ensure_scratch(Ctx* c, size_t bytes);
+
+void count_launch(int n = 1);
+int set_error(int status, const std::string& msg);
+int cuda_check(const char* what);
+
+}  // namespace i8t_dev
