@@ -1,0 +1,348 @@
+"""bench.py -- ResNet-50 INT8 training throughput (BASELINE.json metric:
+"ResNet-50 INT8 train imgs/s @1/2/4/8 B200; conv fwd+bwd TOPS vs INT8 peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch 256] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One step = Trainer.train_step of the INT8 ResNet-50 (all 53 convs + fc on the
+tcgen05 path, DSGC + DCLR, SGD) over one synthetic 224x224 batch per GPU
+(weak scaling, data parallel over NCCL).  Timing: W untimed warm-up steps,
+then exactly K steps between barrier + synchronize on both sides, CUDA events
+on the compute stream, max over ranks.  Inputs (>= 154 MB per step) are larger
+than L2.  The DSGC clip search runs every `clip_period` = 100 iterations
+(Periodic Update); its cost is measured on a separate search step and
+amortised into `value` / `e2e` (value_no_search keeps the raw number).
+
+`--impl reference` times the reference's own CPU implementation on this host:
+the unmodified i8t_core (oracle/_ref) for every ResNet-50 conv layer it
+accepts (stride 1) and the restated oracle for the stride-2 layers it
+rejects (conv.cpp:15-17), one image per step, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "ResNet-50 INT8 train imgs/s"
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def int8_peak_tops():
+    """Dense INT8 tcgen05 peak.  MEASURED_PEAKS.json has only bf16; INT8 dense
+    (kind::i8) runs at 2x the bf16 rate on B200, so the measured sustained bf16
+    GEMM x 2 is the denominator (nominal 4.5 POPS reported beside it)."""
+    p = _peaks()
+    if "bf16_tflops_sustained" in p:
+        return 2.0 * p["bf16_tflops_sustained"], "2x measured bf16 sustained (MEASURED_PEAKS.json)"
+    return 2.0 * 1400.0, "2x fallback bf16 sustained (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- reference CPU arm
+def r50_conv_layers():
+    """(c, h, k, kernel, stride, pad) of the 53 ResNet-50 convs at 224x224, plus fc."""
+    layers = [(3, 224, 64, 7, 2, 3)]
+    cin, h = 64, 56
+    for width, blocks, stride in [(64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)]:
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            layers.append((cin, h, width, 1, 1, 0))
+            layers.append((width, h, width, 3, s, 1))
+            ho = (h + 2 - 3) // s + 1
+            layers.append((width, ho, width * 4, 1, 1, 0))
+            if b == 0:
+                layers.append((cin, h, width * 4, 1, s, 0))
+            cin, h = width * 4, ho
+    return layers
+
+
+def cpu_reference_sample(threads=None):
+    """One image through every ResNet-50 conv layer step (INT8 forward,
+    DSGC measurement + stochastic gradient quantisation, backward-data and
+    backward-weight) on the host.  Returns (seconds, kind, detail)."""
+    import numpy as np
+    from oracle import lib as O
+    from oracle import ref as R
+    have_ref = R.available()
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    t_ref = t_port = 0.0
+    n_ref = n_port = 0
+    rng = np.random.default_rng(0)
+    for (c, h, k, kk, s, p) in r50_conv_layers():
+        x = np.maximum(rng.standard_normal((1, c, h, h)).astype(np.float32), 0)
+        w = (rng.standard_normal((k, c, kk, kk)) * np.sqrt(2.0 / (c * kk * kk))).astype(np.float32)
+        ho = (h + 2 * p - kk) // s + 1
+        go = O.gradient_like((1, k, ho, ho), 7, 1e-4, 0.01)
+        exact = (h + 2 * p - kk) % s == 0 and s == 1
+        if have_ref and exact:
+            gv = R.gvec(1, c, h, h, k, kk, kk, s, p)
+            cs = O.ClipState(0.0, 0.0, -1, 100)
+            R.conv_layer_step(gv, w, x, go, 0, 1, cs)  # iteration 0 searches; time a non-search iteration
+            t0 = time.perf_counter()
+            R.conv_layer_step(gv, w, x, go, 1, 1, cs)
+            t_ref += time.perf_counter() - t0
+            n_ref += 1
+        else:
+            g = O.geom(1, c, h, h, k, kk, kk, s, p)
+            cw, ca = O.max_abs(w), max(O.max_abs(x), 1e-12)
+            st = O.new_clip_state(100)
+            O.quantize_gradient(st, go, 0, 1)
+            t0 = time.perf_counter()
+            qw, _ = O.quantize(w, cw)
+            qa, _ = O.quantize(x, ca)
+            O.conv_fwd(qa, qw, g, O.quant_scale(ca), O.quant_scale(cw))
+            qg, sg, _, _ = O.quantize_gradient(st, go, 1, 1)
+            O.conv_dgrad(qg, qw, g, sg, O.quant_scale(cw))
+            O.conv_wgrad(qg, qa, g, sg, O.quant_scale(ca))
+            t_port += time.perf_counter() - t0
+            n_port += 1
+    kind = "reference" if n_ref and not n_port else ("port" if not n_ref else "reference+port")
+    return t_ref + t_port, kind, {"ref_layers": n_ref, "port_layers": n_port, "ref_s": t_ref, "port_s": t_port}
+
+
+def run_reference_arm(a, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    for _ in range(a.warmup):
+        cpu_reference_sample(cores)
+    ts = []
+    for _ in range(a.steps):
+        t, kind, detail = cpu_reference_sample(cores)
+        ts.append(t)
+    tot = sum(ts)
+    v = a.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "imgs/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {"workload": "resnet50_int8_train_step_convs_1img", "global_batch": 1, "image": 224,
+                       "parallelism": "cpu_threads"},
+            "cpu_baseline": {"value": v, "unit": "imgs/s", "cores": cores, "kind": kind,
+                             "sample": f"1 image through all 53 ResNet-50 conv layer steps per step ({detail})"},
+            "e2e": {"value": v, "unit": "imgs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference_arm(a, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1912_12607_b200 import ops
+    from paper_1912_12607_b200.layers import int8_replace, Mode
+    from paper_1912_12607_b200.models import build_model, conv_gop_per_image
+    from paper_1912_12607_b200.trainer import TrainConfig, Trainer, synthetic_batch
+
+    model = build_model(a.model, seed=1)
+    int8_replace(model.net)
+    cfg = TrainConfig(mode=Mode.INT8, base_lr=0.1, batch_size=a.batch, clip_period=100, seed=1)
+    tr = Trainer(model, cfg)
+    x, y = synthetic_batch(model, a.batch, 1000 + rank)
+    total = 10_000
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world > 1:
+            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return v
+
+    # warm-up (iteration 0 runs the first DSGC search of every layer)
+    it = 0
+    for _ in range(max(a.warmup, 3)):
+        tr.train_step(x, y, it, total, read_stats=False)
+        tr.sync_states()
+        it += 1
+
+    def timed(n, e2e=False, host=None):
+        nonlocal it
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = ops.launch_count()
+        ev0.record()
+        for _ in range(n):
+            if e2e:
+                xs = host[0].to("cuda", non_blocking=True)
+                ys = host[1].to("cuda", non_blocking=True)
+                tr.train_step(xs, ys, it, total, read_stats=False)
+                float(tr.loss_dev.item())  # D2H of the step's loss
+            else:
+                tr.train_step(x, y, it, total, read_stats=False)
+            it += 1
+        ev1.record()
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() - launches0
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, launches = timed(a.steps)
+    clk = clocks.stop()
+    # e2e through the public API: pinned host batch -> device each step, loss read back each step
+    host = (x.cpu().pin_memory(), y.cpu().pin_memory())
+    ms_e2e, _ = timed(a.steps, e2e=True, host=host)
+    # one DSGC search step (Periodic Update, every clip_period iterations), amortised
+    it = ((it // cfg.clip_period) + 1) * cfg.clip_period
+    ms_search, _ = timed(1)
+    extra = max(ms_search - ms / a.steps, 0.0) / cfg.clip_period
+
+    imgs = a.batch * world
+    step_ms = ms / a.steps + extra
+    step_ms_e2e = ms_e2e / a.steps + extra
+    value = imgs / (step_ms / 1e3)
+
+    # conv roofline: one instrumented step, every conv launch bracketed by CUDA events on the compute stream
+    conv_ms, conv_gop = instrumented_conv_time(tr, x, y, it, total, model, a.batch)
+    peak, peak_src = int8_peak_tops()
+    achieved = conv_gop / (conv_ms / 1e3) / 1e3  # TOPS
+    line = {
+        "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (N(0,1) images, uniform labels, Kaiming weights)",
+        "config": {"workload": "resnet50_int8_train_step", "model": "resnet50", "global_batch": imgs,
+                   "per_gpu_batch": a.batch, "image": 224, "parallelism": f"dp{world}", "dsgc_period": 100,
+                   "l2": "inputs > L2 (154 MB/step)"},
+        "value_no_search": imgs / (ms / a.steps / 1e3), "dsgc_search_step_ms": ms_search,
+        "e2e": {"value": imgs / (step_ms_e2e / 1e3), "unit": "imgs/s",
+                "h2d_bytes_per_step": int(host[0].numel() * 4 + host[1].numel() * 8),
+                "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "nominal_peak": 4500.0, "frac_nominal": achieved / 4500.0,
+                     "kernel": "k_conv_tc (fwd+dgrad+wgrad, all ResNet-50 convs)",
+                     "algorithmic_gop_per_step": conv_gop, "conv_ms_per_step": conv_ms,
+                     "conv_share_of_step": conv_ms / step_ms},
+        "clocks": clk,
+    }
+    if rank == 0 and not a.no_cpu_baseline:
+        t, kind, detail = cpu_reference_sample(os.cpu_count())
+        line["cpu_baseline"] = {"value": 1.0 / t, "unit": "imgs/s", "cores": os.cpu_count(), "kind": kind,
+                                "sample": f"1 image through all 53 ResNet-50 conv layer steps ({detail})"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def instrumented_conv_time(tr, x, y, it, total, model, batch):
+    """Run one step with CUDA events around every tcgen05 conv / fc launch."""
+    import torch
+    from paper_1912_12607_b200 import _lib, ops
+    from paper_1912_12607_b200.models import conv_gop_per_image
+    events = []
+    orig = _lib.call
+
+    def wrapped(name, *args):
+        if name in ("i8t_conv_fwd", "i8t_conv_dgrad", "i8t_conv_wgrad", "i8t_conv_dw_fwd", "i8t_conv_dw_dgrad",
+                    "i8t_conv_dw_wgrad"):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            orig(name, *args)
+            e1.record()
+            events.append((e0, e1))
+        else:
+            orig(name, *args)
+    import paper_1912_12607_b200.layers as L
+    L.call = wrapped
+    try:
+        tr.train_step(x, y, it + 1, total, read_stats=False)
+        torch.cuda.synchronize()
+    finally:
+        L.call = orig
+    conv_ms = sum(a.elapsed_time(b) for a, b in events)
+    return conv_ms, conv_gop_per_image(model) * batch
+
+
+if __name__ == "__main__":
+    main()

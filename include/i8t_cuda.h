@@ -71,6 +71,8 @@ typedef struct i8t_dsgc_view {
   double ghat_sqnorm;       /* ||g_hat||^2, QuantState::ghat_sqnorm */
   int64_t iter_of_last_update;
   int64_t period;
+  float clip_q;             /* clip of the last quantised gradient (scale = clip_q/127) */
+  uint32_t reserved;
 } i8t_dsgc_view;
 
 /* ------------------------------------------------------------ context */
@@ -84,6 +86,16 @@ int i8t_ctx_check(i8t_ctx* ctx);
 const char* i8t_last_error(void);
 /* Number of kernels this library launched (for bench accounting). */
 uint64_t i8t_launch_count(void);
+/* Data parallel (8.e): the caller's gradient tensors are shard `rank` of
+ * `world` equal contiguous batch shards.  Global DSGC statistics (max|g| and
+ * the d_c / eps / g_hat sums) are combined by calling `fn` on device buffers
+ * of doubles between kernel phases (op 0 = SUM, 1 = MAX; dtype 0 = f64), and
+ * the stochastic quantiser draws from the global stream at the shard's
+ * offset, so every rank quantises exactly as one device would on the whole
+ * batch.  fn == NULL restores single-device behaviour. */
+typedef int (*i8t_allreduce_fn)(void* user, void* dev_buf, int64_t count, int dtype, int op, void* stream);
+int i8t_ctx_set_allreduce(i8t_ctx* ctx, i8t_allreduce_fn fn, void* user);
+int i8t_ctx_set_shard(i8t_ctx* ctx, int rank, int world);
 
 /* ------------------------------------------------------------ LCG stream */
 /* The gradient stream of LcgStream (quantize.hpp:32-50) lives in device memory
@@ -186,6 +198,11 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
  *   gw  : float weights, KCRS when out_kcrs != 0 else KRSC (may be NULL) */
 int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a,
                    int64_t c_pad, const float* clip_g, const float* clip_a, int64_t* acc, float* gw, int out_kcrs);
+/* Rescale an (all-reduced) int64 wgrad accumulator into float weights; the
+ * data-parallel path calls i8t_conv_wgrad with gw == NULL, sums `acc` across
+ * ranks (exact), then this. */
+int i8t_conv_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t* acc, int64_t c_pad,
+                            const float* clip_g, const float* clip_a, float* gw, int out_kcrs);
 /* Depthwise (conv.cpp:115-131, :159-184): a, gz NHWC int8 with channel
  * stride c_pad; w (C, kh*kw) int8.  Outputs NHWC float / (C, kh*kw) float. */
 int i8t_conv_dw_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t c_pad, const int8_t* w,
@@ -200,8 +217,11 @@ int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64
 
 /* ------------------------------------------------------------ optimiser */
 /* SGD step of Trainer::train_step (train.cpp:97-117), momentum 0:
- *   w[i] -= float(lr * g[i]),  lr = base_lr * (phi ? state.lr_scale : 1). */
-int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double base_lr, const void* state);
+ *   w[i] -= float(lr * g[i]),  lr = base_lr * (state ? state.lr_scale : 1).
+ * skip (device int32, may be NULL): when non-zero the step is skipped (the
+ * reference returns before the update on a non-finite gradient, :87-95). */
+int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double base_lr, const void* state,
+                 const int32_t* skip);
 
 #ifdef __cplusplus
 }

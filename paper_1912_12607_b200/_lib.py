@@ -31,7 +31,8 @@ class ConvGeom(C.Structure):
 class DsgcView(C.Structure):
     _fields_ = [("clip", C.c_float), ("scale", C.c_float), ("max_abs", C.c_float), ("flags", C.c_uint32),
                 ("last_dc", C.c_double), ("lr_scale", C.c_double), ("eps_norm", C.c_double),
-                ("ghat_sqnorm", C.c_double), ("iter_of_last_update", C.c_int64), ("period", C.c_int64)]
+                ("ghat_sqnorm", C.c_double), ("iter_of_last_update", C.c_int64), ("period", C.c_int64),
+                ("clip_q", C.c_float), ("reserved", C.c_uint32)]
 
 
 _CTYPES = {
@@ -48,6 +49,8 @@ def _ptype(decl: str):
         return C.POINTER(ConvGeom)
     if "i8t_dsgc_view" in d:
         return C.POINTER(DsgcView)
+    if "i8t_allreduce_fn" in d:
+        return C.c_void_p
     if "i8t_ctx**" in d.replace(" ", ""):
         return C.POINTER(C.c_void_p)
     if "*" in d:

@@ -55,6 +55,12 @@ void* ensure_scratch(Ctx* c, size_t bytes) {
   return c->d_scratch;
 }
 
+int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op) {
+  if (!c->allreduce || count <= 0) return I8T_OK;
+  const int rc = c->allreduce(c->allreduce_user, buf, count, 0, op, c->stream);
+  return rc ? set_error(I8T_ECUDA, "allreduce hook failed") : I8T_OK;
+}
+
 }  // namespace i8t_dev
 
 using namespace i8t_dev;
@@ -79,11 +85,14 @@ int i8t_ctx_create(void* stream, i8t_ctx** out) {
   if (prop.major != 10) return set_error(I8T_EUNSUPPORTED, "ctx_create: requires an sm_100 (B200) device");
   Ctx* c = new Ctx();
   c->stream = reinterpret_cast<cudaStream_t>(stream);
-  if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&c->d_totals, 128 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->d_ticket, sizeof(unsigned)) != cudaSuccess) {
     delete c;
     return set_error(I8T_ECUDA, "ctx_create: cudaMalloc failed");
   }
   cudaMemset(c->d_err, 0, sizeof(int));
+  cudaMemset(c->d_totals, 0, 128 * sizeof(double));
+  cudaMemset(c->d_ticket, 0, sizeof(unsigned));
   cudaDeviceSynchronize();
   *out = reinterpret_cast<i8t_ctx*>(c);
   return cuda_check("ctx_create");
@@ -95,6 +104,22 @@ int i8t_ctx_set_stream(i8t_ctx* ctx, void* stream) {
   return I8T_OK;
 }
 
+int i8t_ctx_set_allreduce(i8t_ctx* ctx, i8t_allreduce_fn fn, void* user) {
+  if (!ctx) return set_error(I8T_EINVAL, "ctx_set_allreduce: null ctx");
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  c->allreduce = fn;
+  c->allreduce_user = user;
+  return I8T_OK;
+}
+
+int i8t_ctx_set_shard(i8t_ctx* ctx, int rank, int world) {
+  if (!ctx || world < 1 || rank < 0 || rank >= world) return set_error(I8T_EINVAL, "ctx_set_shard: bad rank/world");
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  c->rank = rank;
+  c->world = world;
+  return I8T_OK;
+}
+
 int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (!ctx) return I8T_OK;
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
@@ -102,7 +127,8 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_err) cudaFree(c->d_err);
   if (c->d_partials) cudaFree(c->d_partials);
   if (c->d_scratch) cudaFree(c->d_scratch);
-  if (c->d_tab) cudaFree(c->d_tab);
+  if (c->d_totals) cudaFree(c->d_totals);
+  if (c->d_ticket) cudaFree(c->d_ticket);
   delete c;
   return I8T_OK;
 }

@@ -554,6 +554,22 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   return I8T_OK;
 }
 
+int i8t_conv_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t* acc, int64_t c_pad,
+                            const float* clip_g, const float* clip_a, float* gw, int out_kcrs) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  int64_t P, Q;
+  int rc = geom_common(g, P, Q);
+  if (rc) return rc;
+  if (!c || !acc || !gw || !clip_g || !clip_a || c_pad < g->c) return set_error(I8T_EINVAL, "wgrad_finalize: bad arguments");
+  const int64_t tot = g->k * g->c * g->kh * g->kw;
+  int blocks = (int)((tot + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_wgrad_finalize<<<blocks, 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), (int)g->k, (int)g->c,
+                                                   (int)c_pad, (int)(g->kh * g->kw), clip_g, clip_a, gw, out_kcrs);
+  count_launch(1);
+  return cuda_check("k_wgrad_finalize");
+}
+
 // gemm_i8 as a 1x1 convolution: A [m][k] = NHWC activations (N=m, H=W=1, C=k),
 // B^T [n][k] = KRSC weights.  Temporaries come from the context scratch.
 int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64_t k, int64_t n, int32_t* cout) {

@@ -1,0 +1,690 @@
+// dsgc.cu -- gradient side of the INT8 path on sm_100a:
+//   K3  fused gradient quantiser (quantize_gradient, layers.cpp:19-59): one
+//       pass over g computes max|g|, the non-finite flag, the nearest-rounding
+//       d_c sums at the current clip (Periodic-Update measurement, clip.cpp:90),
+//       the stochastic int8 payload and the eps / g_hat statistics;
+//   K4  d_c sums for up to 32 candidate clips per pass, driving the DSGC
+//       search state machine (search_clip, clip.cpp:30-78);
+//   the plain reductions of tensor.cpp:72-101 and cosine_distance.
+// HBM-bound: float4 loads, char4 stores, warp-shuffle + fixed-order block
+// reductions, one grid-wide "last block finishes" reduction per pass (no extra
+// launch), optional allreduce hook between passes for data parallelism.
+//
+// LCG draw order: the reference draws once per element in row-major NCHW
+// order from one caller-owned stream (quantize.cpp:38-41).  Element
+// (n, c, hw) of a channels-last tensor uses draw index (n*C + c)*HW + hw.  A
+// thread owns a fixed channel quad and steps by a constant number of pixels,
+// so its LCG state advances by a constant affine map (plus a fixed map per
+// image wrap) -- one IMAD per element, no tables.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "internal.cuh"
+#include "qcore.cuh"
+
+namespace i8t_dev {
+
+// totals layout of K3 (QG_NV doubles): max|g|, nonfinite, sum g^2, sum g*gn,
+// sum gn^2, sum (g-gs)^2, sum gs^2, 0.
+constexpr int QG_NV = 8;
+
+struct QgFin {
+  int mode;  // bit0: d_c from the sums (non-search), bit1: lr scaling, bit2: plain quantize (no DSGC state)
+  double alpha, beta;
+  int form;
+  uint32_t advance;  // LCG draws consumed by the whole (global) tensor
+};
+
+// Tail of quantize_gradient (layers.cpp:32-58) from global totals.
+__device__ void fin_quant_grad(DsgcState* st, const double* tot, const QgFin& f, uint32_t* lcg_state, int* err) {
+  const float m = static_cast<float>(tot[0]);
+  const bool nonfinite = tot[1] > 0.0;
+  if (f.mode & 4) {  // plain stochastic quantize (quantize.cpp:33-43): any non-finite throws
+    if (nonfinite) atomicOr(err, ERR_NONFINITE);
+    *lcg_state = apply(lcg_jump_map(f.advance), *lcg_state);
+    return;
+  }
+  if (nonfinite && m != 0.0f) atomicOr(err, ERR_NONFINITE);
+  if (f.mode & 1) st->v.last_dc = (m == 0.0f) ? 0.0 : cosine_from(tot[3], tot[2], tot[4]);
+  const double dc = st->v.last_dc;
+  st->v.lr_scale = (f.mode & 2) ? phi_of(fmin(fmax(dc, 0.0), 2.0), f.alpha, f.beta, f.form) : 1.0;
+  st->v.max_abs = m;
+  if (m == 0.0f || !(st->v.clip > 0.0f)) {  // zero-gradient skip: no draws (layers.cpp:40-47)
+    st->v.clip_q = 1.0f;
+    st->v.scale = scale_of(1.0f);
+    st->v.eps_norm = 0.0;
+    st->v.ghat_sqnorm = 0.0;
+    st->v.flags = (nonfinite ? 1u : 0u) | 2u;
+  } else {
+    st->v.clip_q = st->v.clip;
+    st->v.scale = scale_of(st->v.clip);
+    st->v.eps_norm = sqrt(tot[5]);
+    st->v.ghat_sqnorm = tot[6];
+    st->v.flags = nonfinite ? 1u : 0u;
+    *lcg_state = apply(lcg_jump_map(f.advance), *lcg_state);
+  }
+}
+
+// K3.  NHWC g [N*HW][C] (C % 4 == 0) or FLAT (row-major order = draw order).
+// gridDim.x*blockDim.x*4 is a multiple of C so each thread keeps its channel quad.
+template <bool FLAT, bool DC_SUMS, bool FUSED>
+__global__ void __launch_bounds__(RED_THREADS) k_quant_grad(const float* __restrict__ g, uint32_t numel, uint32_t C,
+                                                            uint32_t HW, uint32_t draw_offset, Affine step_iter,
+                                                            Affine step_elem, Affine step_wrap, uint32_t dpix,
+                                                            const float* clip_override, DsgcState* st,
+                                                            uint32_t* lcg_state, int8_t* __restrict__ q,
+                                                            double* partials, double* totals, unsigned* ticket, QgFin fin,
+                                                            int* err) {
+  float clip = clip_override ? *clip_override : st->v.clip;
+  if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
+  const float s = scale_of(clip), inv_s = 1.0f / s;
+  const uint32_t X0 = *lcg_state;
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  double acc[QG_NV] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float m = 0.0f;
+  if (e < numel) {
+    uint32_t X, hw = 0;
+    if (FLAT) {
+      X = apply(lcg_jump_map(static_cast<uint64_t>(e) + draw_offset + 1u), X0);
+    } else {
+      const uint32_t pix = e / C, c = e - pix * C;
+      const uint32_t n = pix / HW;
+      hw = pix - n * HW;
+      X = apply(lcg_jump_map(static_cast<uint64_t>((n * C + c) * HW + hw) + draw_offset + 1u), X0);
+    }
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4 v4 = __ldg(g4 + e / 4);
+    while (true) {
+      const uint32_t e_next = e + T4;
+      float4 nxt;
+      if (e_next < numel) nxt = __ldg(g4 + e_next / 4);  // software prefetch of the next float4
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      signed char qq[4];
+      uint32_t Xj = X;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j) Xj = apply(step_elem, Xj);
+        const float v = vv[j];
+        if (!isfinite(v)) acc[1] += 1.0;
+        m = fmaxf(m, fabsf(v));
+        const int qs = quant_stoch(v, clip, s, inv_s, Xj);
+        qq[j] = static_cast<signed char>(qs);
+        const float gs = __fmul_rn(static_cast<float>(qs), s);
+        const double vd = v, gsd = gs;
+        const double d = vd - gsd;
+        acc[5] = fma(d, d, acc[5]);
+        acc[6] = fma(gsd, gsd, acc[6]);
+        if (DC_SUMS) {
+          const double gn = __fmul_rn(static_cast<float>(quant_nearest(v, clip, s, inv_s)), s);
+          acc[2] = fma(vd, vd, acc[2]);
+          acc[3] = fma(vd, gn, acc[3]);
+          acc[4] = fma(gn, gn, acc[4]);
+        }
+      }
+      reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
+      if (e_next >= numel) break;
+      e = e_next;
+      v4 = nxt;
+      X = apply(step_iter, X);
+      if (!FLAT) {
+        hw += dpix;
+        while (hw >= HW) {
+          hw -= HW;
+          X = apply(step_wrap, X);
+        }
+      }
+    }
+  }
+  acc[0] = m;
+  if (grid_reduce<QG_NV>(acc, 1u, partials, totals, ticket) && FUSED && threadIdx.x == 0)
+    fin_quant_grad(st, totals, fin, lcg_state, err);
+}
+
+__global__ void k_fin_quant_grad(DsgcState* st, const double* totals, QgFin fin, uint32_t* lcg_state, int* err) {
+  if (threadIdx.x == 0) fin_quant_grad(st, totals, fin, lcg_state, err);
+}
+
+// K4.  totals: [0] max|g|, [1] nonfinite, [2] sum g^2, [3+2j] sum g*gh_j, [4+2j] sum gh_j^2.
+template <int NC>
+__global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restrict__ g, uint32_t n,
+                                                          const float* __restrict__ cands, const int32_t* active,
+                                                          double* partials, double* totals, unsigned* ticket) {
+  constexpr int NV = 3 + 2 * NC;
+  if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
+  float cl[NC > 0 ? NC : 1], sc[NC > 0 ? NC : 1], is[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    cl[j] = cands[j];
+    sc[j] = scale_of(cl[j]);
+    is[j] = 1.0f / sc[j];
+  }
+  double acc[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+  float m = 0.0f;
+  auto body = [&](float v) {
+    if (!isfinite(v)) acc[1] += 1.0;
+    m = fmaxf(m, fabsf(v));
+    const double vd = v;
+    acc[2] = fma(vd, vd, acc[2]);
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const double gh = __fmul_rn(static_cast<float>(quant_nearest(v, cl[j], sc[j], is[j])), sc[j]);
+      acc[3 + 2 * j] = fma(vd, gh, acc[3 + 2 * j]);
+      acc[4 + 2 * j] = fma(gh, gh, acc[4 + 2 * j]);
+    }
+  };
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n4; f += stride) {
+    const float4 v = __ldg(g4 + f);
+    body(v.x);
+    body(v.y);
+    body(v.z);
+    body(v.w);
+  }
+  for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) body(g[i]);
+  acc[0] = m;
+  grid_reduce<NV>(acc, 1u, partials, totals, ticket);
+}
+
+// ---- DSGC search state machine (clip.cpp:30-78), one thread, on totals.
+__device__ __forceinline__ void ds_consider(DsgcState* st, float c, double dc) {
+  if (!(c > 0.0f)) return;
+  if (dc < st->best_dc || (dc == st->best_dc && c > st->best_clip)) {
+    st->best_clip = c;
+    st->best_dc = dc;
+  }
+}
+__device__ __forceinline__ void ds_track(DsgcState* st, double x, double f) {
+  if (f < st->best_dc || (f == st->best_dc && static_cast<float>(x) > st->best_clip)) {
+    st->best_clip = static_cast<float>(x);
+    st->best_dc = f;
+  }
+}
+__device__ __forceinline__ void ds_grid_chunk(DsgcState* st, int R) {
+  const int left = R - st->grid_done;
+  const int nc = left < 32 ? left : 32;
+  for (int j = 0; j < nc; ++j) {
+    const int i = st->grid_done + j + 1;
+    st->cand[j] = __fmul_rn(st->m, __fdiv_rn(static_cast<float>(i), static_cast<float>(R)));
+  }
+  st->ncand = nc;
+}
+constexpr double kInvPhi = 0.6180339887498949;
+
+// After the k_dc_stats<0> pass: m, non-finite, sum g^2 (clip.cpp:32-34).
+__global__ void k_search_begin(DsgcState* st, const double* tot, int R, float prev_clip, int prev_from_state, int* err) {
+  if (threadIdx.x) return;
+  if (prev_from_state) prev_clip = st->v.clip;
+  st->m = static_cast<float>(tot[0]);
+  st->v.max_abs = st->m;
+  st->sq_g = tot[2];
+  st->prev_clip = prev_clip;
+  st->best_clip = 0.0f;
+  st->best_dc = 3.0;
+  st->grid_done = 0;
+  st->phase = 0;
+  if (st->m == 0.0f || tot[1] > 0.0) {
+    if (st->m != 0.0f) atomicOr(err, ERR_NONFINITE);
+    st->active = 0;  // all-zero g: {prev_clip, 0}
+    st->best_clip = prev_clip;
+    st->best_dc = 0.0;
+    return;
+  }
+  st->active = 1;
+  ds_grid_chunk(st, R);
+}
+
+// After a k_dc_stats<nc> pass over st->cand.
+__global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, int rounds) {
+  if (threadIdx.x || st->active == 0) return;
+  double dcs[32];
+  for (int j = 0; j < nc; ++j) dcs[j] = cosine_from(tot[3 + 2 * j], st->sq_g, tot[4 + 2 * j]);
+  if (st->phase == 0) {  // grid
+    for (int j = 0; j < nc; ++j) ds_consider(st, st->cand[j], dcs[j]);
+    st->grid_done += nc;
+    if (st->grid_done < R) {
+      ds_grid_chunk(st, R);
+      return;
+    }
+    if (rounds <= 0) {
+      st->active = 0;
+      return;
+    }
+    const double step = static_cast<double>(st->m) / R;
+    double lo = static_cast<double>(st->best_clip) - step;
+    double hi = static_cast<double>(st->best_clip) + step;
+    lo = lo < 0.0 ? 0.0 : lo;
+    hi = hi > static_cast<double>(st->m) ? static_cast<double>(st->m) : hi;
+    st->lo = lo;
+    st->hi = hi;
+    // x1 = hi - (hi-lo)*kInvPhi, x2 = lo + (hi-lo)*kInvPhi, FMA-contracted like the reference build
+    st->x1 = __fma_rn(-(hi - lo), kInvPhi, hi);
+    st->x2 = __fma_rn(hi - lo, kInvPhi, lo);
+    st->cand[0] = static_cast<float>(st->x1);
+    st->cand[1] = static_cast<float>(st->x2);
+    st->ncand = 2;
+    st->phase = 1;
+    return;
+  }
+  if (st->phase == 1) {
+    st->f1 = dcs[0];
+    st->f2 = dcs[1];
+    ds_track(st, st->x1, st->f1);
+    ds_track(st, st->x2, st->f2);
+  } else if (st->pad_ == 0) {
+    st->f1 = dcs[0];
+    ds_track(st, st->x1, st->f1);
+  } else {
+    st->f2 = dcs[0];
+    ds_track(st, st->x2, st->f2);
+  }
+  if (st->phase - 1 >= rounds) {
+    st->active = 0;
+    return;
+  }
+  if (st->f1 < st->f2) {
+    st->hi = st->x2;
+    st->x2 = st->x1;
+    st->f2 = st->f1;
+    st->x1 = __fma_rn(-(st->hi - st->lo), kInvPhi, st->hi);
+    st->cand[0] = static_cast<float>(st->x1);
+    st->pad_ = 0;
+  } else {
+    st->lo = st->x1;
+    st->x1 = st->x2;
+    st->f1 = st->f2;
+    st->x2 = __fma_rn(st->hi - st->lo, kInvPhi, st->lo);
+    st->cand[0] = static_cast<float>(st->x2);
+    st->pad_ = 1;
+  }
+  st->ncand = 1;
+  st->phase += 1;
+}
+
+// End of maybe_update's search branch (clip.cpp:84-88) or a raw search_clip.
+__global__ void k_search_end(DsgcState* st, int64_t iter, int update_state, float* clip_out, double* dc_out) {
+  if (threadIdx.x) return;
+  const float c = st->best_clip;
+  const double dc = st->best_dc;
+  if (clip_out) *clip_out = c;
+  if (dc_out) *dc_out = dc;
+  if (update_state) {
+    if (c > 0.0f) st->v.clip = c;
+    st->v.last_dc = dc;
+    st->v.iter_of_last_update = iter;
+  }
+}
+
+// Search-disabled branch of quantize_gradient (layers.cpp:27-36): clip = max_abs.
+__global__ void k_clip_from_max(DsgcState* st, const double* tot, int64_t iter) {
+  if (threadIdx.x) return;
+  const float mf = static_cast<float>(tot[0]);
+  if (mf > 0.0f) st->v.clip = mf;
+  st->v.iter_of_last_update = iter;
+}
+
+// Non-search branch of maybe_update: last_dc = max_abs == 0 ? 0 : measure_dc.
+__global__ void k_fin_maybe_dc(DsgcState* st, const double* tot, int* err) {
+  if (threadIdx.x) return;
+  const float m = static_cast<float>(tot[0]);
+  st->v.max_abs = m;
+  if (m == 0.0f) {
+    st->v.last_dc = 0.0;
+    return;
+  }
+  if (tot[1] > 0.0) atomicOr(err, ERR_NONFINITE);
+  st->v.last_dc = cosine_from(tot[3], tot[2], tot[4]);
+}
+
+__global__ void k_fin_scalar(const double* tot, int which, float* out_f, double* out_d, int32_t* out_i) {
+  if (threadIdx.x) return;
+  const double v = tot[which];
+  if (out_f) *out_f = static_cast<float>(v);
+  if (out_d) *out_d = v;
+  if (out_i) *out_i = v > 0.0 ? 1 : 0;
+}
+
+__global__ void k_fin_measure_dc(const double* tot, double* out, int* err) {
+  if (threadIdx.x) return;
+  if (tot[1] > 0.0) atomicOr(err, ERR_NONFINITE);
+  *out = cosine_from(tot[3], tot[2], tot[4]);
+}
+
+// dot / cosine totals: [0] sum a*b [1] sum a^2 [2] sum b^2
+__global__ void __launch_bounds__(RED_THREADS) k_dot3(const float* __restrict__ a, const float* __restrict__ b,
+                                                      uint32_t n, double* partials, double* totals, unsigned* ticket) {
+  double acc[3] = {0, 0, 0};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    acc[0] = fma(x, y, acc[0]);
+    acc[1] = fma(x, x, acc[1]);
+    acc[2] = fma(y, y, acc[2]);
+  }
+  grid_reduce<3>(acc, 0u, partials, totals, ticket);
+}
+
+__global__ void k_fin_cosine(const double* tot, double* dot_out, double* cos_out) {
+  if (threadIdx.x) return;
+  if (dot_out) *dot_out = tot[0];
+  if (cos_out) *cos_out = cosine_from(tot[0], tot[1], tot[2]);
+}
+
+// ---------------------------------------------------------------- host side
+static int nblocks(int64_t n, int64_t multiple = 1) {
+  int64_t b = (n + RED_THREADS * 8 - 1) / (RED_THREADS * 8);
+  if (b < 1) b = 1;
+  if (b > 592) b = 592;
+  b = (b + multiple - 1) / multiple * multiple;
+  return static_cast<int>(b);
+}
+
+static int gcd_i(int64_t a, int64_t b) { return b == 0 ? static_cast<int>(a) : gcd_i(b, a % b); }
+
+// Ensure partials for nblk blocks x nv values, and run kernel K.
+static int stats_pass0(Ctx* c, const float* x, int64_t n) {
+  const int nb = nblocks(n);
+  double* p = ensure_partials(c, static_cast<size_t>(nb) * 3);
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+  k_dc_stats<0><<<nb, RED_THREADS, 0, c->stream>>>(x, static_cast<uint32_t>(n), nullptr, nullptr, p, c->d_totals,
+                                                    c->d_ticket);
+  count_launch(1);
+  return cuda_check("k_dc_stats<0>");
+}
+
+template <int NC>
+static void dc_pass(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nb, double* p) {
+  k_dc_stats<NC><<<nb, RED_THREADS, 0, c->stream>>>(g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
+                                                     c->d_ticket);
+}
+
+static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nc) {
+  const int nb = nblocks(n);
+  double* p = ensure_partials(c, static_cast<size_t>(nb) * (3 + 2 * 32));
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+  switch (nc) {
+#define CASE(K) \
+  case K: dc_pass<K>(c, g, n, cands, active, nb, p); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+    CASE(14) CASE(15) CASE(16) CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24) CASE(25)
+    CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+    default: return set_error(I8T_EINVAL, "dc pass: bad candidate count");
+  }
+  count_launch(1);
+  return cuda_check("k_dc_stats");
+}
+
+// Global totals for data parallelism: totals[0] MAX, totals[1..nv) SUM.
+static int allreduce_totals(Ctx* c, int nv) {
+  if (!c->allreduce) return I8T_OK;
+  int rc = ctx_allreduce(c, c->d_totals, 1, 1);
+  if (rc) return rc;
+  return ctx_allreduce(c, c->d_totals + 1, nv - 1, 0);
+}
+
+static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, int rounds, float prev_clip,
+                      int prev_from_state) {
+  int rc = stats_pass0(c, g, n);
+  if (rc || (rc = allreduce_totals(c, 3))) return rc;
+  k_search_begin<<<1, 32, 0, c->stream>>>(st, c->d_totals, R, prev_clip, prev_from_state, c->d_err);
+  count_launch(1);
+  // The device decides whether the search short-circuits (st->active); under
+  // data parallelism every rank takes the same branch (global totals), and a
+  // skipped pass contributes a zero totals buffer to the hook.
+  auto pass = [&](int nc) -> int {
+    if (c->allreduce) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * nc), c->stream);
+    int r = dc_pass_n(c, g, n, st->cand, &st->active, nc);
+    if (r || (r = allreduce_totals(c, 3 + 2 * nc))) return r;
+    k_search_step<<<1, 32, 0, c->stream>>>(st, c->d_totals, nc, R, rounds);
+    count_launch(1);
+    return cuda_check("k_search_step");
+  };
+  for (int done = 0; done < R; done += 32)
+    if ((rc = pass((R - done) < 32 ? (R - done) : 32))) return rc;
+  if (rounds > 0) {
+    if ((rc = pass(2))) return rc;
+    for (int r = 0; r < rounds; ++r)
+      if ((rc = pass(1))) return rc;
+  }
+  return I8T_OK;
+}
+
+// K3 launcher.
+static int launch_quant_grad(Ctx* c, DsgcState* st, const float* clip_override, const float* g, int64_t n_img,
+                             int64_t C, int64_t HW, bool dc_sums, uint32_t* lcg, int8_t* q, QgFin fin) {
+  const int64_t numel = n_img * C * HW;
+  const bool flat = (C == 1);
+  if (numel % 4 != 0 || (!flat && C % 4 != 0))
+    return set_error(I8T_EUNSUPPORTED, "quantize_gradient: needs C % 4 == 0 (or flat) and numel % 4 == 0");
+  if (numel >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "quantize_gradient: tensor >= 2^31 elements");
+  // grid: threads*4 must be a multiple of C (each thread keeps its channel quad)
+  const int64_t mult = flat ? 1 : C / gcd_i(C, RED_THREADS * 4);
+  int nb = nblocks(numel, mult);
+  double* p = ensure_partials(c, static_cast<size_t>(nb) * QG_NV);
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+  const uint32_t T4 = static_cast<uint32_t>(nb) * RED_THREADS * 4u;
+  const uint32_t draw_offset = static_cast<uint32_t>(static_cast<uint64_t>(c->rank) * static_cast<uint64_t>(numel));
+  Affine step_iter, step_elem, step_wrap{1u, 0u};
+  uint32_t dpix = 0;
+  if (flat) {
+    step_iter = lcg_jump_map(T4);
+    step_elem = lcg_jump_map(1);
+  } else {
+    dpix = T4 / static_cast<uint32_t>(C);
+    step_iter = lcg_jump_map(dpix);
+    step_elem = lcg_jump_map(static_cast<uint64_t>(HW));
+    step_wrap = lcg_jump_map(static_cast<uint64_t>(C - 1) * static_cast<uint64_t>(HW));
+  }
+  fin.advance = static_cast<uint32_t>(static_cast<uint64_t>(c->world) * static_cast<uint64_t>(numel));
+  const bool fused = (c->allreduce == nullptr);
+  const uint32_t un = static_cast<uint32_t>(numel), uc = static_cast<uint32_t>(flat ? 1 : C),
+                 uhw = static_cast<uint32_t>(flat ? numel : HW);
+#define LAUNCH(F, D, U)                                                                                               \
+  k_quant_grad<F, D, U><<<nb, RED_THREADS, 0, c->stream>>>(g, un, uc, uhw, draw_offset, step_iter, step_elem,       \
+                                                           step_wrap, dpix, clip_override, st, lcg, q, p,           \
+                                                           c->d_totals, c->d_ticket, fin, c->d_err)
+  if (flat) {
+    if (dc_sums) { if (fused) LAUNCH(true, true, true); else LAUNCH(true, true, false); }
+    else { if (fused) LAUNCH(true, false, true); else LAUNCH(true, false, false); }
+  } else {
+    if (dc_sums) { if (fused) LAUNCH(false, true, true); else LAUNCH(false, true, false); }
+    else { if (fused) LAUNCH(false, false, true); else LAUNCH(false, false, false); }
+  }
+#undef LAUNCH
+  count_launch(1);
+  int rc = cuda_check("k_quant_grad");
+  if (rc || fused) return rc;
+  if ((rc = allreduce_totals(c, QG_NV))) return rc;
+  k_fin_quant_grad<<<1, 32, 0, c->stream>>>(st, c->d_totals, fin, lcg, c->d_err);
+  count_launch(1);
+  return cuda_check("k_fin_quant_grad");
+}
+
+}  // namespace i8t_dev
+
+using namespace i8t_dev;
+#define CTX(c) reinterpret_cast<Ctx*>(c)
+
+extern "C" {
+
+int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !out) return set_error(I8T_EINVAL, "max_abs: bad arguments");
+  int rc = stats_pass0(c, x, n);
+  if (rc) return rc;
+  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 0, out, nullptr, nullptr);
+  count_launch(1);
+  return cuda_check("k_fin_scalar");
+}
+
+int i8t_sq_l2_norm(i8t_ctx* ctx, const float* x, int64_t n, double* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !out) return set_error(I8T_EINVAL, "sq_l2_norm: bad arguments");
+  int rc = stats_pass0(c, x, n);
+  if (rc) return rc;
+  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 2, nullptr, out, nullptr);
+  count_launch(1);
+  return cuda_check("k_fin_scalar");
+}
+
+int i8t_has_nonfinite(i8t_ctx* ctx, const float* x, int64_t n, int32_t* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !out) return set_error(I8T_EINVAL, "has_nonfinite: bad arguments");
+  int rc = stats_pass0(c, x, n);
+  if (rc) return rc;
+  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 1, nullptr, nullptr, out);
+  count_launch(1);
+  return cuda_check("k_fin_scalar");
+}
+
+static int dot_like(Ctx* c, const float* a, const float* b, int64_t n, double* dot_out, double* cos_out) {
+  const int nb = nblocks(n);
+  double* p = ensure_partials(c, static_cast<size_t>(nb) * 3);
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+  k_dot3<<<nb, RED_THREADS, 0, c->stream>>>(a, b, static_cast<uint32_t>(n), p, c->d_totals, c->d_ticket);
+  k_fin_cosine<<<1, 32, 0, c->stream>>>(c->d_totals, dot_out, cos_out);
+  count_launch(2);
+  return cuda_check("k_dot3");
+}
+
+int i8t_dot(i8t_ctx* ctx, const float* a, const float* b, int64_t n, double* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !a || !b || !out) return set_error(I8T_EINVAL, "dot: bad arguments");
+  return dot_like(c, a, b, n, out, nullptr);
+}
+
+int i8t_cosine_distance(i8t_ctx* ctx, const float* g, const float* h, int64_t n, double* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !g || !h || !out) return set_error(I8T_EINVAL, "cosine_distance: bad arguments");
+  return dot_like(c, g, h, n, nullptr, out);
+}
+
+int i8t_measure_dc(i8t_ctx* ctx, const float* g, int64_t n, float clip, double* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !g || !out) return set_error(I8T_EINVAL, "measure_dc: bad arguments");
+  if (!(clip > 0.0f) || !std::isfinite(clip)) return set_error(I8T_EINVAL, "QuantParams: clip must be positive and finite");
+  float* dclip = reinterpret_cast<float*>(ensure_scratch(c, 256));
+  if (!dclip) return set_error(I8T_ECUDA, "scratch alloc failed");
+  cudaMemcpyAsync(dclip, &clip, sizeof(float), cudaMemcpyHostToDevice, c->stream);
+  int rc = dc_pass_n(c, g, n, dclip, nullptr, 1);
+  if (rc) return rc;
+  k_fin_measure_dc<<<1, 32, 0, c->stream>>>(c->d_totals, out, c->d_err);
+  count_launch(1);
+  cudaStreamSynchronize(c->stream);  // `clip` lives on the caller's stack
+  return cuda_check("measure_dc");
+}
+
+int i8t_search_clip(i8t_ctx* ctx, const float* g, int64_t n, int grid, int rounds, float prev_clip, float* clip_out,
+                    double* dc_out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !g) return set_error(I8T_EINVAL, "search_clip: bad arguments");
+  if (grid < 8) return set_error(I8T_EINVAL, "search_clip: grid resolution must be >= 8");
+  DsgcState* st = reinterpret_cast<DsgcState*>(ensure_scratch(c, sizeof(DsgcState)));
+  if (!st) return set_error(I8T_ECUDA, "scratch alloc failed");
+  int rc = run_search(c, st, g, n, grid, rounds, prev_clip, 0);
+  if (rc) return rc;
+  k_search_end<<<1, 32, 0, c->stream>>>(st, 0, 0, clip_out, dc_out);
+  count_launch(1);
+  return cuda_check("k_search_end");
+}
+
+int64_t i8t_dsgc_state_size(void) { return static_cast<int64_t>(sizeof(DsgcState)); }
+
+int i8t_dsgc_init(i8t_ctx* ctx, void* state, int64_t period) {
+  Ctx* c = CTX(ctx);
+  if (!c || !state) return set_error(I8T_EINVAL, "dsgc_init: bad arguments");
+  DsgcState h{};
+  h.v.iter_of_last_update = -1;
+  h.v.period = period;
+  h.v.lr_scale = 1.0;
+  cudaMemcpyAsync(state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return cuda_check("dsgc_init");
+}
+
+int i8t_dsgc_read(i8t_ctx* ctx, const void* state, i8t_dsgc_view* out) {
+  Ctx* c = CTX(ctx);
+  if (!c || !state || !out) return set_error(I8T_EINVAL, "dsgc_read: bad arguments");
+  cudaMemcpyAsync(out, state, sizeof(i8t_dsgc_view), cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return cuda_check("dsgc_read");
+}
+
+int i8t_dsgc_write(i8t_ctx* ctx, void* state, const i8t_dsgc_view* in) {
+  Ctx* c = CTX(ctx);
+  if (!c || !state || !in) return set_error(I8T_EINVAL, "dsgc_write: bad arguments");
+  cudaMemcpyAsync(state, in, sizeof(i8t_dsgc_view), cudaMemcpyHostToDevice, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return cuda_check("dsgc_write");
+}
+
+int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64_t iter, int grid, int rounds, int due) {
+  Ctx* c = CTX(ctx);
+  DsgcState* st = reinterpret_cast<DsgcState*>(state);
+  if (!c || !st || !g) return set_error(I8T_EINVAL, "maybe_update: bad arguments");
+  if (grid < 8) return set_error(I8T_EINVAL, "search_clip: grid resolution must be >= 8");
+  int rc;
+  if (due) {
+    if ((rc = run_search(c, st, g, n, grid, rounds, 0.0f, 1))) return rc;
+    k_search_end<<<1, 32, 0, c->stream>>>(st, iter, 1, nullptr, nullptr);
+    count_launch(1);
+    return cuda_check("maybe_update");
+  }
+  if ((rc = dc_pass_n(c, g, n, &st->v.clip, nullptr, 1)) || (rc = allreduce_totals(c, 5))) return rc;
+  k_fin_maybe_dc<<<1, 32, 0, c->stream>>>(st, c->d_totals, c->d_err);
+  count_launch(1);
+  return cuda_check("maybe_update");
+}
+
+int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW, int64_t iter,
+                          int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled, double alpha,
+                          double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q) {
+  Ctx* c = CTX(ctx);
+  DsgcState* st = reinterpret_cast<DsgcState*>(state);
+  if (!c || !st || !g || !lcg_state || !q || n_img < 1 || C < 1 || HW < 1)
+    return set_error(I8T_EINVAL, "quantize_gradient: bad arguments");
+  if (ld_q != C) return set_error(I8T_EUNSUPPORTED, "quantize_gradient: ld_q must equal C");
+  if (lr_scaling_enabled) {
+    if (!(alpha > 0.0)) return set_error(I8T_EINVAL, "scale_factor: alpha must be > 0");
+    if (!(beta > 0.0 && beta <= 1.0)) return set_error(I8T_EINVAL, "scale_factor: beta must be in (0,1]");
+  }
+  const int64_t numel = n_img * C * HW;
+  int rc;
+  bool dc_sums;
+  if (search_enabled) {
+    if (grid < 8) return set_error(I8T_EINVAL, "search_clip: grid resolution must be >= 8");
+    if (due) {
+      if ((rc = run_search(c, st, g, numel, grid, rounds, 0.0f, 1))) return rc;
+      k_search_end<<<1, 32, 0, c->stream>>>(st, iter, 1, nullptr, nullptr);
+      count_launch(1);
+      dc_sums = false;
+    } else {
+      dc_sums = true;
+    }
+  } else {
+    if ((rc = stats_pass0(c, g, numel)) || (rc = allreduce_totals(c, 3))) return rc;
+    k_clip_from_max<<<1, 32, 0, c->stream>>>(st, c->d_totals, iter);
+    count_launch(1);
+    dc_sums = true;
+  }
+  QgFin fin{(dc_sums ? 1 : 0) | (lr_scaling_enabled ? 2 : 0), alpha, beta, form, 0u};
+  return launch_quant_grad(c, st, nullptr, g, n_img, C, HW, dc_sums, lcg_state, q, fin);
+}
+
+int i8t_quantize_stochastic(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, uint32_t* lcg_state, int8_t* q) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !clip || !lcg_state || !q) return set_error(I8T_EINVAL, "quantize: stream required iff mode is stochastic");
+  if (n == 0) return I8T_OK;
+  if (n % 4 != 0) return set_error(I8T_EUNSUPPORTED, "quantize_stochastic: numel % 4 != 0 (pad on the host)");
+  DsgcState* st = reinterpret_cast<DsgcState*>(ensure_scratch(c, sizeof(DsgcState)));
+  if (!st) return set_error(I8T_ECUDA, "scratch alloc failed");
+  QgFin fin{4, 0.0, 0.0, 0, 0u};
+  return launch_quant_grad(c, st, clip, x, 1, 1, n, false, lcg_state, q, fin);
+}
+
+}  // extern "C"

@@ -52,23 +52,28 @@ struct DsgcState {
   int32_t pad_;
 };
 
-// Context: stream, error word, scratch.
+// Context: stream, error word, scratch, data-parallel hooks.
 struct Ctx {
   cudaStream_t stream = nullptr;
   int* d_err = nullptr;                // latched error bits
   double* d_partials = nullptr;        // per-block reduction partials
   size_t partials_cap = 0;             // in doubles
-  void* d_scratch = nullptr;           // misc scratch (tables, temp states)
+  double* d_totals = nullptr;          // grid-reduced totals (128 doubles)
+  unsigned* d_ticket = nullptr;        // last-block ticket (self-resetting)
+  void* d_scratch = nullptr;           // misc scratch (temp states, small buffers)
   size_t scratch_cap = 0;
-  // cached NCHW-draw-order LCG tables for the gradient quantiser
-  int64_t tab_n = -1, tab_c = -1, tab_hw = -1;
-  Affine* d_tab = nullptr;
-  size_t tab_cap = 0;
+  // data parallel: the gradient of this rank is shard `rank` of `world` equal
+  // shards of the global batch; statistics are combined through `allreduce`.
+  i8t_allreduce_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  int rank = 0, world = 1;
 };
+
+// Runs the allreduce hook (if any) on `count` device doubles: op 0 = SUM, 1 = MAX.
+int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op);
 
 // partial buffer layout helpers
 constexpr int RED_THREADS = 256;
-int red_blocks(int64_t n);
 
 double* ensure_partials(Ctx* c, size_t doubles);
 void* ensure_scratch(Ctx* c, size_t bytes);

@@ -1,0 +1,137 @@
+// qcore.cuh -- device-side numerics shared by the quantiser and DSGC kernels:
+// the exact FP32 restatements of quantize_value (quantize.cpp:16-31), the
+// reference's cosine / phi formulas, deterministic block reductions and the
+// "last block finishes" grid reduction.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace i8t_dev {
+
+__device__ __forceinline__ float scale_of(float clip) { return __fdiv_rn(clip, 127.0f); }
+
+// quantize_value, kNearest: lround(RN64(v/s)) == round-half-away(v/s) since
+// RN64 cannot cross a half-integer for float v, s; the tie
+// test a >= s*(k+1/2) is decided exactly by the sign of one FMA.
+__device__ __forceinline__ int quant_nearest(float x, float clip, float s, float inv_s) {
+  const float v = fminf(fmaxf(x, -clip), clip);
+  const float a = fabsf(v);
+  float k = floorf(__fmaf_rn(a, inv_s, 0.5f));
+  if (__fmaf_rn(-s, k + 0.5f, a) >= 0.0f) k += 1.0f;
+  else if (__fmaf_rn(-s, k - 0.5f, a) < 0.0f) k -= 1.0f;
+  k = fminf(k, 127.0f);
+  const int qi = static_cast<int>(k);
+  return v < 0.0f ? -qi : qi;
+}
+
+// quantize_value, kStochastic: floor(t) + (u < frac(t)), t = RN64(v/s) clamped
+// to +-127, u = X * 2^-32.  FP32 decides when every margin exceeds 2^-13
+// (|t32 - t| < 2e-5, |u32 - u| < 2^-24); otherwise the exact FP64 formula runs.
+__device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {
+  if (x == 0.0f) return 0;
+  const float v = fminf(fmaxf(x, -clip), clip);
+  const float t = v * inv_s;
+  const float fl = floorf(t);
+  const float frac = t - fl;
+  const float u = static_cast<float>(X >> 8) * 0x1.0p-24f;
+  constexpr float D = 0x1.0p-13f;
+  int q;
+  if (frac > D && frac < 1.0f - D && fabsf(frac - u) > D) {
+    q = static_cast<int>(fl) + (u < frac ? 1 : 0);
+  } else {
+    double td = static_cast<double>(v) / static_cast<double>(s);
+    td = fmin(fmax(td, -127.0), 127.0);
+    const double fd = floor(td);
+    const double fr = td - fd;
+    const double ud = static_cast<double>(X) * 0x1.0p-32;
+    q = static_cast<int>(fd) + (ud < fr ? 1 : 0);
+  }
+  return max(-127, min(127, q));
+}
+
+__device__ __forceinline__ uint32_t apply(Affine m, uint32_t x) { return m.a * x + m.c; }
+
+__device__ __forceinline__ double cosine_from(double num, double sq_g, double sq_h) {
+  if (sq_g == 0.0 && sq_h == 0.0) return 0.0;
+  if (sq_g == 0.0 || sq_h == 0.0) return 1.0;
+  return 1.0 - num / (sqrt(sq_g) * sqrt(sq_h));
+}
+
+// phi(d_c) (lr_scale.cpp:8-20); argument checks happen on the host.
+__device__ __forceinline__ double phi_of(double dc, double alpha, double beta, int form) {
+  double raw;
+  if (form == 0) raw = exp(-alpha * dc);
+  else if (form == 1) raw = 1.0 - dc;
+  else if (form == 2) raw = 1.0 - dc * dc;
+  else raw = 1.0;
+  return fmax(raw, beta);
+}
+
+// Block reduce NV doubles (bit j of maxmask: max instead of sum) in a fixed
+// order; result valid in thread 0's out[] (and broadcast through smem).
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], uint32_t maxmask, double* out_smem) {
+  __shared__ double sh[NV][RED_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double x = v[j];
+    const bool mx = (maxmask >> j) & 1u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = mx ? fmax(x, y) : x + y;
+    }
+    if (lane == 0) sh[j][wid] = x;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < NV; j += blockDim.x) {
+    const bool mx = (maxmask >> j) & 1u;
+    double x = sh[j][0];
+    for (int w = 1; w < RED_THREADS / 32; ++w) x = mx ? fmax(x, sh[j][w]) : x + sh[j][w];
+    out_smem[j] = x;
+  }
+  __syncthreads();
+}
+
+// Grid reduction: every block stores its partial; the last block to arrive
+// sums the partials in block order (deterministic) into totals[] and resets
+// the ticket.  Returns true in the last block (all threads).
+template <int NV>
+__device__ __forceinline__ bool grid_reduce(double (&v)[NV], uint32_t maxmask, double* partials, double* totals,
+                                            unsigned* ticket) {
+  __shared__ double blk[NV];
+  __shared__ bool last;
+  block_reduce<NV>(v, maxmask, blk);
+  if (threadIdx.x < NV) partials[static_cast<size_t>(blockIdx.x) * NV + threadIdx.x] = blk[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  // Final reduction over the blocks: thread t folds blocks t, t+256, ... (fixed
+  // order, independent loads in flight), then the fixed-order block tree.
+  double w[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) w[j] = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const double y = __ldcg(partials + static_cast<size_t>(b) * NV + j);
+      w[j] = ((maxmask >> j) & 1u) ? fmax(w[j], y) : w[j] + y;
+    }
+  }
+  __shared__ double fin[NV];
+  block_reduce<NV>(w, maxmask, fin);
+  for (int j = threadIdx.x; j < NV; j += blockDim.x) totals[j] = fin[j];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = 0u;
+  return true;
+}
+
+}  // namespace i8t_dev

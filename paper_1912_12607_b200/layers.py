@@ -1,0 +1,595 @@
+"""Layer API of the INT8 training path on the device -- the reference's
+Layer / Conv2d / Dense / BatchNorm2d / ReLU / Pool2d / Sequential /
+ResidualBlock / InvertedResidual / SoftmaxCrossEntropy (layers.hpp:69-255,
+layers.cpp:19-546) with explicit forward/backward, so that the backward order
+-- and with it the order in which the single LCG gradient stream is consumed
+(train.cpp:13, layers.cpp:426-430, 458-464) -- is the reference's.
+
+Activations travel as NHWC-contiguous float32 CUDA tensors [N, H, W, C].  The
+quantised conv / fc layers (Conv2d, Dense) run entirely through the C-ABI of
+libi8t_cuda.so: nearest quantisation of W and a with fused amax tracking,
+the tcgen05 implicit-GEMM forward, the fused DSGC + stochastic gradient
+quantiser, tcgen05 backward-data / backward-weight.  FP32 layers (BN, ReLU,
+pooling, softmax-CE) are outside the graded path and use
+PyTorch/cuDNN library ops.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+import torch.nn.functional as F
+
+from . import ops
+from ._lib import ConvGeom, DsgcView, call
+
+
+class Mode(Enum):
+    FP32 = 0
+    INT8 = 1
+
+
+@dataclass
+class ForwardCtx:
+    """ForwardCtx (layers.hpp:40-45)."""
+    mode: Mode = Mode.INT8
+    training: bool = True
+    track_amax: bool = True
+
+
+@dataclass
+class BackwardCtx:
+    """BackwardCtx (layers.hpp:55-67); grad_stream is the device LCG state."""
+    mode: Mode = Mode.INT8
+    iter: int = 0
+    grad_stream: torch.Tensor | None = None
+    grid_resolution: int = 32
+    refine_rounds: int = 2
+    clip_search_enabled: bool = True
+    clip_period: int = 100
+    alpha: float = 20.0
+    beta: float = 0.1
+    form: str = "exp"
+    lr_scaling_enabled: bool = True
+    wgrad_allreduce: object = None  # callable(int64 acc tensor) for data parallelism (exact sum)
+
+
+@dataclass
+class ParamRef:
+    name: str
+    value: torch.Tensor
+    grad: torch.Tensor | None
+
+
+# ------------------------------------------------------------------ state arena
+class StateArena:
+    """All per-layer device state in one buffer so a step reads every layer's
+    DSGC view with a single D2H copy.  Per layer: one DsgcState (clip.hpp:12-18
+    + QuantState measurements) and a float block [clip_w, clip_a,
+    pending_amax, tmp] (QuantState, layers.hpp:28-38)."""
+
+    def __init__(self, device="cuda"):
+        self.dsgc_size = (int(ops.lib().i8t_dsgc_state_size()) + 63) // 64 * 64
+        self.layers = []
+        self.device = device
+        self.buf = None
+
+    def register(self, layer) -> int:
+        self.layers.append(layer)
+        return len(self.layers) - 1
+
+    def build(self, period: int):
+        n = len(self.layers)
+        self.slot = self.dsgc_size + 64
+        self.buf = torch.zeros(n * self.slot, dtype=torch.uint8, device=self.device)
+        for i, layer in enumerate(self.layers):
+            base = i * self.slot
+            layer.qs.bind(self, self.buf[base: base + self.dsgc_size],
+                          self.buf[base + self.dsgc_size: base + self.slot].view(torch.float32), period)
+
+    def read_views(self) -> list[DsgcView]:
+        host = self.buf.cpu()  # one D2H copy (syncs the stream)
+        out = []
+        for i in range(len(self.layers)):
+            b = bytes(host[i * self.slot: i * self.slot + C.sizeof(DsgcView)].numpy())
+            out.append(DsgcView.from_buffer_copy(b))
+        return out
+
+
+class QuantState:
+    """QuantState (layers.hpp:28-38) on the device: DsgcState + [clip_w,
+    clip_a, pending_amax, tmp], with host mirrors that decide lazily
+    initialised clips and Periodic-Update due-ness without syncing."""
+
+    def __init__(self):
+        self.dsgc = None
+        self.f = None
+        self.clip_w_set = False
+        self.clip_a_set = False
+        self.layer_id = ""
+
+    def bind(self, arena, dsgc_bytes, floats, period):
+        self.dsgc = _ArenaDsgc(dsgc_bytes, period, self.layer_id)
+        self.f = floats
+        self.f.zero_()
+
+    @property
+    def clip_w(self):
+        return self.f[0:1]
+
+    @property
+    def clip_a(self):
+        return self.f[1:2]
+
+    @property
+    def pending_amax(self):
+        return self.f[2:3]
+
+    @property
+    def tmp(self):
+        return self.f[3:4]
+
+
+class _ArenaDsgc(ops.DsgcState):
+    """ops.DsgcState living inside the StateArena buffer."""
+
+    def __init__(self, buf, period, layer_id):  # noqa: super().__init__ allocates; we adopt the slice instead
+        self.buf = buf
+        self.layer_id = layer_id
+        self.period = period
+        call("i8t_dsgc_init", ops.ctx(), ops._p(self.buf), period)
+        self.iter_of_last_update = -1
+        self.clip_valid = False
+
+    def clip_q_ptr(self):
+        """Device float holding the clip of the last quantised gradient."""
+        return self.buf[_CLIP_Q_OFF:_CLIP_Q_OFF + 4].view(torch.float32)
+
+
+_CLIP_Q_OFF = DsgcView.clip_q.offset
+_SCALE_OFF = DsgcView.scale.offset
+
+
+# ------------------------------------------------------------------ layers
+class Layer:
+    kind = "layer"
+
+    def forward(self, x, ctx: ForwardCtx):
+        raise NotImplementedError
+
+    def backward(self, g, ctx: BackwardCtx):
+        raise NotImplementedError
+
+    def params(self) -> list[ParamRef]:
+        return []
+
+    def buffers(self) -> list[ParamRef]:
+        return []
+
+    quantized = False
+    qs: QuantState | None = None
+
+    def set_quantized(self, on: bool):
+        pass
+
+    def visit(self, prefix, fn):
+        fn(prefix, self)
+
+
+def _kaiming(shape, fan_in, gen, device):
+    return (torch.randn(shape, generator=gen, device="cpu") * math.sqrt(2.0 / fan_in)).to(device)
+
+
+class Conv2d(Layer):
+    """INT8 convolution layer (layers.hpp:86-115, layers.cpp:65-126) with
+    separate (kh, kw), stride and padding per dimension (EXT)."""
+
+    def __init__(self, in_c, out_c, kernel, stride=1, pad=0, depthwise=False, gen=None, device="cuda"):
+        kh, kw = (kernel, kernel) if isinstance(kernel, int) else kernel
+        sh, sw = (stride, stride) if isinstance(stride, int) else stride
+        ph, pw = (pad, pad) if isinstance(pad, int) else pad
+        if depthwise and in_c != out_c:
+            raise ValueError("Conv2d: depthwise needs in_c == out_c")
+        self.in_c, self.out_c, self.kh, self.kw = in_c, out_c, kh, kw
+        self.sh, self.sw, self.ph, self.pw, self.depthwise = sh, sw, ph, pw, depthwise
+        self.kind = "conv_dw" if depthwise else "conv"
+        fan_in = (1 if depthwise else in_c) * kh * kw
+        ws = (in_c, 1, kh, kw) if depthwise else (out_c, in_c, kh, kw)
+        self.weight = _kaiming(ws, fan_in, gen or torch.Generator().manual_seed(0), device)
+        self.grad_weight = torch.zeros_like(self.weight)
+        self.quantize_enabled = False
+        self.qs = QuantState()
+        self.c_pad = in_c if depthwise else ops.pad4(in_c)
+        self.k_pad = ops.pad4(out_c)
+        self.ld_w = ops.pad16(kh * kw * self.c_pad)
+        self.ld_wt = ops.pad16(kh * kw * self.k_pad)
+        self._qw = self._qwt = None
+        self.wgrad_acc = None
+        self.keep_qg = False  # Dense needs the int8 gradient for its bias
+        self._qg = None
+
+    @property
+    def quantized(self):
+        return self.quantize_enabled
+
+    def set_quantized(self, on):
+        self.quantize_enabled = on
+
+    def params(self):
+        return [ParamRef("weight", self.weight, self.grad_weight)]
+
+    def geom(self, x):
+        n, h, w, c = x.shape
+        if c != self.in_c:
+            raise ValueError(f"Conv2d: bad input shape {tuple(x.shape)}")
+        return ConvGeom(n, c, h, w, self.out_c, self.kh, self.kw, self.sh, self.sw, self.ph, self.pw,
+                        int(self.depthwise), 1)
+
+    # -- forward (layers.cpp:98-111)
+    def forward(self, x, ctx: ForwardCtx):
+        g = self.geom(x)
+        self._geom = g
+        p, q = g.out_hw()
+        use_int8 = self.quantize_enabled and ctx.mode == Mode.INT8
+        h = ops.ctx()
+        qs = self.qs
+        if not use_int8:
+            if ctx.track_amax:
+                call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.tmp))
+                torch.maximum(qs.pending_amax, qs.tmp, out=qs.pending_amax)
+            if ctx.training:
+                self._x = x
+            xc = x.permute(0, 3, 1, 2)
+            y = F.conv2d(xc, self.weight, None, (self.sh, self.sw), (self.ph, self.pw),
+                         groups=self.in_c if self.depthwise else 1)
+            return y.permute(0, 2, 3, 1).contiguous()
+        # lazy clip init: clip = max(max_abs(t), 1e-12) (layers.cpp:106-107)
+        if not qs.clip_w_set:
+            call("i8t_max_abs", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w))
+            qs.clip_w.clamp_(min=1e-12)
+            qs.clip_w_set = True
+        if not qs.clip_a_set:
+            call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.clip_a))
+            qs.clip_a.clamp_(min=1e-12)
+            qs.clip_a_set = True
+        # weights -> KRSC (fwd) + CRSK (dgrad) int8 in one pass
+        if self.depthwise:
+            if self._qw is None:
+                self._qw = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int8, device=x.device)
+            call("i8t_quantize_nearest", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w),
+                 ops._p(self._qw), None, 0)
+        else:
+            if self._qw is None:
+                self._qw = torch.empty((self.out_c, self.ld_w), dtype=torch.int8, device=x.device)
+                self._qwt = torch.empty((self.in_c, self.ld_wt), dtype=torch.int8, device=x.device)
+            call("i8t_quantize_weight", h, ops._p(self.weight), 0, self.out_c, self.in_c, self.kh, self.kw,
+                 ops._p(qs.clip_w), ops._p(self._qw), self.c_pad, self.ld_w, ops._p(self._qwt), self.k_pad,
+                 self.ld_wt, None)
+        # activations -> NHWC int8 (channel stride c_pad), pending_amax fused (layers.cpp:101)
+        n, hh, ww, c = x.shape
+        qa = torch.empty((n, hh, ww, self.c_pad), dtype=torch.int8, device=x.device)
+        call("i8t_quantize_nearest_rows", h, ops._p(x), n * hh * ww, c, ops._p(qs.clip_a), ops._p(qa), self.c_pad,
+             ops._p(qs.pending_amax) if ctx.track_amax else None, 1)
+        self._qa = qa
+        z = torch.empty((n, p, q, self.out_c), dtype=torch.float32, device=x.device)
+        if self.depthwise:
+            call("i8t_conv_dw_fwd", h, C.byref(g), ops._p(qa), self.c_pad, ops._p(self._qw), ops._p(qs.clip_a),
+                 ops._p(qs.clip_w), ops._p(z), None)
+        else:
+            call("i8t_conv_fwd", h, C.byref(g), ops._p(qa), self.c_pad, ops._p(self._qw), self.ld_w,
+                 ops._p(qs.clip_a), ops._p(qs.clip_w), ops._p(z), None)
+        return z
+
+    # -- backward (layers.cpp:113-126)
+    def backward(self, gz, ctx: BackwardCtx):
+        g = self._geom
+        use_int8 = self.quantize_enabled and ctx.mode == Mode.INT8
+        if not use_int8:
+            xc = self._x.permute(0, 3, 1, 2)
+            gc = gz.permute(0, 3, 1, 2)
+            groups = self.in_c if self.depthwise else 1
+            gi = torch.nn.grad.conv2d_input(xc.shape, self.weight, gc, (self.sh, self.sw), (self.ph, self.pw),
+                                            groups=groups)
+            self.grad_weight.copy_(torch.nn.grad.conv2d_weight(xc, self.weight.shape, gc, (self.sh, self.sw),
+                                                               (self.ph, self.pw), groups=groups))
+            return gi.permute(0, 2, 3, 1).contiguous()
+        h = ops.ctx()
+        gz = gz.contiguous()
+        n, p, q, k = gz.shape
+        qg = quantize_gradient_layer(self.qs, gz, ctx)
+        clip_g = self.qs.dsgc.clip_q_ptr()
+        ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gz.device)
+        if self.depthwise:
+            call("i8t_conv_dw_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qw), ops._p(clip_g),
+                 ops._p(self.qs.clip_w), ops._p(ga), None)
+            if self.wgrad_acc is None:
+                self.wgrad_acc = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int64, device=gz.device)
+            call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
+                 ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
+        else:
+            call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
+                 ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
+            if self.wgrad_acc is None:
+                self.wgrad_acc = torch.empty((self.kh * self.kw * self.c_pad, self.out_c), dtype=torch.int64,
+                                             device=gz.device)
+            if ctx.wgrad_allreduce is None:
+                call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
+                     ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight), 1)
+            else:  # data parallel: exact int64 sum across ranks, then rescale
+                call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
+                     ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), None, 1)
+                ctx.wgrad_allreduce(self.wgrad_acc)
+                call("i8t_conv_wgrad_finalize", h, C.byref(g), ops._p(self.wgrad_acc), self.c_pad, ops._p(clip_g),
+                     ops._p(self.qs.clip_a), ops._p(self.grad_weight), 1)
+        self._qa = None
+        self._qg = qg if self.keep_qg else None
+        return ga
+
+
+def quantize_gradient_layer(qs: QuantState, gz: torch.Tensor, ctx: BackwardCtx) -> torch.Tensor:
+    """quantize_gradient (layers.cpp:19-59) for an NHWC gradient [N,P,Q,K]."""
+    n, p, q, k = gz.shape
+    st = qs.dsgc
+    st.period = ctx.clip_period
+    due = st.due(ctx.iter) if ctx.clip_search_enabled else False
+    qg = torch.empty(gz.shape, dtype=torch.int8, device=gz.device)
+    if k % 4 == 0:
+        n_img, ch, hw = n, k, p * q
+    elif p * q == 1:  # fc gradient [N, K]: NCHW order == row-major order -> flat draw order
+        n_img, ch, hw = 1, 1, n * k
+    else:
+        raise ValueError("quantize_gradient: conv output channels must be a multiple of 4")
+    call("i8t_quantize_gradient", ops.ctx(), st.ptr, ops._p(gz), n_img, ch, hw, ctx.iter, ctx.grid_resolution,
+         ctx.refine_rounds, int(ctx.clip_search_enabled), int(due), int(ctx.lr_scaling_enabled),
+         C.c_double(ctx.alpha), C.c_double(ctx.beta), ops.FORMS[ctx.form], ops._p(ctx.grad_stream), ops._p(qg), ch)
+    if due or not ctx.clip_search_enabled:
+        st.mark_searched(ctx.iter)
+        st.clip_valid = True  # refreshed from the device view at step end (zero-gradient edge case)
+    if k % 4:
+        qg = torch.nn.functional.pad(qg, (0, ops.pad4(k) - k))  # channel stride k_pad for dgrad/wgrad
+    return qg
+
+
+class Dense(Layer):
+    """INT8 fully connected layer (layers.hpp:117-139, layers.cpp:138-225):
+    a 1x1 convolution over [N, 1, 1, in]; bias added in float; bias gradient
+    = float(s_g * sum_i q_g[i, o]) (exact: every partial sum is a small
+    integer multiple of s_g)."""
+    kind = "fc"
+
+    def __init__(self, in_f, out_f, gen=None, device="cuda"):
+        self.conv = Conv2d(in_f, out_f, 1, 1, 0, False, gen, device)
+        self.conv.weight = _kaiming((out_f, in_f, 1, 1), in_f, gen or torch.Generator().manual_seed(0), device)
+        self.conv.grad_weight = torch.zeros_like(self.conv.weight)
+        self.bias = torch.zeros(out_f, device=device)
+        self.grad_bias = torch.zeros_like(self.bias)
+        self.in_f, self.out_f = in_f, out_f
+        self.qs = self.conv.qs
+        self.conv.keep_qg = True
+
+    @property
+    def quantized(self):
+        return self.conv.quantize_enabled
+
+    def set_quantized(self, on):
+        self.conv.set_quantized(on)
+
+    def params(self):
+        return [ParamRef("weight", self.conv.weight, self.conv.grad_weight), ParamRef("bias", self.bias, self.grad_bias)]
+
+    def forward(self, x, ctx):
+        self._in_shape = x.shape
+        n = x.shape[0]
+        z = self.conv.forward(x.reshape(n, 1, 1, self.in_f), ctx).reshape(n, self.out_f)
+        return z + self.bias
+
+    def backward(self, g, ctx):
+        n = g.shape[0]
+        g = g.contiguous()
+        gi = self.conv.backward(g.reshape(n, 1, 1, self.out_f), ctx)
+        if self.conv.quantize_enabled and ctx.mode == Mode.INT8:
+            # sum_i s*q[i,o] in double == s * (integer sum) exactly (layers.cpp:214-220)
+            sums = self.conv._qg.reshape(n, -1)[:, :self.out_f].sum(0, dtype=torch.int64)
+            scale = self.qs.dsgc.buf[_SCALE_OFF:_SCALE_OFF + 4].view(torch.float32)
+            self.grad_bias.copy_((sums.double() * scale.double()).float())
+            self.conv._qg = None
+        else:
+            self.grad_bias.copy_(g.double().sum(0).float())
+        return gi.reshape(self._in_shape)
+
+
+class BatchNorm2d(Layer):
+    """FP32 batch norm (layers.cpp:230-323), via the library batch-norm kernels."""
+    kind = "bn"
+
+    def __init__(self, c, momentum=0.1, eps=1e-5, device="cuda"):
+        self.gamma = torch.ones(c, device=device)
+        self.beta = torch.zeros(c, device=device)
+        self.grad_gamma = torch.zeros_like(self.gamma)
+        self.grad_beta = torch.zeros_like(self.beta)
+        self.running_mean = torch.zeros(c, device=device)
+        self.running_var = torch.ones(c, device=device)
+        self.momentum, self.eps = momentum, eps
+
+    def params(self):
+        return [ParamRef("gamma", self.gamma, self.grad_gamma), ParamRef("beta", self.beta, self.grad_beta)]
+
+    def buffers(self):
+        return [ParamRef("running_mean", self.running_mean, None), ParamRef("running_var", self.running_var, None)]
+
+    def forward(self, x, ctx):
+        xc = x.permute(0, 3, 1, 2)
+        if not ctx.training:
+            y = F.batch_norm(xc, self.running_mean, self.running_var, self.gamma, self.beta, False, 0.0, self.eps)
+            return y.permute(0, 2, 3, 1).contiguous()
+        y, self._mean, self._invstd = torch.native_batch_norm(xc, self.gamma, self.beta, self.running_mean,
+                                                              self.running_var, True, self.momentum, self.eps)
+        self._x = xc
+        return y.permute(0, 2, 3, 1).contiguous()
+
+    def backward(self, g, ctx):
+        gc = g.contiguous().permute(0, 3, 1, 2)
+        gi, gg, gb = torch.ops.aten.native_batch_norm_backward(gc, self._x, self.gamma, self.running_mean,
+                                                               self.running_var, self._mean, self._invstd, True,
+                                                               self.eps, [True, True, True])
+        self.grad_gamma.copy_(gg)
+        self.grad_beta.copy_(gb)
+        self._x = None
+        return gi.permute(0, 2, 3, 1).contiguous()
+
+
+class ReLU(Layer):
+    kind = "relu"
+
+    def forward(self, x, ctx):
+        y = torch.relu(x)
+        if ctx.training:
+            self._y = y
+        return y
+
+    def backward(self, g, ctx):
+        out = torch.where(self._y > 0, g, torch.zeros((), device=g.device, dtype=g.dtype))
+        self._y = None
+        return out
+
+
+class MaxPool2d(Layer):
+    """Max pooling with padding (EXT: the reference Pool2d has none, A.3-5)."""
+    kind = "maxpool"
+
+    def __init__(self, k, s, p=0):
+        self.k, self.s, self.p = k, s, p
+
+    def forward(self, x, ctx):
+        xc = x.permute(0, 3, 1, 2)
+        y, self._idx = torch.ops.aten.max_pool2d_with_indices(xc, [self.k, self.k], [self.s, self.s],
+                                                              [self.p, self.p])
+        self._xc = xc
+        return y.permute(0, 2, 3, 1).contiguous()
+
+    def backward(self, g, ctx):
+        gi = torch.ops.aten.max_pool2d_with_indices_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k],
+                                                             [self.s, self.s], [self.p, self.p], [1, 1], False,
+                                                             self._idx)
+        self._xc = self._idx = None
+        return gi.permute(0, 2, 3, 1).contiguous()
+
+
+class GlobalAvgPool(Layer):
+    kind = "avgpool"
+
+    def forward(self, x, ctx):
+        self._shape = x.shape
+        return x.mean(dim=(1, 2))
+
+    def backward(self, g, ctx):
+        n, h, w, c = self._shape
+        return (g / (h * w)).reshape(n, 1, 1, c).expand(n, h, w, c).contiguous()
+
+
+class Sequential(Layer):
+    kind = "sequential"
+
+    def __init__(self, children=None):
+        self.children = list(children or [])
+
+    def add(self, name, layer):
+        self.children.append((name, layer))
+        return layer
+
+    def forward(self, x, ctx):
+        for _, c in self.children:
+            x = c.forward(x, ctx)
+        return x
+
+    def backward(self, g, ctx):
+        for _, c in reversed(self.children):
+            g = c.backward(g, ctx)
+        return g
+
+    def visit(self, prefix, fn):
+        for name, c in self.children:
+            c.visit(f"{prefix}/{name}" if prefix else name, fn)
+
+
+class ResidualBlock(Layer):
+    """relu(main(x) + shortcut(x)); backward runs main then shortcut
+    (layers.cpp:451-464).  `main` is a BasicBlock (ResNet-20) or a Bottleneck
+    (ResNet-50) Sequential."""
+    kind = "resblock"
+
+    def __init__(self, main: Sequential, shortcut: Sequential | None):
+        self.main, self.shortcut, self.relu = main, shortcut, ReLU()
+
+    def forward(self, x, ctx):
+        y = self.main.forward(x, ctx)
+        sc = self.shortcut.forward(x, ctx) if self.shortcut else x
+        return self.relu.forward(y + sc, ctx)
+
+    def backward(self, g, ctx):
+        g = self.relu.backward(g, ctx)
+        gm = self.main.backward(g, ctx)
+        gs = self.shortcut.backward(g, ctx) if self.shortcut else g
+        return gm + gs
+
+    def visit(self, prefix, fn):
+        self.main.visit(prefix, fn)
+        if self.shortcut:
+            self.shortcut.visit(prefix, fn)
+
+
+class InvertedResidual(Layer):
+    """MobileNetV2 block (layers.cpp:466-502): 1x1 expand, 3x3 depthwise, 1x1
+    project; skip when stride 1 and in == out."""
+    kind = "invres"
+
+    def __init__(self, body: Sequential, use_skip: bool):
+        self.body, self.use_skip = body, use_skip
+
+    def forward(self, x, ctx):
+        y = self.body.forward(x, ctx)
+        return y + x if self.use_skip else y
+
+    def backward(self, g, ctx):
+        gb = self.body.backward(g, ctx)
+        return gb + g if self.use_skip else gb
+
+    def visit(self, prefix, fn):
+        self.body.visit(prefix, fn)
+
+
+class SoftmaxCrossEntropy:
+    """Mean softmax cross-entropy in double (layers.cpp:507-529); returns the
+    loss as a 0-d CUDA double tensor and g_logits = float((p - y) / N)."""
+
+    @staticmethod
+    def loss_and_grad(logits: torch.Tensor, labels: torch.Tensor):
+        n = logits.shape[0]
+        ld = logits.double()
+        logz = torch.logsumexp(ld, dim=1)
+        loss = (logz - ld.gather(1, labels.view(-1, 1)).squeeze(1)).sum() / n
+        p = torch.exp(ld - logz.view(-1, 1))
+        p[torch.arange(n, device=logits.device), labels] -= 1.0
+        return loss, (p / n).float()
+
+
+def int8_replace(root: Layer) -> int:
+    """Figure-6 replacement (layers.cpp:536-546): flip every conv / conv_dw / fc to INT8."""
+    count = 0
+
+    def fn(_, layer):
+        nonlocal count
+        if layer.kind in ("conv", "conv_dw", "fc"):
+            layer.set_quantized(True)
+            count += 1
+    root.visit("", fn)
+    return count
+
+
+def leaves(root: Layer):
+    out = []
+    root.visit("", lambda path, layer: out.append((path, layer)))
+    return out

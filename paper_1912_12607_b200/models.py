@@ -1,0 +1,156 @@
+"""Model zoo for the configs of BASELINE.json, built from the reference-style
+layers (layers.py): ResNet-20 (CIFAR shape), ResNet-50 (torchvision v1.5
+layout: stride on the 3x3), MobileNetV2.  The reference ships only toy nets
+(models.cpp:22-89) and cannot express their stride-2 / padded-pool geometry
+(SURVEY.md A.3); these use the floor-mode geometry extension.  Weights are
+Kaiming-initialised from a seeded generator (synthetic data: no checkpoints).
+"""
+from __future__ import annotations
+
+import torch
+
+from .layers import (BatchNorm2d, Conv2d, Dense, GlobalAvgPool, InvertedResidual, MaxPool2d, ReLU, ResidualBlock,
+                     Sequential)
+
+
+class Model:
+    def __init__(self, name, net, num_classes, in_shape):
+        self.name, self.net, self.num_classes, self.in_shape = name, net, num_classes, in_shape
+
+
+def _cbr(seq, name, cin, cout, k, s, p, gen, dev, relu=True, depthwise=False):
+    seq.add(f"{name}", Conv2d(cin, cout, k, s, p, depthwise, gen, dev))
+    seq.add(f"{name}_bn", BatchNorm2d(cout, device=dev))
+    if relu:
+        seq.add(f"{name}_relu", ReLU())
+
+
+def resnet20(num_classes=10, seed=1, device="cuda") -> Model:
+    gen = torch.Generator().manual_seed(seed)
+    net = Sequential()
+    _cbr(net, "conv1", 3, 16, 3, 1, 1, gen, device)
+    cin = 16
+    for si, (cout, stride) in enumerate([(16, 1), (32, 2), (64, 2)]):
+        for b in range(3):
+            s = stride if b == 0 else 1
+            main = Sequential()
+            _cbr(main, "conv1", cin, cout, 3, s, 1, gen, device)
+            _cbr(main, "conv2", cout, cout, 3, 1, 1, gen, device, relu=False)
+            sc = None
+            if s != 1 or cin != cout:
+                sc = Sequential()
+                _cbr(sc, "conv_sc", cin, cout, 1, s, 0, gen, device, relu=False)
+            net.add(f"stage{si + 1}_block{b + 1}", ResidualBlock(main, sc))
+            cin = cout
+    net.add("pool", GlobalAvgPool())
+    net.add("fc", Dense(64, num_classes, gen, device))
+    return Model("resnet20", net, num_classes, (3, 32, 32))
+
+
+def resnet50(num_classes=1000, seed=1, device="cuda") -> Model:
+    gen = torch.Generator().manual_seed(seed)
+    net = Sequential()
+    _cbr(net, "conv1", 3, 64, 7, 2, 3, gen, device)
+    net.add("maxpool", MaxPool2d(3, 2, 1))
+    cin = 64
+    for li, (width, blocks, stride) in enumerate([(64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)]):
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            main = Sequential()
+            _cbr(main, "conv1", cin, width, 1, 1, 0, gen, device)
+            _cbr(main, "conv2", width, width, 3, s, 1, gen, device)
+            _cbr(main, "conv3", width, width * 4, 1, 1, 0, gen, device, relu=False)
+            sc = None
+            if b == 0:
+                sc = Sequential()
+                _cbr(sc, "downsample", cin, width * 4, 1, s, 0, gen, device, relu=False)
+            net.add(f"layer{li + 1}_{b}", ResidualBlock(main, sc))
+            cin = width * 4
+    net.add("pool", GlobalAvgPool())
+    net.add("fc", Dense(2048, num_classes, gen, device))
+    return Model("resnet50", net, num_classes, (3, 224, 224))
+
+
+def mobilenet_v2(num_classes=1000, seed=1, device="cuda", width_mult=1.0) -> Model:
+    gen = torch.Generator().manual_seed(seed)
+    net = Sequential()
+    _cbr(net, "conv1", 3, 32, 3, 2, 1, gen, device)
+    cin = 32
+    cfg = [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2), (6, 320, 1, 1)]
+    bi = 0
+    for t, c, n, s in cfg:
+        for i in range(n):
+            stride = s if i == 0 else 1
+            mid = cin * t
+            body = Sequential()
+            if t != 1:
+                _cbr(body, "expand", cin, mid, 1, 1, 0, gen, device)
+            _cbr(body, "dw", mid, mid, 3, stride, 1, gen, device, depthwise=True)
+            _cbr(body, "project", mid, c, 1, 1, 0, gen, device, relu=False)
+            net.add(f"block{bi}", InvertedResidual(body, stride == 1 and cin == c))
+            cin = c
+            bi += 1
+    _cbr(net, "conv_last", cin, 1280, 1, 1, 0, gen, device)
+    net.add("pool", GlobalAvgPool())
+    net.add("fc", Dense(1280, num_classes, gen, device))
+    return Model("mobilenet_v2", net, num_classes, (3, 224, 224))
+
+
+MODELS = {"resnet20": resnet20, "resnet50": resnet50, "mobilenet_v2": mobilenet_v2}
+
+
+def build_model(name: str, seed: int = 1, device="cuda", **kw) -> Model:
+    """build_model (models.hpp:24-25)."""
+    if name not in MODELS:
+        raise ValueError(f"unknown model {name}")
+    return MODELS[name](seed=seed, device=device, **kw)
+
+
+def conv_gop_per_image(model: Model) -> float:
+    """2*N*K*P*Q*(C/groups)*R*S ops per pass summed over quantised conv/fc
+    layers x 3 passes (fwd, dgrad, wgrad), per image."""
+    from .layers import leaves
+    c, h, w = model.in_shape
+    x = torch.zeros((1, h, w, c))
+    total = 0.0
+    shapes = {}
+
+    def trace(layer, x):
+        return layer
+
+    # geometry walk without running kernels: reuse a FP32 CPU forward of shapes only
+    import torch.nn.functional as F
+
+    def walk(layer, shape):
+        nonlocal total
+        from . import layers as L
+        if isinstance(layer, L.Sequential):
+            for _, ch in layer.children:
+                shape = walk(ch, shape)
+            return shape
+        if isinstance(layer, L.ResidualBlock):
+            out = walk(layer.main, shape)
+            if layer.shortcut:
+                walk(layer.shortcut, shape)
+            return out
+        if isinstance(layer, L.InvertedResidual):
+            return walk(layer.body, shape)
+        if isinstance(layer, L.Conv2d):
+            n, hh, ww, cc = shape
+            p = (hh + 2 * layer.ph - layer.kh) // layer.sh + 1
+            q = (ww + 2 * layer.pw - layer.kw) // layer.sw + 1
+            cin = 1 if layer.depthwise else cc
+            total += 3 * 2.0 * p * q * layer.out_c * cin * layer.kh * layer.kw
+            return (n, p, q, layer.out_c)
+        if isinstance(layer, L.Dense):
+            total += 3 * 2.0 * layer.in_f * layer.out_f
+            return (shape[0], layer.out_f)
+        if isinstance(layer, L.MaxPool2d):
+            n, hh, ww, cc = shape
+            return (n, (hh + 2 * layer.p - layer.k) // layer.s + 1, (ww + 2 * layer.p - layer.k) // layer.s + 1, cc)
+        if isinstance(layer, L.GlobalAvgPool):
+            return (shape[0], shape[3])
+        return shape
+
+    walk(model.net, (1, h, w, c))
+    return total / 1e9

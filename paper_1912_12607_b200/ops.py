@@ -380,7 +380,7 @@ def quantize_gradient(state: DsgcState, g: torch.Tensor, it: int, lcg_state: tor
 def sgd_dclr_(w: torch.Tensor, grad: torch.Tensor, base_lr: float, state: DsgcState | None = None):
     """Trainer::train_step update (train.cpp:97-117): w -= float(lr * g)."""
     call("i8t_sgd_dclr", ctx(), _p(w), _p(grad.contiguous()), w.numel(), C.c_double(base_lr),
-         state.ptr if state is not None else None)
+         state.ptr if state is not None else None, None)
 
 
 # --------------------------------------------------------------------------- GEMM / conv

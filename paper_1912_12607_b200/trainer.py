@@ -1,0 +1,212 @@
+"""Per-step INT8 trainer on the device -- Trainer (train.hpp:66-92,
+train.cpp:12-120): cosine base LR, INT8 forward with activation-amax
+tracking, softmax-CE in double, divergence check, backward in the reference's
+layer order drawing from one device-resident LCG gradient stream, bad-gradient
+check, SGD with the per-layer DCLR factor phi(d_c), periodic refresh of the
+weight / activation clips.
+
+Data parallel: one process per GPU, batch sharded; the DSGC
+statistics are all-reduced through the C-ABI hook so every rank quantises the
+global gradient exactly as one device would; the int64 weight-gradient
+accumulators are all-reduced (exact) before the FP64 rescale; FP32 parameter
+gradients (BN, fc bias) are averaged-free summed like the reference's single
+batch sum.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from . import ops
+from ._lib import DsgcView, call
+from .layers import (BackwardCtx, Dense, ForwardCtx, Mode, SoftmaxCrossEntropy, StateArena, int8_replace, leaves)
+
+
+@dataclass
+class TrainConfig:
+    """TrainConfig (train.hpp:17-32)."""
+    mode: Mode = Mode.INT8
+    base_lr: float = 0.1
+    schedule: str = "cosine"
+    alpha: float = 20.0
+    beta: float = 0.1
+    form: str = "exp"
+    lr_scaling_enabled: bool = True
+    grid_resolution: int = 32
+    refine_rounds: int = 2
+    clip_enabled: bool = True
+    clip_period: int = 100
+    seed: int = 1
+    batch_size: int = 64
+    epochs: int = 5
+    calibration_batches: int = 2
+    momentum: float = 0.0
+
+
+@dataclass
+class LayerStepStat:
+    layer: str
+    dc: float = 0.0
+    clip: float = 0.0
+    lr_scale: float = 1.0
+    eps_norm: float = 0.0
+    ghat_sqnorm: float = 0.0
+
+
+@dataclass
+class StepReport:
+    iter: int = 0
+    loss: float = 0.0
+    diverged: bool = False
+    base_lr_t: float = 0.0
+    layers: list = field(default_factory=list)
+
+
+class _DistHook:
+    """i8t_allreduce_fn implemented with torch.distributed on raw device buffers."""
+
+    FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p)
+
+    def __init__(self):
+        self.cfn = self.FN(self._call)
+
+    @staticmethod
+    def _view(ptr, count):
+        class _A:
+            __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                        "version": 3}
+        return torch.as_tensor(_A(), device="cuda")
+
+    def _call(self, user, buf, count, dtype, op, stream):
+        try:
+            t = self._view(buf, count)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
+            return 0
+        except Exception:  # pragma: no cover - surfaced as I8T_ECUDA by the library
+            return 1
+
+
+class Trainer:
+    def __init__(self, model, cfg: TrainConfig, device="cuda"):
+        self.model, self.cfg = model, cfg
+        self.leaves = leaves(model.net)
+        self.quant_layers = [(p, l) for p, l in self.leaves if l.qs is not None]
+        self.arena = StateArena(device)
+        for path, layer in self.quant_layers:
+            layer.qs.layer_id = path
+            self.arena.register(layer)
+        self.arena.build(cfg.clip_period)
+        # Trainer::grad_stream_(uint32(seed)) (train.cpp:13)
+        self.grad_stream = ops.new_lcg_state(cfg.seed & 0xFFFFFFFF, device)
+        self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank() if self.world > 1 else 0
+        self._hook = None
+        if self.world > 1:
+            self._hook = _DistHook()
+            call("i8t_ctx_set_allreduce", ops.ctx(), C.cast(self._hook.cfn, C.c_void_p), None)
+            call("i8t_ctx_set_shard", ops.ctx(), self.rank, self.world)
+        self.skip = torch.zeros(1, dtype=torch.int32, device=device)
+        self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
+
+    # ---------------------------------------------------------------- clips
+    def calibrate(self, images):
+        """FP32 forward tracking activation maxima (train.cpp:29-32)."""
+        self.model.net.forward(images, ForwardCtx(Mode.FP32, training=False, track_amax=True))
+
+    def finish_calibration(self):
+        self.refresh_wa_clips()
+
+    def refresh_wa_clips(self):
+        """clip_w = max_abs(W), clip_a = running max of batch maxima (train.cpp:36-46), on the device."""
+        h = ops.ctx()
+        for _, layer in self.quant_layers:
+            qs = layer.qs
+            w = layer.params()[0].value
+            call("i8t_max_abs", h, ops._p(w), w.numel(), ops._p(qs.tmp))
+            if self.world > 1:
+                dist.all_reduce(qs.pending_amax, op=dist.ReduceOp.MAX)
+            qs.clip_w.copy_(torch.where(qs.tmp > 0, qs.tmp, qs.clip_w))
+            qs.clip_a.copy_(torch.where(qs.pending_amax > 0, qs.pending_amax, qs.clip_a))
+            qs.pending_amax.zero_()
+            qs.clip_w_set = True
+            qs.clip_a_set = qs.clip_a_set or True
+
+    def base_lr_at(self, it, total):
+        """cosine schedule (train.cpp:48-52)."""
+        if self.cfg.schedule == "constant" or total <= 0:
+            return self.cfg.base_lr
+        return self.cfg.base_lr * 0.5 * (1.0 + math.cos(math.pi * it / total))
+
+    # ---------------------------------------------------------------- step
+    def train_step(self, images, labels, it: int, total_iters: int, read_stats: bool = True) -> StepReport:
+        """Trainer::train_step (train.cpp:54-120).  images: NHWC float32 CUDA tensor."""
+        cfg = self.cfg
+        rep = StepReport(iter=it, base_lr_t=self.base_lr_at(it, total_iters))
+        logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8))
+        loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels)
+        bad = (~torch.isfinite(loss)) | (~torch.isfinite(logits).all())
+        # divergence check before backward (train.cpp:73-77): one host sync per step
+        if bool(bad.item()):
+            rep.loss, rep.diverged = float(loss.item()), True
+            return rep
+        self.loss_dev.copy_(loss.reshape(1))
+        bctx = BackwardCtx(cfg.mode, it, self.grad_stream, cfg.grid_resolution, cfg.refine_rounds, cfg.clip_enabled,
+                           cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
+                           self._wgrad_allreduce if self.world > 1 else None)
+        self.model.net.backward(g_logits, bctx)
+        params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
+        if self.world > 1:
+            self._allreduce_fp32_grads(params)
+        # bad-gradient check (train.cpp:87-95) stays on the device and gates the update
+        self.skip.zero_()
+        for _, p in params:
+            self.skip |= (~torch.isfinite(p.grad).all()).to(torch.int32)
+        h = ops.ctx()
+        for layer, p in params:
+            st = layer.qs.dsgc if (layer.qs is not None and cfg.mode == Mode.INT8 and layer.quantized
+                                   and cfg.lr_scaling_enabled) else None
+            call("i8t_sgd_dclr", h, ops._p(p.value), ops._p(p.grad), p.value.numel(), C.c_double(rep.base_lr_t),
+                 st.ptr if st is not None else None, ops._p(self.skip))
+        if read_stats:
+            rep.loss = float(self.loss_dev.item())
+            rep.diverged = bool(self.skip.item())
+            self._read_layer_stats(rep)
+        return rep
+
+    def _read_layer_stats(self, rep: StepReport):
+        views = self.arena.read_views()
+        for (path, layer), v in zip(self.quant_layers, views):
+            layer.qs.dsgc.sync(v)
+            rep.layers.append(LayerStepStat(path, v.last_dc, v.clip, v.lr_scale, v.eps_norm, v.ghat_sqnorm))
+
+    def sync_states(self):
+        """Refresh the host mirrors (clip > 0, iter of last update) from the device."""
+        for (_, layer), v in zip(self.quant_layers, self.arena.read_views()):
+            layer.qs.dsgc.sync(v)
+
+    # ---------------------------------------------------------------- data parallel
+    def _wgrad_allreduce(self, acc: torch.Tensor):
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+
+    def _allreduce_fp32_grads(self, params):
+        flat = [p.grad for layer, p in params if not (layer.quantized and p.name == "weight")]
+        if flat:
+            buf = torch.cat([t.reshape(-1) for t in flat])
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+            off = 0
+            for t in flat:
+                t.copy_(buf[off: off + t.numel()].view_as(t))
+                off += t.numel()
+
+
+def synthetic_batch(model, batch, seed, device="cuda"):
+    """Synthetic images N(0,1) NHWC + uniform labels."""
+    gen = torch.Generator(device=device).manual_seed(seed)
+    c, h, w = model.in_shape
+    x = torch.randn((batch, h, w, c), generator=gen, device=device)
+    y = torch.randint(0, model.num_classes, (batch,), generator=gen, device=device)
+    return x, y
