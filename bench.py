@@ -264,6 +264,13 @@ def main():
         barrier()
         return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() - launches0
 
+    if os.environ.get("I8T_PROFILE_STEP"):  # ncu --profile-from-start off: capture exactly one normal step
+        barrier()
+        torch.cuda.cudart().cudaProfilerStart()
+        tr.train_step(x, y, it, total, read_stats=False)
+        barrier()
+        torch.cuda.cudart().cudaProfilerStop()
+        it += 1
     clocks = ClockSampler(local)
     clocks.start()
     ms, launches = timed(a.steps)

@@ -223,6 +223,16 @@ int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64
 int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double base_lr, const void* state,
                  const int32_t* skip);
 
+/* All parameters in one launch: w and grad are flat arenas; segment i covers
+ * [seg_off[i], seg_off[i+1]) (multiples of 4, device int64) and uses the
+ * DCLR factor of device state seg_state[i] (device array of pointers; NULL
+ * entry = phi 1).  Same arithmetic as i8t_sgd_dclr per element. */
+int i8t_sgd_dclr_multi(i8t_ctx* ctx, float* w, const float* grad, int nseg, const int64_t* seg_off,
+                       const void* const* seg_state, double base_lr, const int32_t* skip);
+/* Non-finite scan of a flat gradient arena: *flag = 1 if any element is
+ * NaN/Inf (has_nonfinite, tensor.cpp:96-101, over every parameter gradient). */
+int i8t_nonfinite_flag(i8t_ctx* ctx, const float* x, int64_t n, int32_t* flag);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,20 @@ void* ensure_scratch(Ctx* c, size_t bytes) {
   return c->d_scratch;
 }
 
+void* ensure_wgrad(Ctx* c, size_t bytes) {
+  if (bytes <= c->wgrad_cap) return c->d_wgrad;
+  cudaStreamSynchronize(c->stream);
+  if (c->d_wgrad) cudaFree(c->d_wgrad);
+  c->d_wgrad = nullptr;
+  size_t cap = bytes + bytes / 4;
+  if (cudaMalloc(&c->d_wgrad, cap) != cudaSuccess) {
+    c->wgrad_cap = 0;
+    return nullptr;
+  }
+  c->wgrad_cap = cap;
+  return c->d_wgrad;
+}
+
 int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op) {
   if (!c->allreduce || count <= 0) return I8T_OK;
   const int rc = c->allreduce(c->allreduce_user, buf, count, 0, op, c->stream);
@@ -128,6 +142,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_partials) cudaFree(c->d_partials);
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->d_totals) cudaFree(c->d_totals);
+  if (c->d_wgrad) cudaFree(c->d_wgrad);
   if (c->d_ticket) cudaFree(c->d_ticket);
   delete c;
   return I8T_OK;

@@ -1,23 +1,29 @@
 // conv_tc.cu -- INT8 convolutions as implicit GEMMs on 5th-gen tensor cores
 // (tcgen05.mma.cta_group::1.kind::i8, int32 accumulators in TMEM).
 //
-//   FWD   D[npq][k]   = sum_{r,s,c} A_im2col[npq][(r,s,c)] * W_krsc[k][(r,s,c)]
-//   DGRAD D[nhw][c]   = sum_{r,s,k} G_col2im[nhw][(r,s,k)] * W_crsk[c][(r,s,k)]
-//   WGRAD D[(r,s,c)][k] = sum_{npq} A_im2col[npq][(r,s,c)] * G[npq][k]   (split over npq)
+//   FWD   D[npq][k]     = sum_{r,s,c} A_im2col[npq][(r,s,c)] * W_krsc[k][(r,s,c)]
+//   DGRAD D[nhw][c]     = sum_{r,s,k} G_col2im[nhw][(r,s,k)] * W_crsk[c][(r,s,k)]
+//   WGRAD D[(r,s,c)][k] = sum_{npq} A_im2col[npq][(r,s,c)] * G[npq][k]   (npq split)
 //
-// One CTA computes a 128 x BN tile.  Eight producer warps gather the operand
-// rows (implicit im2col / col2im, zero padding via cp.async zero-fill) straight
-// into SWIZZLE_128B shared-memory tiles; a ring of STAGES buffers is handed to
-// a single MMA-issuing thread through mbarriers; the MMA thread's
-// tcgen05.commit frees a stage; after the last k-tile the same eight warps
-// drain TMEM (tcgen05.ld) and apply the reference's FP64 rescale epilogue
-// float(double(s_x)*double(s_y)*acc) (conv.cpp:139-143, :190-191, :201-203),
-// or, for WGRAD, add the exact int32 split partial into an int64 accumulator.
-// FWD/DGRAD operands are K-major; WGRAD operands are MN-major (the reduction
-// runs over pixel rows), which tcgen05 supports for int8.
+// Persistent, warp-specialised CTA (one per SM) walking a static tile queue:
+//   warps 0-7   gather the implicit-im2col / col2im operand rows straight into
+//               SWIZZLE_128B smem tiles with cp.async (zero padding = zero-fill);
+//               thread 0 also issues the weight tile as one TMA
+//               (cp.async.bulk.tensor, SWIZZLE_128B) for FWD / DGRAD;
+//   warp 8      one elected thread issues tcgen05.mma (4 x K=32 per stage),
+//               tcgen05.commit frees the smem stage / publishes the accumulator;
+//   warps 9-12  drain TMEM (tcgen05.ld) and apply the reference's FP64 rescale
+//               float(double(s_x)*double(s_y)*acc) (conv.cpp:139-143, 190-191,
+//               201-203), or for WGRAD add the exact int32 split partial into
+//               the int64 accumulator.
+// The accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue
+// of tile i overlaps the main loop of tile i+1.  FWD/DGRAD operands are
+// K-major; WGRAD operands are MN-major (the reduction runs over pixel rows).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <mutex>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -35,65 +41,92 @@ struct ConvArgs {
   int64_t M;      // GEMM rows
   int Ng;         // GEMM cols (valid)
   int64_t Kd;     // reduction length (valid)
-  int k_tiles;    // k tiles per CTA
+  int k_tiles;    // k tiles per split
+  int m_tiles, n_tiles, splits;
   const float* clip_x;
   const float* clip_y;
   float* out;
   int64_t ldo;
   int32_t* acc32;
-  unsigned long long* acc64;
+  int use_tma_out;  // epilogue writes through the output tensor map (else direct stores)
+  int m_pad;        // WGRAD: rows per split in the int32 partial workspace
 };
 
 constexpr int BM = 128;
 constexpr int BKB = 128;  // bytes of reduction per stage (4 MMAs of K=32)
 constexpr int NPROD = 256;
-constexpr int NTHREADS = NPROD + 32;
+constexpr int MMA_WARP = 8;
+constexpr int EPI_WARP0 = 9;
+constexpr int NEPI = 128;
+constexpr int NTHREADS = NPROD + 32 + NEPI;  // 416
 
 template <int MODE, int BN>
 struct Cfg {
-  static constexpr int STAGES = 4;
   static constexpr int A_BYTES = BM * BKB;  // 16 KB
-  // B: K-major [BN rows][128 B] or MN-major [128 rows][128 B] x ceil(BN/128)
   static constexpr int B_SUB = (BN + 127) / 128;
   static constexpr int B_BYTES = (MODE == MODE_WGRAD) ? 128 * 128 * B_SUB : BN * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // per epilogue warp: 2 x [32 rows x 128 B] staging
+  static constexpr int BUDGET = 232448 - EPI_BYTES - 1024 - 256;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr bool TMA_B = (MODE != MODE_WGRAD);
 };
 
 __device__ __forceinline__ int ifloordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
+struct TileCoord {
+  int m_tile, n_tile, split;
+};
+__device__ __forceinline__ TileCoord tile_of(const ConvArgs& a, int t) {
+  const int per_split = a.m_tiles * a.n_tiles;
+  TileCoord c;
+  c.split = t / per_split;
+  const int r = t - c.split * per_split;
+  c.m_tile = r / a.n_tiles;  // n fastest: CTAs sharing an A tile run together (L2 reuse)
+  c.n_tile = r - c.m_tile * a.n_tiles;
+  return c;
+}
+__device__ __forceinline__ int tile_nk(const ConvArgs& a, int split) {
+  const int total_kt = static_cast<int>((a.Kd + BKB - 1) / BKB);
+  const int k0 = split * a.k_tiles;
+  const int n = total_kt - k0;
+  return n < a.k_tiles ? n : a.k_tiles;
+}
+
 template <int MODE, int BN, int VA, int VB>
-__global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args) {
+__global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_b,
+                                                          const __grid_constant__ CUtensorMap tmap_out) {
   using C = Cfg<MODE, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
-  const int n0 = blockIdx.y * BN;
-  const int kt0 = blockIdx.z * args.k_tiles;  // first k tile of this split
-  int nk = args.k_tiles;
-  {
-    const int64_t total_kt = (args.Kd + BKB - 1) / BKB;
-    if (kt0 + nk > total_kt) nk = static_cast<int>(total_kt - kt0);
-  }
+  const int total_tiles = args.m_tiles * args.n_tiles * args.splits;
 
-  if (warp == 8) {
+  if (warp == MMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < C::STAGES; ++s) {
         mbar_init(&full[s], NPROD);
         mbar_init(&empty[s], 1);
       }
-      mbar_init(tmem_full, 1);
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], NEPI);
+      }
       fence_mbar_init();
+      if constexpr (C::TMA_B) tma_prefetch(&tmap_b);
+      if (args.use_tma_out) tma_prefetch(&tmap_out);
     }
     __syncwarp();
     tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -104,243 +137,248 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 8) {
-    // ------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0 && nk > 0) {
-      constexpr bool AMN = (MODE == MODE_WGRAD), BMN = (MODE == MODE_WGRAD);
-      constexpr uint32_t idesc = make_idesc_i8(BM, BN, AMN, BMN);
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % C::STAGES;
-        mbar_wait(&full[s], (kt / C::STAGES) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BKB / 32; ++kk) {
-          uint64_t ad, bd;
-          if constexpr (MODE == MODE_WGRAD) {
-            // MN-major: 32 reduction rows per MMA = 4096 B; SBO = 8-row atom stride, LBO = 128-col sub-tile stride
-            ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 4096, 16384, 1024);
-            bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 4096, 16384, 1024);
-          } else {
-            // K-major: 32 bytes of reduction per MMA inside the 128 B swizzled row; SBO = 8 rows x 128 B
-            ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 32, 16, 1024);
-            bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 32, 16, 1024);
-          }
-          mma_i8(tmem_base, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
-        }
-        mma_commit(&empty[s]);
-      }
-      mma_commit(tmem_full);
-    }
-  } else {
-    // ------------------------------------------------ producers (warps 0-7)
+  if (warp < MMA_WARP) {
+    // ================================================= producers (warps 0-7)
     constexpr int PPR_A = BKB / VA;                 // pieces per 128 B row
     constexpr int ROWS_PER_PASS_A = NPROD / PPR_A;  // rows covered per pass
     constexpr int PASSES_A = BM / ROWS_PER_PASS_A;
     const int ja = tid % PPR_A, ra0 = tid / PPR_A;
-
-    // per-row precompute for FWD / DGRAD (rows are output/input pixels, fixed per CTA)
-    int rowA_n[PASSES_A], rowA_y[PASSES_A], rowA_x[PASSES_A];
-    bool rowA_ok[PASSES_A];
-    if constexpr (MODE != MODE_WGRAD) {
+    int kc = 0;  // global stage counter across tiles
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileCoord tc = tile_of(args, t);
+      const int64_t m0 = static_cast<int64_t>(tc.m_tile) * BM;
+      const int n0 = tc.n_tile * BN;
+      const int kt0 = tc.split * args.k_tiles;
+      const int nk = tile_nk(args, tc.split);
+      int rowA_n[PASSES_A], rowA_y[PASSES_A], rowA_x[PASSES_A];
+      bool rowA_ok[PASSES_A];
+      if constexpr (MODE != MODE_WGRAD) {
 #pragma unroll
-      for (int i = 0; i < PASSES_A; ++i) {
-        const int64_t m = m0 + ra0 + i * ROWS_PER_PASS_A;
-        rowA_ok[i] = m < args.M;
-        const int64_t mm = rowA_ok[i] ? m : 0;
-        if constexpr (MODE == MODE_FWD) {
-          const int64_t pq = static_cast<int64_t>(args.P) * args.Q;
-          const int n = static_cast<int>(mm / pq);
-          const int rem = static_cast<int>(mm - static_cast<int64_t>(n) * pq);
-          const int p = rem / args.Q, q = rem - (rem / args.Q) * args.Q;
-          rowA_n[i] = n;
-          rowA_y[i] = p * args.sh - args.ph;
-          rowA_x[i] = q * args.sw - args.pw;
-        } else {
-          const int64_t hw = static_cast<int64_t>(args.H) * args.W;
-          const int n = static_cast<int>(mm / hw);
-          const int rem = static_cast<int>(mm - static_cast<int64_t>(n) * hw);
-          const int h = rem / args.W, w = rem - (rem / args.W) * args.W;
-          rowA_n[i] = n;
-          rowA_y[i] = h + args.ph;
-          rowA_x[i] = w + args.pw;
+        for (int i = 0; i < PASSES_A; ++i) {
+          const int64_t m = m0 + ra0 + i * ROWS_PER_PASS_A;
+          rowA_ok[i] = m < args.M;
+          const int mm = rowA_ok[i] ? static_cast<int>(m) : 0;
+          if constexpr (MODE == MODE_FWD) {
+            const int pq = args.P * args.Q;
+            const int n = mm / pq, rem = mm - n * pq;
+            const int p = rem / args.Q, q = rem - p * args.Q;
+            rowA_n[i] = n;
+            rowA_y[i] = p * args.sh - args.ph;
+            rowA_x[i] = q * args.sw - args.pw;
+          } else {
+            const int hw = args.H * args.W;
+            const int n = mm / hw, rem = mm - n * hw;
+            const int h = rem / args.W, w = rem - h * args.W;
+            rowA_n[i] = n;
+            rowA_y[i] = h + args.ph;
+            rowA_x[i] = w + args.pw;
+          }
         }
       }
-    }
-
-    constexpr int LAG = C::STAGES - 1;
-    for (int kt = 0; kt < nk; ++kt) {
-      const int s = kt % C::STAGES;
-      if (kt >= C::STAGES) mbar_wait(&empty[s], ((kt / C::STAGES) - 1) & 1);
-      const uint32_t a_st = smem_u32(sA + s * C::A_BYTES);
-      const uint32_t b_st = smem_u32(sB + s * C::B_BYTES);
-      const int64_t kbase = static_cast<int64_t>(kt0 + kt) * BKB;
-
-      if constexpr (MODE == MODE_FWD || MODE == MODE_DGRAD) {
-        // ---- A: implicit im2col (FWD) / col2im gather (DGRAD) rows, K-major
-        const int64_t kk = kbase + ja * VA;
-        const bool kok = kk < args.Kd;
-        const int CH = (MODE == MODE_FWD) ? args.Cp : args.Kp;
-        const int tap = kok ? static_cast<int>(kk / CH) : 0;
-        const int ch = kok ? static_cast<int>(kk - static_cast<int64_t>(tap) * CH) : 0;
-        const int r = tap / args.S, sx = tap - (tap / args.S) * args.S;
-#pragma unroll
-        for (int i = 0; i < PASSES_A; ++i) {
-          const int row = ra0 + i * ROWS_PER_PASS_A;
-          bool ok = kok && rowA_ok[i];
-          const int8_t* src = args.act;
-          if constexpr (MODE == MODE_FWD) {
-            const int ih = rowA_y[i] + r, iw = rowA_x[i] + sx;
-            ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
-            if (ok) src = args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + ch;
-          } else {
-            const int pn = rowA_y[i] - r, qn = rowA_x[i] - sx;
-            int p = 0, q = 0;
-            if (args.sh == 1) p = pn; else { p = ifloordiv(pn, args.sh); ok = ok && (pn - p * args.sh) == 0; }
-            if (args.sw == 1) q = qn; else { q = ifloordiv(qn, args.sw); ok = ok && (qn - q * args.sw) == 0; }
-            ok = ok && p >= 0 && p < args.P && q >= 0 && q < args.Q;
-            src = args.gz;
-            if (ok) src = args.gz + ((static_cast<int64_t>(rowA_n[i]) * args.P + p) * args.Q + q) * args.Kp + ch;
+      for (int kt = 0; kt < nk; ++kt, ++kc) {
+        const int s = kc % C::STAGES;
+        if (kc >= C::STAGES) mbar_wait(&empty[s], ((kc / C::STAGES) - 1) & 1);
+        const uint32_t a_st = smem_u32(sA + s * C::A_BYTES);
+        const uint32_t b_st = smem_u32(sB + s * C::B_BYTES);
+        const int64_t kbase = static_cast<int64_t>(kt0 + kt) * BKB;
+        if constexpr (MODE == MODE_FWD || MODE == MODE_DGRAD) {
+          if (tid == 0) {  // weight tile [BN rows][128 B] by TMA (OOB rows / columns zero-filled)
+            mbar_expect_tx(&full[s], C::B_BYTES);
+            tma_load_2d(b_st, &tmap_b, &full[s], static_cast<int>(kbase), n0);
           }
-          cp_async_vec<VA>(a_st + sw128_offset(row, ja * VA), src, ok);
-        }
-        // ---- B: weight rows, K-major (16 B pieces; rows zero-padded to ldw)
-        constexpr int PPR_B = BKB / 16;
-        constexpr int RPP_B = NPROD / PPR_B;  // 32 rows per pass
-        constexpr int PASSES_B = (BN + RPP_B - 1) / RPP_B;
-        const int jb = tid % PPR_B, rb0 = tid / PPR_B;
-        const int64_t kb = kbase + jb * 16;
+          const int64_t kk = kbase + ja * VA;
+          const bool kok = kk < args.Kd;
+          const int CH = (MODE == MODE_FWD) ? args.Cp : args.Kp;
+          const int tap = kok ? static_cast<int>(kk / CH) : 0;
+          const int ch = kok ? static_cast<int>(kk - static_cast<int64_t>(tap) * CH) : 0;
+          const int r = tap / args.S, sx = tap - r * args.S;
 #pragma unroll
-        for (int i = 0; i < PASSES_B; ++i) {
-          const int row = rb0 + i * RPP_B;
-          if (row < BN) {
-            const int gr = n0 + row;
-            const bool ok = gr < args.Ng && kb < args.ldw;
-            const int8_t* src = ok ? args.wt + static_cast<int64_t>(gr) * args.ldw + kb : args.wt;
-            cp_async16(b_st + sw128_offset(row, jb * 16), src, ok ? 16u : 0u);
+          for (int i = 0; i < PASSES_A; ++i) {
+            const int row = ra0 + i * ROWS_PER_PASS_A;
+            bool ok = kok && rowA_ok[i];
+            const int8_t* src = args.act;
+            if constexpr (MODE == MODE_FWD) {
+              const int ih = rowA_y[i] + r, iw = rowA_x[i] + sx;
+              ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
+              if (ok) src = args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + ch;
+            } else {
+              const int pn = rowA_y[i] - r, qn = rowA_x[i] - sx;
+              int p, q;
+              if (args.sh == 1) p = pn; else { p = ifloordiv(pn, args.sh); ok = ok && (pn - p * args.sh) == 0; }
+              if (args.sw == 1) q = qn; else { q = ifloordiv(qn, args.sw); ok = ok && (qn - q * args.sw) == 0; }
+              ok = ok && p >= 0 && p < args.P && q >= 0 && q < args.Q;
+              src = args.gz;
+              if (ok) src = args.gz + ((static_cast<int64_t>(rowA_n[i]) * args.P + p) * args.Q + q) * args.Kp + ch;
+            }
+            cp_async_vec<VA>(a_st + sw128_offset(row, ja * VA), src, ok);
           }
-        }
-      } else {
-        // ---- WGRAD: smem rows = npq (reduction), columns = M bytes (A) / N bytes (B), MN-major
-        const int64_t pq = static_cast<int64_t>(args.P) * args.Q;
-        // A: act im2col^T.  column piece ja -> m = m0 + ja*VA -> (tap, c) fixed per CTA
-        const int64_t mA = m0 + ja * VA;
-        const bool mok = mA < args.M;
-        const int tapA = mok ? static_cast<int>(mA / args.Cp) : 0;
-        const int cA = mok ? static_cast<int>(mA - static_cast<int64_t>(tapA) * args.Cp) : 0;
-        const int rA = tapA / args.S, sA_ = tapA - (tapA / args.S) * args.S;
+        } else {
+          // ---- WGRAD: smem rows = npq (reduction), columns = M bytes (A) / N bytes (B), MN-major
+          const int pq = args.P * args.Q;
+          const int64_t mA = m0 + ja * VA;
+          const bool mok = mA < args.M;
+          const int tapA = mok ? static_cast<int>(mA / args.Cp) : 0;
+          const int cA = mok ? static_cast<int>(mA - static_cast<int64_t>(tapA) * args.Cp) : 0;
+          const int rA = tapA / args.S, sA_ = tapA - rA * args.S;
 #pragma unroll 4
-        for (int i = 0; i < PASSES_A; ++i) {
-          const int row = ra0 + i * ROWS_PER_PASS_A;
-          const int64_t kd = kbase + row;
-          bool ok = mok && kd < args.Kd;
-          const int8_t* src = args.act;
-          if (ok) {
-            const int n = static_cast<int>(kd / pq);
-            const int rem = static_cast<int>(kd - static_cast<int64_t>(n) * pq);
-            const int p = rem / args.Q, q = rem - (rem / args.Q) * args.Q;
-            const int ih = p * args.sh - args.ph + rA, iw = q * args.sw - args.pw + sA_;
-            ok = ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
-            if (ok) src = args.act + ((static_cast<int64_t>(n) * args.H + ih) * args.W + iw) * args.Cp + cA;
+          for (int i = 0; i < PASSES_A; ++i) {
+            const int row = ra0 + i * ROWS_PER_PASS_A;
+            const int64_t kd = kbase + row;
+            bool ok = mok && kd < args.Kd;
+            const int8_t* src = args.act;
+            if (ok) {
+              const int kdi = static_cast<int>(kd);
+              const int n = kdi / pq, rem = kdi - n * pq;
+              const int p = rem / args.Q, q = rem - p * args.Q;
+              const int ih = p * args.sh - args.ph + rA, iw = q * args.sw - args.pw + sA_;
+              ok = ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
+              if (ok) src = args.act + ((static_cast<int64_t>(n) * args.H + ih) * args.W + iw) * args.Cp + cA;
+            }
+            cp_async_vec<VA>(a_st + sw128_offset(row, ja * VA), src, ok);
           }
-          cp_async_vec<VA>(a_st + sw128_offset(row, ja * VA), src, ok);
-        }
-        // B: G rows (npq) x BN channel bytes, in 128-column sub-tiles
-        constexpr int PPR_B = BKB / VB;
-        constexpr int RPP_B = NPROD / PPR_B;
-        constexpr int PASSES_B = BM / RPP_B;
-        const int jb = tid % PPR_B, rb0 = tid / PPR_B;
+          constexpr int PPR_B = BKB / VB;
+          constexpr int RPP_B = NPROD / PPR_B;
+          constexpr int PASSES_B = BM / RPP_B;
+          const int jb = tid % PPR_B, rb0 = tid / PPR_B;
 #pragma unroll
-        for (int sub = 0; sub < C::B_SUB; ++sub) {
-          const int col = sub * 128 + jb * VB;
-          if (col < BN) {
-            const int kch = n0 + col;
-            const bool cok = kch < args.Kp;
+          for (int sub = 0; sub < C::B_SUB; ++sub) {
+            const int col = sub * 128 + jb * VB;
+            if (col < BN) {
+              const int kch = n0 + col;
+              const bool cok = kch < args.Kp;
 #pragma unroll 4
-            for (int i = 0; i < PASSES_B; ++i) {
-              const int row = rb0 + i * RPP_B;
-              const int64_t kd = kbase + row;
-              const bool ok = cok && kd < args.Kd;
-              const int8_t* src = ok ? args.gz + kd * args.Kp + kch : args.gz;
-              cp_async_vec<VB>(b_st + sub * 16384 + sw128_offset(row, jb * VB), src, ok);
+              for (int i = 0; i < PASSES_B; ++i) {
+                const int row = rb0 + i * RPP_B;
+                const int64_t kd = kbase + row;
+                const bool ok = cok && kd < args.Kd;
+                const int8_t* src = ok ? args.gz + kd * args.Kp + kch : args.gz;
+                cp_async_vec<VB>(b_st + sub * 16384 + sw128_offset(row, jb * VB), src, ok);
+              }
             }
           }
         }
-      }
-      cp_async_commit();
-      if (kt >= LAG) {
-        cp_async_wait<LAG>();
-        fence_proxy_async_smem();
-        mbar_arrive(&full[(kt - LAG) % C::STAGES]);
+        // the stage's full barrier completes when every producer's copies have
+        // landed (no producer-side wait: the loads of several stages overlap)
+        cp_async_mbar_arrive(&full[s]);
       }
     }
     cp_async_wait<0>();
-    fence_proxy_async_smem();
-    for (int kt = (nk > LAG ? nk - LAG : 0); kt < nk; ++kt) mbar_arrive(&full[kt % C::STAGES]);
-
-    // ------------------------------------------------ epilogue (same 8 warps)
-    if (nk > 0) {
-      mbar_wait(tmem_full, 0);
-      tc_fence_after();
+  } else if (warp == MMA_WARP) {
+    // ================================================= MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr bool MN = (MODE == MODE_WGRAD);
+      constexpr uint32_t idesc = make_idesc_i8(BM, BN, MN, MN);
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      int kc = 0, it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const TileCoord tc = tile_of(args, t);
+        const int nk = tile_nk(args, tc.split);
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kt = 0; kt < nk; ++kt, ++kc) {
+          const int s = kc % C::STAGES;
+          mbar_wait(&full[s], (kc / C::STAGES) & 1);
+          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma operand reads
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKB / 32; ++kk) {
+            uint64_t ad, bd;
+            if constexpr (MN) {
+              // MN-major: 32 reduction rows per MMA = 4096 B; SBO = 8-row atom stride, LBO = 128-col sub-tile
+              ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 4096, 16384, 1024);
+              bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 4096, 16384, 1024);
+            } else {
+              // K-major: 32 B of reduction per MMA inside the 128 B swizzled row; SBO = 8 rows x 128 B
+              ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 32, 16, 1024);
+              bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 32, 16, 1024);
+            }
+            mma_i8(d_tmem, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[acc]);
+      }
     }
-    const int quad = warp & 3, half = warp >> 2;
+    __syncwarp();
+  } else {
+    // ================================================= epilogue (warps 9-12)
+    const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = quad * 32 + lane;
-    const int64_t m = m0 + row;
     const double rescale =
         static_cast<double>(__fdiv_rn(*args.clip_x, 127.0f)) * static_cast<double>(__fdiv_rn(*args.clip_y, 127.0f));
-    constexpr int HALF = BN / 2;
+    uint8_t* stage_base = sEpi + (warp - EPI_WARP0) * (2 * 32 * 128);
+    int it = 0, nst = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      const TileCoord tc = tile_of(args, t);
+      const int64_t m = static_cast<int64_t>(tc.m_tile) * BM + row;
+      const int n0 = tc.n_tile * BN;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-    for (int cc = 0; cc < HALF; cc += 16) {
-      const int col = half * HALF + cc;
-      uint32_t v[16];
-      if (nk > 0) {
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(col), v);
+      for (int col = 0; col < BN; col += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_row + static_cast<uint32_t>(col), v);
         tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0;
-      }
-      if (m >= args.M) continue;
-      if constexpr (MODE == MODE_WGRAD) {
-        unsigned long long* dst = args.acc64 + m * args.Ng;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int gc = n0 + col + i;
-          const int32_t a = static_cast<int32_t>(v[i]);
-          if (gc < args.Ng && a != 0) atomicAdd(dst + gc, static_cast<unsigned long long>(static_cast<long long>(a)));
+        if (col + 32 >= BN) {  // last read of this accumulator: hand it back to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
         }
-      } else {
         const int gc0 = n0 + col;
-        if (args.out) {
-          float* dst = args.out + m * args.ldo + gc0;
-          if (gc0 + 16 <= args.Ng && (args.ldo % 4) == 0 && (gc0 % 4) == 0) {
+        if (args.use_tma_out) {
+          // 32x32 sub-tile -> swizzled smem staging (double-buffered) -> one TMA bulk store
+          uint8_t* buf = stage_base + (nst & 1) * (32 * 128);
+          if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
+          __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              float4 f;
-              f.x = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i + 0])));
-              f.y = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i + 1])));
-              f.z = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i + 2])));
-              f.w = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i + 3])));
-              *reinterpret_cast<float4*>(dst + i) = f;
+          for (int j = 0; j < 8; ++j) {
+            uint4 w;
+            if constexpr (MODE == MODE_WGRAD) {
+              w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+              w.x = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 0]))));
+              w.y = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 1]))));
+              w.z = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 2]))));
+              w.w = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 3]))));
             }
-          } else {
+            *reinterpret_cast<uint4*>(buf + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16))) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * BM + quad * 32;
+            tma_store_2d(&tmap_out, smem_u32(buf), gc0, r0);
+            bulk_commit();
+          }
+          ++nst;
+        } else if (m < args.M) {
+          if constexpr (MODE != MODE_WGRAD) {
+            if (args.out) {
+              float* dst = args.out + m * args.ldo + gc0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (gc0 + i < args.Ng) dst[i] = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i])));
+              for (int i = 0; i < 32; ++i)
+                if (gc0 + i < args.Ng)
+                  dst[i] = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i])));
+            }
           }
         }
-        if (args.acc32) {
+        if (args.acc32 && m < args.M && MODE != MODE_WGRAD) {
           int32_t* dst = args.acc32 + m * args.Ng + gc0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
+          for (int i = 0; i < 32; ++i)
             if (gc0 + i < args.Ng) dst[i] = static_cast<int32_t>(v[i]);
         }
       }
     }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
@@ -368,6 +406,29 @@ __global__ void k_wgrad_finalize(const long long* __restrict__ acc, int K, int C
   }
 }
 
+// WGRAD split reduction: acc[m][k] = sum_s part[s][m][k] (int64, exact, fixed order),
+// optionally rescaled into float weights (KCRS or KRSC).
+__global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int m_pad, int Kp, int M, int K, int C,
+                               int Cp, int RS, long long* __restrict__ acc, const float* clip_g, const float* clip_a,
+                               float* __restrict__ gw, int out_kcrs) {
+  const double rescale =
+      static_cast<double>(__fdiv_rn(*clip_g, 127.0f)) * static_cast<double>(__fdiv_rn(*clip_a, 127.0f));
+  const int64_t tot = static_cast<int64_t>(M) * K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = static_cast<int>(i / K), k = static_cast<int>(i - static_cast<int64_t>(m) * K);
+    long long sum = 0;
+    for (int sp = 0; sp < splits; ++sp) sum += __ldg(part + (static_cast<int64_t>(sp) * m_pad + m) * Kp + k);
+    if (acc) acc[i] = sum;
+    if (gw) {
+      const int rs = m / Cp, c = m - rs * Cp;
+      if (c < C) {
+        const int64_t o = out_kcrs ? (static_cast<int64_t>(k) * C + c) * RS + rs : (static_cast<int64_t>(k) * RS + rs) * C + c;
+        gw[o] = static_cast<float>(rescale * static_cast<double>(sum));
+      }
+    }
+  }
+}
+
 __global__ void k_transpose_i8(const int8_t* __restrict__ src, int64_t rows, int64_t cols, int8_t* __restrict__ dst,
                                int64_t ld_dst) {
   const int64_t tot = rows * cols;
@@ -389,47 +450,112 @@ __global__ void k_pad_rows_i8(const int8_t* __restrict__ src, int64_t rows, int6
 // ---------------------------------------------------------------- host side
 static int vec_of(int64_t ch) { return (ch % 16 == 0) ? 16 : (ch % 8 == 0) ? 8 : 4; }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D int8 weight matrix [rows][ld] -> TMA map with box {128 B, box_rows}, SWIZZLE_128B.
+static int make_weight_map(CUtensorMap* map, const int8_t* w, int64_t rows, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(w), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return I8T_OK;
+}
+
+// 2-D [rows][ld] fp32/int32 output -> TMA store map, box {32 elements, 32 rows}, SWIZZLE_128B.
+static int make_out_map(CUtensorMap* map, void* base, int64_t cols, int64_t rows, int64_t ld, bool is_int) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, is_int ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string(int(r)) + ")");
+  return I8T_OK;
+}
+
+static bool tma_out_ok(const void* p, int64_t ld) {
+  return p && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int MODE, int BN, int VA, int VB>
-static int launch_one(cudaStream_t st, const ConvArgs& a, dim3 grid) {
+static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& map, const CUtensorMap& omap) {
   using C = Cfg<MODE, BN>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_conv_tc<MODE, BN, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
-  k_conv_tc<MODE, BN, VA, VB><<<grid, NTHREADS, C::SMEM, st>>>(a);
+  const int tiles = a.m_tiles * a.n_tiles * a.splits;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k_conv_tc<MODE, BN, VA, VB><<<grid, NTHREADS, C::SMEM, st>>>(a, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
 }
 
 template <int MODE, int BN>
-static int dispatch_vec(cudaStream_t st, const ConvArgs& a, dim3 grid, int va, int vb) {
+static int dispatch_vec(cudaStream_t st, const ConvArgs& a, const CUtensorMap& m, const CUtensorMap& o, int va, int vb) {
   if constexpr (MODE == MODE_WGRAD) {
     if (vb == 16) {
-      if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, grid);
-      if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, grid);
-      return launch_one<MODE, BN, 4, 16>(st, a, grid);
+      if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, m, o);
+      if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, m, o);
+      return launch_one<MODE, BN, 4, 16>(st, a, m, o);
     }
     if (vb == 8) {
-      if (va == 16) return launch_one<MODE, BN, 16, 8>(st, a, grid);
-      if (va == 8) return launch_one<MODE, BN, 8, 8>(st, a, grid);
-      return launch_one<MODE, BN, 4, 8>(st, a, grid);
+      if (va == 16) return launch_one<MODE, BN, 16, 8>(st, a, m, o);
+      if (va == 8) return launch_one<MODE, BN, 8, 8>(st, a, m, o);
+      return launch_one<MODE, BN, 4, 8>(st, a, m, o);
     }
-    if (va == 16) return launch_one<MODE, BN, 16, 4>(st, a, grid);
-    if (va == 8) return launch_one<MODE, BN, 8, 4>(st, a, grid);
-    return launch_one<MODE, BN, 4, 4>(st, a, grid);
+    if (va == 16) return launch_one<MODE, BN, 16, 4>(st, a, m, o);
+    if (va == 8) return launch_one<MODE, BN, 8, 4>(st, a, m, o);
+    return launch_one<MODE, BN, 4, 4>(st, a, m, o);
   } else {
-    if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, grid);
-    if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, grid);
-    return launch_one<MODE, BN, 4, 16>(st, a, grid);
+    if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, m, o);
+    if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, m, o);
+    return launch_one<MODE, BN, 4, 16>(st, a, m, o);
   }
 }
 
 template <int MODE>
-static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, dim3 grid, int va, int vb) {
-  if (bn == 64) return dispatch_vec<MODE, 64>(st, a, grid, va, vb);
-  if (bn == 128) return dispatch_vec<MODE, 128>(st, a, grid, va, vb);
-  return dispatch_vec<MODE, 256>(st, a, grid, va, vb);
+static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, const CUtensorMap& m, const CUtensorMap& o, int va,
+                    int vb) {
+  if (bn == 64) return dispatch_vec<MODE, 64>(st, a, m, o, va, vb);
+  if (bn == 128) return dispatch_vec<MODE, 128>(st, a, m, o, va, vb);
+  return dispatch_vec<MODE, 256>(st, a, m, o, va, vb);
 }
 
 static int pick_bn(int64_t ng) { return ng <= 64 ? 64 : (ng <= 128 ? 128 : 256); }
@@ -446,9 +572,16 @@ static int geom_common(const i8t_conv_geom* g, int64_t& P, int64_t& Q) {
     return set_error(I8T_EINVAL, "ConvGeometry: output size is not a positive integer");
   P = (g->h + 2 * g->pad_h - g->kh) / g->stride_h + 1;
   Q = (g->w + 2 * g->pad_w - g->kw) / g->stride_w + 1;
-  if (g->n * g->h * g->w > (int64_t)1 << 31 || g->n * P * Q > (int64_t)1 << 31)
+  if (g->n * g->h * g->w >= (int64_t)1 << 31 || g->n * P * Q >= (int64_t)1 << 31 ||
+      g->n * g->h * g->w * g->c >= (int64_t)1 << 40)
     return set_error(I8T_EUNSUPPORTED, "conv: tensor too large");
   return I8T_OK;
+}
+
+static void fill_geom(ConvArgs& x, const i8t_conv_geom* g, int64_t P, int64_t Q) {
+  x.N = (int)g->n; x.H = (int)g->h; x.W = (int)g->w;
+  x.R = (int)g->kh; x.S = (int)g->kw; x.sh = (int)g->stride_h; x.sw = (int)g->stride_w; x.ph = (int)g->pad_h; x.pw = (int)g->pad_w;
+  x.P = (int)P; x.Q = (int)Q;
 }
 
 }  // namespace i8t_dev
@@ -470,16 +603,18 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   if (ld_w < Kd || ld_w % 16 != 0) return set_error(I8T_EUNSUPPORTED, "conv_fwd: ld_w must be >= kh*kw*c_pad and a multiple of 16");
   if (g->kh * g->kw * g->c > 130000) return set_error(I8T_EINVAL, "conv: reduction depth exceeds i32 overflow bound");
   ConvArgs x{};
-  x.act = a; x.gz = nullptr; x.wt = w; x.ldw = ld_w;
-  x.N = (int)g->n; x.H = (int)g->h; x.W = (int)g->w; x.Cp = (int)c_pad; x.Kp = (int)g->k;
-  x.R = (int)g->kh; x.S = (int)g->kw; x.sh = (int)g->stride_h; x.sw = (int)g->stride_w; x.ph = (int)g->pad_h; x.pw = (int)g->pad_w;
-  x.P = (int)P; x.Q = (int)Q;
+  fill_geom(x, g, P, Q);
+  x.act = a; x.gz = nullptr; x.wt = w; x.ldw = ld_w; x.Cp = (int)c_pad; x.Kp = (int)g->k;
   x.M = g->n * P * Q; x.Ng = (int)g->k; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_a; x.clip_y = clip_w; x.out = z; x.ldo = g->k; x.acc32 = acc;
   const int bn = pick_bn(g->k);
-  dim3 grid((unsigned)((x.M + BM - 1) / BM), (unsigned)((g->k + bn - 1) / bn), 1);
-  return dispatch<MODE_FWD>(c->stream, x, bn, grid, vec_of(c_pad), 16);
+  x.m_tiles = (int)((x.M + BM - 1) / BM); x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
+  CUtensorMap map, omap{};
+  if ((rc = make_weight_map(&map, w, g->k, ld_w, bn))) return rc;
+  x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
+  if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;
+  return dispatch<MODE_FWD>(c->stream, x, bn, map, omap, vec_of(c_pad), 16);
 }
 
 int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt, int64_t ld_wt,
@@ -496,16 +631,18 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (g->k > 130000) return set_error(I8T_EINVAL, "conv: reduction depth exceeds i32 overflow bound");
   if (g->k * g->kh * g->kw > 133000) return set_error(I8T_EUNSUPPORTED, "conv_dgrad: int32 accumulator bound");
   ConvArgs x{};
-  x.act = nullptr; x.gz = gz; x.wt = wt; x.ldw = ld_wt;
-  x.N = (int)g->n; x.H = (int)g->h; x.W = (int)g->w; x.Cp = (int)g->c; x.Kp = (int)k_pad;
-  x.R = (int)g->kh; x.S = (int)g->kw; x.sh = (int)g->stride_h; x.sw = (int)g->stride_w; x.ph = (int)g->pad_h; x.pw = (int)g->pad_w;
-  x.P = (int)P; x.Q = (int)Q;
+  fill_geom(x, g, P, Q);
+  x.act = nullptr; x.gz = gz; x.wt = wt; x.ldw = ld_wt; x.Cp = (int)g->c; x.Kp = (int)k_pad;
   x.M = g->n * g->h * g->w; x.Ng = (int)g->c; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
   const int bn = pick_bn(g->c);
-  dim3 grid((unsigned)((x.M + BM - 1) / BM), (unsigned)((g->c + bn - 1) / bn), 1);
-  return dispatch<MODE_DGRAD>(c->stream, x, bn, grid, vec_of(k_pad), 16);
+  x.m_tiles = (int)((x.M + BM - 1) / BM); x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
+  CUtensorMap map, omap{};
+  if ((rc = make_weight_map(&map, wt, g->c, ld_wt, bn))) return rc;
+  x.use_tma_out = tma_out_ok(ga, g->c) ? 1 : 0;
+  if (x.use_tma_out && (rc = make_out_map(&omap, ga, g->c, x.M, g->c, false))) return rc;
+  return dispatch<MODE_DGRAD>(c->stream, x, bn, map, omap, vec_of(k_pad), 16);
 }
 
 int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a, int64_t c_pad,
@@ -519,39 +656,41 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (c_pad < g->c || c_pad % 4 != 0 || k_pad < g->k || k_pad % 4 != 0)
     return set_error(I8T_EUNSUPPORTED, "conv_wgrad: channel strides must be multiples of 4");
   ConvArgs x{};
-  x.act = a; x.gz = gz; x.wt = nullptr; x.ldw = 0;
-  x.N = (int)g->n; x.H = (int)g->h; x.W = (int)g->w; x.Cp = (int)c_pad; x.Kp = (int)k_pad;
-  x.R = (int)g->kh; x.S = (int)g->kw; x.sh = (int)g->stride_h; x.sw = (int)g->stride_w; x.ph = (int)g->pad_h; x.pw = (int)g->pad_w;
-  x.P = (int)P; x.Q = (int)Q;
+  fill_geom(x, g, P, Q);
+  x.act = a; x.gz = gz; x.wt = nullptr; x.ldw = 0; x.Cp = (int)c_pad; x.Kp = (int)k_pad;
   x.M = g->kh * g->kw * c_pad; x.Ng = (int)g->k; x.Kd = g->n * P * Q;
   const int bn = pick_bn(g->k);
   const int64_t m_tiles = (x.M + BM - 1) / BM, n_tiles = (g->k + bn - 1) / bn;
   const int64_t total_kt = (x.Kd + BKB - 1) / BKB;
-  // split the npq reduction: <= 1015 k-tiles (129,920 rows) per split keeps each int32 partial exact,
-  // and enough splits to give ~2 CTAs per SM.
-  int64_t splits = (2 * 148 + m_tiles * n_tiles - 1) / (m_tiles * n_tiles);
+  // split the npq reduction: <= 1015 k-tiles (129,920 rows) per split keeps each
+  // int32 partial exact; aim for ~4 tiles per SM so the persistent queue balances.
+  int64_t splits = (4 * num_sms() + m_tiles * n_tiles - 1) / (m_tiles * n_tiles);
   if (splits < 1) splits = 1;
   int64_t per = (total_kt + splits - 1) / splits;
   if (per > 1015) per = 1015;
-  if (per < 4 && total_kt >= 4) per = 4;
+  if (per < 8 && total_kt >= 8) per = 8;
   splits = (total_kt + per - 1) / per;
   x.k_tiles = (int)per;
-  x.acc64 = reinterpret_cast<unsigned long long*>(acc);
+  x.m_tiles = (int)m_tiles; x.n_tiles = (int)n_tiles; x.splits = (int)splits;
+  x.m_pad = (int)(m_tiles * BM);
   x.clip_x = clip_g; x.clip_y = clip_a;
-  cudaMemsetAsync(acc, 0, sizeof(int64_t) * x.M * g->k, c->stream);
-  dim3 grid((unsigned)m_tiles, (unsigned)n_tiles, (unsigned)splits);
-  rc = dispatch<MODE_WGRAD>(c->stream, x, bn, grid, vec_of(c_pad), vec_of(k_pad));
+  // per-split int32 partial tiles [splits][m_pad][k_pad], TMA-stored, reduced below in a fixed order
+  const size_t part_bytes = sizeof(int32_t) * static_cast<size_t>(splits) * x.m_pad * k_pad;
+  int32_t* part = reinterpret_cast<int32_t*>(ensure_wgrad(c, part_bytes));
+  if (!part) return set_error(I8T_ECUDA, "wgrad workspace alloc failed");
+  CUtensorMap map{}, omap{};  // no weight operand in WGRAD
+  x.use_tma_out = 1;
+  if ((rc = make_out_map(&omap, part, k_pad, splits * x.m_pad, k_pad, true))) return rc;
+  rc = dispatch<MODE_WGRAD>(c->stream, x, bn, map, omap, vec_of(c_pad), vec_of(k_pad));
   if (rc) return rc;
-  if (gw) {
-    const int64_t tot = g->k * g->c * g->kh * g->kw;
-    int blocks = (int)((tot + 255) / 256);
-    if (blocks > 4096) blocks = 4096;
-    k_wgrad_finalize<<<blocks, 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), (int)g->k, (int)g->c,
-                                                     (int)c_pad, (int)(g->kh * g->kw), clip_g, clip_a, gw, out_kcrs);
-    count_launch(1);
-    return cuda_check("k_wgrad_finalize");
-  }
-  return I8T_OK;
+  const int64_t tot = x.M * g->k;
+  int blocks = (int)((tot + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_wgrad_reduce<<<blocks, 256, 0, c->stream>>>(part, (int)splits, x.m_pad, (int)k_pad, (int)x.M, (int)g->k, (int)g->c,
+                                                 (int)c_pad, (int)(g->kh * g->kw), reinterpret_cast<long long*>(acc),
+                                                 clip_g, clip_a, gw, out_kcrs);
+  count_launch(1);
+  return cuda_check("k_wgrad_reduce");
 }
 
 int i8t_conv_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t* acc, int64_t c_pad,

@@ -188,6 +188,44 @@ __global__ void __launch_bounds__(256) k_sgd_dclr(float* __restrict__ w, const f
     w[i] -= static_cast<float>(lr * static_cast<double>(grad[i]));
 }
 
+// Segmented SGD+DCLR over flat arenas: one launch for every parameter.
+__global__ void __launch_bounds__(256) k_sgd_dclr_multi(float* __restrict__ w, const float* __restrict__ grad,
+                                                        int nseg, const int64_t* __restrict__ seg_off,
+                                                        const void* const* __restrict__ seg_state, double base_lr,
+                                                        const int32_t* skip) {
+  if (skip && *skip) return;
+  const int64_t n4 = seg_off[nseg] / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 4;
+    int lo = 0, hi = nseg - 1;  // segment with seg_off[s] <= e < seg_off[s+1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (seg_off[mid] <= e) lo = mid;
+      else hi = mid - 1;
+    }
+    const DsgcState* st = reinterpret_cast<const DsgcState*>(seg_state[lo]);
+    const double lr = st ? base_lr * st->v.lr_scale : base_lr;
+    float4 a = reinterpret_cast<float4*>(w)[i];
+    const float4 g = __ldg(reinterpret_cast<const float4*>(grad) + i);
+    a.x -= static_cast<float>(lr * static_cast<double>(g.x));
+    a.y -= static_cast<float>(lr * static_cast<double>(g.y));
+    a.z -= static_cast<float>(lr * static_cast<double>(g.z));
+    a.w -= static_cast<float>(lr * static_cast<double>(g.w));
+    reinterpret_cast<float4*>(w)[i] = a;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_nonfinite_flag(const float* __restrict__ x, int64_t n, int32_t* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+    bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+  }
+  for (int64_t i = (n / 4) * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 // ---- layout helpers
 __global__ void k_nhwc_to_nchw_f32(const float* __restrict__ src, uint32_t C, uint32_t HW, uint32_t ld,
                                    float* __restrict__ dst) {
@@ -327,6 +365,27 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
                                                           reinterpret_cast<const DsgcState*>(state), skip);
   count_launch(1);
   return cuda_check("k_sgd_dclr");
+}
+
+int i8t_sgd_dclr_multi(i8t_ctx* ctx, float* w, const float* grad, int nseg, const int64_t* seg_off,
+                       const void* const* seg_state, double base_lr, const int32_t* skip) {
+  Ctx* c = CTX(ctx);
+  if (!c || !w || !grad || nseg < 1 || !seg_off || !seg_state) return set_error(I8T_EINVAL, "sgd_multi: bad arguments");
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(grad)) & 15u)
+    return set_error(I8T_EUNSUPPORTED, "sgd_multi: arenas must be 16-byte aligned");
+  k_sgd_dclr_multi<<<148 * 8, 256, 0, c->stream>>>(w, grad, nseg, seg_off, seg_state, base_lr, skip);
+  count_launch(1);
+  return cuda_check("k_sgd_dclr_multi");
+}
+
+int i8t_nonfinite_flag(i8t_ctx* ctx, const float* x, int64_t n, int32_t* flag) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !flag) return set_error(I8T_EINVAL, "nonfinite_flag: bad arguments");
+  if (reinterpret_cast<uintptr_t>(x) & 15u) return set_error(I8T_EUNSUPPORTED, "nonfinite_flag: 16-byte alignment");
+  cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream);
+  k_nonfinite_flag<<<148 * 4, 256, 0, c->stream>>>(x, n, flag);
+  count_launch(1);
+  return cuda_check("k_nonfinite_flag");
 }
 
 int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, int64_t hw, int64_t ld, float* dst) {

@@ -166,6 +166,10 @@ class Layer:
     def params(self) -> list[ParamRef]:
         return []
 
+    def param_attrs(self) -> list[tuple]:
+        """(owner, value attribute, grad attribute) per parameter, in params() order."""
+        return []
+
     def buffers(self) -> list[ParamRef]:
         return []
 
@@ -210,6 +214,7 @@ class Conv2d(Layer):
         self.wgrad_acc = None
         self.keep_qg = False  # Dense needs the int8 gradient for its bias
         self._qg = None
+        self.need_input_grad = True  # False for the first layer: the image gradient is discarded
 
     @property
     def quantized(self):
@@ -220,6 +225,9 @@ class Conv2d(Layer):
 
     def params(self):
         return [ParamRef("weight", self.weight, self.grad_weight)]
+
+    def param_attrs(self):
+        return [(self, "weight", "grad_weight")]
 
     def geom(self, x):
         n, h, w, c = x.shape
@@ -301,17 +309,19 @@ class Conv2d(Layer):
         n, p, q, k = gz.shape
         qg = quantize_gradient_layer(self.qs, gz, ctx)
         clip_g = self.qs.dsgc.clip_q_ptr()
-        ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gz.device)
+        ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gz.device) if self.need_input_grad else None
         if self.depthwise:
-            call("i8t_conv_dw_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qw), ops._p(clip_g),
-                 ops._p(self.qs.clip_w), ops._p(ga), None)
+            if self.need_input_grad:
+                call("i8t_conv_dw_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qw), ops._p(clip_g),
+                     ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
                 self.wgrad_acc = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int64, device=gz.device)
             call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
                  ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
         else:
-            call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
-                 ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
+            if self.need_input_grad:
+                call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
+                     ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
                 self.wgrad_acc = torch.empty((self.kh * self.kw * self.c_pad, self.out_c), dtype=torch.int64,
                                              device=gz.device)
@@ -380,6 +390,9 @@ class Dense(Layer):
     def params(self):
         return [ParamRef("weight", self.conv.weight, self.conv.grad_weight), ParamRef("bias", self.bias, self.grad_bias)]
 
+    def param_attrs(self):
+        return [(self.conv, "weight", "grad_weight"), (self, "bias", "grad_bias")]
+
     def forward(self, x, ctx):
         self._in_shape = x.shape
         n = x.shape[0]
@@ -416,6 +429,9 @@ class BatchNorm2d(Layer):
 
     def params(self):
         return [ParamRef("gamma", self.gamma, self.grad_gamma), ParamRef("beta", self.beta, self.grad_beta)]
+
+    def param_attrs(self):
+        return [(self, "gamma", "grad_gamma"), (self, "beta", "grad_beta")]
 
     def buffers(self):
         return [ParamRef("running_mean", self.running_mean, None), ParamRef("running_var", self.running_var, None)]

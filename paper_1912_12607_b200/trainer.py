@@ -109,8 +109,39 @@ class Trainer:
             self._hook = _DistHook()
             call("i8t_ctx_set_allreduce", ops.ctx(), C.cast(self._hook.cfn, C.c_void_p), None)
             call("i8t_ctx_set_shard", ops.ctx(), self.rank, self.world)
+        # the gradient w.r.t. the input images is discarded: the first conv skips backward-data
+        first = self.leaves[0][1]
+        if hasattr(first, "need_input_grad"):
+            first.need_input_grad = False
         self.skip = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
+        self._build_param_arenas(device)
+
+    def _build_param_arenas(self, device):
+        """Every parameter / gradient becomes a view into one flat arena
+        (segments padded to 4 floats) so the bad-gradient scan and the DCLR
+        SGD step are one launch each."""
+        segs, total = [], 0
+        for _, layer in self.leaves:
+            for owner, va, ga in layer.param_attrs():
+                v = getattr(owner, va)
+                segs.append((layer, owner, va, ga, total, v.numel(), v.shape))
+                total += (v.numel() + 3) // 4 * 4
+        self.pflat = torch.zeros(total, dtype=torch.float32, device=device)
+        self.gflat = torch.zeros(total, dtype=torch.float32, device=device)
+        offs, states = [], []
+        cfg = self.cfg
+        for layer, owner, va, ga, off, n, shape in segs:
+            self.pflat[off: off + n].copy_(getattr(owner, va).reshape(-1))
+            setattr(owner, va, self.pflat[off: off + n].view(shape))
+            setattr(owner, ga, self.gflat[off: off + n].view(shape))
+            offs.append(off)
+            use_phi = layer.qs is not None and cfg.mode == Mode.INT8 and layer.quantized and cfg.lr_scaling_enabled
+            states.append(layer.qs.dsgc.buf.data_ptr() if use_phi else 0)
+        offs.append(total)
+        self.seg_off = torch.tensor(offs, dtype=torch.int64, device=device)
+        self.seg_state = torch.tensor(states, dtype=torch.int64, device=device)
+        self.nseg = len(segs)
 
     # ---------------------------------------------------------------- clips
     def calibrate(self, images):
@@ -158,19 +189,14 @@ class Trainer:
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
                            self._wgrad_allreduce if self.world > 1 else None)
         self.model.net.backward(g_logits, bctx)
-        params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
         if self.world > 1:
+            params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
             self._allreduce_fp32_grads(params)
         # bad-gradient check (train.cpp:87-95) stays on the device and gates the update
-        self.skip.zero_()
-        for _, p in params:
-            self.skip |= (~torch.isfinite(p.grad).all()).to(torch.int32)
         h = ops.ctx()
-        for layer, p in params:
-            st = layer.qs.dsgc if (layer.qs is not None and cfg.mode == Mode.INT8 and layer.quantized
-                                   and cfg.lr_scaling_enabled) else None
-            call("i8t_sgd_dclr", h, ops._p(p.value), ops._p(p.grad), p.value.numel(), C.c_double(rep.base_lr_t),
-                 st.ptr if st is not None else None, ops._p(self.skip))
+        call("i8t_nonfinite_flag", h, ops._p(self.gflat), self.gflat.numel(), ops._p(self.skip))
+        call("i8t_sgd_dclr_multi", h, ops._p(self.pflat), ops._p(self.gflat), self.nseg, ops._p(self.seg_off),
+             ops._p(self.seg_state), C.c_double(rep.base_lr_t), ops._p(self.skip))
         if read_stats:
             rep.loss = float(self.loss_dev.item())
             rep.diverged = bool(self.skip.item())
