@@ -57,8 +57,8 @@ constexpr int BKB = 128;  // bytes of reduction per stage (4 MMAs of K=32)
 constexpr int NPROD = 256;
 constexpr int MMA_WARP = 8;
 constexpr int EPI_WARP0 = 9;
-constexpr int NEPI = 128;
-constexpr int NTHREADS = NPROD + 32 + NEPI;  // 416
+constexpr int NEPI = 256;                    // 8 epilogue warps: 2 per TMEM lane quadrant
+constexpr int NTHREADS = NPROD + 32 + NEPI;  // 544
 
 template <int MODE, int BN>
 struct Cfg {
@@ -66,7 +66,7 @@ struct Cfg {
   static constexpr int B_SUB = (BN + 127) / 128;
   static constexpr int B_BYTES = (MODE == MODE_WGRAD) ? 128 * 128 * B_SUB : BN * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // per epilogue warp: 2 x [32 rows x 128 B] staging
+  static constexpr int EPI_BYTES = 8 * 32 * 128;  // per epilogue warp: one [32 rows x 128 B] staging tile
   static constexpr int BUDGET = 232448 - EPI_BYTES - 1024 - 256;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     constexpr int ROWS_PER_PASS_A = NPROD / PPR_A;  // rows covered per pass
     constexpr int PASSES_A = BM / ROWS_PER_PASS_A;
     const int ja = tid % PPR_A, ra0 = tid / PPR_A;
+    const int adv_p = BKB / args.Q, adv_q = BKB - adv_p * args.Q;  // WGRAD: 128 pixels = adv_p rows + adv_q
     int kc = 0;  // global stage counter across tiles
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       const TileCoord tc = tile_of(args, t);
@@ -214,27 +215,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           }
         } else {
           // ---- WGRAD: smem rows = npq (reduction), columns = M bytes (A) / N bytes (B), MN-major
-          const int pq = args.P * args.Q;
           const int64_t mA = m0 + ja * VA;
           const bool mok = mA < args.M;
           const int tapA = mok ? static_cast<int>(mA / args.Cp) : 0;
           const int cA = mok ? static_cast<int>(mA - static_cast<int64_t>(tapA) * args.Cp) : 0;
           const int rA = tapA / args.S, sA_ = tapA - rA * args.S;
-#pragma unroll 4
+          if (kt == 0) {  // decode this thread's rows once per tile, then advance 128 pixels per k-tile
+#pragma unroll
+            for (int i = 0; i < PASSES_A; ++i) {
+              const int kdi = static_cast<int>(kbase) + ra0 + i * ROWS_PER_PASS_A;
+              const int pq = args.P * args.Q;
+              const int n = kdi / pq, rem = kdi - n * pq;
+              rowA_n[i] = n;
+              rowA_y[i] = rem / args.Q;
+              rowA_x[i] = rem - rowA_y[i] * args.Q;
+            }
+          }
+#pragma unroll
           for (int i = 0; i < PASSES_A; ++i) {
             const int row = ra0 + i * ROWS_PER_PASS_A;
             const int64_t kd = kbase + row;
             bool ok = mok && kd < args.Kd;
             const int8_t* src = args.act;
-            if (ok) {
-              const int kdi = static_cast<int>(kd);
-              const int n = kdi / pq, rem = kdi - n * pq;
-              const int p = rem / args.Q, q = rem - p * args.Q;
-              const int ih = p * args.sh - args.ph + rA, iw = q * args.sw - args.pw + sA_;
-              ok = ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
-              if (ok) src = args.act + ((static_cast<int64_t>(n) * args.H + ih) * args.W + iw) * args.Cp + cA;
-            }
+            const int ih = rowA_y[i] * args.sh - args.ph + rA, iw = rowA_x[i] * args.sw - args.pw + sA_;
+            ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
+            if (ok) src = args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + cA;
             cp_async_vec<VA>(a_st + sw128_offset(row, ja * VA), src, ok);
+            // advance (n, p, q) by BKB pixels for the next k-tile
+            int q = rowA_x[i] + adv_q, p = rowA_y[i] + adv_p, n = rowA_n[i];
+            if (q >= args.Q) { q -= args.Q; ++p; }
+            while (p >= args.P) { p -= args.P; ++n; }
+            rowA_x[i] = q; rowA_y[i] = p; rowA_n[i] = n;
           }
           constexpr int PPR_B = BKB / VB;
           constexpr int RPP_B = NPROD / PPR_B;
@@ -305,10 +316,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   } else {
     // ================================================= epilogue (warps 9-12)
     const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int half = (warp - EPI_WARP0) >> 2;  // which half of the BN columns
     const int row = quad * 32 + lane;
     const double rescale =
         static_cast<double>(__fdiv_rn(*args.clip_x, 127.0f)) * static_cast<double>(__fdiv_rn(*args.clip_y, 127.0f));
-    uint8_t* stage_base = sEpi + (warp - EPI_WARP0) * (2 * 32 * 128);
+    uint8_t* stage_base = sEpi + (warp - EPI_WARP0) * (32 * 128);
     int it = 0, nst = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
       const TileCoord tc = tile_of(args, t);
@@ -318,20 +330,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      constexpr int HALF = BN / 2 < 32 ? 32 : BN / 2;
+      const int c_begin = half * HALF, c_end = (half + 1) * HALF < BN ? (half + 1) * HALF : BN;
+      if (c_begin >= c_end) {  // BN == 32 would leave the second half idle
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
 #pragma unroll 1
-      for (int col = 0; col < BN; col += 32) {
+      for (int col = c_begin; col < c_end; col += 32) {
         uint32_t v[32];
         tmem_ld32(t_row + static_cast<uint32_t>(col), v);
         tmem_ld_wait();
-        if (col + 32 >= BN) {  // last read of this accumulator: hand it back to the MMA warp
+        if (col + 32 >= c_end) {  // last read of this accumulator: hand it back to the MMA warp
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
         const int gc0 = n0 + col;
         if (args.use_tma_out) {
           // 32x32 sub-tile -> swizzled smem staging (double-buffered) -> one TMA bulk store
-          uint8_t* buf = stage_base + (nst & 1) * (32 * 128);
-          if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
+          uint8_t* buf = stage_base;
+          if (lane == 0) bulk_wait_read<0>();  // the previous store has finished reading the buffer
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -560,6 +579,20 @@ static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, const CUtensorMa
 
 static int pick_bn(int64_t ng) { return ng <= 64 ? 64 : (ng <= 128 ? 128 : 256); }
 
+// Tile width for FWD / DGRAD: the widest tile unless that leaves the persistent
+// queue badly quantised (tiles per SM small and fractional); then halve it.
+static int pick_bn_balanced(int64_t ng, int64_t m_tiles, int sms) {
+  int bn = pick_bn(ng);
+  while (bn > 64) {
+    const int64_t tiles = m_tiles * ((ng + bn - 1) / bn);
+    const double per = static_cast<double>(tiles) / sms;
+    const double waste = (static_cast<double>((tiles + sms - 1) / sms) - per) / static_cast<double>((tiles + sms - 1) / sms);
+    if (per >= 8.0 || waste <= 0.12) break;
+    bn /= 2;
+  }
+  return bn;
+}
+
 static int geom_common(const i8t_conv_geom* g, int64_t& P, int64_t& Q) {
   if (!g) return set_error(I8T_EINVAL, "conv: null geometry");
   if (g->n < 1 || g->c < 1 || g->h < 1 || g->w < 1 || g->k < 1 || g->kh < 1 || g->kw < 1 || g->stride_h < 1 ||
@@ -608,8 +641,9 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   x.M = g->n * P * Q; x.Ng = (int)g->k; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_a; x.clip_y = clip_w; x.out = z; x.ldo = g->k; x.acc32 = acc;
-  const int bn = pick_bn(g->k);
-  x.m_tiles = (int)((x.M + BM - 1) / BM); x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
+  x.m_tiles = (int)((x.M + BM - 1) / BM);
+  const int bn = pick_bn_balanced(g->k, x.m_tiles, num_sms());
+  x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
   CUtensorMap map, omap{};
   if ((rc = make_weight_map(&map, w, g->k, ld_w, bn))) return rc;
   x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
@@ -636,8 +670,9 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   x.M = g->n * g->h * g->w; x.Ng = (int)g->c; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
-  const int bn = pick_bn(g->c);
-  x.m_tiles = (int)((x.M + BM - 1) / BM); x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
+  x.m_tiles = (int)((x.M + BM - 1) / BM);
+  const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
+  x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
   CUtensorMap map, omap{};
   if ((rc = make_weight_map(&map, wt, g->c, ld_wt, bn))) return rc;
   x.use_tma_out = tma_out_ok(ga, g->c) ? 1 : 0;
