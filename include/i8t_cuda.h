@@ -84,6 +84,12 @@ int i8t_ctx_destroy(i8t_ctx* ctx);
 /* Synchronise the stream; report and clear any latched device error. */
 int i8t_ctx_check(i8t_ctx* ctx);
 const char* i8t_last_error(void);
+/* Device memory for hosts that do not link a CUDA runtime (the C++ shim):
+ * synchronous on the context's stream.  kind: 0 host->device, 1 device->host,
+ * 2 device->device. */
+int i8t_device_alloc(i8t_ctx* ctx, uint64_t bytes, void** out);
+int i8t_device_free(i8t_ctx* ctx, void* ptr);
+int i8t_memcpy(i8t_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
 /* Number of kernels this library launched (for bench accounting). */
 uint64_t i8t_launch_count(void);
 /* Data parallel (8.e): the caller's gradient tensors are shard `rank` of

@@ -16,6 +16,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libi8t_cuda.so")
+SHIM = os.path.join(PKG, "libi8t.so")              # drop-in C++ API (include/i8t/i8t.hpp)
+SHIM_SRC = os.path.join(CSRC, "host", "i8t_api.cpp")
+SHIM_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")
+SHIM_TEST = os.path.join(ROOT, "tests", "cpp", "test_shim")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
@@ -47,9 +51,27 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    inc = os.path.join(ROOT, "include")
+    if _stale(SHIM, [SHIM_SRC, LIB, os.path.join(inc, "i8t", "i8t.hpp"), os.path.join(inc, "i8t_cuda.h")]):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-I" + inc, SHIM_SRC, "-o", SHIM,
+              "-L" + PKG, "-li8t_cuda", "-Wl,-rpath,$ORIGIN"], "shim")
+    if _stale(SHIM_TEST, [SHIM_TEST_SRC, SHIM]):
+        _run(["g++", "-std=c++20", "-O2", "-I" + inc, SHIM_TEST_SRC, "-o", SHIM_TEST, "-L" + PKG, "-li8t",
+              "-li8t_cuda", "-Wl,-rpath," + os.path.relpath(PKG, os.path.dirname(SHIM_TEST)).join(["$ORIGIN/", ""])],
+             "shim test")
     if verbose:
-        print("built", LIB)
+        print("built", LIB, SHIM)
     return LIB
+
+
+def _stale(out, deps):
+    return not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps)
+
+
+def _run(cmd, what):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"{what} build failed:\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -112,6 +112,34 @@ int i8t_ctx_create(void* stream, i8t_ctx** out) {
   return cuda_check("ctx_create");
 }
 
+int i8t_device_alloc(i8t_ctx* ctx, uint64_t bytes, void** out) {
+  if (!ctx || !out) return set_error(I8T_EINVAL, "device_alloc: bad arguments");
+  *out = nullptr;
+  if (bytes == 0) return I8T_OK;
+  if (cudaMalloc(out, bytes) != cudaSuccess) return set_error(I8T_ECUDA, "device_alloc: cudaMalloc failed");
+  return I8T_OK;
+}
+
+int i8t_device_free(i8t_ctx* ctx, void* ptr) {
+  if (!ctx) return set_error(I8T_EINVAL, "device_free: null ctx");
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (ptr) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(ptr);
+  }
+  return cuda_check("device_free");
+}
+
+int i8t_memcpy(i8t_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind) {
+  if (!ctx || (bytes && (!dst || !src)) || kind < 0 || kind > 2) return set_error(I8T_EINVAL, "memcpy: bad arguments");
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!bytes) return I8T_OK;
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  cudaMemcpyAsync(dst, src, bytes, k, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return cuda_check("memcpy");
+}
+
 int i8t_ctx_set_stream(i8t_ctx* ctx, void* stream) {
   if (!ctx) return set_error(I8T_EINVAL, "ctx_set_stream: null ctx");
   reinterpret_cast<Ctx*>(ctx)->stream = reinterpret_cast<cudaStream_t>(stream);

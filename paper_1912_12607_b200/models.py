@@ -108,7 +108,9 @@ def build_model(name: str, seed: int = 1, device="cuda", **kw) -> Model:
 
 def conv_gop_per_image(model: Model) -> float:
     """2*N*K*P*Q*(C/groups)*R*S ops per pass summed over quantised conv/fc
-    layers x 3 passes (fwd, dgrad, wgrad), per image."""
+    layers x 3 passes (fwd, dgrad, wgrad), per image, minus the
+    first conv's dgrad (the image gradient is never computed): 24.299 GOP for
+    ResNet-50 at 224x224."""
     from .layers import leaves
     c, h, w = model.in_shape
     x = torch.zeros((1, h, w, c))
@@ -140,7 +142,10 @@ def conv_gop_per_image(model: Model) -> float:
             p = (hh + 2 * layer.ph - layer.kh) // layer.sh + 1
             q = (ww + 2 * layer.pw - layer.kw) // layer.sw + 1
             cin = 1 if layer.depthwise else cc
-            total += 3 * 2.0 * p * q * layer.out_c * cin * layer.kh * layer.kw
+            # fwd + wgrad always; dgrad unless the layer's input gradient is discarded (the stem)
+            passes = 3 if layer.need_input_grad and not first[0] else 2
+            first[0] = False
+            total += passes * 2.0 * p * q * layer.out_c * cin * layer.kh * layer.kw
             return (n, p, q, layer.out_c)
         if isinstance(layer, L.Dense):
             total += 3 * 2.0 * layer.in_f * layer.out_f
@@ -152,5 +157,6 @@ def conv_gop_per_image(model: Model) -> float:
             return (shape[0], shape[3])
         return shape
 
+    first = [True]
     walk(model.net, (1, h, w, c))
     return total / 1e9
