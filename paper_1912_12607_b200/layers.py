@@ -494,6 +494,53 @@ class MaxPool2d(Layer):
         return gi.permute(0, 2, 3, 1).contiguous()
 
 
+class AvgPool2d(Layer):
+    """k x k average pooling, stride s, padding p (count_include_pad like torchvision)."""
+    kind = "avgpool2d"
+
+    def __init__(self, k, s, p=0):
+        self.k, self.s, self.p = k, s, p
+
+    def forward(self, x, ctx):
+        xc = x.permute(0, 3, 1, 2)
+        self._xc = xc
+        y = F.avg_pool2d(xc, self.k, self.s, self.p)
+        return y.permute(0, 2, 3, 1).contiguous()
+
+    def backward(self, g, ctx):
+        gi = torch.ops.aten.avg_pool2d_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k], [self.s, self.s],
+                                                [self.p, self.p], False, True, None)
+        self._xc = None
+        return gi.permute(0, 2, 3, 1).contiguous()
+
+
+class Concat(Layer):
+    """Parallel branches whose NHWC outputs are concatenated along channels
+    (Inception blocks).  Backward splits the gradient per branch and runs the
+    branches in forward order (the LCG stream is consumed in that order)."""
+    kind = "concat"
+
+    def __init__(self, branches):
+        self.branches = list(branches)
+
+    def forward(self, x, ctx):
+        outs = [b.forward(x, ctx) for b in self.branches]
+        self._sizes = [o.shape[-1] for o in outs]
+        return torch.cat(outs, dim=-1)
+
+    def backward(self, g, ctx):
+        parts = torch.split(g, self._sizes, dim=-1)
+        gi = None
+        for b, gp in zip(self.branches, parts):
+            r = b.backward(gp.contiguous(), ctx)
+            gi = r if gi is None else gi + r
+        return gi
+
+    def visit(self, prefix, fn):
+        for i, b in enumerate(self.branches):
+            b.visit(f"{prefix}/b{i}" if prefix else f"b{i}", fn)
+
+
 class GlobalAvgPool(Layer):
     kind = "avgpool"
 

@@ -9,8 +9,8 @@ from __future__ import annotations
 
 import torch
 
-from .layers import (BatchNorm2d, Conv2d, Dense, GlobalAvgPool, InvertedResidual, MaxPool2d, ReLU, ResidualBlock,
-                     Sequential)
+from .layers import (AvgPool2d, BatchNorm2d, Concat, Conv2d, Dense, GlobalAvgPool, InvertedResidual, MaxPool2d, ReLU,
+                     ResidualBlock, Sequential)
 
 
 class Model:
@@ -96,7 +96,81 @@ def mobilenet_v2(num_classes=1000, seed=1, device="cuda", width_mult=1.0) -> Mod
     return Model("mobilenet_v2", net, num_classes, (3, 224, 224))
 
 
-MODELS = {"resnet20": resnet20, "resnet50": resnet50, "mobilenet_v2": mobilenet_v2}
+def _basic(cin, cout, k, s=1, p=0, gen=None, dev="cuda"):
+    seq = Sequential()
+    _cbr(seq, "conv", cin, cout, k, s, p, gen, dev)
+    return seq
+
+
+def _chain(specs, gen, dev):
+    """specs: list of (cin, cout, kernel, stride, pad) conv-bn-relu units."""
+    seq = Sequential()
+    for i, (ci, co, k, s, p) in enumerate(specs):
+        _cbr(seq, f"conv{i}", ci, co, k, s, p, gen, dev)
+    return seq
+
+
+def _pool_branch(pool, cin, cout, gen, dev):
+    seq = Sequential()
+    seq.add("pool", pool)
+    if cout:
+        _cbr(seq, "conv", cin, cout, 1, 1, 0, gen, dev)
+    return seq
+
+
+def inception_v3(num_classes=1000, seed=1, device="cuda") -> Model:
+    """InceptionV3 (torchvision layout, no aux head) at 299x299: 94 convs incl.
+    the asymmetric 1x7 / 7x1 / 1x3 / 3x1 kernels with (0,3)/(3,0)/(0,1)/(1,0)
+    padding that the reference's single-pad geometry cannot express (A.3-2)."""
+    g, d = torch.Generator().manual_seed(seed), device
+    net = Sequential()
+    for name, (ci, co, k, s, p) in [("c1a", (3, 32, 3, 2, 0)), ("c2a", (32, 32, 3, 1, 0)), ("c2b", (32, 64, 3, 1, 1))]:
+        _cbr(net, name, ci, co, k, s, p, g, d)
+    net.add("pool1", MaxPool2d(3, 2))
+    _cbr(net, "c3b", 64, 80, 1, 1, 0, g, d)
+    _cbr(net, "c4a", 80, 192, 3, 1, 0, g, d)
+    net.add("pool2", MaxPool2d(3, 2))
+    cin = 192
+    for i, pf in enumerate((32, 64, 64)):  # InceptionA x3
+        net.add(f"mixed5{'bcd'[i]}", Concat([
+            _basic(cin, 64, 1, gen=g, dev=d),
+            _chain([(cin, 48, 1, 1, 0), (48, 64, 5, 1, 2)], g, d),
+            _chain([(cin, 64, 1, 1, 0), (64, 96, 3, 1, 1), (96, 96, 3, 1, 1)], g, d),
+            _pool_branch(AvgPool2d(3, 1, 1), cin, pf, g, d)]))
+        cin = 224 + pf
+    net.add("mixed6a", Concat([  # InceptionB
+        _basic(cin, 384, 3, 2, 0, g, d),
+        _chain([(cin, 64, 1, 1, 0), (64, 96, 3, 1, 1), (96, 96, 3, 2, 0)], g, d),
+        _pool_branch(MaxPool2d(3, 2), cin, 0, g, d)]))
+    cin = 768
+    for i, c7 in enumerate((128, 160, 160, 192)):  # InceptionC x4
+        net.add(f"mixed6{'bcde'[i]}", Concat([
+            _basic(cin, 192, 1, gen=g, dev=d),
+            _chain([(cin, c7, 1, 1, 0), (c7, c7, (1, 7), 1, (0, 3)), (c7, 192, (7, 1), 1, (3, 0))], g, d),
+            _chain([(cin, c7, 1, 1, 0), (c7, c7, (7, 1), 1, (3, 0)), (c7, c7, (1, 7), 1, (0, 3)),
+                    (c7, c7, (7, 1), 1, (3, 0)), (c7, 192, (1, 7), 1, (0, 3))], g, d),
+            _pool_branch(AvgPool2d(3, 1, 1), cin, 192, g, d)]))
+    net.add("mixed7a", Concat([  # InceptionD
+        _chain([(768, 192, 1, 1, 0), (192, 320, 3, 2, 0)], g, d),
+        _chain([(768, 192, 1, 1, 0), (192, 192, (1, 7), 1, (0, 3)), (192, 192, (7, 1), 1, (3, 0)),
+                (192, 192, 3, 2, 0)], g, d),
+        _pool_branch(MaxPool2d(3, 2), 768, 0, g, d)]))
+    cin = 1280
+    for i in range(2):  # InceptionE x2
+        b3 = Sequential()
+        _cbr(b3, "conv", cin, 384, 1, 1, 0, g, d)
+        b3.add("split", Concat([_basic(384, 384, (1, 3), 1, (0, 1), g, d), _basic(384, 384, (3, 1), 1, (1, 0), g, d)]))
+        bd = _chain([(cin, 448, 1, 1, 0), (448, 384, 3, 1, 1)], g, d)
+        bd.add("split", Concat([_basic(384, 384, (1, 3), 1, (0, 1), g, d), _basic(384, 384, (3, 1), 1, (1, 0), g, d)]))
+        net.add(f"mixed7{'bc'[i]}", Concat([_basic(cin, 320, 1, gen=g, dev=d), b3, bd,
+                                            _pool_branch(AvgPool2d(3, 1, 1), cin, 192, g, d)]))
+        cin = 2048
+    net.add("pool", GlobalAvgPool())
+    net.add("fc", Dense(2048, num_classes, g, d))
+    return Model("inception_v3", net, num_classes, (3, 299, 299))
+
+
+MODELS = {"resnet20": resnet20, "resnet50": resnet50, "mobilenet_v2": mobilenet_v2, "inception_v3": inception_v3}
 
 
 def build_model(name: str, seed: int = 1, device="cuda", **kw) -> Model:
@@ -111,17 +185,8 @@ def conv_gop_per_image(model: Model) -> float:
     layers x 3 passes (fwd, dgrad, wgrad), per image, minus the
     first conv's dgrad (the image gradient is never computed): 24.299 GOP for
     ResNet-50 at 224x224."""
-    from .layers import leaves
     c, h, w = model.in_shape
-    x = torch.zeros((1, h, w, c))
     total = 0.0
-    shapes = {}
-
-    def trace(layer, x):
-        return layer
-
-    # geometry walk without running kernels: reuse a FP32 CPU forward of shapes only
-    import torch.nn.functional as F
 
     def walk(layer, shape):
         nonlocal total
@@ -137,11 +202,19 @@ def conv_gop_per_image(model: Model) -> float:
             return out
         if isinstance(layer, L.InvertedResidual):
             return walk(layer.body, shape)
+        if isinstance(layer, L.Concat):
+            outs = [walk(b, shape) for b in layer.branches]
+            return outs[0][:3] + (sum(o[3] for o in outs),)
+        if isinstance(layer, L.AvgPool2d):
+            n, hh, ww, cc = shape
+            return (n, (hh + 2 * layer.p - layer.k) // layer.s + 1, (ww + 2 * layer.p - layer.k) // layer.s + 1, cc)
         if isinstance(layer, L.Conv2d):
             n, hh, ww, cc = shape
             p = (hh + 2 * layer.ph - layer.kh) // layer.sh + 1
             q = (ww + 2 * layer.pw - layer.kw) // layer.sw + 1
             cin = 1 if layer.depthwise else cc
+            if not layer.depthwise and cc != layer.in_c:
+                raise ValueError(f"channel mismatch in model walk: {cc} vs {layer.in_c}")
             # fwd + wgrad always; dgrad unless the layer's input gradient is discarded (the stem)
             passes = 3 if layer.need_input_grad and not first[0] else 2
             first[0] = False

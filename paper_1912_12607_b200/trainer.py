@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import torch
 import torch.distributed as dist
 
-from . import ops
+from . import dp, ops
 from ._lib import DsgcView, call
 from .layers import (BackwardCtx, Dense, ForwardCtx, Mode, SoftmaxCrossEntropy, StateArena, int8_replace, leaves)
 
@@ -91,7 +91,7 @@ class _DistHook:
 
 
 class Trainer:
-    def __init__(self, model, cfg: TrainConfig, device="cuda"):
+    def __init__(self, model, cfg: TrainConfig, device="cuda", force_dp_hook: bool = False):
         self.model, self.cfg = model, cfg
         self.leaves = leaves(model.net)
         self.quant_layers = [(p, l) for p, l in self.leaves if l.qs is not None]
@@ -105,7 +105,7 @@ class Trainer:
         self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank() if self.world > 1 else 0
         self._hook = None
-        if self.world > 1:
+        if self.world > 1 or force_dp_hook:  # force: exercise the data-parallel phases at world size 1
             self._hook = _DistHook()
             call("i8t_ctx_set_allreduce", ops.ctx(), C.cast(self._hook.cfn, C.c_void_p), None)
             call("i8t_ctx_set_shard", ops.ctx(), self.rank, self.world)
@@ -187,7 +187,7 @@ class Trainer:
         self.loss_dev.copy_(loss.reshape(1))
         bctx = BackwardCtx(cfg.mode, it, self.grad_stream, cfg.grid_resolution, cfg.refine_rounds, cfg.clip_enabled,
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
-                           self._wgrad_allreduce if self.world > 1 else None)
+                           self._wgrad_allreduce if self._hook is not None else None)
         self.model.net.backward(g_logits, bctx)
         if self.world > 1:
             params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
@@ -216,7 +216,7 @@ class Trainer:
 
     # ---------------------------------------------------------------- data parallel
     def _wgrad_allreduce(self, acc: torch.Tensor):
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+        dp.allreduce_int64_(acc)
 
     def _allreduce_fp32_grads(self, params):
         flat = [p.grad for layer, p in params if not (layer.quantized and p.name == "weight")]
