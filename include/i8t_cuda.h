@@ -229,6 +229,38 @@ int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64
 int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double base_lr, const void* state,
                  const int32_t* skip);
 
+/* ------------------------------------------------------------ fused BatchNorm2d + ReLU
+ * BatchNorm2d (layers.cpp:230-323) and ReLU (:328-344) are FP32 layers the
+ * reference never quantises; these fuse them into the INT8 path's HBM passes.
+ * Tensors are NHWC [m = N*H*W][c] fp32, c % 4 == 0.  bn: device doubles [5c]
+ * (mean, invstd, s1/m, s2/m, gamma*invstd), filled by the calls below.
+ * mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0, 2 mask_y > 0. */
+int i8t_bn_fwd_stats(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, double momentum, double eps, double* bn,
+                     float* running_mean, float* running_var);
+/* q = quantize_nearest(act(bn(z)), clip) with running max|act| -> *amax: the
+ * next conv's input quantiser (layers.cpp:101, 109) fused with BN + ReLU. */
+int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+                     const float* beta, int relu, const float* clip, int8_t* q, float* amax);
+/* y = act(bn(z) + residual): residual = res (fp32) or bn'(res_z) (NULL: none). */
+int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+               const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
+               const float* res_gamma, const float* res_beta, float* y);
+/* BN backward reduction: dbeta = sum g_m, dgamma = sum g_m * x_hat. */
+int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,
+                      const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* grad_gamma,
+                      float* grad_beta);
+/* gz = BN backward (materialised fp32). */
+int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
+                     const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz);
+/* quantize_gradient (layers.cpp:19-59) of the BN-backward value computed on
+ * the fly (non-search iterations: maybe_update's measurement branch). */
+int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const float* z, int64_t n_img, int64_t c,
+                             int64_t hw, const double* bn, const float* gamma, const float* beta, int mask_mode,
+                             const float* mask_y, int lr_scaling_enabled, double alpha, double beta_, int form,
+                             uint32_t* lcg_state, int8_t* q);
+/* out = a + g * (y > 0) (ResidualBlock backward with an identity shortcut). */
+int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y, int64_t n, float* out);
+
 /* All parameters in one launch: w and grad are flat arenas; segment i covers
  * [seg_off[i], seg_off[i+1]) (multiples of 4, device int64) and uses the
  * DCLR factor of device state seg_state[i] (device array of pointers; NULL

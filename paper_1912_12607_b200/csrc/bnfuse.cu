@@ -1,0 +1,464 @@
+// bnfuse.cu -- BatchNorm2d (layers.cpp:230-323) + ReLU fused around the INT8
+// convolutions so the FP32 activation / gradient between two convs is read
+// the minimum number of times:
+//   forward   z --(column stats)--> mean, invstd
+//             z --(BN-apply + ReLU + nearest quantise + amax)--> int8 input of the next conv
+//             z --(BN-apply [+ residual] + ReLU)--> fp32 block output (only where it is reused)
+//   backward  g, z --(column sums, ReLU mask recomputed from z)--> dgamma, dbeta, coefficients
+//             g, z --(BN-backward apply -> K3 stochastic quantiser + DSGC sums)--> int8 gradient
+// Numerics follow the reference BN: double statistics, biased variance,
+// x_hat = float((z-mean)*invstd), y = float(gamma*x_hat_d + beta),
+// g_in = float(gamma*invstd * (g - s1/m - x_hat*(s2/m))).
+// Tensors are NHWC [m][c] fp32 with c % 4 == 0.  bn: device doubles [5c] =
+// mean, invstd, s1/m, s2/m, gamma*invstd.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "internal.cuh"
+#include "qcore.cuh"
+#include "qgrad.cuh"
+
+namespace i8t_dev {
+
+constexpr int BN_GROUP = 128;  // channels per column-reduction block group
+
+struct ColArgs {
+  const float* z;
+  const float* g;       // MODE 1
+  const float* mask_y;  // MODE 1, mask 2
+  const float* gamma;
+  const float* beta;
+  double* bn;
+  uint32_t m, c;
+  int mask_mode;        // 0 none, 1 relu(bn(z)) > 0, 2 mask_y > 0
+  double momentum, eps;
+  float* running_mean;  // MODE 0
+  float* running_var;
+  float* grad_gamma;    // MODE 1
+  float* grad_beta;
+};
+
+__device__ __forceinline__ float bn_y(double gm, double xv, double bt) { return static_cast<float>(fma(gm, xv, bt)); }
+
+// Column sums over the m rows for one 128-channel group per blockIdx.y.
+// MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets) {
+  const uint32_t c0 = blockIdx.y * BN_GROUP;
+  const uint32_t gw = min(static_cast<uint32_t>(BN_GROUP), a.c - c0);  // group width (multiple of 4)
+  const uint32_t lpr = gw / 4;                                         // lanes per row
+  const uint32_t rpw = 32 / lpr;                                       // rows per warp per step
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = lane < rpw * lpr;
+  const uint32_t quad = lane % lpr, sub = lane / lpr;
+  const uint32_t ch = c0 + quad * 4;
+  double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
+  double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0}, gmm[4] = {0, 0, 0, 0}, bt[4] = {0, 0, 0, 0};
+  if (MODE == 1 && active) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mean[j] = a.bn[ch + j];
+      invstd[j] = a.bn[a.c + ch + j];
+      gmm[j] = a.gamma[ch + j];
+      bt[j] = a.beta[ch + j];
+    }
+  }
+  if (active) {
+    const uint32_t row_step = gridDim.x * 8 * rpw;
+    for (uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub; r < a.m; r += row_step) {
+      const size_t off = static_cast<size_t>(r) * a.c + ch;
+      const float4 zv = __ldg(reinterpret_cast<const float4*>(a.z + off));
+      const float zz[4] = {zv.x, zv.y, zv.z, zv.w};
+      if (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc0[j] += static_cast<double>(zz[j]);
+          acc1[j] = fma(static_cast<double>(zz[j]), static_cast<double>(zz[j]), acc1[j]);
+        }
+      } else {
+        const float4 gv = __ldg(reinterpret_cast<const float4*>(a.g + off));
+        const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+        float mk[4] = {1, 1, 1, 1};
+        if (a.mask_mode == 2) {
+          const float4 yv = __ldg(reinterpret_cast<const float4*>(a.mask_y + off));
+          mk[0] = yv.x > 0.0f; mk[1] = yv.y > 0.0f; mk[2] = yv.z > 0.0f; mk[3] = yv.w > 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
+          const float xh = static_cast<float>(xv);
+          if (a.mask_mode == 1) mk[j] = bn_y(gmm[j], xv, bt[j]) > 0.0f;
+          const float gm = mk[j] != 0.0f ? gg[j] : 0.0f;
+          acc0[j] += static_cast<double>(gm);
+          acc1[j] = fma(static_cast<double>(gm), static_cast<double>(xh), acc1[j]);
+        }
+      }
+    }
+  }
+  // block reduction in a fixed order: warps, then sub-rows
+  __shared__ double red[8][32][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    red[warp][lane][j] = acc0[j];
+    red[warp][lane][4 + j] = acc1[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < gw) {
+    const uint32_t q = threadIdx.x / 4, j = threadIdx.x % 4;
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < 8; ++w)
+      for (uint32_t sr = 0; sr < rpw; ++sr) {
+        s0 += red[w][sr * lpr + q][j];
+        s1 += red[w][sr * lpr + q][4 + j];
+      }
+    double* p = partials + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (2 * BN_GROUP);
+    p[threadIdx.x] = s0;
+    p[BN_GROUP + threadIdx.x] = s1;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.y], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < gw) {
+    double s0 = 0.0, s1 = 0.0;
+    for (uint32_t b = 0; b < gridDim.x; ++b) {
+      const double* p = partials + (static_cast<size_t>(blockIdx.y) * gridDim.x + b) * (2 * BN_GROUP);
+      s0 += __ldcg(p + threadIdx.x);
+      s1 += __ldcg(p + BN_GROUP + threadIdx.x);
+    }
+    const uint32_t cc = c0 + threadIdx.x;
+    const double m = static_cast<double>(a.m);
+    if (MODE == 0) {  // layers.cpp:260-268
+      const double mean_c = s0 / m;
+      const double var = fmax(s1 / m - mean_c * mean_c, 0.0);
+      const double inv = 1.0 / sqrt(var + a.eps);
+      a.bn[cc] = mean_c;
+      a.bn[a.c + cc] = inv;
+      if (a.running_mean) {
+        a.running_mean[cc] = static_cast<float>((1.0 - a.momentum) * a.running_mean[cc] + a.momentum * mean_c);
+        a.running_var[cc] = static_cast<float>((1.0 - a.momentum) * a.running_var[cc] + a.momentum * var);
+      }
+    } else {  // layers.cpp:285-300
+      a.grad_beta[cc] = static_cast<float>(s0);
+      a.grad_gamma[cc] = static_cast<float>(s1);
+      a.bn[2 * a.c + cc] = s0 / m;
+      a.bn[3 * a.c + cc] = s1 / m;
+      a.bn[4 * a.c + cc] = static_cast<double>(a.gamma[cc]) * a.bn[a.c + cc];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tickets[blockIdx.y] = 0u;
+}
+
+// Per-thread channel-quad coefficients of a BN layer.
+struct BnQuad {
+  double mean[4], invstd[4], gm[4], bt[4];
+  __device__ __forceinline__ void load(const double* bn, const float* gamma, const float* beta, uint32_t c,
+                                       uint32_t c0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mean[j] = bn[c0 + j];
+      invstd[j] = bn[c + c0 + j];
+      gm[j] = gamma[c0 + j];
+      bt[j] = beta[c0 + j];
+    }
+  }
+  __device__ __forceinline__ float y(int j, float z) const {
+    return bn_y(gm[j], (static_cast<double>(z) - mean[j]) * invstd[j], bt[j]);
+  }
+};
+
+// Forward: q = quantize_nearest(act(bn(z))), running max|act| (layers.cpp:101, 108-109).
+__global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ z, uint32_t n, uint32_t c,
+                                                      const double* bn, const float* gamma, const float* beta, int relu,
+                                                      const float* clip_p, int8_t* __restrict__ q, float* amax,
+                                                      int* err) {
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  float m = 0.0f;
+  bool bad = false;
+  if (e < n) {
+    BnQuad k;
+    k.load(bn, gamma, beta, c, e % c);
+    for (; e < n; e += T4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(z + e));
+      const float zz[4] = {v.x, v.y, v.z, v.w};
+      signed char qq[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float y = k.y(j, zz[j]);
+        if (relu) y = y > 0.0f ? y : 0.0f;
+        bad |= !isfinite(y);
+        m = fmaxf(m, fabsf(y));
+        qq[j] = static_cast<signed char>(quant_nearest(y, clip, s, inv_s));
+      }
+      reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
+    }
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+  if (amax) {
+    __shared__ float sm[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) m = fmaxf(m, sm[w]);
+      if (m > 0.0f) atomicMax(reinterpret_cast<int*>(amax), __float_as_int(m));
+    }
+  }
+}
+
+// Forward: y = act(bn(z) [+ residual]); residual is fp32 `res` or a second BN
+// applied lazily to res_z (ResidualBlock, layers.cpp:451-456: float add, then ReLU).
+__global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
+                                                const float* gamma, const float* beta, int relu,
+                                                const float* __restrict__ res, const float* __restrict__ res_z,
+                                                const double* res_bn, const float* res_gamma, const float* res_beta,
+                                                float* __restrict__ y) {
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  if (e >= n) return;
+  BnQuad k, kr;
+  k.load(bn, gamma, beta, c, e % c);
+  if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
+  for (; e < n; e += T4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(z + e));
+    const float zz[4] = {v.x, v.y, v.z, v.w};
+    float rr[4] = {0, 0, 0, 0};
+    if (res) {
+      const float4 r = __ldg(reinterpret_cast<const float4*>(res + e));
+      rr[0] = r.x; rr[1] = r.y; rr[2] = r.z; rr[3] = r.w;
+    } else if (res_z) {
+      const float4 r = __ldg(reinterpret_cast<const float4*>(res_z + e));
+      rr[0] = kr.y(0, r.x); rr[1] = kr.y(1, r.y); rr[2] = kr.y(2, r.z); rr[3] = kr.y(3, r.w);
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float t = k.y(j, zz[j]);
+      if (res || res_z) t = __fadd_rn(t, rr[j]);
+      o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+    }
+    reinterpret_cast<float4*>(y)[e / 4] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Backward value source: g_in = float(gamma*invstd * (g_m - s1/m - x_hat*(s2/m))).
+struct BnBwdSrc {
+  const float* g;
+  const float* z;
+  const float* mask_y;
+  const double* bn;
+  const float* gamma;
+  const float* beta;
+  uint32_t c;
+  int mask_mode;
+  double mean[4], invstd[4], gm[4], bt[4], a[4], b[4], k[4];
+  __device__ __forceinline__ void init(uint32_t c0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mean[j] = bn[c0 + j];
+      invstd[j] = bn[c + c0 + j];
+      a[j] = bn[2 * c + c0 + j];
+      b[j] = bn[3 * c + c0 + j];
+      k[j] = bn[4 * c + c0 + j];
+      gm[j] = gamma[c0 + j];
+      bt[j] = beta[c0 + j];
+    }
+  }
+  __device__ __forceinline__ float4 load(uint32_t e4) const {
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + e4);
+    const float4 zv = __ldg(reinterpret_cast<const float4*>(z) + e4);
+    const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, zz[4] = {zv.x, zv.y, zv.z, zv.w};
+    float mk[4] = {1, 1, 1, 1};
+    if (mask_mode == 2) {
+      const float4 yv = __ldg(reinterpret_cast<const float4*>(mask_y) + e4);
+      mk[0] = yv.x > 0.0f; mk[1] = yv.y > 0.0f; mk[2] = yv.z > 0.0f; mk[3] = yv.w > 0.0f;
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
+      const float xh = static_cast<float>(xv);
+      if (mask_mode == 1) mk[j] = bn_y(gm[j], xv, bt[j]) > 0.0f;
+      const float gmk = mk[j] != 0.0f ? gg[j] : 0.0f;
+      o[j] = static_cast<float>(k[j] * (static_cast<double>(gmk) - a[j] - static_cast<double>(xh) * b[j]));
+    }
+    return make_float4(o[0], o[1], o[2], o[3]);
+  }
+};
+
+__global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc src, uint32_t n, float* __restrict__ out) {
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  if (e >= n) return;
+  src.init(e % src.c);
+  for (; e < n; e += T4) reinterpret_cast<float4*>(out)[e / 4] = src.load(e / 4);
+}
+
+// out = a + g * (y > 0): identity-shortcut gradient joined with the main branch.
+__global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a, const float* __restrict__ g,
+                                                    const float* __restrict__ y, uint32_t n4, float* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const float4 av = __ldg(reinterpret_cast<const float4*>(a) + i), gv = __ldg(reinterpret_cast<const float4*>(g) + i),
+                 yv = __ldg(reinterpret_cast<const float4*>(y) + i);
+    float4 o;
+    o.x = __fadd_rn(av.x, yv.x > 0.0f ? gv.x : 0.0f);
+    o.y = __fadd_rn(av.y, yv.y > 0.0f ? gv.y : 0.0f);
+    o.z = __fadd_rn(av.z, yv.z > 0.0f ? gv.z : 0.0f);
+    o.w = __fadd_rn(av.w, yv.w > 0.0f ? gv.w : 0.0f);
+    reinterpret_cast<float4*>(out)[i] = o;
+  }
+}
+
+// ---------------------------------------------------------------- host
+static int ew_blocks(int64_t n, int64_t c) {
+  // grid such that blocks*256*4 % c == 0 (fixed channel quad per thread)
+  const int64_t mult = c / gcd_i(c, 1024);
+  int64_t b = (n / 4 + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  b = (b + mult - 1) / mult * mult;
+  return static_cast<int>(b);
+}
+
+static unsigned* tickets(Ctx* c) {
+  if (!c->d_tickets) {
+    if (cudaMalloc(&c->d_tickets, 64 * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    cudaMemset(c->d_tickets, 0, 64 * sizeof(unsigned));
+  }
+  return c->d_tickets;
+}
+
+static int colsum(Ctx* c, const ColArgs& a, int mode) {
+  const int groups = static_cast<int>((a.c + BN_GROUP - 1) / BN_GROUP);
+  if (groups > 64) return set_error(I8T_EUNSUPPORTED, "bn: more than 8192 channels");
+  int bx = static_cast<int>((a.m + 8 * 64 - 1) / (8 * 64));
+  const int cap = (148 * 4 + groups - 1) / groups;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  double* p = ensure_partials(c, static_cast<size_t>(bx) * groups * 2 * BN_GROUP);
+  unsigned* t = tickets(c);
+  if (!p || !t) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
+  dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
+  if (mode == 0) k_bn_colsum<0><<<grid, 256, 0, c->stream>>>(a, p, t);
+  else k_bn_colsum<1><<<grid, 256, 0, c->stream>>>(a, p, t);
+  count_launch(1);
+  return cuda_check("k_bn_colsum");
+}
+
+static int bn_check(int64_t m, int64_t c, const void* z) {
+  if (m < 1 || c < 4 || c % 4 != 0 || !z) return set_error(I8T_EUNSUPPORTED, "bn: needs c % 4 == 0");
+  if (m * c >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "bn: tensor >= 2^31 elements");
+  if (reinterpret_cast<uintptr_t>(z) & 15u) return set_error(I8T_EUNSUPPORTED, "bn: 16-byte alignment");
+  return I8T_OK;
+}
+
+}  // namespace i8t_dev
+
+using namespace i8t_dev;
+#define CTX(c) reinterpret_cast<Ctx*>(c)
+
+extern "C" {
+
+int i8t_bn_fwd_stats(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, double momentum, double eps, double* bn,
+                     float* running_mean, float* running_var) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !bn) return set_error(I8T_EINVAL, "bn_fwd_stats: bad arguments");
+  ColArgs a{};
+  a.z = z; a.bn = bn; a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c);
+  a.momentum = momentum; a.eps = eps; a.running_mean = running_mean; a.running_var = running_var;
+  return colsum(cx, a, 0);
+}
+
+int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+                     const float* beta, int relu, const float* clip, int8_t* q, float* amax) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !bn || !gamma || !beta || !clip || !q) return set_error(I8T_EINVAL, "bn_act_quant: bad arguments");
+  k_bn_act_quant<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c),
+                                                               bn, gamma, beta, relu, clip, q, amax, cx->d_err);
+  count_launch(1);
+  return cuda_check("k_bn_act_quant");
+}
+
+int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+               const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
+               const float* res_gamma, const float* res_beta, float* y) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !bn || !gamma || !beta || !y || (res_z && (!res_bn || !res_gamma || !res_beta)))
+    return set_error(I8T_EINVAL, "bn_act: bad arguments");
+  k_bn_act<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c), bn,
+                                                         gamma, beta, relu, res, res_z, res_bn, res_gamma, res_beta, y);
+  count_launch(1);
+  return cuda_check("k_bn_act");
+}
+
+int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,
+                      const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* grad_gamma,
+                      float* grad_beta) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !g || !bn || !gamma || !beta || !grad_gamma || !grad_beta || mask_mode < 0 || mask_mode > 2 ||
+      (mask_mode == 2 && !mask_y))
+    return set_error(I8T_EINVAL, "bn_bwd_reduce: bad arguments");
+  ColArgs a{};
+  a.z = z; a.g = g; a.mask_y = mask_y; a.gamma = gamma; a.beta = beta; a.bn = bn;
+  a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = mask_mode;
+  a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
+  return colsum(cx, a, 1);
+}
+
+int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
+                     const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !g || !bn || !gz || (mask_mode == 2 && !mask_y)) return set_error(I8T_EINVAL, "bn_bwd_apply: bad arguments");
+  BnBwdSrc src{g, z, mask_y, bn, gamma, beta, static_cast<uint32_t>(c), mask_mode};
+  k_bn_bwd_apply<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(src, static_cast<uint32_t>(m * c), gz);
+  count_launch(1);
+  return cuda_check("k_bn_bwd_apply");
+}
+
+int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const float* z, int64_t n_img, int64_t c,
+                             int64_t hw, const double* bn, const float* gamma, const float* beta, int mask_mode,
+                             const float* mask_y, int lr_scaling_enabled, double alpha, double beta_, int form,
+                             uint32_t* lcg_state, int8_t* q) {
+  Ctx* cx = CTX(ctx);
+  DsgcState* st = reinterpret_cast<DsgcState*>(state);
+  int rc = bn_check(n_img * hw, c, z);
+  if (rc) return rc;
+  if (!cx || !st || !g || !bn || !gamma || !beta || !lcg_state || !q || (mask_mode == 2 && !mask_y))
+    return set_error(I8T_EINVAL, "quantize_gradient_bn: bad arguments");
+  if (lr_scaling_enabled && (!(alpha > 0.0) || !(beta_ > 0.0 && beta_ <= 1.0)))
+    return set_error(I8T_EINVAL, "scale_factor: alpha must be > 0, beta in (0,1]");
+  BnBwdSrc src{g, z, mask_y, bn, gamma, beta, static_cast<uint32_t>(c), mask_mode};
+  QgFin fin{1 | (lr_scaling_enabled ? 2 : 0), alpha, beta_, form, 0u};
+  return launch_quant_grad_src(cx, st, nullptr, src, n_img, c, hw, true, lcg_state, q, fin);
+}
+
+int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y, int64_t n, float* out) {
+  Ctx* cx = CTX(ctx);
+  if (!cx || !a || !g || !y || !out || n % 4 != 0) return set_error(I8T_EINVAL, "add_masked: bad arguments");
+  if (!n) return I8T_OK;
+  int b = static_cast<int>((n / 4 + 255) / 256);
+  if (b > 148 * 8) b = 148 * 8;
+  k_add_masked<<<b, 256, 0, cx->stream>>>(a, g, y, static_cast<uint32_t>(n / 4), out);
+  count_launch(1);
+  return cuda_check("k_add_masked");
+}
+
+}  // extern "C"

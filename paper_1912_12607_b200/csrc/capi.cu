@@ -172,6 +172,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_totals) cudaFree(c->d_totals);
   if (c->d_wgrad) cudaFree(c->d_wgrad);
   if (c->d_ticket) cudaFree(c->d_ticket);
+  if (c->d_tickets) cudaFree(c->d_tickets);
   delete c;
   return I8T_OK;
 }

@@ -22,129 +22,9 @@
 
 #include "internal.cuh"
 #include "qcore.cuh"
+#include "qgrad.cuh"
 
 namespace i8t_dev {
-
-// totals layout of K3 (QG_NV doubles): max|g|, nonfinite, sum g^2, sum g*gn,
-// sum gn^2, sum (g-gs)^2, sum gs^2, 0.
-constexpr int QG_NV = 8;
-
-struct QgFin {
-  int mode;  // bit0: d_c from the sums (non-search), bit1: lr scaling, bit2: plain quantize (no DSGC state)
-  double alpha, beta;
-  int form;
-  uint32_t advance;  // LCG draws consumed by the whole (global) tensor
-};
-
-// Tail of quantize_gradient (layers.cpp:32-58) from global totals.
-__device__ void fin_quant_grad(DsgcState* st, const double* tot, const QgFin& f, uint32_t* lcg_state, int* err) {
-  const float m = static_cast<float>(tot[0]);
-  const bool nonfinite = tot[1] > 0.0;
-  if (f.mode & 4) {  // plain stochastic quantize (quantize.cpp:33-43): any non-finite throws
-    if (nonfinite) atomicOr(err, ERR_NONFINITE);
-    *lcg_state = apply(lcg_jump_map(f.advance), *lcg_state);
-    return;
-  }
-  if (nonfinite && m != 0.0f) atomicOr(err, ERR_NONFINITE);
-  if (f.mode & 1) st->v.last_dc = (m == 0.0f) ? 0.0 : cosine_from(tot[3], tot[2], tot[4]);
-  const double dc = st->v.last_dc;
-  st->v.lr_scale = (f.mode & 2) ? phi_of(fmin(fmax(dc, 0.0), 2.0), f.alpha, f.beta, f.form) : 1.0;
-  st->v.max_abs = m;
-  if (m == 0.0f || !(st->v.clip > 0.0f)) {  // zero-gradient skip: no draws (layers.cpp:40-47)
-    st->v.clip_q = 1.0f;
-    st->v.scale = scale_of(1.0f);
-    st->v.eps_norm = 0.0;
-    st->v.ghat_sqnorm = 0.0;
-    st->v.flags = (nonfinite ? 1u : 0u) | 2u;
-  } else {
-    st->v.clip_q = st->v.clip;
-    st->v.scale = scale_of(st->v.clip);
-    st->v.eps_norm = sqrt(tot[5]);
-    st->v.ghat_sqnorm = tot[6];
-    st->v.flags = nonfinite ? 1u : 0u;
-    *lcg_state = apply(lcg_jump_map(f.advance), *lcg_state);
-  }
-}
-
-// K3.  NHWC g [N*HW][C] (C % 4 == 0) or FLAT (row-major order = draw order).
-// gridDim.x*blockDim.x*4 is a multiple of C so each thread keeps its channel quad.
-template <bool FLAT, bool DC_SUMS, bool FUSED>
-__global__ void __launch_bounds__(RED_THREADS) k_quant_grad(const float* __restrict__ g, uint32_t numel, uint32_t C,
-                                                            uint32_t HW, uint32_t draw_offset, Affine step_iter,
-                                                            Affine step_elem, Affine step_wrap, uint32_t dpix,
-                                                            const float* clip_override, DsgcState* st,
-                                                            uint32_t* lcg_state, int8_t* __restrict__ q,
-                                                            double* partials, double* totals, unsigned* ticket, QgFin fin,
-                                                            int* err) {
-  float clip = clip_override ? *clip_override : st->v.clip;
-  if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
-  const float s = scale_of(clip), inv_s = 1.0f / s;
-  const uint32_t X0 = *lcg_state;
-  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
-  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
-  double acc[QG_NV] = {0, 0, 0, 0, 0, 0, 0, 0};
-  float m = 0.0f;
-  if (e < numel) {
-    uint32_t X, hw = 0;
-    if (FLAT) {
-      X = apply(lcg_jump_map(static_cast<uint64_t>(e) + draw_offset + 1u), X0);
-    } else {
-      const uint32_t pix = e / C, c = e - pix * C;
-      const uint32_t n = pix / HW;
-      hw = pix - n * HW;
-      X = apply(lcg_jump_map(static_cast<uint64_t>((n * C + c) * HW + hw) + draw_offset + 1u), X0);
-    }
-    const float4* g4 = reinterpret_cast<const float4*>(g);
-    float4 v4 = __ldg(g4 + e / 4);
-    while (true) {
-      const uint32_t e_next = e + T4;
-      float4 nxt;
-      if (e_next < numel) nxt = __ldg(g4 + e_next / 4);  // software prefetch of the next float4
-      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-      signed char qq[4];
-      uint32_t Xj = X;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j) Xj = apply(step_elem, Xj);
-        const float v = vv[j];
-        if (!isfinite(v)) acc[1] += 1.0;
-        m = fmaxf(m, fabsf(v));
-        const int qs = quant_stoch(v, clip, s, inv_s, Xj);
-        qq[j] = static_cast<signed char>(qs);
-        const float gs = __fmul_rn(static_cast<float>(qs), s);
-        const double vd = v, gsd = gs;
-        const double d = vd - gsd;
-        acc[5] = fma(d, d, acc[5]);
-        acc[6] = fma(gsd, gsd, acc[6]);
-        if (DC_SUMS) {
-          const double gn = __fmul_rn(static_cast<float>(quant_nearest(v, clip, s, inv_s)), s);
-          acc[2] = fma(vd, vd, acc[2]);
-          acc[3] = fma(vd, gn, acc[3]);
-          acc[4] = fma(gn, gn, acc[4]);
-        }
-      }
-      reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
-      if (e_next >= numel) break;
-      e = e_next;
-      v4 = nxt;
-      X = apply(step_iter, X);
-      if (!FLAT) {
-        hw += dpix;
-        while (hw >= HW) {
-          hw -= HW;
-          X = apply(step_wrap, X);
-        }
-      }
-    }
-  }
-  acc[0] = m;
-  if (grid_reduce<QG_NV>(acc, 1u, partials, totals, ticket) && FUSED && threadIdx.x == 0)
-    fin_quant_grad(st, totals, fin, lcg_state, err);
-}
-
-__global__ void k_fin_quant_grad(DsgcState* st, const double* totals, QgFin fin, uint32_t* lcg_state, int* err) {
-  if (threadIdx.x == 0) fin_quant_grad(st, totals, fin, lcg_state, err);
-}
 
 // K4.  totals: [0] max|g|, [1] nonfinite, [2] sum g^2, [3+2j] sum g*gh_j, [4+2j] sum gh_j^2.
 template <int NC>
@@ -375,15 +255,6 @@ __global__ void k_fin_cosine(const double* tot, double* dot_out, double* cos_out
 }
 
 // ---------------------------------------------------------------- host side
-static int nblocks(int64_t n, int64_t multiple = 1) {
-  int64_t b = (n + RED_THREADS * 8 - 1) / (RED_THREADS * 8);
-  if (b < 1) b = 1;
-  if (b > 592) b = 592;
-  b = (b + multiple - 1) / multiple * multiple;
-  return static_cast<int>(b);
-}
-
-static int gcd_i(int64_t a, int64_t b) { return b == 0 ? static_cast<int>(a) : gcd_i(b, a % b); }
 
 // Ensure partials for nblk blocks x nv values, and run kernel K.
 static int stats_pass0(Ctx* c, const float* x, int64_t n) {
@@ -419,14 +290,6 @@ static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, cons
   return cuda_check("k_dc_stats");
 }
 
-// Global totals for data parallelism: totals[0] MAX, totals[1..nv) SUM.
-static int allreduce_totals(Ctx* c, int nv) {
-  if (!c->allreduce) return I8T_OK;
-  int rc = ctx_allreduce(c, c->d_totals, 1, 1);
-  if (rc) return rc;
-  return ctx_allreduce(c, c->d_totals + 1, nv - 1, 0);
-}
-
 static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, int rounds, float prev_clip,
                       int prev_from_state) {
   int rc = stats_pass0(c, g, n);
@@ -454,55 +317,10 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
   return I8T_OK;
 }
 
-// K3 launcher.
 static int launch_quant_grad(Ctx* c, DsgcState* st, const float* clip_override, const float* g, int64_t n_img,
                              int64_t C, int64_t HW, bool dc_sums, uint32_t* lcg, int8_t* q, QgFin fin) {
-  const int64_t numel = n_img * C * HW;
-  const bool flat = (C == 1);
-  if (numel % 4 != 0 || (!flat && C % 4 != 0))
-    return set_error(I8T_EUNSUPPORTED, "quantize_gradient: needs C % 4 == 0 (or flat) and numel % 4 == 0");
-  if (numel >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "quantize_gradient: tensor >= 2^31 elements");
-  // grid: threads*4 must be a multiple of C (each thread keeps its channel quad)
-  const int64_t mult = flat ? 1 : C / gcd_i(C, RED_THREADS * 4);
-  int nb = nblocks(numel, mult);
-  double* p = ensure_partials(c, static_cast<size_t>(nb) * QG_NV);
-  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
-  const uint32_t T4 = static_cast<uint32_t>(nb) * RED_THREADS * 4u;
-  const uint32_t draw_offset = static_cast<uint32_t>(static_cast<uint64_t>(c->rank) * static_cast<uint64_t>(numel));
-  Affine step_iter, step_elem, step_wrap{1u, 0u};
-  uint32_t dpix = 0;
-  if (flat) {
-    step_iter = lcg_jump_map(T4);
-    step_elem = lcg_jump_map(1);
-  } else {
-    dpix = T4 / static_cast<uint32_t>(C);
-    step_iter = lcg_jump_map(dpix);
-    step_elem = lcg_jump_map(static_cast<uint64_t>(HW));
-    step_wrap = lcg_jump_map(static_cast<uint64_t>(C - 1) * static_cast<uint64_t>(HW));
-  }
-  fin.advance = static_cast<uint32_t>(static_cast<uint64_t>(c->world) * static_cast<uint64_t>(numel));
-  const bool fused = (c->allreduce == nullptr);
-  const uint32_t un = static_cast<uint32_t>(numel), uc = static_cast<uint32_t>(flat ? 1 : C),
-                 uhw = static_cast<uint32_t>(flat ? numel : HW);
-#define LAUNCH(F, D, U)                                                                                               \
-  k_quant_grad<F, D, U><<<nb, RED_THREADS, 0, c->stream>>>(g, un, uc, uhw, draw_offset, step_iter, step_elem,       \
-                                                           step_wrap, dpix, clip_override, st, lcg, q, p,           \
-                                                           c->d_totals, c->d_ticket, fin, c->d_err)
-  if (flat) {
-    if (dc_sums) { if (fused) LAUNCH(true, true, true); else LAUNCH(true, true, false); }
-    else { if (fused) LAUNCH(true, false, true); else LAUNCH(true, false, false); }
-  } else {
-    if (dc_sums) { if (fused) LAUNCH(false, true, true); else LAUNCH(false, true, false); }
-    else { if (fused) LAUNCH(false, false, true); else LAUNCH(false, false, false); }
-  }
-#undef LAUNCH
-  count_launch(1);
-  int rc = cuda_check("k_quant_grad");
-  if (rc || fused) return rc;
-  if ((rc = allreduce_totals(c, QG_NV))) return rc;
-  k_fin_quant_grad<<<1, 32, 0, c->stream>>>(st, c->d_totals, fin, lcg, c->d_err);
-  count_launch(1);
-  return cuda_check("k_fin_quant_grad");
+  return launch_quant_grad_src(c, st, clip_override, PlainSrc{reinterpret_cast<const float4*>(g)}, n_img, C, HW,
+                               dc_sums, lcg, q, fin);
 }
 
 }  // namespace i8t_dev

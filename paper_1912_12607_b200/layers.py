@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -62,6 +63,106 @@ class ParamRef:
     name: str
     value: torch.Tensor
     grad: torch.Tensor | None
+
+
+# ------------------------------------------------------------------ lazy values
+# BN + ReLU are fused into the INT8 path's HBM passes (csrc/bnfuse.cu): a BN
+# forward returns LazyAct (act(bn(z)) not materialised), which the next
+# Conv2d quantises in one pass; a BN backward returns BnGrad, which the
+# previous Conv2d feeds straight into the stochastic gradient quantiser.  Any
+# other consumer calls dense() / dense_grad() and gets a plain tensor.
+# "fused" (default): lazy values as above; "eager": the same kernels with every
+# value materialised at once (bit-identical results, used to test the
+# plumbing); "torch": torch's fp32 batch norm.
+BN_IMPL = os.environ.get("I8T_BN", "fused")
+
+
+class LazyAct:
+    """act(bn(z)) with z the NHWC conv output and `bn` its BatchNorm2d layer."""
+
+    def __init__(self, z, bn, relu=False):
+        self.z, self.bn, self.relu = z, bn, relu
+
+    @property
+    def shape(self):
+        return self.z.shape
+
+    @property
+    def device(self):
+        return self.z.device
+
+    def numel(self):
+        return self.z.numel()
+
+    def materialize(self, res=None):
+        n, h, w, c = self.z.shape
+        y = torch.empty_like(self.z)
+        r, rz, rbn = (None, None, None)
+        if isinstance(res, LazyAct):
+            rz, rbn = res.z, res.bn
+        elif res is not None:
+            r = res
+        call("i8t_bn_act", ops.ctx(), ops._p(self.z), n * h * w, c, ops._p(self.bn.stats), ops._p(self.bn.gamma),
+             ops._p(self.bn.beta), int(self.relu), ops._p(r), ops._p(rz), ops._p(rbn.stats) if rbn else None,
+             ops._p(rbn.gamma) if rbn else None, ops._p(rbn.beta) if rbn else None, ops._p(y))
+        return y
+
+
+class MaskedGrad:
+    """g * mask: mode 1 = ReLU mask of act(bn(z)) of `bn`, mode 2 = (mask_y > 0)."""
+
+    def __init__(self, g, mode, bn=None, mask_y=None):
+        self.g, self.mode, self.bn, self.mask_y = g, mode, bn, mask_y
+
+    @property
+    def shape(self):
+        return self.g.shape
+
+    @property
+    def device(self):
+        return self.g.device
+
+    def numel(self):
+        return self.g.numel()
+
+    def materialize(self):
+        if self.mode == 2:
+            return torch.where(self.mask_y > 0, self.g, torch.zeros((), device=self.g.device))
+        y = LazyAct(self.bn._z, self.bn, relu=True).materialize()
+        return torch.where(y > 0, self.g, torch.zeros((), device=self.g.device))
+
+
+class BnGrad:
+    """BN backward of (g, mask) not yet materialised (sums already reduced)."""
+
+    def __init__(self, g, bn, mode, mask_y):
+        self.g, self.bn, self.mode, self.mask_y = g, bn, mode, mask_y
+
+    @property
+    def shape(self):
+        return self.g.shape
+
+    @property
+    def device(self):
+        return self.g.device
+
+    def numel(self):
+        return self.g.numel()
+
+    def materialize(self):
+        n, h, w, c = self.g.shape
+        out = torch.empty_like(self.g)
+        call("i8t_bn_bwd_apply", ops.ctx(), ops._p(self.g), ops._p(self.bn._z), n * h * w, c, ops._p(self.bn.stats),
+             ops._p(self.bn.gamma), ops._p(self.bn.beta), self.mode, ops._p(self.mask_y), ops._p(out))
+        return out
+
+
+def dense(x):
+    return x.materialize() if isinstance(x, LazyAct) else x
+
+
+def dense_grad(g):
+    return g.materialize() if isinstance(g, (MaskedGrad, BnGrad)) else g
 
 
 # ------------------------------------------------------------------ state arena
@@ -244,6 +345,10 @@ class Conv2d(Layer):
         use_int8 = self.quantize_enabled and ctx.mode == Mode.INT8
         h = ops.ctx()
         qs = self.qs
+        fuse_in = (isinstance(x, LazyAct) and use_int8 and qs.clip_a_set and not self.depthwise
+                   and self.c_pad == self.in_c)
+        if not fuse_in:
+            x = dense(x)
         if not use_int8:
             if ctx.track_amax:
                 call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.tmp))
@@ -259,7 +364,7 @@ class Conv2d(Layer):
             call("i8t_max_abs", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w))
             qs.clip_w.clamp_(min=1e-12)
             qs.clip_w_set = True
-        if not qs.clip_a_set:
+        if not qs.clip_a_set and not fuse_in:
             call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.clip_a))
             qs.clip_a.clamp_(min=1e-12)
             qs.clip_a_set = True
@@ -278,11 +383,18 @@ class Conv2d(Layer):
                  self.ld_wt, None)
         # activations -> NHWC int8 (channel stride c_pad), pending_amax fused (layers.cpp:101)
         n, hh, ww, c = x.shape
-        qa = torch.empty((n, hh, ww, self.c_pad), dtype=torch.int8, device=x.device)
-        call("i8t_quantize_nearest_rows", h, ops._p(x), n * hh * ww, c, ops._p(qs.clip_a), ops._p(qa), self.c_pad,
-             ops._p(qs.pending_amax) if ctx.track_amax else None, 1)
+        dev = x.z.device if fuse_in else x.device
+        qa = torch.empty((n, hh, ww, self.c_pad), dtype=torch.int8, device=dev)
+        if fuse_in:  # BN-apply + ReLU + nearest quantise + amax in one pass over z
+            bn = x.bn
+            call("i8t_bn_act_quant", h, ops._p(x.z), n * hh * ww, c, ops._p(bn.stats), ops._p(bn.gamma),
+                 ops._p(bn.beta), int(x.relu), ops._p(qs.clip_a), ops._p(qa),
+                 ops._p(qs.pending_amax) if ctx.track_amax else None)
+        else:
+            call("i8t_quantize_nearest_rows", h, ops._p(x), n * hh * ww, c, ops._p(qs.clip_a), ops._p(qa),
+                 self.c_pad, ops._p(qs.pending_amax) if ctx.track_amax else None, 1)
         self._qa = qa
-        z = torch.empty((n, p, q, self.out_c), dtype=torch.float32, device=x.device)
+        z = torch.empty((n, p, q, self.out_c), dtype=torch.float32, device=dev)
         if self.depthwise:
             call("i8t_conv_dw_fwd", h, C.byref(g), ops._p(qa), self.c_pad, ops._p(self._qw), ops._p(qs.clip_a),
                  ops._p(qs.clip_w), ops._p(z), None)
@@ -295,6 +407,10 @@ class Conv2d(Layer):
     def backward(self, gz, ctx: BackwardCtx):
         g = self._geom
         use_int8 = self.quantize_enabled and ctx.mode == Mode.INT8
+        fuse_g = (isinstance(gz, BnGrad) and use_int8 and ctx.clip_search_enabled
+                  and not self.qs.dsgc.due(ctx.iter) and gz.shape[-1] % 4 == 0)
+        if not fuse_g:
+            gz = dense_grad(gz)
         if not use_int8:
             xc = self._x.permute(0, 3, 1, 2)
             gc = gz.permute(0, 3, 1, 2)
@@ -305,17 +421,20 @@ class Conv2d(Layer):
                                                                (self.ph, self.pw), groups=groups))
             return gi.permute(0, 2, 3, 1).contiguous()
         h = ops.ctx()
-        gz = gz.contiguous()
-        n, p, q, k = gz.shape
-        qg = quantize_gradient_layer(self.qs, gz, ctx)
+        if fuse_g:  # BN backward computed on the fly inside the stochastic quantiser
+            qg = quantize_gradient_bn_layer(self.qs, gz, ctx)
+        else:
+            gz = gz.contiguous()
+            qg = quantize_gradient_layer(self.qs, gz, ctx)
         clip_g = self.qs.dsgc.clip_q_ptr()
-        ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gz.device) if self.need_input_grad else None
+        gdev = qg.device
+        ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gdev) if self.need_input_grad else None
         if self.depthwise:
             if self.need_input_grad:
                 call("i8t_conv_dw_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qw), ops._p(clip_g),
                      ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
-                self.wgrad_acc = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int64, device=gz.device)
+                self.wgrad_acc = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int64, device=gdev)
             call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
                  ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
         else:
@@ -324,7 +443,7 @@ class Conv2d(Layer):
                      ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
                 self.wgrad_acc = torch.empty((self.kh * self.kw * self.c_pad, self.out_c), dtype=torch.int64,
-                                             device=gz.device)
+                                             device=gdev)
             if ctx.wgrad_allreduce is None:
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
                      ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight), 1)
@@ -363,6 +482,20 @@ def quantize_gradient_layer(qs: QuantState, gz: torch.Tensor, ctx: BackwardCtx) 
     return qg
 
 
+def quantize_gradient_bn_layer(qs: QuantState, gz: "BnGrad", ctx: BackwardCtx) -> torch.Tensor:
+    """quantize_gradient (layers.cpp:19-59) of a pending BN backward value on a
+    non-search iteration: one pass reads (g, z) and writes the int8 gradient."""
+    n, p, q, k = gz.shape
+    st = qs.dsgc
+    st.period = ctx.clip_period
+    qg = torch.empty(gz.shape, dtype=torch.int8, device=gz.g.device)
+    bn = gz.bn
+    call("i8t_quantize_gradient_bn", ops.ctx(), st.ptr, ops._p(gz.g), ops._p(bn._z), n, k, p * q, ops._p(bn.stats),
+         ops._p(bn.gamma), ops._p(bn.beta), gz.mode, ops._p(gz.mask_y), int(ctx.lr_scaling_enabled),
+         C.c_double(ctx.alpha), C.c_double(ctx.beta), ops.FORMS[ctx.form], ops._p(ctx.grad_stream), ops._p(qg))
+    return qg
+
+
 class Dense(Layer):
     """INT8 fully connected layer (layers.hpp:117-139, layers.cpp:138-225):
     a 1x1 convolution over [N, 1, 1, in]; bias added in float; bias gradient
@@ -394,12 +527,14 @@ class Dense(Layer):
         return [(self.conv, "weight", "grad_weight"), (self, "bias", "grad_bias")]
 
     def forward(self, x, ctx):
+        x = dense(x)
         self._in_shape = x.shape
         n = x.shape[0]
         z = self.conv.forward(x.reshape(n, 1, 1, self.in_f), ctx).reshape(n, self.out_f)
         return z + self.bias
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
         n = g.shape[0]
         g = g.contiguous()
         gi = self.conv.backward(g.reshape(n, 1, 1, self.out_f), ctx)
@@ -415,10 +550,14 @@ class Dense(Layer):
 
 
 class BatchNorm2d(Layer):
-    """FP32 batch norm (layers.cpp:230-323), via the library batch-norm kernels."""
+    """FP32 batch norm (layers.cpp:230-323).  Training: statistics and apply
+    run in csrc/bnfuse.cu with the reference's double arithmetic; the forward
+    returns a LazyAct and the backward a BnGrad so the neighbouring INT8
+    convolutions fuse them into their quantisation passes."""
     kind = "bn"
 
     def __init__(self, c, momentum=0.1, eps=1e-5, device="cuda"):
+        self.c = c
         self.gamma = torch.ones(c, device=device)
         self.beta = torch.zeros(c, device=device)
         self.grad_gamma = torch.zeros_like(self.gamma)
@@ -426,6 +565,8 @@ class BatchNorm2d(Layer):
         self.running_mean = torch.zeros(c, device=device)
         self.running_var = torch.ones(c, device=device)
         self.momentum, self.eps = momentum, eps
+        self.stats = torch.zeros(5 * c, dtype=torch.float64, device=device)  # mean, invstd, s1/m, s2/m, gamma*invstd
+        self._z = None
 
     def params(self):
         return [ParamRef("gamma", self.gamma, self.grad_gamma), ParamRef("beta", self.beta, self.grad_beta)]
@@ -436,18 +577,45 @@ class BatchNorm2d(Layer):
     def buffers(self):
         return [ParamRef("running_mean", self.running_mean, None), ParamRef("running_var", self.running_var, None)]
 
+    def _fusable(self, x):
+        return BN_IMPL != "torch" and isinstance(x, torch.Tensor) and self.c % 4 == 0 and x.is_contiguous()
+
     def forward(self, x, ctx):
-        xc = x.permute(0, 3, 1, 2)
+        x = dense(x)
         if not ctx.training:
+            xc = x.permute(0, 3, 1, 2)
             y = F.batch_norm(xc, self.running_mean, self.running_var, self.gamma, self.beta, False, 0.0, self.eps)
             return y.permute(0, 2, 3, 1).contiguous()
+        if self._fusable(x):
+            n, h, w, c = x.shape
+            call("i8t_bn_fwd_stats", ops.ctx(), ops._p(x), n * h * w, c, C.c_double(self.momentum),
+                 C.c_double(self.eps), ops._p(self.stats), ops._p(self.running_mean), ops._p(self.running_var))
+            self._z = x
+            self._torch = False
+            return LazyAct(x, self).materialize() if BN_IMPL == "eager" else LazyAct(x, self)
+        xc = x.permute(0, 3, 1, 2)
         y, self._mean, self._invstd = torch.native_batch_norm(xc, self.gamma, self.beta, self.running_mean,
                                                               self.running_var, True, self.momentum, self.eps)
         self._x = xc
+        self._torch = True
         return y.permute(0, 2, 3, 1).contiguous()
 
     def backward(self, g, ctx):
-        gc = g.contiguous().permute(0, 3, 1, 2)
+        if not self._torch:
+            mode, mask_y = 0, None
+            if isinstance(g, MaskedGrad):
+                if g.mode == 1 and g.bn is not self:
+                    g = g.materialize()
+                else:
+                    mode, mask_y, g = g.mode, g.mask_y, g.g
+            g = dense_grad(g).contiguous()
+            n, h, w, c = g.shape
+            call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(self._z), n * h * w, c, ops._p(self.stats),
+                 ops._p(self.gamma), ops._p(self.beta), mode, ops._p(mask_y), ops._p(self.grad_gamma),
+                 ops._p(self.grad_beta))
+            gb = BnGrad(g, self, mode, mask_y)
+            return gb.materialize() if BN_IMPL == "eager" else gb
+        gc = dense_grad(g).contiguous().permute(0, 3, 1, 2)
         gi, gg, gb = torch.ops.aten.native_batch_norm_backward(gc, self._x, self.gamma, self.running_mean,
                                                                self.running_var, self._mean, self._invstd, True,
                                                                self.eps, [True, True, True])
@@ -461,12 +629,19 @@ class ReLU(Layer):
     kind = "relu"
 
     def forward(self, x, ctx):
-        y = torch.relu(x)
+        if isinstance(x, LazyAct) and not x.relu:
+            self._bn = x.bn  # mask recomputed from bn(z) in the backward (mask mode 1)
+            return LazyAct(x.z, x.bn, relu=True)
+        self._bn = None
+        y = torch.relu(dense(x))
         if ctx.training:
             self._y = y
         return y
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
+        if self._bn is not None:
+            return MaskedGrad(g, 1, bn=self._bn)
         out = torch.where(self._y > 0, g, torch.zeros((), device=g.device, dtype=g.dtype))
         self._y = None
         return out
@@ -480,6 +655,7 @@ class MaxPool2d(Layer):
         self.k, self.s, self.p = k, s, p
 
     def forward(self, x, ctx):
+        x = dense(x)
         xc = x.permute(0, 3, 1, 2)
         y, self._idx = torch.ops.aten.max_pool2d_with_indices(xc, [self.k, self.k], [self.s, self.s],
                                                               [self.p, self.p])
@@ -487,6 +663,7 @@ class MaxPool2d(Layer):
         return y.permute(0, 2, 3, 1).contiguous()
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
         gi = torch.ops.aten.max_pool2d_with_indices_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k],
                                                              [self.s, self.s], [self.p, self.p], [1, 1], False,
                                                              self._idx)
@@ -502,12 +679,14 @@ class AvgPool2d(Layer):
         self.k, self.s, self.p = k, s, p
 
     def forward(self, x, ctx):
+        x = dense(x)
         xc = x.permute(0, 3, 1, 2)
         self._xc = xc
         y = F.avg_pool2d(xc, self.k, self.s, self.p)
         return y.permute(0, 2, 3, 1).contiguous()
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
         gi = torch.ops.aten.avg_pool2d_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k], [self.s, self.s],
                                                 [self.p, self.p], False, True, None)
         self._xc = None
@@ -524,15 +703,16 @@ class Concat(Layer):
         self.branches = list(branches)
 
     def forward(self, x, ctx):
-        outs = [b.forward(x, ctx) for b in self.branches]
+        x = dense(x)
+        outs = [dense(b.forward(x, ctx)) for b in self.branches]
         self._sizes = [o.shape[-1] for o in outs]
         return torch.cat(outs, dim=-1)
 
     def backward(self, g, ctx):
-        parts = torch.split(g, self._sizes, dim=-1)
+        parts = torch.split(dense_grad(g), self._sizes, dim=-1)
         gi = None
         for b, gp in zip(self.branches, parts):
-            r = b.backward(gp.contiguous(), ctx)
+            r = dense_grad(b.backward(gp.contiguous(), ctx))
             gi = r if gi is None else gi + r
         return gi
 
@@ -545,10 +725,12 @@ class GlobalAvgPool(Layer):
     kind = "avgpool"
 
     def forward(self, x, ctx):
+        x = dense(x)
         self._shape = x.shape
         return x.mean(dim=(1, 2))
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
         n, h, w, c = self._shape
         return (g / (h * w)).reshape(n, 1, 1, c).expand(n, h, w, c).contiguous()
 
@@ -588,14 +770,30 @@ class ResidualBlock(Layer):
         self.main, self.shortcut, self.relu = main, shortcut, ReLU()
 
     def forward(self, x, ctx):
+        x = dense(x)
         y = self.main.forward(x, ctx)
         sc = self.shortcut.forward(x, ctx) if self.shortcut else x
-        return self.relu.forward(y + sc, ctx)
+        if isinstance(y, LazyAct) and not y.relu:  # relu(bn3(z3) + shortcut) in one pass
+            out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc)
+            self._y, self._fused = out, True
+            return out
+        self._fused = False
+        return self.relu.forward(dense(y) + dense(sc), ctx)
 
     def backward(self, g, ctx):
+        g = dense_grad(g)
+        if self._fused:
+            gl = MaskedGrad(g, 2, mask_y=self._y)
+            gm = dense_grad(self.main.backward(gl, ctx))
+            if self.shortcut:
+                gs = dense_grad(self.shortcut.backward(gl, ctx))
+                return gm + gs
+            out = torch.empty_like(gm)
+            call("i8t_add_masked", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._y), gm.numel(), ops._p(out))
+            return out
         g = self.relu.backward(g, ctx)
-        gm = self.main.backward(g, ctx)
-        gs = self.shortcut.backward(g, ctx) if self.shortcut else g
+        gm = dense_grad(self.main.backward(g, ctx))
+        gs = dense_grad(self.shortcut.backward(g, ctx)) if self.shortcut else g
         return gm + gs
 
     def visit(self, prefix, fn):
@@ -613,11 +811,15 @@ class InvertedResidual(Layer):
         self.body, self.use_skip = body, use_skip
 
     def forward(self, x, ctx):
+        x = dense(x)
         y = self.body.forward(x, ctx)
-        return y + x if self.use_skip else y
+        if self.use_skip:
+            return y.materialize(res=x) if isinstance(y, LazyAct) else y + x
+        return y
 
     def backward(self, g, ctx):
-        gb = self.body.backward(g, ctx)
+        g = dense_grad(g)
+        gb = dense_grad(self.body.backward(g, ctx))
         return gb + g if self.use_skip else gb
 
     def visit(self, prefix, fn):
