@@ -40,6 +40,9 @@ struct ColArgs {
 };
 
 __device__ __forceinline__ float bn_y(double gm, double xv, double bt) { return static_cast<float>(fma(gm, xv, bt)); }
+// float(gamma*x_hat + beta) > 0 without the conversion: RN32(d) > 0 <=> d > 2^-150
+// (2^-150 itself rounds to +0 under ties-to-even).
+__device__ __forceinline__ bool bn_pos(double gm, double xv, double bt) { return fma(gm, xv, bt) > 0x1.0p-150; }
 
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
@@ -65,33 +68,44 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     }
   }
   if (active) {
+    // U rows per thread per trip: all loads of a trip are issued before any math
+    constexpr int U = 4;
     const uint32_t row_step = gridDim.x * 8 * rpw;
-    for (uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub; r < a.m; r += row_step) {
-      const size_t off = static_cast<size_t>(r) * a.c + ch;
-      const float4 zv = __ldg(reinterpret_cast<const float4*>(a.z + off));
-      const float zz[4] = {zv.x, zv.y, zv.z, zv.w};
-      if (MODE == 0) {
+    uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub;
+    for (; r < a.m; r += U * row_step) {
+      float4 zv[U], gv[U], yv[U];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc0[j] += static_cast<double>(zz[j]);
-          acc1[j] = fma(static_cast<double>(zz[j]), static_cast<double>(zz[j]), acc1[j]);
-        }
-      } else {
-        const float4 gv = __ldg(reinterpret_cast<const float4*>(a.g + off));
-        const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
-        float mk[4] = {1, 1, 1, 1};
-        if (a.mask_mode == 2) {
-          const float4 yv = __ldg(reinterpret_cast<const float4*>(a.mask_y + off));
-          mk[0] = yv.x > 0.0f; mk[1] = yv.y > 0.0f; mk[2] = yv.z > 0.0f; mk[3] = yv.w > 0.0f;
-        }
+      for (int u = 0; u < U; ++u) {
+        const uint32_t ru = r + u * row_step;
+        const size_t off = static_cast<size_t>(ru < a.m ? ru : r) * a.c + ch;
+        zv[u] = __ldg(reinterpret_cast<const float4*>(a.z + off));
+        if (MODE == 1) gv[u] = __ldg(reinterpret_cast<const float4*>(a.g + off));
+        if (MODE == 1 && a.mask_mode == 2) yv[u] = __ldg(reinterpret_cast<const float4*>(a.mask_y + off));
+      }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
-          const float xh = static_cast<float>(xv);
-          if (a.mask_mode == 1) mk[j] = bn_y(gmm[j], xv, bt[j]) > 0.0f;
-          const float gm = mk[j] != 0.0f ? gg[j] : 0.0f;
-          acc0[j] += static_cast<double>(gm);
-          acc1[j] = fma(static_cast<double>(gm), static_cast<double>(xh), acc1[j]);
+      for (int u = 0; u < U; ++u) {
+        if (r + u * row_step >= a.m) break;
+        const float zz[4] = {zv[u].x, zv[u].y, zv[u].z, zv[u].w};
+        if (MODE == 0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double zd = zz[j];
+            acc0[j] += zd;
+            acc1[j] = fma(zd, zd, acc1[j]);
+          }
+        } else {
+          const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+          const float yy[4] = {yv[u].x, yv[u].y, yv[u].z, yv[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
+            bool mk = true;
+            if (a.mask_mode == 1) mk = bn_pos(gmm[j], xv, bt[j]);
+            else if (a.mask_mode == 2) mk = yy[j] > 0.0f;
+            const double gm = mk ? static_cast<double>(gg[j]) : 0.0;
+            acc0[j] += gm;
+            acc1[j] = fma(gm, rn24(xv), acc1[j]);
+          }
         }
       }
     }
@@ -185,19 +199,26 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
   if (e < n) {
     BnQuad k;
     k.load(bn, gamma, beta, c, e % c);
-    for (; e < n; e += T4) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(z + e));
-      const float zz[4] = {v.x, v.y, v.z, v.w};
-      signed char qq[4];
+    for (; e < n; e += 2 * T4) {  // two float4 loads in flight per thread
+      const bool two = e + T4 < n;
+      const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e));
+      const float4 v1 = two ? __ldg(reinterpret_cast<const float4*>(z + e + T4)) : v0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float y = k.y(j, zz[j]);
-        if (relu) y = y > 0.0f ? y : 0.0f;
-        bad |= !isfinite(y);
-        m = fmaxf(m, fabsf(y));
-        qq[j] = static_cast<signed char>(quant_nearest(y, clip, s, inv_s));
+      for (int h = 0; h < 2; ++h) {
+        if (h && !two) break;
+        const float4 v = h ? v1 : v0;
+        const float zz[4] = {v.x, v.y, v.z, v.w};
+        signed char qq[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float y = k.y(j, zz[j]);
+          if (relu) y = y > 0.0f ? y : 0.0f;
+          bad |= !isfinite(y);
+          m = fmaxf(m, fabsf(y));
+          qq[j] = static_cast<signed char>(quant_nearest(y, clip, s, inv_s));
+        }
+        reinterpret_cast<char4*>(q)[(e + h * T4) / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
       }
-      reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
     }
   }
   if (bad) atomicOr(err, ERR_NONFINITE);
@@ -227,29 +248,42 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
   BnQuad k, kr;
   k.load(bn, gamma, beta, c, e % c);
   if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
-  for (; e < n; e += T4) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(z + e));
-    const float zz[4] = {v.x, v.y, v.z, v.w};
-    float rr[4] = {0, 0, 0, 0};
-    if (res) {
-      const float4 r = __ldg(reinterpret_cast<const float4*>(res + e));
-      rr[0] = r.x; rr[1] = r.y; rr[2] = r.z; rr[3] = r.w;
-    } else if (res_z) {
-      const float4 r = __ldg(reinterpret_cast<const float4*>(res_z + e));
-      rr[0] = kr.y(0, r.x); rr[1] = kr.y(1, r.y); rr[2] = kr.y(2, r.z); rr[3] = kr.y(3, r.w);
+  for (; e < n; e += 2 * T4) {  // two float4 loads (per input) in flight per thread
+    const bool two = e + T4 < n;
+    const uint32_t e1 = two ? e + T4 : e;
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e)), v1 = __ldg(reinterpret_cast<const float4*>(z + e1));
+    float4 r0 = make_float4(0, 0, 0, 0), r1 = r0;
+    if (res || res_z) {
+      const float* rp = res ? res : res_z;
+      r0 = __ldg(reinterpret_cast<const float4*>(rp + e));
+      r1 = __ldg(reinterpret_cast<const float4*>(rp + e1));
     }
-    float o[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float t = k.y(j, zz[j]);
-      if (res || res_z) t = __fadd_rn(t, rr[j]);
-      o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+    for (int h = 0; h < 2; ++h) {
+      if (h && !two) break;
+      const float4 v = h ? v1 : v0, r = h ? r1 : r0;
+      const float zz[4] = {v.x, v.y, v.z, v.w};
+      float rr[4] = {r.x, r.y, r.z, r.w};
+      if (res_z) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
+      }
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float t = k.y(j, zz[j]);
+        if (res || res_z) t = __fadd_rn(t, rr[j]);
+        o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+      }
+      reinterpret_cast<float4*>(y)[(e + h * T4) / 4] = make_float4(o[0], o[1], o[2], o[3]);
     }
-    reinterpret_cast<float4*>(y)[e / 4] = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
-// Backward value source: g_in = float(gamma*invstd * (g_m - s1/m - x_hat*(s2/m))).
+// Backward value source: g_in = float(gamma*invstd * (g_m - s1/m - x_hat*(s2/m))),
+// g_m = g masked by the ReLU that followed the BN (MASK 1: relu(bn(z)) > 0
+// recomputed from z; MASK 2: a stored output y > 0; MASK 0: none).
+template <int MASK>
 struct BnBwdSrc {
   const float* g;
   const float* z;
@@ -258,8 +292,10 @@ struct BnBwdSrc {
   const float* gamma;
   const float* beta;
   uint32_t c;
-  int mask_mode;
   double mean[4], invstd[4], gm[4], bt[4], a[4], b[4], k[4];
+  struct Raw {
+    float4 g, z, y;
+  };
   __device__ __forceinline__ void init(uint32_t c0) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -268,33 +304,38 @@ struct BnBwdSrc {
       a[j] = bn[2 * c + c0 + j];
       b[j] = bn[3 * c + c0 + j];
       k[j] = bn[4 * c + c0 + j];
-      gm[j] = gamma[c0 + j];
-      bt[j] = beta[c0 + j];
+      if (MASK == 1) {
+        gm[j] = gamma[c0 + j];
+        bt[j] = beta[c0 + j];
+      }
     }
   }
-  __device__ __forceinline__ float4 load(uint32_t e4) const {
-    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + e4);
-    const float4 zv = __ldg(reinterpret_cast<const float4*>(z) + e4);
-    const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, zz[4] = {zv.x, zv.y, zv.z, zv.w};
-    float mk[4] = {1, 1, 1, 1};
-    if (mask_mode == 2) {
-      const float4 yv = __ldg(reinterpret_cast<const float4*>(mask_y) + e4);
-      mk[0] = yv.x > 0.0f; mk[1] = yv.y > 0.0f; mk[2] = yv.z > 0.0f; mk[3] = yv.w > 0.0f;
-    }
+  __device__ __forceinline__ Raw fetch(uint32_t e4) const {
+    Raw r;
+    r.g = __ldg(reinterpret_cast<const float4*>(g) + e4);
+    r.z = __ldg(reinterpret_cast<const float4*>(z) + e4);
+    if (MASK == 2) r.y = __ldg(reinterpret_cast<const float4*>(mask_y) + e4);
+    return r;
+  }
+  __device__ __forceinline__ float4 value(const Raw& r) const {
+    const float gg[4] = {r.g.x, r.g.y, r.g.z, r.g.w}, zz[4] = {r.z.x, r.z.y, r.z.z, r.z.w};
     float o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
-      const float xh = static_cast<float>(xv);
-      if (mask_mode == 1) mk[j] = bn_y(gm[j], xv, bt[j]) > 0.0f;
-      const float gmk = mk[j] != 0.0f ? gg[j] : 0.0f;
-      o[j] = static_cast<float>(k[j] * (static_cast<double>(gmk) - a[j] - static_cast<double>(xh) * b[j]));
+      bool mk = true;
+      if (MASK == 1) mk = bn_pos(gm[j], xv, bt[j]);
+      if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
+      const double gd = mk ? static_cast<double>(gg[j]) : 0.0;
+      o[j] = static_cast<float>(k[j] * (gd - a[j] - rn24(xv) * b[j]));
     }
     return make_float4(o[0], o[1], o[2], o[3]);
   }
+  __device__ __forceinline__ float4 load(uint32_t e4) const { return value(fetch(e4)); }
 };
 
-__global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc src, uint32_t n, float* __restrict__ out) {
+template <int MASK>
+__global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc<MASK> src, uint32_t n, float* __restrict__ out) {
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   if (e >= n) return;
@@ -427,8 +468,11 @@ int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, in
   int rc = bn_check(m, c, z);
   if (rc) return rc;
   if (!cx || !g || !bn || !gz || (mask_mode == 2 && !mask_y)) return set_error(I8T_EINVAL, "bn_bwd_apply: bad arguments");
-  BnBwdSrc src{g, z, mask_y, bn, gamma, beta, static_cast<uint32_t>(c), mask_mode};
-  k_bn_bwd_apply<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(src, static_cast<uint32_t>(m * c), gz);
+  const uint32_t un = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
+  const int nb = ew_blocks(m * c, c);
+  if (mask_mode == 1) k_bn_bwd_apply<1><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else if (mask_mode == 2) k_bn_bwd_apply<2><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else k_bn_bwd_apply<0><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   count_launch(1);
   return cuda_check("k_bn_bwd_apply");
 }
@@ -445,9 +489,13 @@ int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const fl
     return set_error(I8T_EINVAL, "quantize_gradient_bn: bad arguments");
   if (lr_scaling_enabled && (!(alpha > 0.0) || !(beta_ > 0.0 && beta_ <= 1.0)))
     return set_error(I8T_EINVAL, "scale_factor: alpha must be > 0, beta in (0,1]");
-  BnBwdSrc src{g, z, mask_y, bn, gamma, beta, static_cast<uint32_t>(c), mask_mode};
   QgFin fin{1 | (lr_scaling_enabled ? 2 : 0), alpha, beta_, form, 0u};
-  return launch_quant_grad_src(cx, st, nullptr, src, n_img, c, hw, true, lcg_state, q, fin);
+  const uint32_t uc = static_cast<uint32_t>(c);
+  if (mask_mode == 1)
+    return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
+  if (mask_mode == 2)
+    return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
+  return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
 }
 
 int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y, int64_t n, float* out) {

@@ -33,25 +33,30 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
                                                           double* partials, double* totals, unsigned* ticket) {
   constexpr int NV = 3 + 2 * NC;
   if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
+  // per-candidate dequantisation tables double(float(q) * s_j) in dynamic smem
+  extern __shared__ double dq_tab[];
   float cl[NC > 0 ? NC : 1], sc[NC > 0 ? NC : 1], is[NC > 0 ? NC : 1];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     cl[j] = cands[j];
     sc[j] = scale_of(cl[j]);
     is[j] = 1.0f / sc[j];
+    build_dequant_table(dq_tab + j * 256, sc[j]);
   }
+  if (NC > 0) __syncthreads();
   double acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.0;
   float m = 0.0f;
+  bool bad = false;
   auto body = [&](float v) {
-    if (!isfinite(v)) acc[1] += 1.0;
+    bad |= !isfinite(v);
     m = fmaxf(m, fabsf(v));
     const double vd = v;
     acc[2] = fma(vd, vd, acc[2]);
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
-      const double gh = __fmul_rn(static_cast<float>(quant_nearest(v, cl[j], sc[j], is[j])), sc[j]);
+      const double gh = dq_tab[j * 256 + 127 + quant_nearest(v, cl[j], sc[j], is[j])];
       acc[3 + 2 * j] = fma(vd, gh, acc[3 + 2 * j]);
       acc[4 + 2 * j] = fma(gh, gh, acc[4 + 2 * j]);
     }
@@ -68,6 +73,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
   }
   for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) body(g[i]);
   acc[0] = m;
+  acc[1] = bad ? 1.0 : 0.0;
   grid_reduce<NV>(acc, 1u, partials, totals, ticket);
 }
 
@@ -269,7 +275,13 @@ static int stats_pass0(Ctx* c, const float* x, int64_t n) {
 
 template <int NC>
 static void dc_pass(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nb, double* p) {
-  k_dc_stats<NC><<<nb, RED_THREADS, 0, c->stream>>>(g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
+  constexpr int smem = NC * 256 * static_cast<int>(sizeof(double));
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_dc_stats<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  k_dc_stats<NC><<<nb, RED_THREADS, smem, c->stream>>>(g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
                                                      c->d_ticket);
 }
 

@@ -13,34 +13,44 @@ namespace i8t_dev {
 
 __device__ __forceinline__ float scale_of(float clip) { return __fdiv_rn(clip, 127.0f); }
 
+// x + RMAGIC rounds x (|x| < 2^22) to an integer held in the low mantissa bits:
+// rint on the FMA pipe, and the integer is __float_as_int(x + RMAGIC) - RMAGIC_BITS.
+// (FRND / F2I / I2F run on the quarter-rate XU pipe, which bounded K3 / K4.)
+constexpr float RMAGIC = 12582912.0f;  // 1.5 * 2^23
+constexpr int RMAGIC_BITS = 0x4B400000;
+
 // quantize_value, kNearest: lround(RN64(v/s)) == round-half-away(v/s) since
 // RN64 cannot cross a half-integer for float v, s; the tie
 // test a >= s*(k+1/2) is decided exactly by the sign of one FMA.
 __device__ __forceinline__ int quant_nearest(float x, float clip, float s, float inv_s) {
   const float v = fminf(fmaxf(x, -clip), clip);
   const float a = fabsf(v);
-  float k = floorf(__fmaf_rn(a, inv_s, 0.5f));
-  if (__fmaf_rn(-s, k + 0.5f, a) >= 0.0f) k += 1.0f;
-  else if (__fmaf_rn(-s, k - 0.5f, a) < 0.0f) k -= 1.0f;
-  k = fminf(k, 127.0f);
-  const int qi = static_cast<int>(k);
-  return v < 0.0f ? -qi : qi;
+  const float kb = __fadd_rn(__fmul_rn(a, inv_s), RMAGIC);
+  const float k = __fsub_rn(kb, RMAGIC);
+  int ki = __float_as_int(kb) - RMAGIC_BITS;
+  if (__fmaf_rn(-s, k + 0.5f, a) >= 0.0f) ++ki;
+  else if (__fmaf_rn(-s, k - 0.5f, a) < 0.0f) --ki;
+  ki = min(ki, 127);
+  return v < 0.0f ? -ki : ki;
 }
 
-// quantize_value, kStochastic: floor(t) + (u < frac(t)), t = RN64(v/s) clamped
-// to +-127, u = X * 2^-32.  FP32 decides when every margin exceeds 2^-13
-// (|t32 - t| < 2e-5, |u32 - u| < 2^-24); otherwise the exact FP64 formula runs.
+// quantize_value, kStochastic: floor(t) + (u < frac(t)) == ceil(t - u) for
+// t = RN64(v/s) clamped to +-127, u = X * 2^-32 (u == frac gives floor(t) both
+// ways).  FP32 decides when y = t - u is more than 2^-13 away from an integer
+// (the estimates of t and u are within 2^-15); otherwise the exact FP64
+// formula runs.  u is formed from the top 23 bits without a conversion.
 __device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {
   if (x == 0.0f) return 0;
   const float v = fminf(fmaxf(x, -clip), clip);
-  const float t = v * inv_s;
-  const float fl = floorf(t);
-  const float frac = t - fl;
-  const float u = static_cast<float>(X >> 8) * 0x1.0p-24f;
+  const float t = __fmul_rn(v, inv_s);
+  const float u = __fsub_rn(__uint_as_float(0x3F800000u | (X >> 9)), 1.0f);
+  const float y = __fsub_rn(t, u);
+  const float rb = __fadd_rn(y, RMAGIC);
+  const float d = __fsub_rn(y, __fsub_rn(rb, RMAGIC));
   constexpr float D = 0x1.0p-13f;
   int q;
-  if (frac > D && frac < 1.0f - D && fabsf(frac - u) > D) {
-    q = static_cast<int>(fl) + (u < frac ? 1 : 0);
+  if (fabsf(d) > D) {
+    q = (__float_as_int(rb) - RMAGIC_BITS) + (d > 0.0f ? 1 : 0);
   } else {
     double td = static_cast<double>(v) / static_cast<double>(s);
     td = fmin(fmax(td, -127.0), 127.0);
@@ -50,6 +60,25 @@ __device__ __forceinline__ int quant_stoch(float x, float clip, float s, float i
     q = static_cast<int>(fd) + (ud < fr ? 1 : 0);
   }
   return max(-127, min(127, q));
+}
+
+// double(float(x)) without the two XU conversions: round the 53-bit
+// significand to 24 bits (nearest-even) in the integer pipe.  Exact for
+// |x| in the float normal range and for 0; the float-subnormal range takes
+// the converting path.
+__device__ __forceinline__ double rn24(double x) {
+  long long b = __double_as_longlong(x);
+  b += 0x0FFFFFFFLL + ((b >> 29) & 1);
+  b &= ~0x1FFFFFFFLL;
+  double r = __longlong_as_double(b);
+  if (fabs(x) < 0x1.0p-126) r = static_cast<double>(static_cast<float>(x));
+  return r;
+}
+
+// Dequantised values double(float(q) * s) for q in [-127, 127] (quantize.cpp:81-87),
+// built once per block in shared memory: tab[q + 127].
+__device__ __forceinline__ void build_dequant_table(double* tab, float s) {
+  for (int i = threadIdx.x; i < 255; i += blockDim.x) tab[i] = __fmul_rn(static_cast<float>(i - 127), s);
 }
 
 __device__ __forceinline__ uint32_t apply(Affine m, uint32_t x) { return m.a * x + m.c; }

@@ -10,12 +10,16 @@
 
 namespace i8t_dev {
 
-// Input source: a float4 of consecutive elements per call; init() receives
-// the first channel of the thread's fixed channel quad (NHWC) before any load.
+// Input source: fetch() issues the raw loads of one float4 of consecutive
+// elements (so the kernel can keep several in flight), value() turns them into
+// the gradient values; init() receives the first channel of the thread's fixed
+// channel quad (NHWC) before any load.
 struct PlainSrc {
   const float4* g;
+  using Raw = float4;
   __device__ __forceinline__ void init(uint32_t) {}
-  __device__ __forceinline__ float4 load(uint32_t e4) const { return __ldg(g + e4); }
+  __device__ __forceinline__ Raw fetch(uint32_t e4) const { return __ldg(g + e4); }
+  __device__ __forceinline__ float4 value(const Raw& r) const { return r; }
 };
 
 // totals layout of K3 (QG_NV doubles): max|g|, nonfinite, sum g^2, sum g*gn,
@@ -61,21 +65,28 @@ static __device__ void fin_quant_grad(DsgcState* st, const double* tot, const Qg
 
 // K3.  NHWC g [N*HW][C] (C % 4 == 0) or FLAT (row-major order = draw order).
 // gridDim.x*blockDim.x*4 is a multiple of C so each thread keeps its channel quad.
+// Two float4 fetches stay in flight ahead of the one being quantised; the
+// dequantised values come from a per-block table (no conversions on the XU pipe
+// except double(g)).
 template <class Src, bool FLAT, bool DC_SUMS, bool FUSED>
-__global__ void __launch_bounds__(RED_THREADS) k_quant_grad(Src src, uint32_t numel, uint32_t C,
+__global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t numel, uint32_t C,
                                                             uint32_t HW, uint32_t draw_offset, Affine step_iter,
                                                             Affine step_elem, Affine step_wrap, uint32_t dpix,
                                                             const float* clip_override, DsgcState* st,
                                                             uint32_t* lcg_state, int8_t* __restrict__ q,
                                                             double* partials, double* totals, unsigned* ticket, QgFin fin,
                                                             int* err) {
+  __shared__ double tab[256];
   float clip = clip_override ? *clip_override : st->v.clip;
   if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
   const float s = scale_of(clip), inv_s = 1.0f / s;
+  build_dequant_table(tab, s);
+  __syncthreads();
   const uint32_t X0 = *lcg_state;
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
-  double acc[QG_NV] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0, a6 = 0.0;
+  bool bad = false;
   float m = 0.0f;
   if (e < numel) {
     uint32_t X, hw = 0;
@@ -89,11 +100,14 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_grad(Src src, uint32_t nu
       X = apply(lcg_jump_map(static_cast<uint64_t>((n * C + c) * HW + hw) + draw_offset + 1u), X0);
       src.init(c);
     }
-    float4 v4 = src.load(e / 4);
+    typename Src::Raw r0 = src.fetch(e / 4), r1 = r0;
+    uint32_t e1 = e + T4;
+    if (e1 < numel) r1 = src.fetch(e1 / 4);
     while (true) {
-      const uint32_t e_next = e + T4;
-      float4 nxt;
-      if (e_next < numel) nxt = src.load(e_next / 4);  // software prefetch of the next float4
+      const uint32_t e2 = e1 + T4;  // < 2^31 + 2*T4: no wrap
+      typename Src::Raw r2 = r1;
+      if (e2 < numel) r2 = src.fetch(e2 / 4);
+      const float4 v4 = src.value(r0);
       const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
       signed char qq[4];
       uint32_t Xj = X;
@@ -101,26 +115,27 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_grad(Src src, uint32_t nu
       for (int j = 0; j < 4; ++j) {
         if (j) Xj = apply(step_elem, Xj);
         const float v = vv[j];
-        if (!isfinite(v)) acc[1] += 1.0;
+        bad |= !isfinite(v);
         m = fmaxf(m, fabsf(v));
         const int qs = quant_stoch(v, clip, s, inv_s, Xj);
         qq[j] = static_cast<signed char>(qs);
-        const float gs = __fmul_rn(static_cast<float>(qs), s);
-        const double vd = v, gsd = gs;
+        const double vd = v, gsd = tab[qs + 127];
         const double d = vd - gsd;
-        acc[5] = fma(d, d, acc[5]);
-        acc[6] = fma(gsd, gsd, acc[6]);
+        a5 = fma(d, d, a5);
+        a6 = fma(gsd, gsd, a6);
         if (DC_SUMS) {
-          const double gn = __fmul_rn(static_cast<float>(quant_nearest(v, clip, s, inv_s)), s);
-          acc[2] = fma(vd, vd, acc[2]);
-          acc[3] = fma(vd, gn, acc[3]);
-          acc[4] = fma(gn, gn, acc[4]);
+          const double gn = tab[quant_nearest(v, clip, s, inv_s) + 127];
+          a2 = fma(vd, vd, a2);
+          a3 = fma(vd, gn, a3);
+          a4 = fma(gn, gn, a4);
         }
       }
       reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
-      if (e_next >= numel) break;
-      e = e_next;
-      v4 = nxt;
+      if (e1 >= numel) break;
+      e = e1;
+      e1 = e2;
+      r0 = r1;
+      r1 = r2;
       X = apply(step_iter, X);
       if (!FLAT) {
         hw += dpix;
@@ -131,7 +146,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_grad(Src src, uint32_t nu
       }
     }
   }
-  acc[0] = m;
+  double acc[QG_NV] = {m, bad ? 1.0 : 0.0, a2, a3, a4, a5, a6, 0.0};
   if (grid_reduce<QG_NV>(acc, 1u, partials, totals, ticket) && FUSED && threadIdx.x == 0)
     fin_quant_grad(st, totals, fin, lcg_state, err);
 }
@@ -140,10 +155,10 @@ static __global__ void k_fin_quant_grad(DsgcState* st, const double* totals, QgF
   if (threadIdx.x == 0) fin_quant_grad(st, totals, fin, lcg_state, err);
 }
 
-inline int nblocks(int64_t n, int64_t multiple = 1) {
+inline int nblocks(int64_t n, int64_t multiple = 1, int64_t cap = 592) {
   int64_t b = (n + RED_THREADS * 8 - 1) / (RED_THREADS * 8);
   if (b < 1) b = 1;
-  if (b > 592) b = 592;
+  if (b > cap) b = cap;
   b = (b + multiple - 1) / multiple * multiple;
   return static_cast<int>(b);
 }
@@ -169,7 +184,7 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
   if (numel >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "quantize_gradient: tensor >= 2^31 elements");
   // grid: threads*4 must be a multiple of C (each thread keeps its channel quad)
   const int64_t mult = flat ? 1 : C / gcd_i(C, RED_THREADS * 4);
-  int nb = nblocks(numel, mult);
+  int nb = nblocks(numel, mult, 2 * 148);  // one resident wave (__launch_bounds__(256, 2))
   double* p = ensure_partials(c, static_cast<size_t>(nb) * QG_NV);
   if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
   const uint32_t T4 = static_cast<uint32_t>(nb) * RED_THREADS * 4u;

@@ -60,6 +60,40 @@ def test_quantize_stochastic_bit_exact_and_stream(ops):
         assert ops.lcg_value(st) == st_ref
 
 
+def _lcg_draws(seed, n):
+    """u_i = X_{i+1} * 2^-32 of the reference LcgStream (quantize.hpp:32-50)."""
+    out = np.empty(n, np.float64)
+    x = seed & 0xFFFFFFFF
+    for i in range(n):
+        x = (1664525 * x + 1013904223) & 0xFFFFFFFF
+        out[i] = x * 2.0 ** -32
+    return out
+
+
+@pytest.mark.parametrize("clip", [0.9, 3e-5, 127.0])
+def test_quantize_stochastic_adversarial(ops, clip):
+    """Inputs placed so that frac(x/s) sits on, or within a few ulp of, the
+    element's own draw u (the FP32 fast path's decision boundary), plus exact
+    multiples of s, the clip edges and values beyond the clip."""
+    n, seed = 40_000, 99
+    u = _lcg_draws(seed, n)
+    s = O.quant_scale(clip)
+    rng = np.random.default_rng(5)
+    k = rng.integers(-127, 127, n).astype(np.float64)
+    x = ((k + u) * s).astype(np.float32)
+    kind = rng.integers(0, 6, n)
+    x = np.where(kind == 1, np.nextafter(x, np.float32(np.inf)), x)
+    x = np.where(kind == 2, np.nextafter(x, np.float32(-np.inf)), x)
+    x = np.where(kind == 3, (k * s).astype(np.float32), x)
+    edge = np.array([clip, -clip, np.nextafter(np.float32(clip), np.float32(0)), 2 * clip, -3 * clip], np.float32)
+    x = np.where(kind == 4, edge[rng.integers(0, len(edge), n)], x).astype(np.float32)
+    ref, st_ref = O.quantize(x, clip, True, seed)
+    st = ops.new_lcg_state(seed)
+    got = ops.quantize(t(x), clip, stochastic=True, stream_state=st).cpu().numpy()
+    np.testing.assert_array_equal(got, ref)
+    assert ops.lcg_value(st) == st_ref
+
+
 def test_quantize_stochastic_odd_length(ops):
     x = np.linspace(-1, 1, 1001).astype(np.float32)
     ref, st_ref = O.quantize(x, 0.9, True, 77)
