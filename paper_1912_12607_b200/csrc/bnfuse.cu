@@ -44,6 +44,12 @@ __device__ __forceinline__ float bn_y(double gm, double xv, double bt) { return 
 // (2^-150 itself rounds to +0 under ties-to-even).
 __device__ __forceinline__ bool bn_pos(double gm, double xv, double bt) { return fma(gm, xv, bt) > 0x1.0p-150; }
 
+// x_hat = double(float(xv)) through the converting instructions; out of line so
+// the rare call stays a branch instead of predicated XU work in the hot loop.
+__device__ __noinline__ void exact_xh4(const double* xv, double* xh) {
+  for (int j = 0; j < 4; ++j) xh[j] = static_cast<double>(static_cast<float>(xv[j]));
+}
+
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
 template <int MODE>
@@ -96,15 +102,22 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
         } else {
           const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
           const float yy[4] = {yv[u].x, yv[u].y, yv[u].z, yv[u].w};
+          double xv[4], xh[4], gm[4];
+          bool sub = false;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
+            xv[j] = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
             bool mk = true;
-            if (a.mask_mode == 1) mk = bn_pos(gmm[j], xv, bt[j]);
+            if (a.mask_mode == 1) mk = bn_pos(gmm[j], xv[j], bt[j]);
             else if (a.mask_mode == 2) mk = yy[j] > 0.0f;
-            const double gm = mk ? static_cast<double>(gg[j]) : 0.0;
-            acc0[j] += gm;
-            acc1[j] = fma(gm, rn24(xv), acc1[j]);
+            gm[j] = mk ? static_cast<double>(gg[j]) : 0.0;
+            xh[j] = rn24(xv[j], sub);
+          }
+          if (sub) exact_xh4(xv, xh);  // float-subnormal x_hat: a real (rare) branch
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc0[j] += gm[j];
+            acc1[j] = fma(gm[j], xh[j], acc1[j]);
           }
         }
       }
@@ -317,7 +330,9 @@ struct BnBwdSrc {
     if (MASK == 2) r.y = __ldg(reinterpret_cast<const float4*>(mask_y) + e4);
     return r;
   }
-  __device__ __forceinline__ float4 value(const Raw& r) const {
+  // exact (reference) value, and the fast one that flags float-subnormal x_hat
+  template <bool FAST>
+  __device__ __forceinline__ float4 value_t(const Raw& r, bool& slow) const {
     const float gg[4] = {r.g.x, r.g.y, r.g.z, r.g.w}, zz[4] = {r.z.x, r.z.y, r.z.z, r.z.w};
     float o[4];
 #pragma unroll
@@ -327,10 +342,16 @@ struct BnBwdSrc {
       if (MASK == 1) mk = bn_pos(gm[j], xv, bt[j]);
       if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
       const double gd = mk ? static_cast<double>(gg[j]) : 0.0;
-      o[j] = static_cast<float>(k[j] * (gd - a[j] - rn24(xv) * b[j]));
+      const double xh = FAST ? rn24(xv, slow) : static_cast<double>(static_cast<float>(xv));
+      o[j] = static_cast<float>(k[j] * (gd - a[j] - xh * b[j]));
     }
     return make_float4(o[0], o[1], o[2], o[3]);
   }
+  __device__ __forceinline__ float4 value(const Raw& r) const {
+    bool dummy = false;
+    return value_t<false>(r, dummy);
+  }
+  __device__ __forceinline__ float4 value_fast(const Raw& r, bool& slow) const { return value_t<true>(r, slow); }
   __device__ __forceinline__ float4 load(uint32_t e4) const { return value(fetch(e4)); }
 };
 

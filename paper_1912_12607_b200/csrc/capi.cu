@@ -69,6 +69,19 @@ void* ensure_wgrad(Ctx* c, size_t bytes) {
   return c->d_wgrad;
 }
 
+void* ensure_fold(Ctx* c, size_t bytes) {
+  if (bytes <= c->fold_cap) return c->d_fold;
+  cudaStreamSynchronize(c->stream);
+  if (c->d_fold) cudaFree(c->d_fold);
+  c->d_fold = nullptr;
+  if (cudaMalloc(&c->d_fold, bytes) != cudaSuccess) {
+    c->fold_cap = 0;
+    return nullptr;
+  }
+  c->fold_cap = bytes;
+  return c->d_fold;
+}
+
 int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op) {
   if (!c->allreduce || count <= 0) return I8T_OK;
   const int rc = c->allreduce(c->allreduce_user, buf, count, 0, op, c->stream);
@@ -171,6 +184,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->d_totals) cudaFree(c->d_totals);
   if (c->d_wgrad) cudaFree(c->d_wgrad);
+  if (c->d_fold) cudaFree(c->d_fold);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_tickets) cudaFree(c->d_tickets);
   delete c;

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <mutex>
 
 #include "internal.cuh"
@@ -50,7 +52,22 @@ struct ConvArgs {
   int32_t* acc32;
   int use_tma_out;  // epilogue writes through the output tensor map (else direct stores)
   int m_pad;        // WGRAD: rows per split in the int32 partial workspace
+  // DGRAD stride phase (sh or sw > 1): rows are the input pixels
+  // (n, hh*sh + fh, ww*sw + fw) of one phase, the reduction runs over that
+  // phase's taps r = r0 + ir*sh, s = s0 + is*sw only (p = hh + dh - ir,
+  // q = ww + dw - is), every k-tile inside one tap (Kp % 128 == 0).
+  int phase;
+  int Hq, Wq, fh, fw, r0, s0, ns, dh, dw;
 };
+
+// output row of GEMM row m (identity except in DGRAD phase mode)
+__device__ __forceinline__ int64_t out_row_of(const ConvArgs& a, int64_t m) {
+  if (!a.phase) return m;
+  const int hwq = a.Hq * a.Wq;
+  const int n = static_cast<int>(m / hwq), rem = static_cast<int>(m - static_cast<int64_t>(n) * hwq);
+  const int hh = rem / a.Wq, ww = rem - hh * a.Wq;
+  return (static_cast<int64_t>(n) * a.H + hh * a.sh + a.fh) * a.W + ww * a.sw + a.fw;
+}
 
 constexpr int BM = 128;
 constexpr int BKB = 128;  // bytes of reduction per stage (4 MMAs of K=32)
@@ -166,6 +183,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             rowA_n[i] = n;
             rowA_y[i] = p * args.sh - args.ph;
             rowA_x[i] = q * args.sw - args.pw;
+          } else if (args.phase) {
+            const int hwq = args.Hq * args.Wq;
+            const int n = mm / hwq, rem = mm - n * hwq;
+            const int hh = rem / args.Wq, ww = rem - hh * args.Wq;
+            rowA_n[i] = n;
+            rowA_y[i] = hh + args.dh;
+            rowA_x[i] = ww + args.dw;
           } else {
             const int hw = args.H * args.W;
             const int n = mm / hw, rem = mm - n * hw;
@@ -185,14 +209,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         if constexpr (MODE == MODE_FWD || MODE == MODE_DGRAD) {
           if (tid == 0) {  // weight tile [BN rows][128 B] by TMA (OOB rows / columns zero-filled)
             mbar_expect_tx(&full[s], C::B_BYTES);
-            tma_load_2d(b_st, &tmap_b, &full[s], static_cast<int>(kbase), n0);
+            int bx = static_cast<int>(kbase);
+            if (MODE == MODE_DGRAD && args.phase) {  // compact tap index -> CRSK column of (r, s)
+              const int it = static_cast<int>(kbase / args.Kp);
+              const int ir = it / args.ns, is = it - ir * args.ns;
+              bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp +
+                   static_cast<int>(kbase - static_cast<int64_t>(it) * args.Kp);
+            }
+            tma_load_2d(b_st, &tmap_b, &full[s], bx, n0);
           }
           const int64_t kk = kbase + ja * VA;
           const bool kok = kk < args.Kd;
           const int CH = (MODE == MODE_FWD) ? args.Cp : args.Kp;
           const int tap = kok ? static_cast<int>(kk / CH) : 0;
           const int ch = kok ? static_cast<int>(kk - static_cast<int64_t>(tap) * CH) : 0;
-          const int r = tap / args.S, sx = tap - r * args.S;
+          const int tS = (MODE == MODE_DGRAD && args.phase) ? args.ns : args.S;
+          const int r = tap / tS, sx = tap - r * tS;
 #pragma unroll
           for (int i = 0; i < PASSES_A; ++i) {
             const int row = ra0 + i * ROWS_PER_PASS_A;
@@ -202,6 +234,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               const int ih = rowA_y[i] + r, iw = rowA_x[i] + sx;
               ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
               if (ok) src = args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + ch;
+            } else if (args.phase) {
+              const int p = rowA_y[i] - r, q = rowA_x[i] - sx;  // r, sx = compact (ir, is)
+              ok = ok && p >= 0 && p < args.P && q >= 0 && q < args.Q;
+              src = args.gz;
+              if (ok) src = args.gz + ((static_cast<int64_t>(rowA_n[i]) * args.P + p) * args.Q + q) * args.Kp + ch;
             } else {
               const int pn = rowA_y[i] - r, qn = rowA_x[i] - sx;
               int p, q;
@@ -376,16 +413,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         } else if (m < args.M) {
           if constexpr (MODE != MODE_WGRAD) {
             if (args.out) {
-              float* dst = args.out + m * args.ldo + gc0;
+              float* dst = args.out + out_row_of(args, m) * args.ldo + gc0;
+              if (gc0 + 32 <= args.Ng && (args.ldo % 4) == 0) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (gc0 + i < args.Ng)
-                  dst[i] = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i])));
+                for (int j = 0; j < 8; ++j) {
+                  float4 w;
+                  w.x = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 0])));
+                  w.y = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 1])));
+                  w.z = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 2])));
+                  w.w = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 3])));
+                  reinterpret_cast<float4*>(dst)[j] = w;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (gc0 + i < args.Ng)
+                    dst[i] = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i])));
+              }
             }
           }
         }
         if (args.acc32 && m < args.M && MODE != MODE_WGRAD) {
-          int32_t* dst = args.acc32 + m * args.Ng + gc0;
+          int32_t* dst = args.acc32 + out_row_of(args, m) * args.Ng + gc0;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (gc0 + i < args.Ng) dst[i] = static_cast<int32_t>(v[i]);
@@ -444,6 +493,90 @@ __global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int
         const int64_t o = out_kcrs ? (static_cast<int64_t>(k) * C + c) * RS + rs : (static_cast<int64_t>(k) * RS + rs) * C + c;
         gw[o] = static_cast<float>(rescale * static_cast<double>(sum));
       }
+    }
+  }
+}
+
+// Narrow-channel convolutions (c_pad == 4, e.g. the RGB stem): fold the kw
+// horizontal taps into the channel dimension,
+//   X'[n][h][q][s*4 + c] = X[n][h][q*sw + s - pw][c]  (zero outside; bytes 4*kw..31 zero),
+// so the conv becomes (C' = 32, W' = Q, S' = 1, stride (sh, 1), pad (ph, 0)) with
+// 32-byte operand pieces instead of 4-byte ones.  Its reduction order (r, s, c)
+// is the original KRSC order, so the weight rows only gain 4 zero bytes per r.
+__global__ void k_fold_taps(const int8_t* __restrict__ x, int64_t NH, int W, int Q, int kw, int sw, int pw,
+                            int8_t* __restrict__ xf) {
+  const int64_t tot = NH * Q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nh = i / Q;
+    const int q = static_cast<int>(i - nh * Q);
+    const int32_t* row = reinterpret_cast<const int32_t*>(x) + nh * W;
+    int32_t w[8];
+#pragma unroll
+    for (int sx = 0; sx < 8; ++sx) {
+      const int wx = q * sw + sx - pw;
+      w[sx] = (sx < kw && wx >= 0 && wx < W) ? __ldg(row + wx) : 0;
+    }
+    int4* o = reinterpret_cast<int4*>(xf + i * 32);
+    o[0] = make_int4(w[0], w[1], w[2], w[3]);
+    o[1] = make_int4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+// KRSC [K][ldw] (c_pad 4) -> [K][R*32]: each r's kw*4 bytes, zero padded to 32.
+__global__ void k_fold_weights(const int8_t* __restrict__ w, int64_t ldw, int K, int R, int kw, int8_t* __restrict__ wf) {
+  const int tot = K * R * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const int k = i / (R * 32), rem = i - k * R * 32, r = rem / 32, j = rem - r * 32;
+    wf[i] = j < 4 * kw ? w[k * ldw + r * kw * 4 + j] : static_cast<int8_t>(0);
+  }
+}
+
+// folded wgrad accumulator [R*32][K] -> original [(r*kw + s)*4 + c][K]
+__global__ void k_unfold_wacc(const long long* __restrict__ accf, int R, int kw, int K, long long* __restrict__ acc) {
+  const int tot = R * kw * 4 * K;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const int m = i / K, k = i - m * K;
+    const int r = m / (kw * 4), j = m - r * kw * 4;
+    acc[i] = accf[(r * 32 + j) * K + k];
+  }
+}
+
+static bool foldable(const i8t_conv_geom* g, int64_t c_pad) {
+  static const bool off = getenv("I8T_NO_FOLD") != nullptr;
+  return !off && c_pad == 4 && !g->depthwise && g->kw > 1 && g->kw <= 8;
+}
+
+static i8t_conv_geom folded_geom(const i8t_conv_geom* g, int64_t Q) {
+  i8t_conv_geom f = *g;
+  f.c = 32; f.w = Q; f.kw = 1; f.stride_w = 1; f.pad_w = 0;
+  return f;
+}
+
+static int8_t* fold_input(Ctx* c, const i8t_conv_geom* g, int64_t Q, const int8_t* a, size_t extra, int8_t** extra_out) {
+  const size_t xbytes = static_cast<size_t>(g->n * g->h * Q) * 32;
+  int8_t* buf = reinterpret_cast<int8_t*>(ensure_fold(c, xbytes + extra + 256));
+  if (!buf) return nullptr;
+  const int64_t tot = g->n * g->h * Q;
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+  k_fold_taps<<<blocks, 256, 0, c->stream>>>(a, g->n * g->h, (int)g->w, (int)Q, (int)g->kw, (int)g->stride_w,
+                                             (int)g->pad_w, buf);
+  count_launch(1);
+  *extra_out = buf + ((xbytes + 255) / 256) * 256;
+  return buf;
+}
+
+// DGRAD phase with no taps (e.g. 1x1 stride 2, odd pixels): rows are zero.
+__global__ void k_zero_phase(ConvArgs a) {
+  const int64_t rows = static_cast<int64_t>(a.N) * a.Hq * a.Wq;
+  const int c4 = a.Ng / 4;  // Ng % 4 == 0 on this path
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t m = blockIdx.x * 8ll + warp; m < rows; m += gridDim.x * 8ll) {
+    const int64_t o = out_row_of(a, m);
+    float4* dst = reinterpret_cast<float4*>(a.out + o * a.ldo);
+    int4* acc = a.acc32 ? reinterpret_cast<int4*>(a.acc32 + o * a.Ng) : nullptr;
+    for (int c = lane; c < c4; c += 32) {
+      if (a.out) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (acc) acc[c] = make_int4(0, 0, 0, 0);
     }
   }
 }
@@ -617,6 +750,54 @@ static void fill_geom(ConvArgs& x, const i8t_conv_geom* g, int64_t P, int64_t Q)
   x.P = (int)P; x.Q = (int)Q;
 }
 
+// Strided DGRAD as sh*sw stride-1 sub-problems: phase (fh, fw) holds the input
+// pixels h = hh*sh + fh, w = ww*sw + fw; only the taps with
+// (fh + ph - r) % sh == 0 and (fw + pw - s) % sw == 0 reach them, so no MMA
+// runs on the zero-stuffed positions of the reference's col2im (conv.cpp:60-84).
+static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, const int8_t* gz, int64_t k_pad,
+                        const int8_t* wt, int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga,
+                        int32_t* acc) {
+  const int sh = (int)g->stride_h, sw = (int)g->stride_w;
+  for (int fh = 0; fh < sh; ++fh) {
+    for (int fw = 0; fw < sw; ++fw) {
+      ConvArgs x{};
+      fill_geom(x, g, P, Q);
+      x.act = nullptr; x.gz = gz; x.wt = wt; x.ldw = ld_wt; x.Cp = (int)g->c; x.Kp = (int)k_pad;
+      x.phase = 1; x.fh = fh; x.fw = fw;
+      x.Hq = (int)((g->h - fh + sh - 1) / sh);
+      x.Wq = (int)((g->w - fw + sw - 1) / sw);
+      if (x.Hq <= 0 || x.Wq <= 0) continue;
+      x.r0 = (int)((fh + g->pad_h) % sh);
+      x.s0 = (int)((fw + g->pad_w) % sw);
+      const int nr = x.r0 < g->kh ? (int)((g->kh - 1 - x.r0) / sh + 1) : 0;
+      x.ns = x.s0 < g->kw ? (int)((g->kw - 1 - x.s0) / sw + 1) : 0;
+      x.dh = (int)((fh + g->pad_h - x.r0) / sh);
+      x.dw = (int)((fw + g->pad_w - x.s0) / sw);
+      x.M = g->n * x.Hq * x.Wq; x.Ng = (int)g->c;
+      x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
+      x.use_tma_out = 0;
+      if (nr == 0 || x.ns == 0) {
+        const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
+        k_zero_phase<<<blocks, 256, 0, c->stream>>>(x);
+        count_launch(1);
+        int rc = cuda_check("k_zero_phase");
+        if (rc) return rc;
+        continue;
+      }
+      x.Kd = (int64_t)nr * x.ns * k_pad;
+      x.k_tiles = (int)((x.Kd + BKB - 1) / BKB);
+      x.m_tiles = (int)((x.M + BM - 1) / BM);
+      const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
+      x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
+      CUtensorMap map, omap{};
+      int rc = make_weight_map(&map, wt, g->c, ld_wt, bn);
+      if (rc) return rc;
+      if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, map, omap, vec_of(k_pad), 16))) return rc;
+    }
+  }
+  return I8T_OK;
+}
+
 }  // namespace i8t_dev
 
 using namespace i8t_dev;
@@ -635,6 +816,17 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   const int64_t Kd = g->kh * g->kw * c_pad;
   if (ld_w < Kd || ld_w % 16 != 0) return set_error(I8T_EUNSUPPORTED, "conv_fwd: ld_w must be >= kh*kw*c_pad and a multiple of 16");
   if (g->kh * g->kw * g->c > 130000) return set_error(I8T_EINVAL, "conv: reduction depth exceeds i32 overflow bound");
+  if (foldable(g, c_pad)) {
+    int8_t* wf = nullptr;
+    const int8_t* xf = fold_input(c, g, Q, a, static_cast<size_t>(g->k) * g->kh * 32, &wf);
+    if (!xf) return set_error(I8T_ECUDA, "conv_fwd: fold buffer alloc failed");
+    const int tot = (int)(g->k * g->kh * 32);
+    k_fold_weights<<<(tot + 255) / 256, 256, 0, c->stream>>>(w, ld_w, (int)g->k, (int)g->kh, (int)g->kw, wf);
+    count_launch(1);
+    if ((rc = cuda_check("k_fold"))) return rc;
+    const i8t_conv_geom f = folded_geom(g, Q);
+    return i8t_conv_fwd(ctx, &f, xf, 32, wf, g->kh * 32, clip_a, clip_w, z, acc);
+  }
   ConvArgs x{};
   fill_geom(x, g, P, Q);
   x.act = a; x.gz = nullptr; x.wt = w; x.ldw = ld_w; x.Cp = (int)c_pad; x.Kp = (int)g->k;
@@ -664,6 +856,10 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (ld_wt < Kd || ld_wt % 16 != 0) return set_error(I8T_EUNSUPPORTED, "conv_dgrad: ld_wt must be >= kh*kw*k_pad, multiple of 16");
   if (g->k > 130000) return set_error(I8T_EINVAL, "conv: reduction depth exceeds i32 overflow bound");
   if (g->k * g->kh * g->kw > 133000) return set_error(I8T_EUNSUPPORTED, "conv_dgrad: int32 accumulator bound");
+  if ((g->stride_h > 1 || g->stride_w > 1) && k_pad % 128 == 0 && g->c % 4 == 0 && (ld_wt % 16) == 0) {
+    static const bool off = getenv("I8T_NO_DGRAD_PHASE") != nullptr;
+    if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc);
+  }
   ConvArgs x{};
   fill_geom(x, g, P, Q);
   x.act = nullptr; x.gz = gz; x.wt = wt; x.ldw = ld_wt; x.Cp = (int)g->c; x.Kp = (int)k_pad;
@@ -690,6 +886,20 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (g->depthwise) return set_error(I8T_EINVAL, "conv_wgrad: use i8t_conv_dw_wgrad for depthwise");
   if (c_pad < g->c || c_pad % 4 != 0 || k_pad < g->k || k_pad % 4 != 0)
     return set_error(I8T_EUNSUPPORTED, "conv_wgrad: channel strides must be multiples of 4");
+  if (foldable(g, c_pad)) {
+    int8_t* ex = nullptr;
+    const int8_t* xf = fold_input(c, g, Q, a, sizeof(long long) * static_cast<size_t>(g->kh * 32 * g->k), &ex);
+    if (!xf) return set_error(I8T_ECUDA, "conv_wgrad: fold buffer alloc failed");
+    int64_t* accf = reinterpret_cast<int64_t*>(ex);
+    const i8t_conv_geom f = folded_geom(g, Q);
+    if ((rc = i8t_conv_wgrad(ctx, &f, gz, k_pad, xf, 32, clip_g, clip_a, accf, nullptr, out_kcrs))) return rc;
+    const int tot = (int)(g->kh * g->kw * 4 * g->k);
+    k_unfold_wacc<<<(tot + 255) / 256, 256, 0, c->stream>>>(reinterpret_cast<const long long*>(accf), (int)g->kh,
+                                                            (int)g->kw, (int)g->k, reinterpret_cast<long long*>(acc));
+    count_launch(1);
+    if ((rc = cuda_check("k_unfold_wacc"))) return rc;
+    return gw ? i8t_conv_wgrad_finalize(ctx, g, acc, c_pad, clip_g, clip_a, gw, out_kcrs) : I8T_OK;
+  }
   ConvArgs x{};
   fill_geom(x, g, P, Q);
   x.act = a; x.gz = gz; x.wt = nullptr; x.ldw = 0; x.Cp = (int)c_pad; x.Kp = (int)k_pad;
@@ -697,14 +907,29 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   const int bn = pick_bn(g->k);
   const int64_t m_tiles = (x.M + BM - 1) / BM, n_tiles = (g->k + bn - 1) / bn;
   const int64_t total_kt = (x.Kd + BKB - 1) / BKB;
-  // split the npq reduction: <= 1015 k-tiles (129,920 rows) per split keeps each
-  // int32 partial exact; aim for ~4 tiles per SM so the persistent queue balances.
-  int64_t splits = (4 * num_sms() + m_tiles * n_tiles - 1) / (m_tiles * n_tiles);
-  if (splits < 1) splits = 1;
-  int64_t per = (total_kt + splits - 1) / splits;
-  if (per > 1015) per = 1015;
-  if (per < 8 && total_kt >= 8) per = 8;
-  splits = (total_kt + per - 1) / per;
+  // split the npq reduction (<= 1015 k-tiles = 129,920 rows per split keeps each
+  // int32 partial exact): pick the split count minimising
+  //   waves * (k-tiles per split + C0),  waves = ceil(tiles / SMs),
+  // C0 ~ the per-tile prologue + partial write-out in k-tile units.
+  const int64_t mn = m_tiles * n_tiles, sms = num_sms();
+  static const int c0 = [] {
+    const char* e = getenv("I8T_WGRAD_C0");
+    return e ? atoi(e) : 6;
+  }();
+  int64_t per = total_kt, best = -1;
+  for (int64_t sp = (total_kt + 1014) / 1015; sp <= total_kt; ++sp) {
+    const int64_t pk = (total_kt + sp - 1) / sp;
+    if (pk < 8 && sp > 1) break;
+    const int64_t nsp = (total_kt + pk - 1) / pk;  // splits actually used
+    const int64_t waves = (mn * nsp + sms - 1) / sms;
+    const int64_t cost = waves * (pk + c0);
+    if (best < 0 || cost < best) {
+      best = cost;
+      per = pk;
+    }
+    if (mn * nsp > 16 * sms) break;
+  }
+  int64_t splits = (total_kt + per - 1) / per;
   x.k_tiles = (int)per;
   x.m_tiles = (int)m_tiles; x.n_tiles = (int)n_tiles; x.splits = (int)splits;
   x.m_pad = (int)(m_tiles * BM);

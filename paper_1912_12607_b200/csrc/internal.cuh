@@ -65,6 +65,8 @@ struct Ctx {
   size_t scratch_cap = 0;
   void* d_wgrad = nullptr;             // per-split int32 wgrad partial tiles
   size_t wgrad_cap = 0;
+  void* d_fold = nullptr;              // tap-folded activations / weights (narrow-channel convs)
+  size_t fold_cap = 0;
   // data parallel: the gradient of this rank is shard `rank` of `world` equal
   // shards of the global batch; statistics are combined through `allreduce`.
   i8t_allreduce_fn allreduce = nullptr;
@@ -81,6 +83,7 @@ constexpr int RED_THREADS = 256;
 double* ensure_partials(Ctx* c, size_t doubles);
 void* ensure_scratch(Ctx* c, size_t bytes);
 void* ensure_wgrad(Ctx* c, size_t bytes);
+void* ensure_fold(Ctx* c, size_t bytes);
 
 void count_launch(int n = 1);
 int set_error(int status, const std::string& msg);

@@ -34,45 +34,60 @@ __device__ __forceinline__ int quant_nearest(float x, float clip, float s, float
   return v < 0.0f ? -ki : ki;
 }
 
-// quantize_value, kStochastic: floor(t) + (u < frac(t)) == ceil(t - u) for
-// t = RN64(v/s) clamped to +-127, u = X * 2^-32 (u == frac gives floor(t) both
-// ways).  FP32 decides when y = t - u is more than 2^-13 away from an integer
-// (the estimates of t and u are within 2^-15); otherwise the exact FP64
-// formula runs.  u is formed from the top 23 bits without a conversion.
-__device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {
-  if (x == 0.0f) return 0;
-  const float v = fminf(fmaxf(x, -clip), clip);
-  const float t = __fmul_rn(v, inv_s);
+// Branch-free fast paths for the hot loops: they take t = float(clamp(v)) * inv_s
+// (within 2^-15 of RN64(v/s)) and raise `slow` when the FP32 decision is
+// within 2^-13 of a rounding boundary; the caller then redoes the element
+// with the exact functions below.
+constexpr float QD = 0x1.0p-13f;
+
+// kNearest: round-half-away(|t|) with the sign of t.
+__device__ __forceinline__ int qn_fast(float t, bool& slow) {
+  const float at = fabsf(t);
+  const float kb = __fadd_rn(at, RMAGIC);
+  const float dn = __fsub_rn(at, __fsub_rn(kb, RMAGIC));  // in [-1/2, 1/2]
+  slow |= fabsf(dn) > 0.5f - QD;
+  const int ki = min(__float_as_int(kb) - RMAGIC_BITS, 127);
+  return t < 0.0f ? -ki : ki;
+}
+
+// kStochastic: floor(t) + (u < frac(t)) == ceil(t - u) for t = RN64(v/s)
+// clamped to +-127, u = X * 2^-32 (u == frac gives floor(t) both ways).  u is
+// formed from the top 23 bits without a conversion; ceil(y) lies in
+// [-127, 127] whenever the decision is not flagged slow.
+__device__ __forceinline__ int qs_fast(float t, uint32_t X, bool& slow) {
   const float u = __fsub_rn(__uint_as_float(0x3F800000u | (X >> 9)), 1.0f);
   const float y = __fsub_rn(t, u);
   const float rb = __fadd_rn(y, RMAGIC);
   const float d = __fsub_rn(y, __fsub_rn(rb, RMAGIC));
-  constexpr float D = 0x1.0p-13f;
-  int q;
-  if (fabsf(d) > D) {
-    q = (__float_as_int(rb) - RMAGIC_BITS) + (d > 0.0f ? 1 : 0);
-  } else {
-    double td = static_cast<double>(v) / static_cast<double>(s);
-    td = fmin(fmax(td, -127.0), 127.0);
-    const double fd = floor(td);
-    const double fr = td - fd;
-    const double ud = static_cast<double>(X) * 0x1.0p-32;
-    q = static_cast<int>(fd) + (ud < fr ? 1 : 0);
-  }
+  slow |= !(fabsf(d) > QD);
+  return (__float_as_int(rb) - RMAGIC_BITS) + (d > 0.0f ? 1 : 0);
+}
+
+// quantize_value, kStochastic, exact: the FP32 fast path where it decides,
+// else the reference's FP64 formula (quantize.cpp:16-31).
+__device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {
+  const float v = fminf(fmaxf(x, -clip), clip);
+  bool slow = false;
+  const int qf = qs_fast(__fmul_rn(v, inv_s), X, slow);
+  if (!slow) return qf;
+  double td = static_cast<double>(v) / static_cast<double>(s);
+  td = fmin(fmax(td, -127.0), 127.0);
+  const double fd = floor(td);
+  const double fr = td - fd;
+  const double ud = static_cast<double>(X) * 0x1.0p-32;
+  const int q = static_cast<int>(fd) + (ud < fr ? 1 : 0);
   return max(-127, min(127, q));
 }
 
 // double(float(x)) without the two XU conversions: round the 53-bit
 // significand to 24 bits (nearest-even) in the integer pipe.  Exact for
-// |x| in the float normal range and for 0; the float-subnormal range takes
-// the converting path.
-__device__ __forceinline__ double rn24(double x) {
+// |x| >= 2^-126 (float normal range); smaller |x| (incl. 0) raise `slow`.
+__device__ __forceinline__ double rn24(double x, bool& slow) {
   long long b = __double_as_longlong(x);
   b += 0x0FFFFFFFLL + ((b >> 29) & 1);
   b &= ~0x1FFFFFFFLL;
-  double r = __longlong_as_double(b);
-  if (fabs(x) < 0x1.0p-126) r = static_cast<double>(static_cast<float>(x));
-  return r;
+  slow |= fabs(x) < 0x1.0p-126;
+  return __longlong_as_double(b);
 }
 
 // Dequantised values double(float(q) * s) for q in [-127, 127] (quantize.cpp:81-87),

@@ -20,6 +20,7 @@ struct PlainSrc {
   __device__ __forceinline__ void init(uint32_t) {}
   __device__ __forceinline__ Raw fetch(uint32_t e4) const { return __ldg(g + e4); }
   __device__ __forceinline__ float4 value(const Raw& r) const { return r; }
+  __device__ __forceinline__ float4 value_fast(const Raw& r, bool&) const { return r; }
 };
 
 // totals layout of K3 (QG_NV doubles): max|g|, nonfinite, sum g^2, sum g*gn,
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
   const float s = scale_of(clip), inv_s = 1.0f / s;
   build_dequant_table(tab, s);
   __syncthreads();
+  const double* tab0 = tab + 127;  // tab0[q], q in [-127, 127]
   const uint32_t X0 = *lcg_state;
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
@@ -107,24 +109,45 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
       const uint32_t e2 = e1 + T4;  // < 2^31 + 2*T4: no wrap
       typename Src::Raw r2 = r1;
       if (e2 < numel) r2 = src.fetch(e2 / 4);
-      const float4 v4 = src.value(r0);
-      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-      signed char qq[4];
-      uint32_t Xj = X;
+      // fast path for the float4 (branch-free); any element within 2^-13 of a
+      // rounding boundary (or with a float-subnormal BN x_hat) redoes the
+      // float4 with the exact functions
+      bool slow = false;
+      const float4 v4 = src.value_fast(r0, slow);
+      float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      uint32_t Xs[4];
+      Xs[0] = X;
+#pragma unroll
+      for (int j = 1; j < 4; ++j) Xs[j] = apply(step_elem, Xs[j - 1]);
+      int qs[4], qn[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (j) Xj = apply(step_elem, Xj);
+        const float t = __fmul_rn(fminf(fmaxf(vv[j], -clip), clip), inv_s);
+        qs[j] = qs_fast(t, Xs[j], slow);
+        if (DC_SUMS) qn[j] = qn_fast(t, slow);
+      }
+      if (slow) {
+        const float4 w4 = src.value(r0);
+        vv[0] = w4.x; vv[1] = w4.y; vv[2] = w4.z; vv[3] = w4.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          qs[j] = quant_stoch(vv[j], clip, s, inv_s, Xs[j]);
+          if (DC_SUMS) qn[j] = quant_nearest(vv[j], clip, s, inv_s);
+        }
+      }
+      signed char qq[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
         const float v = vv[j];
         bad |= !isfinite(v);
         m = fmaxf(m, fabsf(v));
-        const int qs = quant_stoch(v, clip, s, inv_s, Xj);
-        qq[j] = static_cast<signed char>(qs);
-        const double vd = v, gsd = tab[qs + 127];
+        qq[j] = static_cast<signed char>(qs[j]);
+        const double vd = v, gsd = tab0[qs[j]];
         const double d = vd - gsd;
         a5 = fma(d, d, a5);
         a6 = fma(gsd, gsd, a6);
         if (DC_SUMS) {
-          const double gn = tab[quant_nearest(v, clip, s, inv_s) + 127];
+          const double gn = tab0[qn[j]];
           a2 = fma(vd, vd, a2);
           a3 = fma(vd, gn, a3);
           a4 = fma(gn, gn, a4);

@@ -32,11 +32,18 @@ GEOMS = [
     (1, 64, 9, 9, 128, 3, 3, 2, 1, None, None, False),   # stride 2, floor mode
     (2, 32, 7, 7, 48, 1, 1, 1, 0, None, None, False),    # 1x1
     (2, 48, 10, 10, 40, 1, 1, 2, 0, None, None, False),  # 1x1 stride 2 (downsample)
-    (1, 3, 20, 20, 16, 7, 7, 2, 3, None, None, False),   # stem-like, C=3 (vec 4)
+    (1, 3, 20, 20, 16, 7, 7, 2, 3, None, None, False),   # stem-like, C=3 (tap-folded)
+    (2, 4, 12, 10, 24, 3, 5, 1, 1, 2, 2, False),         # C=4, kw=5, stride_w 2 (tap-folded)
+    (2, 3, 30, 30, 64, 7, 7, 2, 3, None, None, False),   # stem, even size, K=64
     (2, 24, 9, 9, 24, 3, 3, 1, 1, None, None, False),    # C=24 (vec 8)
     (1, 32, 9, 11, 40, 1, 7, 1, 0, 1, 3, False),         # 1x7 asym pad
     (1, 32, 11, 9, 40, 7, 1, 1, 3, 1, 0, False),         # 7x1 asym pad
     (1, 256, 7, 7, 300, 3, 3, 1, 1, None, None, False),  # N > 256 tile
+    # strided dgrad through the stride-phase decomposition (k % 128 == 0)
+    (2, 40, 11, 11, 128, 1, 1, 2, 0, None, None, False),  # 1x1 s2, zero phases, odd H
+    (2, 64, 10, 10, 256, 3, 3, 2, 1, None, None, False),  # 3x3 s2, four phases
+    (1, 24, 9, 10, 128, 3, 3, 2, 1, 1, 1, False),         # stride (2, 1)
+    (1, 16, 13, 13, 128, 7, 7, 2, 3, None, None, False),  # 7x7 s2 p3
     (3, 8, 6, 6, 8, 3, 3, 1, 1, None, None, True),       # depthwise
     (2, 40, 9, 9, 40, 3, 3, 2, 1, None, None, True),     # depthwise stride 2
 ]

@@ -88,12 +88,49 @@ def quant_case(n_elems, reps):
     return res
 
 
+def r50_table(reps):
+    """Every distinct ResNet-50 conv shape (batch 256) x multiplicity: measured
+    time per direction vs the attainable max(ops/peak, bytes/HBM) time."""
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from r50_roofline import layer_cost, r50_convs
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+    peak_ops, peak_bw = 2.0 * peaks["bf16_tflops_sustained"] * 1e12, peaks["hbm_gbs"] * 1e9
+    shapes = {}
+    for name, n, c, h, k, r, s, p in r50_convs():
+        key = (n, c, h, k, r, s, p, name == "stem")
+        shapes[key] = shapes.get(key, 0) + 1
+    rows, tot_meas, tot_att = [], 0.0, 0.0
+    for (n, c, h, k, r, s, p, stem), mult in shapes.items():
+        res = conv_case(f"{c}-{k}@{h} {r}x{r}/s{s}", n, c, h, k, r, s, p, reps)
+        cost = layer_cost(n, c, h, k, r, s, p, peak_ops, peak_bw, skip_dgrad=stem)
+        for d, (o, b, t_att) in cost.items():
+            t = res[d + "_ms"] * 1e-3
+            tot_meas += mult * t
+            tot_att += mult * t_att
+            rows.append({"shape": res["name"], "dir": d, "mult": mult, "ms": t * 1e3, "att_ms": t_att * 1e3,
+                         "frac_att": t_att / t, "tops": o / t / 1e12,
+                         "bound": "tensor" if o / peak_ops >= b / peak_bw else "hbm"})
+            print(f"{res['name']:22s} {d:5s} x{mult} {t * 1e3:8.4f} ms  att {t_att * 1e3:8.4f} ms  "
+                  f"{100 * t_att / t:5.1f}%  {o / t / 1e12:7.1f} TOPS  {rows[-1]['bound']}", flush=True)
+    print(f"TOTAL conv per step: measured {tot_meas * 1e3:.2f} ms, attainable {tot_att * 1e3:.2f} ms "
+          f"({100 * tot_att / tot_meas:.1f}%)", flush=True)
+    return {"rows": rows, "measured_ms": tot_meas * 1e3, "attainable_ms": tot_att * 1e3}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--r50", action="store_true", help="per-layer table of all ResNet-50 conv shapes")
     a = ap.parse_args()
+    if a.r50:
+        out = r50_table(a.reps)
+        if a.json:
+            with open(a.json, "w") as f:
+                json.dump(out, f, indent=1)
+        return
     B = a.batch
     cases = [
         ("config1_3x3_64", 32, 64, 56, 64, 3, 1, 1),
