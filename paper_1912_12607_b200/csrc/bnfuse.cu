@@ -44,12 +44,6 @@ __device__ __forceinline__ float bn_y(double gm, double xv, double bt) { return 
 // (2^-150 itself rounds to +0 under ties-to-even).
 __device__ __forceinline__ bool bn_pos(double gm, double xv, double bt) { return fma(gm, xv, bt) > 0x1.0p-150; }
 
-// x_hat = double(float(xv)) through the converting instructions; out of line so
-// the rare call stays a branch instead of predicated XU work in the hot loop.
-__device__ __noinline__ void exact_xh4(const double* xv, double* xh) {
-  for (int j = 0; j < 4; ++j) xh[j] = static_cast<double>(static_cast<float>(xv[j]));
-}
-
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
 template <int MODE>
@@ -75,27 +69,34 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   }
   if (active) {
     // U rows per thread per trip: all loads of a trip are issued before any math
-    constexpr int U = 4;
+    constexpr int U = MODE == 0 ? 8 : 2;
     const uint32_t row_step = gridDim.x * 8 * rpw;
     uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub;
-    for (; r < a.m; r += U * row_step) {
-      float4 zv[U], gv[U], yv[U];
+    // software pipeline: the U rows of the next trip are loaded before the
+    // current trip's math, so U (x tensors) 16-byte loads are always in flight
+    float4 zv[U], gv[U], yv[U], zn[U], gn[U], yn[U];
+    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t ru = r + u * row_step;
+        const uint32_t ru = rr + u * row_step;
         const size_t off = static_cast<size_t>(ru < a.m ? ru : r) * a.c + ch;
-        zv[u] = __ldg(reinterpret_cast<const float4*>(a.z + off));
-        if (MODE == 1) gv[u] = __ldg(reinterpret_cast<const float4*>(a.g + off));
-        if (MODE == 1 && a.mask_mode == 2) yv[u] = __ldg(reinterpret_cast<const float4*>(a.mask_y + off));
+        zd[u] = ldg_stream(a.z + off);
+        if (MODE == 1) gd[u] = ldg_stream(a.g + off);
+        if (MODE == 1 && a.mask_mode == 2) yd[u] = ldg_stream(a.mask_y + off);
       }
+    };
+    if (r < a.m) fetch(r, zv, gv, yv);
+    for (; r < a.m; r += U * row_step) {
+      const uint32_t rn = r + U * row_step;
+      if (rn < a.m) fetch(rn, zn, gn, yn);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (r + u * row_step >= a.m) break;
+        const bool valid = r + u * row_step < a.m;  // rows past the end re-read row r: not accumulated
         const float zz[4] = {zv[u].x, zv[u].y, zv[u].z, zv[u].w};
         if (MODE == 0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const double zd = zz[j];
+            const double zd = valid ? static_cast<double>(zz[j]) : 0.0;
             acc0[j] += zd;
             acc1[j] = fma(zd, zd, acc1[j]);
           }
@@ -107,19 +108,29 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             xv[j] = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
-            bool mk = true;
-            if (a.mask_mode == 1) mk = bn_pos(gmm[j], xv[j], bt[j]);
-            else if (a.mask_mode == 2) mk = yy[j] > 0.0f;
+            bool mk = valid;
+            if (a.mask_mode == 1) mk = mk && bn_pos(gmm[j], xv[j], bt[j]);
+            else if (a.mask_mode == 2) mk = mk && yy[j] > 0.0f;
             gm[j] = mk ? static_cast<double>(gg[j]) : 0.0;
             xh[j] = rn24(xv[j], sub);
           }
-          if (sub) exact_xh4(xv, xh);  // float-subnormal x_hat: a real (rare) branch
+          if (__any_sync(__activemask(), sub)) {  // float-subnormal x_hat (rare): the converting path
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (fabs(xv[j]) < 0x1.0p-126) xh[j] = static_cast<double>(static_cast<float>(xv[j]));
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             acc0[j] += gm[j];
             acc1[j] = fma(gm[j], xh[j], acc1[j]);
           }
         }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        zv[u] = zn[u];
+        if (MODE == 1) gv[u] = gn[u];
+        if (MODE == 1 && a.mask_mode == 2) yv[u] = yn[u];
       }
     }
   }
@@ -150,12 +161,45 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // last block: tpc threads per column fold the per-block partials (block
+  // b -> part b % tpc, fixed order), then a fixed-order sum over the parts
+  const uint32_t tpc = blockDim.x / gw;
+  double s0 = 0.0, s1 = 0.0;
+  if (threadIdx.x < gw * tpc) {
+    const uint32_t col = threadIdx.x % gw, part = threadIdx.x / gw;
+    // 8 independent load/add chains (latency-bound L2 reads), combined in a fixed order
+    double a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const double* base = partials + static_cast<size_t>(blockIdx.y) * gridDim.x * (2 * BN_GROUP) + col;
+    uint32_t b = part;
+    for (; b + 7 * tpc < gridDim.x; b += 8 * tpc) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double* p = base + static_cast<size_t>(b + k * tpc) * (2 * BN_GROUP);
+        a0[k] += __ldcg(p);
+        a1[k] += __ldcg(p + BN_GROUP);
+      }
+    }
+    for (int k = 0; b < gridDim.x; b += tpc, ++k) {
+      const double* p = base + static_cast<size_t>(b) * (2 * BN_GROUP);
+      a0[k] += __ldcg(p);
+      a1[k] += __ldcg(p + BN_GROUP);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      s0 += a0[k];
+      s1 += a1[k];
+    }
+  }
+  __shared__ double fold[2][256];
+  fold[0][threadIdx.x] = s0;
+  fold[1][threadIdx.x] = s1;
+  __syncthreads();
   if (threadIdx.x < gw) {
-    double s0 = 0.0, s1 = 0.0;
-    for (uint32_t b = 0; b < gridDim.x; ++b) {
-      const double* p = partials + (static_cast<size_t>(blockIdx.y) * gridDim.x + b) * (2 * BN_GROUP);
-      s0 += __ldcg(p + threadIdx.x);
-      s1 += __ldcg(p + BN_GROUP + threadIdx.x);
+    s0 = 0.0;
+    s1 = 0.0;
+    for (uint32_t part = 0; part < tpc; ++part) {
+      s0 += fold[0][part * gw + threadIdx.x];
+      s1 += fold[1][part * gw + threadIdx.x];
     }
     const uint32_t cc = c0 + threadIdx.x;
     const double m = static_cast<double>(a.m);
@@ -402,7 +446,7 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   const int groups = static_cast<int>((a.c + BN_GROUP - 1) / BN_GROUP);
   if (groups > 64) return set_error(I8T_EUNSUPPORTED, "bn: more than 8192 channels");
   int bx = static_cast<int>((a.m + 8 * 64 - 1) / (8 * 64));
-  const int cap = (148 * 4 + groups - 1) / groups;
+  const int cap = (148 * 2 + groups - 1) / groups;  // one resident wave (~100-128 registers)
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
   double* p = ensure_partials(c, static_cast<size_t>(bx) * groups * 2 * BN_GROUP);

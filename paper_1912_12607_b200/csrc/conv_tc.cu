@@ -60,6 +60,15 @@ struct ConvArgs {
   int Hq, Wq, fh, fw, r0, s0, ns, dh, dw;
 };
 
+// exact int32 -> double on the FP64 pipe (no XU conversion): 2^52 + (x + 2^31) - (2^52 + 2^31)
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+  return __hiloint2double(0x43300000, static_cast<int>(x ^ 0x80000000u)) - 4503601774854144.0;
+}
+// reference rescale float(double(s_x) * double(s_y) * acc) (conv.cpp:139-143)
+__device__ __forceinline__ float dequant_acc(double rescale, uint32_t v) {
+  return static_cast<float>(rescale * i32_to_f64(v));
+}
+
 // output row of GEMM row m (identity except in DGRAD phase mode)
 __device__ __forceinline__ int64_t out_row_of(const ConvArgs& a, int64_t m) {
   if (!a.phase) return m;
@@ -357,8 +366,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     const int row = quad * 32 + lane;
     const double rescale =
         static_cast<double>(__fdiv_rn(*args.clip_x, 127.0f)) * static_cast<double>(__fdiv_rn(*args.clip_y, 127.0f));
-    uint8_t* stage_base = sEpi + (warp - EPI_WARP0) * (32 * 128);
+    const uint32_t stage_s = smem_u32(sEpi + (warp - EPI_WARP0) * (32 * 128));
     int it = 0, nst = 0;
+    constexpr int HALF = BN / 2 < 32 ? 32 : BN / 2;
+    constexpr int NCH = HALF / 32;  // 32-column chunks per epilogue warp per tile
+    const int c_begin0 = half * HALF;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
       const TileCoord tc = tile_of(args, t);
       const int64_t m = static_cast<int64_t>(tc.m_tile) * BM + row;
@@ -367,15 +379,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      constexpr int HALF = BN / 2 < 32 ? 32 : BN / 2;
-      const int c_begin = half * HALF, c_end = (half + 1) * HALF < BN ? (half + 1) * HALF : BN;
+      const int c_begin = c_begin0, c_end = (half + 1) * HALF < BN ? (half + 1) * HALF : BN;
       if (c_begin >= c_end) {  // BN == 32 would leave the second half idle
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         continue;
       }
-#pragma unroll 1
-      for (int col = c_begin; col < c_end; col += 32) {
+      auto chunk = [&](const int ci) {
+        const int col = c_begin + ci * 32;
         uint32_t v[32];
         tmem_ld32(t_row + static_cast<uint32_t>(col), v);
         tmem_ld_wait();
@@ -385,8 +396,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         }
         const int gc0 = n0 + col;
         if (args.use_tma_out) {
-          // 32x32 sub-tile -> swizzled smem staging (double-buffered) -> one TMA bulk store
-          uint8_t* buf = stage_base;
+          // 32x32 sub-tile -> swizzled smem staging -> one TMA bulk store
+          const uint32_t buf_s = stage_s;
           if (lane == 0) bulk_wait_read<0>();  // the previous store has finished reading the buffer
           __syncwarp();
 #pragma unroll
@@ -395,18 +406,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             if constexpr (MODE == MODE_WGRAD) {
               w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
-              w.x = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 0]))));
-              w.y = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 1]))));
-              w.z = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 2]))));
-              w.w = __float_as_uint(static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 3]))));
+              w.x = __float_as_uint(dequant_acc(rescale, v[4 * j + 0]));
+              w.y = __float_as_uint(dequant_acc(rescale, v[4 * j + 1]));
+              w.z = __float_as_uint(dequant_acc(rescale, v[4 * j + 2]));
+              w.w = __float_as_uint(dequant_acc(rescale, v[4 * j + 3]));
             }
-            *reinterpret_cast<uint4*>(buf + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16))) = w;
+            sts128(buf_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * BM + quad * 32;
-            tma_store_2d(&tmap_out, smem_u32(buf), gc0, r0);
+            tma_store_2d(&tmap_out, buf_s, gc0, r0);
             bulk_commit();
           }
           ++nst;
@@ -418,17 +429,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   float4 w;
-                  w.x = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 0])));
-                  w.y = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 1])));
-                  w.z = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 2])));
-                  w.w = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[4 * j + 3])));
+                  w.x = dequant_acc(rescale, v[4 * j + 0]);
+                  w.y = dequant_acc(rescale, v[4 * j + 1]);
+                  w.z = dequant_acc(rescale, v[4 * j + 2]);
+                  w.w = dequant_acc(rescale, v[4 * j + 3]);
                   reinterpret_cast<float4*>(dst)[j] = w;
                 }
               } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
-                  if (gc0 + i < args.Ng)
-                    dst[i] = static_cast<float>(rescale * static_cast<double>(static_cast<int32_t>(v[i])));
+                  if (gc0 + i < args.Ng) dst[i] = dequant_acc(rescale, v[i]);
               }
             }
           }
@@ -439,7 +449,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           for (int i = 0; i < 32; ++i)
             if (gc0 + i < args.Ng) dst[i] = static_cast<int32_t>(v[i]);
         }
-      }
+      };
+#pragma unroll 1
+      for (int ci = 0; ci < NCH; ++ci) chunk(ci);
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
@@ -842,6 +854,7 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;
   return dispatch<MODE_FWD>(c->stream, x, bn, map, omap, vec_of(c_pad), 16);
 }
+
 
 int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt, int64_t ld_wt,
                    const float* clip_g, const float* clip_w, float* ga, int32_t* acc) {

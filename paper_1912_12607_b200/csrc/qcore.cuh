@@ -11,6 +11,17 @@
 
 namespace i8t_dev {
 
+// Streaming 16-byte load the compiler keeps in program order (asm volatile):
+// loops that issue several of these before using them get the memory-level
+// parallelism they ask for instead of loads sunk next to their uses.
+__device__ __forceinline__ float4 ldg_stream(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ float scale_of(float clip) { return __fdiv_rn(clip, 127.0f); }
 
 // x + RMAGIC rounds x (|x| < 2^22) to an integer held in the low mantissa bits:

@@ -284,3 +284,4 @@ def test_fused_int8_tracks_torch_bn():
     for a, b in zip(ra, rb):
         assert np.isfinite(a.loss) and not a.diverged
         assert a.loss == pytest.approx(b.loss, rel=2e-2)
+

@@ -31,6 +31,7 @@ gw = torch.empty((k, c, kk, kk), device="cuda")
 for _ in range(a.reps):
     if a.mode == "fwd":
         ops.conv_fwd_nhwc(g, qa, cp, qw, qw.shape[1], one, one, z_out=z)
+
     elif a.mode == "dgrad":
         ops.conv_dgrad_nhwc(g, qg, kp, qwt, qwt.shape[1], one, one, out=ga)
     else:
