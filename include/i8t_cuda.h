@@ -237,6 +237,17 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
  * mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0, 2 mask_y > 0. */
 int i8t_bn_fwd_stats(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, double momentum, double eps, double* bn,
                      float* running_mean, float* running_var);
+/* Max pooling k x k / stride s / zero-free padding `pad` on NHWC fp32 (the
+ * reference Pool2d, layers.cpp:346-380, has no padding: EXT).  x [n,h,w,c],
+ * y [n,P,Q,c], idx [n,P,Q,c] uint8 window slot (dy*k + dx) of the first max.
+ * With bn != NULL the input is act(bn(x)) (bn: i8t_bn_fwd_stats output,
+ * relu: apply ReLU) computed on the fly: the stem's BN + ReLU + pool in one pass. */
+int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int64_t s,
+                    int64_t pad, const double* bn, const float* gamma, const float* beta, int relu, float* y,
+                    uint8_t* idx);
+/* gx [n,h,w,c] = sum of gy over the windows whose argmax (idx) is (h, w). */
+int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n, int64_t h, int64_t w, int64_t c,
+                    int64_t k, int64_t s, int64_t pad, float* gx);
 /* q = quantize_nearest(act(bn(z)), clip) with running max|act| -> *amax: the
  * next conv's input quantiser (layers.cpp:101, 109) fused with BN + ReLU. */
 int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,

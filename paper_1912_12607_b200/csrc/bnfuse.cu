@@ -18,6 +18,7 @@
 #include "internal.cuh"
 #include "qcore.cuh"
 #include "qgrad.cuh"
+#include "bncore.cuh"
 
 namespace i8t_dev {
 
@@ -38,11 +39,6 @@ struct ColArgs {
   float* grad_gamma;    // MODE 1
   float* grad_beta;
 };
-
-__device__ __forceinline__ float bn_y(double gm, double xv, double bt) { return static_cast<float>(fma(gm, xv, bt)); }
-// float(gamma*x_hat + beta) > 0 without the conversion: RN32(d) > 0 <=> d > 2^-150
-// (2^-150 itself rounds to +0 under ties-to-even).
-__device__ __forceinline__ bool bn_pos(double gm, double xv, double bt) { return fma(gm, xv, bt) > 0x1.0p-150; }
 
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
@@ -224,24 +220,6 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   __syncthreads();
   if (threadIdx.x == 0) tickets[blockIdx.y] = 0u;
 }
-
-// Per-thread channel-quad coefficients of a BN layer.
-struct BnQuad {
-  double mean[4], invstd[4], gm[4], bt[4];
-  __device__ __forceinline__ void load(const double* bn, const float* gamma, const float* beta, uint32_t c,
-                                       uint32_t c0) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      mean[j] = bn[c0 + j];
-      invstd[j] = bn[c + c0 + j];
-      gm[j] = gamma[c0 + j];
-      bt[j] = beta[c0 + j];
-    }
-  }
-  __device__ __forceinline__ float y(int j, float z) const {
-    return bn_y(gm[j], (static_cast<double>(z) - mean[j]) * invstd[j], bt[j]);
-  }
-};
 
 // Forward: q = quantize_nearest(act(bn(z))), running max|act| (layers.cpp:101, 108-109).
 __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ z, uint32_t n, uint32_t c,

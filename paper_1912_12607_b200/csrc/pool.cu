@@ -1,0 +1,149 @@
+// pool.cu -- max pooling with padding on NHWC fp32 (the EXT of SURVEY.md A.3-5:
+// the reference Pool2d, layers.cpp:346-380, has no padding), fused with the
+// BatchNorm + ReLU that precede it in the ResNet stem:
+//   forward   y[n,p,q,c] = max over the k x k window of act(bn(z)) (or of x),
+//             idx = the window slot (dy*k + dx) of the first maximum, one byte;
+//   backward  gx[n,h,w,c] = sum of gy over the windows whose argmax is (h, w),
+//             gathered per input pixel in increasing (p, q) order.
+// Padded positions never win (they are skipped, i.e. -inf).  NaN wins like
+// torch's max_pool2d.  One thread per (pixel, channel quad); float4 I/O.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "bncore.cuh"
+#include "internal.cuh"
+
+namespace i8t_dev {
+
+struct PoolGeom {
+  int N, H, W, C, P, Q, k, s, pad;
+};
+
+template <bool BN>
+__global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x, PoolGeom g, const double* bn,
+                                                     const float* gamma, const float* beta, int relu,
+                                                     float* __restrict__ y, uint8_t* __restrict__ idx) {
+  const int c4n = g.C / 4;
+  const int64_t tot = static_cast<int64_t>(g.N) * g.P * g.Q * c4n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = static_cast<int>(i % c4n);
+    const int64_t pix = i / c4n;
+    const int q = static_cast<int>(pix % g.Q);
+    const int64_t np = pix / g.Q;
+    const int p = static_cast<int>(np % g.P), n = static_cast<int>(np / g.P);
+    BnQuad k;
+    if (BN) k.load(bn, gamma, beta, g.C, c4 * 4);
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int arg[4] = {0, 0, 0, 0};
+    bool any[4] = {false, false, false, false};
+    const int h0 = p * g.s - g.pad, w0 = q * g.s - g.pad;
+    for (int dy = 0; dy < g.k; ++dy) {
+      const int h = h0 + dy;
+      if (h < 0 || h >= g.H) continue;
+      for (int dx = 0; dx < g.k; ++dx) {
+        const int w = w0 + dx;
+        if (w < 0 || w >= g.W) continue;
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(x + ((static_cast<int64_t>(n) * g.H + h) * g.W + w) * g.C) + c4);
+        float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (BN) {
+            v[j] = k.y(j, v[j]);
+            if (relu) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+          }
+          if (!any[j] || v[j] > best[j] || isnan(v[j])) {  // torch's max_pool2d update rule
+            best[j] = v[j];
+            arg[j] = dy * g.k + dx;
+            any[j] = true;
+          }
+        }
+      }
+    }
+    reinterpret_cast<float4*>(y)[i] = make_float4(best[0], best[1], best[2], best[3]);
+    reinterpret_cast<uchar4*>(idx)[i] = make_uchar4(arg[0], arg[1], arg[2], arg[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ gy, const uint8_t* __restrict__ idx,
+                                                     PoolGeom g, float* __restrict__ gx) {
+  const int c4n = g.C / 4;
+  const int64_t tot = static_cast<int64_t>(g.N) * g.H * g.W * c4n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = static_cast<int>(i % c4n);
+    const int64_t pix = i / c4n;
+    const int w = static_cast<int>(pix % g.W);
+    const int64_t nh = pix / g.W;
+    const int h = static_cast<int>(nh % g.H), n = static_cast<int>(nh / g.H);
+    // windows p with p*s - pad <= h <= p*s - pad + k - 1
+    const int hp = h + g.pad, wp = w + g.pad;
+    const int p_lo = hp - g.k + 1 <= 0 ? 0 : (hp - g.k + g.s) / g.s, p_hi = min(hp / g.s, g.P - 1);
+    const int q_lo = wp - g.k + 1 <= 0 ? 0 : (wp - g.k + g.s) / g.s, q_hi = min(wp / g.s, g.Q - 1);
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int p = p_lo; p <= p_hi; ++p) {
+      const int dy = hp - p * g.s;
+      for (int q = q_lo; q <= q_hi; ++q) {
+        const int slot = dy * g.k + (wp - q * g.s);
+        const int64_t o = ((static_cast<int64_t>(n) * g.P + p) * g.Q + q) * c4n + c4;
+        const uchar4 a = reinterpret_cast<const uchar4*>(idx)[o];
+        const float4 v = __ldg(reinterpret_cast<const float4*>(gy) + o);
+        if (a.x == slot) acc[0] = __fadd_rn(acc[0], v.x);
+        if (a.y == slot) acc[1] = __fadd_rn(acc[1], v.y);
+        if (a.z == slot) acc[2] = __fadd_rn(acc[2], v.z);
+        if (a.w == slot) acc[3] = __fadd_rn(acc[3], v.w);
+      }
+    }
+    reinterpret_cast<float4*>(gx)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
+static int pool_geom(int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int64_t s, int64_t pad, PoolGeom* g) {
+  if (n < 1 || h < 1 || w < 1 || c < 4 || c % 4 != 0 || k < 1 || k > 15 || s < 1 || pad < 0 || 2 * pad > k)
+    return set_error(I8T_EINVAL, "maxpool: bad geometry (needs c % 4 == 0, k <= 15, pad <= k/2)");
+  if (h + 2 * pad < k || w + 2 * pad < k) return set_error(I8T_EINVAL, "maxpool: window larger than the input");
+  g->N = (int)n; g->H = (int)h; g->W = (int)w; g->C = (int)c; g->k = (int)k; g->s = (int)s; g->pad = (int)pad;
+  g->P = (int)((h + 2 * pad - k) / s + 1);
+  g->Q = (int)((w + 2 * pad - k) / s + 1);
+  return I8T_OK;
+}
+
+static int grid_of(int64_t tot) {
+  int64_t b = (tot + 255) / 256;
+  return static_cast<int>(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+}
+
+}  // namespace i8t_dev
+
+using namespace i8t_dev;
+
+extern "C" {
+
+int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int64_t s,
+                    int64_t pad, const double* bn, const float* gamma, const float* beta, int relu, float* y,
+                    uint8_t* idx) {
+  Ctx* cx = reinterpret_cast<Ctx*>(ctx);
+  PoolGeom g;
+  int rc = pool_geom(n, h, w, c, k, s, pad, &g);
+  if (rc) return rc;
+  if (!cx || !x || !y || !idx || (bn && (!gamma || !beta))) return set_error(I8T_EINVAL, "maxpool_fwd: bad arguments");
+  const int64_t tot = static_cast<int64_t>(g.N) * g.P * g.Q * (g.C / 4);
+  if (bn) k_maxpool_fwd<true><<<grid_of(tot), 256, 0, cx->stream>>>(x, g, bn, gamma, beta, relu, y, idx);
+  else k_maxpool_fwd<false><<<grid_of(tot), 256, 0, cx->stream>>>(x, g, nullptr, nullptr, nullptr, 0, y, idx);
+  count_launch(1);
+  return cuda_check("k_maxpool_fwd");
+}
+
+int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n, int64_t h, int64_t w, int64_t c,
+                    int64_t k, int64_t s, int64_t pad, float* gx) {
+  Ctx* cx = reinterpret_cast<Ctx*>(ctx);
+  PoolGeom g;
+  int rc = pool_geom(n, h, w, c, k, s, pad, &g);
+  if (rc) return rc;
+  if (!cx || !gy || !idx || !gx) return set_error(I8T_EINVAL, "maxpool_bwd: bad arguments");
+  const int64_t tot = static_cast<int64_t>(g.N) * g.H * g.W * (g.C / 4);
+  k_maxpool_bwd<<<grid_of(tot), 256, 0, cx->stream>>>(gy, idx, g, gx);
+  count_launch(1);
+  return cuda_check("k_maxpool_bwd");
+}
+
+}  // extern "C"

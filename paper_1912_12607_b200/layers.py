@@ -648,27 +648,52 @@ class ReLU(Layer):
 
 
 class MaxPool2d(Layer):
-    """Max pooling with padding (EXT: the reference Pool2d has none, A.3-5)."""
+    """Max pooling with padding (EXT: the reference Pool2d has none, A.3-5) on
+    csrc/pool.cu: the one-byte argmax replaces torch's int64 indices, and a
+    preceding lazy BN + ReLU (the ResNet stem) is applied inside the pool so its
+    fp32 output is never materialised."""
     kind = "maxpool"
 
     def __init__(self, k, s, p=0):
         self.k, self.s, self.p = k, s, p
 
     def forward(self, x, ctx):
-        x = dense(x)
-        xc = x.permute(0, 3, 1, 2)
-        y, self._idx = torch.ops.aten.max_pool2d_with_indices(xc, [self.k, self.k], [self.s, self.s],
-                                                              [self.p, self.p])
-        self._xc = xc
-        return y.permute(0, 2, 3, 1).contiguous()
+        lazy = isinstance(x, LazyAct) and x.shape[-1] % 4 == 0
+        src = x.z if lazy else dense(x).contiguous()
+        n, h, w, c = src.shape
+        if c % 4 or 2 * self.p > self.k:
+            xc = src.permute(0, 3, 1, 2)
+            y, self._idx = torch.ops.aten.max_pool2d_with_indices(xc, [self.k, self.k], [self.s, self.s],
+                                                                  [self.p, self.p])
+            self._xc, self._torch = xc, True
+            return y.permute(0, 2, 3, 1).contiguous()
+        P = (h + 2 * self.p - self.k) // self.s + 1
+        Q = (w + 2 * self.p - self.k) // self.s + 1
+        y = torch.empty((n, P, Q, c), dtype=torch.float32, device=src.device)
+        idx = torch.empty((n, P, Q, c), dtype=torch.uint8, device=src.device)
+        bn = x.bn if lazy else None
+        call("i8t_maxpool_fwd", ops.ctx(), ops._p(src), n, h, w, c, self.k, self.s, self.p,
+             ops._p(bn.stats) if bn else None, ops._p(bn.gamma) if bn else None, ops._p(bn.beta) if bn else None,
+             int(x.relu) if lazy else 0, ops._p(y), ops._p(idx))
+        self._torch = False
+        if ctx.training:
+            self._idx, self._in_shape = idx, (n, h, w, c)
+        return y
 
     def backward(self, g, ctx):
-        g = dense_grad(g)
-        gi = torch.ops.aten.max_pool2d_with_indices_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k],
-                                                             [self.s, self.s], [self.p, self.p], [1, 1], False,
-                                                             self._idx)
-        self._xc = self._idx = None
-        return gi.permute(0, 2, 3, 1).contiguous()
+        g = dense_grad(g).contiguous()
+        if self._torch:
+            gi = torch.ops.aten.max_pool2d_with_indices_backward(g.permute(0, 3, 1, 2), self._xc, [self.k, self.k],
+                                                                 [self.s, self.s], [self.p, self.p], [1, 1], False,
+                                                                 self._idx)
+            self._xc = self._idx = None
+            return gi.permute(0, 2, 3, 1).contiguous()
+        n, h, w, c = self._in_shape
+        gx = torch.empty((n, h, w, c), dtype=torch.float32, device=g.device)
+        call("i8t_maxpool_bwd", ops.ctx(), ops._p(g), ops._p(self._idx), n, h, w, c, self.k, self.s, self.p,
+             ops._p(gx))
+        self._idx = None
+        return gx
 
 
 class AvgPool2d(Layer):

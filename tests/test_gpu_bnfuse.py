@@ -285,3 +285,36 @@ def test_fused_int8_tracks_torch_bn():
         assert np.isfinite(a.loss) and not a.diverged
         assert a.loss == pytest.approx(b.loss, rel=2e-2)
 
+
+
+@pytest.mark.parametrize("shape", [(2, 112, 112, 64, 3, 2, 1), (3, 17, 15, 8, 3, 2, 0), (2, 9, 9, 12, 2, 2, 1)])
+@pytest.mark.parametrize("with_bn", [False, True])
+def test_maxpool_matches_torch(ops, shape, with_bn):
+    """csrc/pool.cu vs torch max_pool2d (+ its backward) on act(bn(z)) / x."""
+    n, h, w, c, k, s, p = shape
+    rng = np.random.default_rng(n * h + c)
+    x = rng.standard_normal((n * h * w, c)).astype(np.float32)
+    x[rng.random(x.shape) < 0.05] = 0.0  # ties
+    xt = t(x)
+    if with_bn:
+        gamma, beta = t(rng.uniform(0.5, 1.5, c).astype(np.float32)), t(rng.uniform(-.3, .3, c).astype(np.float32))
+        bn = _stats(ops, xt, c)
+        act = torch.empty_like(xt)
+        ops.call("i8t_bn_act", ops.ctx(), ops._p(xt), n * h * w, c, ops._p(bn), ops._p(gamma), ops._p(beta), 1, None,
+                 None, None, None, None, ops._p(act))
+    else:
+        act = xt
+    ref_in = act.view(n, h, w, c).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    ref = torch.nn.functional.max_pool2d(ref_in, k, s, p)
+    P, Q = ref.shape[2], ref.shape[3]
+    y = torch.empty((n, P, Q, c), device="cuda")
+    idx = torch.empty((n, P, Q, c), dtype=torch.uint8, device="cuda")
+    ops.call("i8t_maxpool_fwd", ops.ctx(), ops._p(xt), n, h, w, c, k, s, p, ops._p(bn) if with_bn else None,
+             ops._p(gamma) if with_bn else None, ops._p(beta) if with_bn else None, 1 if with_bn else 0, ops._p(y),
+             ops._p(idx))
+    assert torch.equal(y, ref.detach().permute(0, 2, 3, 1))
+    gy = torch.randn((n, P, Q, c), device="cuda")
+    ref.backward(gy.permute(0, 3, 1, 2))
+    gx = torch.empty((n, h, w, c), device="cuda")
+    ops.call("i8t_maxpool_bwd", ops.ctx(), ops._p(gy), ops._p(idx), n, h, w, c, k, s, p, ops._p(gx))
+    torch.testing.assert_close(gx, ref_in.grad.permute(0, 2, 3, 1), rtol=1e-6, atol=1e-6)
