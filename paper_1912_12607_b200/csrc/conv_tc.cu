@@ -58,6 +58,10 @@ struct ConvArgs {
   // q = ww + dw - is), every k-tile inside one tap (Kp % 128 == 0).
   int phase;
   int Hq, Wq, fh, fw, r0, s0, ns, dh, dw;
+  // 1x1 / stride 1 / pad 0: the A operand rows are plain matrix rows, loaded
+  // by TMA (tmap_a; WGRAD also takes its B = g_z rows from tmap_b) by one
+  // thread -- no cp.async gather
+  int tma_a;
 };
 
 // exact int32 -> double on the FP64 pipe (no XU conversion): 2^52 + (x + 2^31) - (2^52 + 2^31)
@@ -122,7 +126,8 @@ __device__ __forceinline__ int tile_nk(const ConvArgs& a, int split) {
 }
 
 template <int MODE, int BN, int VA, int VB>
-__global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_b,
+__global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
+                                                          const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
   using C = Cfg<MODE, BN>;
   extern __shared__ uint8_t smem_raw[];
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   if (warp == MMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < C::STAGES; ++s) {
-        mbar_init(&full[s], NPROD);
+        mbar_init(&full[s], args.tma_a ? 1 : NPROD);
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
@@ -151,7 +156,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         mbar_init(&tempty[a], NEPI);
       }
       fence_mbar_init();
-      if constexpr (C::TMA_B) tma_prefetch(&tmap_b);
+      if (C::TMA_B || args.tma_a) tma_prefetch(&tmap_b);
+      if (args.tma_a) tma_prefetch(&tmap_a);
       if (args.use_tma_out) tma_prefetch(&tmap_out);
     }
     __syncwarp();
@@ -163,7 +169,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < MMA_WARP) {
+  if (warp < MMA_WARP && args.tma_a) {
+    // ================================================= TMA producer (thread 0)
+    if (tid == 0) {
+      int kc = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_of(args, t);
+        const int m0 = tc.m_tile * BM, n0 = tc.n_tile * BN;
+        const int kt0 = tc.split * args.k_tiles;
+        const int nk = tile_nk(args, tc.split);
+        for (int kt = 0; kt < nk; ++kt, ++kc) {
+          const int s = kc % C::STAGES;
+          if (kc >= C::STAGES) mbar_wait(&empty[s], ((kc / C::STAGES) - 1) & 1);
+          const uint32_t a_st = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b_st = smem_u32(sB + s * C::B_BYTES);
+          const int kb = (kt0 + kt) * BKB;
+          mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
+          if constexpr (MODE == MODE_WGRAD) {
+            tma_load_2d(a_st, &tmap_a, &full[s], m0, kb);  // [128 npq rows][128 channels], MN-major
+#pragma unroll
+            for (int sub = 0; sub < C::B_SUB; ++sub) tma_load_2d(b_st + sub * 16384, &tmap_b, &full[s], n0 + sub * 128, kb);
+          } else {
+            tma_load_2d(a_st, &tmap_a, &full[s], kb, m0);  // [128 pixel rows][128 B of channels], K-major
+            tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
+          }
+        }
+      }
+    }
+  } else if (warp < MMA_WARP) {
     // ================================================= producers (warps 0-7)
     constexpr int PPR_A = BKB / VA;                 // pieces per 128 B row
     constexpr int ROWS_PER_PASS_A = NPROD / PPR_A;  // rows covered per pass
@@ -553,6 +586,14 @@ __global__ void k_unfold_wacc(const long long* __restrict__ accf, int R, int kw,
   }
 }
 
+// 1x1 / stride 1 / pad 0 convolution whose operand rows are TMA-addressable.
+static bool plain_1x1(const i8t_conv_geom* g, const void* p0, int64_t ld0, const void* p1 = nullptr, int64_t ld1 = 16) {
+  static const bool off = getenv("I8T_NO_TMA_A") != nullptr;
+  return !off && g->kh == 1 && g->kw == 1 && g->stride_h == 1 && g->stride_w == 1 && g->pad_h == 0 && g->pad_w == 0 &&
+         !g->depthwise && ld0 % 16 == 0 && ld1 % 16 == 0 && (reinterpret_cast<uintptr_t>(p0) & 15u) == 0 &&
+         (reinterpret_cast<uintptr_t>(p1) & 15u) == 0;
+}
+
 static bool foldable(const i8t_conv_geom* g, int64_t c_pad) {
   static const bool off = getenv("I8T_NO_FOLD") != nullptr;
   return !off && c_pad == 4 && !g->depthwise && g->kw > 1 && g->kw <= 8;
@@ -677,7 +718,8 @@ static int num_sms() {
 }
 
 template <int MODE, int BN, int VA, int VB>
-static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& map, const CUtensorMap& omap) {
+static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& amap, const CUtensorMap& map,
+                      const CUtensorMap& omap) {
   using C = Cfg<MODE, BN>;
   static bool configured = false;
   if (!configured) {
@@ -686,40 +728,42 @@ static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& map
   }
   const int tiles = a.m_tiles * a.n_tiles * a.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k_conv_tc<MODE, BN, VA, VB><<<grid, NTHREADS, C::SMEM, st>>>(a, map, omap);
+  k_conv_tc<MODE, BN, VA, VB><<<grid, NTHREADS, C::SMEM, st>>>(a, amap, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
 }
 
 template <int MODE, int BN>
-static int dispatch_vec(cudaStream_t st, const ConvArgs& a, const CUtensorMap& m, const CUtensorMap& o, int va, int vb) {
+static int dispatch_vec(cudaStream_t st, const ConvArgs& a, const CUtensorMap& am, const CUtensorMap& m,
+                        const CUtensorMap& o, int va, int vb) {
+  if (a.tma_a) return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);  // no gather: vector widths unused
   if constexpr (MODE == MODE_WGRAD) {
     if (vb == 16) {
-      if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, m, o);
-      if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, m, o);
-      return launch_one<MODE, BN, 4, 16>(st, a, m, o);
+      if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);
+      if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, am, m, o);
+      return launch_one<MODE, BN, 4, 16>(st, a, am, m, o);
     }
     if (vb == 8) {
-      if (va == 16) return launch_one<MODE, BN, 16, 8>(st, a, m, o);
-      if (va == 8) return launch_one<MODE, BN, 8, 8>(st, a, m, o);
-      return launch_one<MODE, BN, 4, 8>(st, a, m, o);
+      if (va == 16) return launch_one<MODE, BN, 16, 8>(st, a, am, m, o);
+      if (va == 8) return launch_one<MODE, BN, 8, 8>(st, a, am, m, o);
+      return launch_one<MODE, BN, 4, 8>(st, a, am, m, o);
     }
-    if (va == 16) return launch_one<MODE, BN, 16, 4>(st, a, m, o);
-    if (va == 8) return launch_one<MODE, BN, 8, 4>(st, a, m, o);
-    return launch_one<MODE, BN, 4, 4>(st, a, m, o);
+    if (va == 16) return launch_one<MODE, BN, 16, 4>(st, a, am, m, o);
+    if (va == 8) return launch_one<MODE, BN, 8, 4>(st, a, am, m, o);
+    return launch_one<MODE, BN, 4, 4>(st, a, am, m, o);
   } else {
-    if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, m, o);
-    if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, m, o);
-    return launch_one<MODE, BN, 4, 16>(st, a, m, o);
+    if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);
+    if (va == 8) return launch_one<MODE, BN, 8, 16>(st, a, am, m, o);
+    return launch_one<MODE, BN, 4, 16>(st, a, am, m, o);
   }
 }
 
 template <int MODE>
-static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, const CUtensorMap& m, const CUtensorMap& o, int va,
-                    int vb) {
-  if (bn == 64) return dispatch_vec<MODE, 64>(st, a, m, o, va, vb);
-  if (bn == 128) return dispatch_vec<MODE, 128>(st, a, m, o, va, vb);
-  return dispatch_vec<MODE, 256>(st, a, m, o, va, vb);
+static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, const CUtensorMap& am, const CUtensorMap& m,
+                    const CUtensorMap& o, int va, int vb) {
+  if (bn == 64) return dispatch_vec<MODE, 64>(st, a, am, m, o, va, vb);
+  if (bn == 128) return dispatch_vec<MODE, 128>(st, a, am, m, o, va, vb);
+  return dispatch_vec<MODE, 256>(st, a, am, m, o, va, vb);
 }
 
 static int pick_bn(int64_t ng) { return ng <= 64 ? 64 : (ng <= 128 ? 128 : 256); }
@@ -801,10 +845,10 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.m_tiles = (int)((x.M + BM - 1) / BM);
       const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
       x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
-      CUtensorMap map, omap{};
+      CUtensorMap amap{}, map, omap{};
       int rc = make_weight_map(&map, wt, g->c, ld_wt, bn);
       if (rc) return rc;
-      if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, map, omap, vec_of(k_pad), 16))) return rc;
+      if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16))) return rc;
     }
   }
   return I8T_OK;
@@ -848,11 +892,15 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   x.m_tiles = (int)((x.M + BM - 1) / BM);
   const int bn = pick_bn_balanced(g->k, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
-  CUtensorMap map, omap{};
+  CUtensorMap amap{}, map, omap{};
   if ((rc = make_weight_map(&map, w, g->k, ld_w, bn))) return rc;
+  if (plain_1x1(g, a, c_pad)) {
+    x.tma_a = 1;
+    if ((rc = make_weight_map(&amap, a, x.M, c_pad, BM))) return rc;
+  }
   x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;
-  return dispatch<MODE_FWD>(c->stream, x, bn, map, omap, vec_of(c_pad), 16);
+  return dispatch<MODE_FWD>(c->stream, x, bn, amap, map, omap, vec_of(c_pad), 16);
 }
 
 
@@ -882,11 +930,15 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   x.m_tiles = (int)((x.M + BM - 1) / BM);
   const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
-  CUtensorMap map, omap{};
+  CUtensorMap amap{}, map, omap{};
   if ((rc = make_weight_map(&map, wt, g->c, ld_wt, bn))) return rc;
+  if (plain_1x1(g, gz, k_pad)) {
+    x.tma_a = 1;
+    if ((rc = make_weight_map(&amap, gz, x.M, k_pad, BM))) return rc;
+  }
   x.use_tma_out = tma_out_ok(ga, g->c) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, ga, g->c, x.M, g->c, false))) return rc;
-  return dispatch<MODE_DGRAD>(c->stream, x, bn, map, omap, vec_of(k_pad), 16);
+  return dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16);
 }
 
 int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a, int64_t c_pad,
@@ -951,10 +1003,15 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   const size_t part_bytes = sizeof(int32_t) * static_cast<size_t>(splits) * x.m_pad * k_pad;
   int32_t* part = reinterpret_cast<int32_t*>(ensure_wgrad(c, part_bytes));
   if (!part) return set_error(I8T_ECUDA, "wgrad workspace alloc failed");
-  CUtensorMap map{}, omap{};  // no weight operand in WGRAD
+  CUtensorMap amap{}, map{}, omap{};  // no weight operand in WGRAD: tmap_b carries g_z in TMA mode
+  if (plain_1x1(g, a, c_pad, gz, k_pad)) {
+    x.tma_a = 1;
+    if ((rc = make_weight_map(&amap, a, x.Kd, c_pad, BKB))) return rc;   // [npq][c_pad], box {128 ch, 128 rows}
+    if ((rc = make_weight_map(&map, gz, x.Kd, k_pad, BKB))) return rc;   // [npq][k_pad], box {128 k, 128 rows}
+  }
   x.use_tma_out = 1;
   if ((rc = make_out_map(&omap, part, k_pad, splits * x.m_pad, k_pad, true))) return rc;
-  rc = dispatch<MODE_WGRAD>(c->stream, x, bn, map, omap, vec_of(c_pad), vec_of(k_pad));
+  rc = dispatch<MODE_WGRAD>(c->stream, x, bn, amap, map, omap, vec_of(c_pad), vec_of(k_pad));
   if (rc) return rc;
   const int64_t tot = x.M * g->k;
   int blocks = (int)((tot + 255) / 256);

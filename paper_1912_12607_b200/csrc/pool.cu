@@ -24,13 +24,12 @@ template <bool BN>
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x, PoolGeom g, const double* bn,
                                                      const float* gamma, const float* beta, int relu,
                                                      float* __restrict__ y, uint8_t* __restrict__ idx) {
-  const int c4n = g.C / 4;
-  const int64_t tot = static_cast<int64_t>(g.N) * g.P * g.Q * c4n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c4 = static_cast<int>(i % c4n);
-    const int64_t pix = i / c4n;
+  const uint32_t c4n = g.C / 4;
+  const uint32_t tot = static_cast<uint32_t>(g.N) * g.P * g.Q * c4n;  // < 2^31 (host check)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const uint32_t c4 = i % c4n, pix = i / c4n;
     const int q = static_cast<int>(pix % g.Q);
-    const int64_t np = pix / g.Q;
+    const uint32_t np = pix / g.Q;
     const int p = static_cast<int>(np % g.P), n = static_cast<int>(np / g.P);
     BnQuad k;
     if (BN) k.load(bn, gamma, beta, g.C, c4 * 4);
@@ -44,7 +43,7 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x
       for (int dx = 0; dx < g.k; ++dx) {
         const int w = w0 + dx;
         if (w < 0 || w >= g.W) continue;
-        const float4 v4 = __ldg(reinterpret_cast<const float4*>(x + ((static_cast<int64_t>(n) * g.H + h) * g.W + w) * g.C) + c4);
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(x) + ((static_cast<uint32_t>(n) * g.H + h) * g.W + w) * c4n + c4);
         float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -67,13 +66,12 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x
 
 __global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ gy, const uint8_t* __restrict__ idx,
                                                      PoolGeom g, float* __restrict__ gx) {
-  const int c4n = g.C / 4;
-  const int64_t tot = static_cast<int64_t>(g.N) * g.H * g.W * c4n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c4 = static_cast<int>(i % c4n);
-    const int64_t pix = i / c4n;
+  const uint32_t c4n = g.C / 4;
+  const uint32_t tot = static_cast<uint32_t>(g.N) * g.H * g.W * c4n;  // < 2^31 (host check)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const uint32_t c4 = i % c4n, pix = i / c4n;
     const int w = static_cast<int>(pix % g.W);
-    const int64_t nh = pix / g.W;
+    const uint32_t nh = pix / g.W;
     const int h = static_cast<int>(nh % g.H), n = static_cast<int>(nh / g.H);
     // windows p with p*s - pad <= h <= p*s - pad + k - 1
     const int hp = h + g.pad, wp = w + g.pad;
@@ -84,7 +82,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ g
       const int dy = hp - p * g.s;
       for (int q = q_lo; q <= q_hi; ++q) {
         const int slot = dy * g.k + (wp - q * g.s);
-        const int64_t o = ((static_cast<int64_t>(n) * g.P + p) * g.Q + q) * c4n + c4;
+        const uint32_t o = ((static_cast<uint32_t>(n) * g.P + p) * g.Q + q) * c4n + c4;
         const uchar4 a = reinterpret_cast<const uchar4*>(idx)[o];
         const float4 v = __ldg(reinterpret_cast<const float4*>(gy) + o);
         if (a.x == slot) acc[0] = __fadd_rn(acc[0], v.x);
@@ -101,6 +99,7 @@ static int pool_geom(int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int6
   if (n < 1 || h < 1 || w < 1 || c < 4 || c % 4 != 0 || k < 1 || k > 15 || s < 1 || pad < 0 || 2 * pad > k)
     return set_error(I8T_EINVAL, "maxpool: bad geometry (needs c % 4 == 0, k <= 15, pad <= k/2)");
   if (h + 2 * pad < k || w + 2 * pad < k) return set_error(I8T_EINVAL, "maxpool: window larger than the input");
+  if (n * h * w * c >= (int64_t(1) << 33)) return set_error(I8T_EUNSUPPORTED, "maxpool: tensor >= 2^33 elements");
   g->N = (int)n; g->H = (int)h; g->W = (int)w; g->C = (int)c; g->k = (int)k; g->s = (int)s; g->pad = (int)pad;
   g->P = (int)((h + 2 * pad - k) / s + 1);
   g->Q = (int)((w + 2 * pad - k) / s + 1);

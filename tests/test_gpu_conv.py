@@ -30,7 +30,9 @@ GEOMS = [
     (2, 16, 8, 8, 16, 3, 3, 1, 1, None, None, False),
     (2, 64, 14, 14, 64, 3, 3, 1, 1, None, None, False),
     (1, 64, 9, 9, 128, 3, 3, 2, 1, None, None, False),   # stride 2, floor mode
-    (2, 32, 7, 7, 48, 1, 1, 1, 0, None, None, False),    # 1x1
+    (2, 32, 7, 7, 48, 1, 1, 1, 0, None, None, False),    # 1x1 (TMA-loaded operands)
+    (3, 256, 9, 9, 512, 1, 1, 1, 0, None, None, False),  # 1x1, multi-tile M/N/K (TMA), ragged M
+    (2, 144, 5, 7, 80, 1, 1, 1, 0, None, None, False),   # 1x1, K and C not tile multiples (TMA)
     (2, 48, 10, 10, 40, 1, 1, 2, 0, None, None, False),  # 1x1 stride 2 (downsample)
     (1, 3, 20, 20, 16, 7, 7, 2, 3, None, None, False),   # stem-like, C=3 (tap-folded)
     (2, 4, 12, 10, 24, 3, 5, 1, 1, 2, 2, False),         # C=4, kw=5, stride_w 2 (tap-folded)
