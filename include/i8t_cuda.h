@@ -232,9 +232,13 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
 /* ------------------------------------------------------------ fused BatchNorm2d + ReLU
  * BatchNorm2d (layers.cpp:230-323) and ReLU (:328-344) are FP32 layers the
  * reference never quantises; these fuse them into the INT8 path's HBM passes.
- * Tensors are NHWC [m = N*H*W][c] fp32, c % 4 == 0.  bn: device doubles [5c]
- * (mean, invstd, s1/m, s2/m, gamma*invstd), filled by the calls below.
- * mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0, 2 mask_y > 0. */
+ * Tensors are NHWC [m = N*H*W][c] fp32, c % 4 == 0.  bn: device doubles [6c]
+ * (mean, invstd, s1/m, s2/m, gamma*invstd, ReLU-mask bounds), filled by the
+ * calls below.  mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0,
+ * 2 mask_y > 0.  With mask_mode 1, i8t_bn_bwd_reduce also stores per channel
+ * the float interval [lo, hi] with relu(bn(z)) > 0 <=> lo <= z <= hi (the map
+ * z -> float(gamma*x_hat + beta) is monotone), which i8t_bn_bwd_apply and
+ * i8t_quantize_gradient_bn then read: call them after i8t_bn_bwd_reduce. */
 int i8t_bn_fwd_stats(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, double momentum, double eps, double* bn,
                      float* running_mean, float* running_var);
 /* Max pooling k x k / stride s / zero-free padding `pad` on NHWC fp32 (the

@@ -53,14 +53,17 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   const uint32_t quad = lane % lpr, sub = lane / lpr;
   const uint32_t ch = c0 + quad * 4;
   double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
-  double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0}, gmm[4] = {0, 0, 0, 0}, bt[4] = {0, 0, 0, 0};
+  double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0};
+  float lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
   if (MODE == 1 && active) {
+    const float2* bounds = reinterpret_cast<const float2*>(a.bn + 5 * a.c);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       mean[j] = a.bn[ch + j];
       invstd[j] = a.bn[a.c + ch + j];
-      gmm[j] = a.gamma[ch + j];
-      bt[j] = a.beta[ch + j];
+      const float2 lh = bounds[ch + j];
+      lo[j] = lh.x;
+      hi[j] = lh.y;
     }
   }
   if (active) {
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
           for (int j = 0; j < 4; ++j) {
             xv[j] = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
             bool mk = valid;
-            if (a.mask_mode == 1) mk = mk && bn_pos(gmm[j], xv[j], bt[j]);
+            if (a.mask_mode == 1) mk = mk && zz[j] >= lo[j] && zz[j] <= hi[j];
             else if (a.mask_mode == 2) mk = mk && yy[j] > 0.0f;
             gm[j] = mk ? static_cast<double>(gg[j]) : 0.0;
             xh[j] = rn24(xv[j], sub);
@@ -327,7 +330,8 @@ struct BnBwdSrc {
   const float* gamma;
   const float* beta;
   uint32_t c;
-  double mean[4], invstd[4], gm[4], bt[4], a[4], b[4], k[4];
+  double mean[4], invstd[4], a[4], b[4], k[4];
+  float lo[4], hi[4];  // MASK 1: relu(bn(z)) > 0 <=> lo <= z <= hi
   struct Raw {
     float4 g, z, y;
   };
@@ -340,8 +344,9 @@ struct BnBwdSrc {
       b[j] = bn[3 * c + c0 + j];
       k[j] = bn[4 * c + c0 + j];
       if (MASK == 1) {
-        gm[j] = gamma[c0 + j];
-        bt[j] = beta[c0 + j];
+        const float2 lh = reinterpret_cast<const float2*>(bn + 5 * c)[c0 + j];
+        lo[j] = lh.x;
+        hi[j] = lh.y;
       }
     }
   }
@@ -361,7 +366,7 @@ struct BnBwdSrc {
     for (int j = 0; j < 4; ++j) {
       const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
       bool mk = true;
-      if (MASK == 1) mk = bn_pos(gm[j], xv, bt[j]);
+      if (MASK == 1) mk = zz[j] >= lo[j] && zz[j] <= hi[j];
       if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
       const double gd = mk ? static_cast<double>(gg[j]) : 0.0;
       const double xh = FAST ? rn24(xv, slow) : static_cast<double>(static_cast<float>(xv));
@@ -399,6 +404,13 @@ __global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a,
     o.w = __fadd_rn(av.w, yv.w > 0.0f ? gv.w : 0.0f);
     reinterpret_cast<float4*>(out)[i] = o;
   }
+}
+
+// ReLU-mask bounds per channel into bn[5c..6c) (as float2).
+__global__ void k_bn_mask_bounds(double* bn, const float* gamma, const float* beta, uint32_t c) {
+  const uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= c) return;
+  reinterpret_cast<float2*>(bn + 5 * c)[ch] = bn_mask_bounds(bn[ch], bn[c + ch], gamma[ch], beta[ch]);
 }
 
 // ---------------------------------------------------------------- host
@@ -502,6 +514,12 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
   a.z = z; a.g = g; a.mask_y = mask_y; a.gamma = gamma; a.beta = beta; a.bn = bn;
   a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = mask_mode;
   a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
+  if (mask_mode == 1) {
+    k_bn_mask_bounds<<<static_cast<unsigned>((c + 127) / 128), 128, 0, cx->stream>>>(bn, gamma, beta,
+                                                                                     static_cast<uint32_t>(c));
+    count_launch(1);
+    if ((rc = cuda_check("k_bn_mask_bounds"))) return rc;
+  }
   return colsum(cx, a, 1);
 }
 

@@ -62,6 +62,7 @@ struct ConvArgs {
   // by TMA (tmap_a; WGRAD also takes its B = g_z rows from tmap_b) by one
   // thread -- no cp.async gather
   int tma_a;
+  int tma_b;  // WGRAD with a gathered A: B = g_z rows still come by TMA (tmap_b)
 };
 
 // exact int32 -> double on the FP64 pipe (no XU conversion): 2^52 + (x + 2^31) - (2^52 + 2^31)
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         mbar_init(&tempty[a], NEPI);
       }
       fence_mbar_init();
-      if (C::TMA_B || args.tma_a) tma_prefetch(&tmap_b);
+      if (C::TMA_B || args.tma_a || args.tma_b) tma_prefetch(&tmap_b);
       if (args.tma_a) tma_prefetch(&tmap_a);
       if (args.use_tma_out) tma_prefetch(&tmap_out);
     }
@@ -326,6 +327,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             while (p >= args.P) { p -= args.P; ++n; }
             rowA_x[i] = q; rowA_y[i] = p; rowA_n[i] = n;
           }
+          if (args.tma_b) {  // g_z rows by TMA (thread 0; same barrier protocol as the FWD weights)
+            if (tid == 0) {
+              mbar_expect_tx(&full[s], C::B_BYTES);
+#pragma unroll
+              for (int sub = 0; sub < C::B_SUB; ++sub)
+                tma_load_2d(b_st + sub * 16384, &tmap_b, &full[s], n0 + sub * 128, static_cast<int>(kbase));
+            }
+          } else {
           constexpr int PPR_B = BKB / VB;
           constexpr int RPP_B = NPROD / PPR_B;
           constexpr int PASSES_B = BM / RPP_B;
@@ -345,6 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                 cp_async_vec<VB>(b_st + sub * 16384 + sw128_offset(row, jb * VB), src, ok);
               }
             }
+          }
           }
         }
         // the stage's full barrier completes when every producer's copies have
@@ -1007,6 +1017,10 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (plain_1x1(g, a, c_pad, gz, k_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, a, x.Kd, c_pad, BKB))) return rc;   // [npq][c_pad], box {128 ch, 128 rows}
+  }
+  static const bool no_tma_b = getenv("I8T_NO_TMA_A") != nullptr;
+  if (x.tma_a || (!no_tma_b && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0)) {
+    x.tma_b = !x.tma_a;
     if ((rc = make_weight_map(&map, gz, x.Kd, k_pad, BKB))) return rc;   // [npq][k_pad], box {128 k, 128 rows}
   }
   x.use_tma_out = 1;

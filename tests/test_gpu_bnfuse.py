@@ -68,7 +68,7 @@ def t(x):
 
 
 def _stats(ops, z, c, rm=None, rv=None):
-    bn = torch.zeros(5 * c, dtype=torch.float64, device="cuda")
+    bn = torch.zeros(6 * c, dtype=torch.float64, device="cuda")
     ops.call("i8t_bn_fwd_stats", ops.ctx(), ops._p(z), z.numel() // c, c, C.c_double(0.1), C.c_double(1e-5),
              ops._p(bn), ops._p(rm), ops._p(rv))
     return bn

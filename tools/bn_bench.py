@@ -28,7 +28,7 @@ for m, c in [(256 * 112 * 112, 64), (256 * 3136, 64), (256 * 3136, 256), (256 * 
     z = torch.randn(m, c, device="cuda")
     g = torch.randn(m, c, device="cuda") * 1e-3
     gamma, beta = torch.ones(c, device="cuda"), torch.zeros(c, device="cuda")
-    bn = torch.zeros(5 * c, dtype=torch.float64, device="cuda")
+    bn = torch.zeros(6 * c, dtype=torch.float64, device="cuda")
     gg, gb = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
     f0 = lambda: ops.call("i8t_bn_fwd_stats", ops.ctx(), ops._p(z), m, c, C.c_double(0.1), C.c_double(1e-5),
                           ops._p(bn), None, None)
