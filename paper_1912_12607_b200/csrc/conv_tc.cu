@@ -893,6 +893,9 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
     const i8t_conv_geom f = folded_geom(g, Q);
     return i8t_conv_fwd(ctx, &f, xf, 32, wf, g->kh * 32, clip_a, clip_w, z, acc);
   }
+  if (conv_sw_eligible(g, c_pad, (int)g->k, (int)P, (int)Q, a, z, ld_w))
+    return conv_sw_run(c, false, g, a, c_pad, (int)g->h, (int)g->w, w, ld_w, (int)g->k, (int)P, (int)Q, clip_a, clip_w,
+                       z, acc);
   ConvArgs x{};
   fill_geom(x, g, P, Q);
   x.act = a; x.gz = nullptr; x.wt = w; x.ldw = ld_w; x.Cp = (int)c_pad; x.Kp = (int)g->k;
@@ -931,6 +934,9 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
     static const bool off = getenv("I8T_NO_DGRAD_PHASE") != nullptr;
     if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc);
   }
+  if (conv_sw_eligible(g, k_pad, (int)g->c, (int)g->h, (int)g->w, gz, ga, ld_wt))
+    return conv_sw_run(c, true, g, gz, k_pad, (int)P, (int)Q, wt, ld_wt, (int)g->c, (int)g->h, (int)g->w, clip_g,
+                       clip_w, ga, acc);
   ConvArgs x{};
   fill_geom(x, g, P, Q);
   x.act = nullptr; x.gz = gz; x.wt = wt; x.ldw = ld_wt; x.Cp = (int)g->c; x.Kp = (int)k_pad;

@@ -86,6 +86,13 @@ void* ensure_wgrad(Ctx* c, size_t bytes);
 void* ensure_fold(Ctx* c, size_t bytes);
 
 void count_launch(int n = 1);
+
+// shifted-window stride-1 convolution (conv_sw.cu)
+bool conv_sw_eligible(const i8t_conv_geom* g, int64_t Cred, int Ng, int OH, int OW, const void* in, const void* out,
+                      int64_t ldw);
+int conv_sw_run(Ctx* c, bool dgrad, const i8t_conv_geom* g, const int8_t* in, int64_t Cred, int IH, int IW,
+                const int8_t* wts, int64_t ldw, int Ng, int OH, int OW, const float* clip_x, const float* clip_y,
+                float* out, int32_t* acc);
 int set_error(int status, const std::string& msg);
 int cuda_check(const char* what);
 

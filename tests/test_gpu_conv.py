@@ -28,7 +28,10 @@ GEOMS = [
     # n, c, h, w, k, kh, kw, stride, pad, stride_w, pad_w, depthwise
     (1, 2, 5, 5, 3, 3, 3, 1, 1, None, None, False),      # spec's fixed case
     (2, 16, 8, 8, 16, 3, 3, 1, 1, None, None, False),
-    (2, 64, 14, 14, 64, 3, 3, 1, 1, None, None, False),
+    (2, 64, 14, 14, 64, 3, 3, 1, 1, None, None, False),   # shifted-window path (conv_sw.cu)
+    (2, 128, 28, 28, 128, 3, 3, 1, 1, None, None, False),  # shifted-window, two n-tiles
+    (1, 64, 30, 30, 192, 3, 3, 1, 1, None, None, False),   # shifted-window, ragged tiles, K < BN
+    (1, 64, 24, 24, 64, 1, 3, 1, 0, 1, 1, False),          # shifted-window 1x3
     (1, 64, 9, 9, 128, 3, 3, 2, 1, None, None, False),   # stride 2, floor mode
     (2, 32, 7, 7, 48, 1, 1, 1, 0, None, None, False),    # 1x1 (TMA-loaded operands)
     (3, 256, 9, 9, 512, 1, 1, 1, 0, None, None, False),  # 1x1, multi-tile M/N/K (TMA), ragged M
