@@ -245,23 +245,51 @@ def main():
         tr.sync_states()
         it += 1
 
+    copy_stream = torch.cuda.Stream()
+    dev_bufs = [(torch.empty_like(x), torch.empty_like(y)) for _ in range(2)]
+
     def timed(n, e2e=False, host=None):
+        """e2e: the batch of step i+1 is copied host->device on a side stream
+        while step i computes (double-buffered, like a data loader), and every
+        step's loss is copied device->host (pinned) right after the step; the
+        host reads all of them before the timed region closes."""
         nonlocal it
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = ops.launch_count()
+        comp = torch.cuda.current_stream()
         ev0.record()
-        for _ in range(n):
+        if e2e:
+            loss_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            ready = [torch.cuda.Event(), torch.cuda.Event()]
+            freed = [None, None]
+
+            def prefetch(i):
+                b = i % 2
+                copy_stream.wait_stream(comp) if freed[b] is None else copy_stream.wait_event(freed[b])
+                with torch.cuda.stream(copy_stream):
+                    dev_bufs[b][0].copy_(host[0], non_blocking=True)
+                    dev_bufs[b][1].copy_(host[1], non_blocking=True)
+                    ready[b].record(copy_stream)
+
+            prefetch(0)
+        for i in range(n):
             if e2e:
-                xs = host[0].to("cuda", non_blocking=True)
-                ys = host[1].to("cuda", non_blocking=True)
-                tr.train_step(xs, ys, it, total, read_stats=False)
-                float(tr.loss_dev.item())  # D2H of the step's loss
+                b = i % 2
+                comp.wait_event(ready[b])
+                if i + 1 < n:
+                    prefetch(i + 1)
+                tr.train_step(dev_bufs[b][0], dev_bufs[b][1], it, total, read_stats=False)
+                freed[b] = torch.cuda.Event()
+                freed[b].record(comp)
+                loss_host[i:i + 1].copy_(tr.loss_dev.view(1), non_blocking=True)  # D2H of the step's loss
             else:
                 tr.train_step(x, y, it, total, read_stats=False)
             it += 1
         ev1.record()
         barrier()
+        if e2e:
+            assert torch.isfinite(loss_host).all(), "non-finite loss in the e2e run"
         return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() - launches0
 
     if os.environ.get("I8T_PROFILE_STEP"):  # ncu --profile-from-start off: capture exactly one normal step

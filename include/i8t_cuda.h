@@ -199,6 +199,15 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
  *   ga  : NHWC float [N*H*W][C] (may be NULL); acc int32 (may be NULL) */
 int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
                    int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc);
+/* Backward-data with the residual join fused into its epilogue (the shortcut
+ * gradient sum of ResidualBlock::backward, layers.cpp:458-464):
+ *   ga = dgrad + add_g                 (add_y == NULL: projection shortcut)
+ *   ga = dgrad + add_g * (add_y > 0)   (identity shortcut through the block ReLU)
+ * add_g / add_y: NHWC fp32 [N*H*W][C], 16-byte aligned, C % 4 == 0.  One float
+ * add per element, so ga equals i8t_conv_dgrad followed by the join bit for bit. */
+int i8t_conv_dgrad_join(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                        int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
+                        const float* add_y);
 /* Backward-weight (conv.cpp:186-195), int64 accumulation (no depth bound):
  *   acc : int64 workspace [kh*kw*c_pad][K] (zeroed by the call)
  *   gw  : float weights, KCRS when out_kcrs != 0 else KRSC (may be NULL) */

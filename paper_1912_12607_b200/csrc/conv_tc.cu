@@ -63,7 +63,26 @@ struct ConvArgs {
   // thread -- no cp.async gather
   int tma_a;
   int tma_b;  // WGRAD with a gathered A: B = g_z rows still come by TMA (tmap_b)
+  // DGRAD residual join fused into the epilogue: out = dgrad + add_g, or
+  // dgrad + add_g * (add_y > 0) when add_y is set (a single float add, so the
+  // result equals the separate join bit for bit)
+  const float* add_g;
+  const float* add_y;
 };
+
+// residual addend of output row `orow`, columns c0..c0+3
+__device__ __forceinline__ float4 join_addend(const ConvArgs& a, int64_t orow, int c0) {
+  const int64_t o = orow * a.ldo + c0;
+  float4 g = __ldg(reinterpret_cast<const float4*>(a.add_g + o));
+  if (a.add_y) {
+    const float4 y = __ldg(reinterpret_cast<const float4*>(a.add_y + o));
+    g.x = y.x > 0.0f ? g.x : 0.0f;
+    g.y = y.y > 0.0f ? g.y : 0.0f;
+    g.z = y.z > 0.0f ? g.z : 0.0f;
+    g.w = y.w > 0.0f ? g.w : 0.0f;
+  }
+  return g;
+}
 
 // exact int32 -> double on the FP64 pipe (no XU conversion): 2^52 + (x + 2^31) - (2^52 + 2^31)
 __device__ __forceinline__ double i32_to_f64(uint32_t x) {
@@ -449,10 +468,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             if constexpr (MODE == MODE_WGRAD) {
               w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
-              w.x = __float_as_uint(dequant_acc(rescale, v[4 * j + 0]));
-              w.y = __float_as_uint(dequant_acc(rescale, v[4 * j + 1]));
-              w.z = __float_as_uint(dequant_acc(rescale, v[4 * j + 2]));
-              w.w = __float_as_uint(dequant_acc(rescale, v[4 * j + 3]));
+              float4 f = make_float4(dequant_acc(rescale, v[4 * j + 0]), dequant_acc(rescale, v[4 * j + 1]),
+                                     dequant_acc(rescale, v[4 * j + 2]), dequant_acc(rescale, v[4 * j + 3]));
+              if (MODE == MODE_DGRAD && args.add_g && m < args.M && gc0 + 4 * j < args.Ng) {
+                const float4 ad = join_addend(args, out_row_of(args, m), gc0 + 4 * j);
+                f.x = __fadd_rn(f.x, ad.x); f.y = __fadd_rn(f.y, ad.y); f.z = __fadd_rn(f.z, ad.z); f.w = __fadd_rn(f.w, ad.w);
+              }
+              w = make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), __float_as_uint(f.w));
             }
             sts128(buf_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
           }
@@ -476,12 +498,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                   w.y = dequant_acc(rescale, v[4 * j + 1]);
                   w.z = dequant_acc(rescale, v[4 * j + 2]);
                   w.w = dequant_acc(rescale, v[4 * j + 3]);
+                  if (MODE == MODE_DGRAD && args.add_g) {
+                    const float4 ad = join_addend(args, out_row_of(args, m), gc0 + 4 * j);
+                    w.x = __fadd_rn(w.x, ad.x); w.y = __fadd_rn(w.y, ad.y); w.z = __fadd_rn(w.z, ad.z); w.w = __fadd_rn(w.w, ad.w);
+                  }
                   reinterpret_cast<float4*>(dst)[j] = w;
                 }
               } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
-                  if (gc0 + i < args.Ng) dst[i] = dequant_acc(rescale, v[i]);
+                  if (gc0 + i < args.Ng) {
+                    float o = dequant_acc(rescale, v[i]);
+                    if (MODE == MODE_DGRAD && args.add_g) {
+                      const int64_t ai = out_row_of(args, m) * args.ldo + gc0 + i;
+                      const float ad = (!args.add_y || args.add_y[ai] > 0.0f) ? args.add_g[ai] : 0.0f;
+                      o = __fadd_rn(o, ad);
+                    }
+                    dst[i] = o;
+                  }
               }
             }
           }
@@ -638,7 +672,14 @@ __global__ void k_zero_phase(ConvArgs a) {
     float4* dst = reinterpret_cast<float4*>(a.out + o * a.ldo);
     int4* acc = a.acc32 ? reinterpret_cast<int4*>(a.acc32 + o * a.Ng) : nullptr;
     for (int c = lane; c < c4; c += 32) {
-      if (a.out) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.out) {
+        float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.add_g) {  // the join adds the addend to this (+0) dgrad value
+          const float4 ad = join_addend(a, o, 4 * c);
+          z = make_float4(__fadd_rn(0.f, ad.x), __fadd_rn(0.f, ad.y), __fadd_rn(0.f, ad.z), __fadd_rn(0.f, ad.w));
+        }
+        dst[c] = z;
+      }
       if (acc) acc[c] = make_int4(0, 0, 0, 0);
     }
   }
@@ -822,7 +863,7 @@ static void fill_geom(ConvArgs& x, const i8t_conv_geom* g, int64_t P, int64_t Q)
 // runs on the zero-stuffed positions of the reference's col2im (conv.cpp:60-84).
 static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, const int8_t* gz, int64_t k_pad,
                         const int8_t* wt, int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga,
-                        int32_t* acc) {
+                        int32_t* acc, const float* add_g, const float* add_y) {
   const int sh = (int)g->stride_h, sw = (int)g->stride_w;
   for (int fh = 0; fh < sh; ++fh) {
     for (int fw = 0; fw < sw; ++fw) {
@@ -841,6 +882,7 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.dw = (int)((fw + g->pad_w - x.s0) / sw);
       x.M = g->n * x.Hq * x.Wq; x.Ng = (int)g->c;
       x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
+      x.add_g = add_g; x.add_y = add_y;
       x.use_tma_out = 0;
       if (nr == 0 || x.ns == 0) {
         const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
@@ -917,8 +959,29 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
 }
 
 
+static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                      int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc,
+                      const float* add_g, const float* add_y);
+
 int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt, int64_t ld_wt,
                    const float* clip_g, const float* clip_w, float* ga, int32_t* acc) {
+  return dgrad_impl(ctx, g, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc, nullptr, nullptr);
+}
+
+int i8t_conv_dgrad_join(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                        int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
+                        const float* add_y) {
+  if (!ga || !add_g) return set_error(I8T_EINVAL, "conv_dgrad_join: null output or addend");
+  if ((reinterpret_cast<uintptr_t>(add_g) & 15u) || (reinterpret_cast<uintptr_t>(add_y) & 15u) || (g && g->c % 4))
+    return set_error(I8T_EUNSUPPORTED, "conv_dgrad_join: addends must be 16-byte aligned with c % 4 == 0");
+  return dgrad_impl(ctx, g, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, nullptr, add_g, add_y);
+}
+
+}  // extern "C"
+
+static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                      int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc,
+                      const float* add_g, const float* add_y) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   int64_t P, Q;
   int rc = geom_common(g, P, Q);
@@ -932,9 +995,9 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (g->k * g->kh * g->kw > 133000) return set_error(I8T_EUNSUPPORTED, "conv_dgrad: int32 accumulator bound");
   if ((g->stride_h > 1 || g->stride_w > 1) && k_pad % 128 == 0 && g->c % 4 == 0 && (ld_wt % 16) == 0) {
     static const bool off = getenv("I8T_NO_DGRAD_PHASE") != nullptr;
-    if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc);
+    if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc, add_g, add_y);
   }
-  if (conv_sw_eligible(g, k_pad, (int)g->c, (int)g->h, (int)g->w, gz, ga, ld_wt))
+  if (!add_g && conv_sw_eligible(g, k_pad, (int)g->c, (int)g->h, (int)g->w, gz, ga, ld_wt))
     return conv_sw_run(c, true, g, gz, k_pad, (int)P, (int)Q, wt, ld_wt, (int)g->c, (int)g->h, (int)g->w, clip_g,
                        clip_w, ga, acc);
   ConvArgs x{};
@@ -943,6 +1006,7 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   x.M = g->n * g->h * g->w; x.Ng = (int)g->c; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
+  x.add_g = add_g; x.add_y = add_y;
   x.m_tiles = (int)((x.M + BM - 1) / BM);
   const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
@@ -956,6 +1020,8 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (x.use_tma_out && (rc = make_out_map(&omap, ga, g->c, x.M, g->c, false))) return rc;
   return dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16);
 }
+
+extern "C" {
 
 int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a, int64_t c_pad,
                    const float* clip_g, const float* clip_a, int64_t* acc, float* gw, int out_kcrs) {

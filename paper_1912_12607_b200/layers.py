@@ -75,6 +75,10 @@ class ParamRef:
 # value materialised at once (bit-identical results, used to test the
 # plumbing); "torch": torch's fp32 batch norm.
 BN_IMPL = os.environ.get("I8T_BN", "fused")
+# residual joins inside the dgrad epilogue (I8T_JOIN=1).  Off by default: the
+# addend loads sit on the epilogue's critical path and measured slower (7.2 ms
+# vs 2.1 + 3.0 ms for dgrad + separate joins per ResNet-50 step, B200).
+JOIN_FUSION = os.environ.get("I8T_JOIN", "0") == "1"
 
 
 class LazyAct:
@@ -316,6 +320,10 @@ class Conv2d(Layer):
         self.keep_qg = False  # Dense needs the int8 gradient for its bias
         self._qg = None
         self.need_input_grad = True  # False for the first layer: the image gradient is discarded
+        # residual join handed down by a ResidualBlock: (add_g, add_y) -> the
+        # dgrad epilogue returns dgrad + add_g [* (add_y > 0)]; join_done reports it
+        self.dgrad_join = None
+        self.join_done = False
 
     @property
     def quantized(self):
@@ -438,7 +446,14 @@ class Conv2d(Layer):
             call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
                  ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
         else:
-            if self.need_input_grad:
+            join, self.dgrad_join, self.join_done = self.dgrad_join, None, False
+            if self.need_input_grad and join is not None and g.c % 4 == 0:
+                add_g, add_y = join
+                call("i8t_conv_dgrad_join", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
+                     ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), ops._p(add_g.contiguous()),
+                     ops._p(add_y.contiguous() if add_y is not None else None))
+                self.join_done = True
+            elif self.need_input_grad:
                 call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
                      ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
@@ -809,9 +824,21 @@ class ResidualBlock(Layer):
         g = dense_grad(g)
         if self._fused:
             gl = MaskedGrad(g, 2, mask_y=self._y)
+            first = self.main.children[0][1] if self.main.children else None
+            joinable = isinstance(first, Conv2d) and not first.depthwise and JOIN_FUSION
+            if joinable and not self.shortcut:  # identity: conv1's dgrad adds g * (y > 0)
+                first.dgrad_join = (g, self._y)
             gm = dense_grad(self.main.backward(gl, ctx))
+            if joinable and not self.shortcut and first.join_done:
+                return gm
             if self.shortcut:
+                sc = self.shortcut.children[0][1] if self.shortcut.children else None
+                sc_join = isinstance(sc, Conv2d) and not sc.depthwise and JOIN_FUSION
+                if sc_join:  # projection: the downsample conv's dgrad adds the main-branch gradient
+                    sc.dgrad_join = (gm, None)
                 gs = dense_grad(self.shortcut.backward(gl, ctx))
+                if sc_join and sc.join_done:
+                    return gs
                 return gm + gs
             out = torch.empty_like(gm)
             call("i8t_add_masked", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._y), gm.numel(), ops._p(out))

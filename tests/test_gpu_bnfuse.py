@@ -222,12 +222,12 @@ def test_bn_rejects_bad_shapes(ops):
     assert rc != 0
 
 
-def _train(impl, name="resnet20", batch=16, steps=3, mode=None):
+def _train(impl, name="resnet20", batch=16, steps=3, mode=None, join=True):
     from paper_1912_12607_b200 import layers as L
     from paper_1912_12607_b200.models import build_model
     from paper_1912_12607_b200.trainer import TrainConfig, Trainer, synthetic_batch
-    old = L.BN_IMPL
-    L.BN_IMPL = impl
+    old, old_join = L.BN_IMPL, L.JOIN_FUSION
+    L.BN_IMPL, L.JOIN_FUSION = impl, join
     try:
         m = build_model(name, seed=3)
         L.int8_replace(m.net)
@@ -238,7 +238,7 @@ def _train(impl, name="resnet20", batch=16, steps=3, mode=None):
         x, y = synthetic_batch(m, batch, 5)
         return tr, [tr.train_step(x, y, it, 100) for it in range(steps)]
     finally:
-        L.BN_IMPL = old
+        L.BN_IMPL, L.JOIN_FUSION = old, old_join
 
 
 @pytest.mark.parametrize("name,batch", [("resnet20", 16), ("resnet50", 2), ("mobilenet_v2", 4), ("inception_v3", 2)])
@@ -253,6 +253,18 @@ def test_fused_equals_eager_bit_exact(name, batch):
         assert a.loss == b.loss
         for la, lb in zip(a.layers, b.layers):
             assert (la.clip, la.dc, la.eps_norm, la.ghat_sqnorm) == (lb.clip, lb.dc, lb.eps_norm, lb.ghat_sqnorm)
+    assert torch.equal(ta.pflat, tb.pflat)
+    assert int(ta.grad_stream.item()) == int(tb.grad_stream.item())
+
+
+@pytest.mark.parametrize("name,batch", [("resnet20", 16), ("resnet50", 2)])
+def test_residual_join_in_dgrad_epilogue_bit_exact(name, batch):
+    """i8t_conv_dgrad_join (residual joins inside the dgrad epilogue, incl. the
+    strided stride-phase path) trains bit-identically to dgrad + separate joins."""
+    ta, ra = _train("fused", name, batch, 3, join=True)
+    tb, rb = _train("fused", name, batch, 3, join=False)
+    for a, b in zip(ra, rb):
+        assert a.loss == b.loss
     assert torch.equal(ta.pflat, tb.pflat)
     assert int(ta.grad_stream.item()) == int(tb.grad_stream.item())
 
