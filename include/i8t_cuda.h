@@ -270,6 +270,12 @@ int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double*
                const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
                const float* res_gamma, const float* res_beta, float* y);
 /* BN backward reduction: dbeta = sum g_m, dgamma = sum g_m * x_hat. */
+/* i8t_bn_act plus q = quantize_nearest(y, clip) (NHWC int8, channel stride c)
+ * with running max|y| -> *amax: the block output and the next conv's int8
+ * input in one pass (layers.cpp:101, 108-109, 451-456). */
+int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+                 const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
+                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax);
 int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,
                       const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* grad_gamma,
                       float* grad_beta);

@@ -275,45 +275,81 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
 
 // Forward: y = act(bn(z) [+ residual]); residual is fp32 `res` or a second BN
 // applied lazily to res_z (ResidualBlock, layers.cpp:451-456: float add, then ReLU).
+// QOUT: also q = quantize_nearest(y, clip) with running max|y| -- the next
+// conv's input quantiser (layers.cpp:101, 108-109) on the value just computed.
+template <bool QOUT>
 __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
                                                 const float* gamma, const float* beta, int relu,
                                                 const float* __restrict__ res, const float* __restrict__ res_z,
                                                 const double* res_bn, const float* res_gamma, const float* res_beta,
-                                                float* __restrict__ y) {
+                                                float* __restrict__ y, const float* clip_p, int8_t* __restrict__ q,
+                                                float* amax, int* err) {
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
-  if (e >= n) return;
-  BnQuad k, kr;
-  k.load(bn, gamma, beta, c, e % c);
-  if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
-  for (; e < n; e += 2 * T4) {  // two float4 loads (per input) in flight per thread
-    const bool two = e + T4 < n;
-    const uint32_t e1 = two ? e + T4 : e;
-    const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e)), v1 = __ldg(reinterpret_cast<const float4*>(z + e1));
-    float4 r0 = make_float4(0, 0, 0, 0), r1 = r0;
-    if (res || res_z) {
-      const float* rp = res ? res : res_z;
-      r0 = __ldg(reinterpret_cast<const float4*>(rp + e));
-      r1 = __ldg(reinterpret_cast<const float4*>(rp + e1));
+  float clip = 1.0f, s = 1.0f, inv_s = 1.0f, m = 0.0f;
+  bool bad = false;
+  if (QOUT) {
+    clip = *clip_p;
+    s = scale_of(clip);
+    inv_s = 1.0f / s;
+  }
+  if (e < n) {
+    BnQuad k, kr;
+    k.load(bn, gamma, beta, c, e % c);
+    if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
+    for (; e < n; e += 2 * T4) {  // two float4 loads (per input) in flight per thread
+      const bool two = e + T4 < n;
+      const uint32_t e1 = two ? e + T4 : e;
+      const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e)), v1 = __ldg(reinterpret_cast<const float4*>(z + e1));
+      float4 r0 = make_float4(0, 0, 0, 0), r1 = r0;
+      if (res || res_z) {
+        const float* rp = res ? res : res_z;
+        r0 = __ldg(reinterpret_cast<const float4*>(rp + e));
+        r1 = __ldg(reinterpret_cast<const float4*>(rp + e1));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h && !two) break;
+        const float4 v = h ? v1 : v0, r = h ? r1 : r0;
+        const float zz[4] = {v.x, v.y, v.z, v.w};
+        float rr[4] = {r.x, r.y, r.z, r.w};
+        if (res_z) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
+        }
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float t = k.y(j, zz[j]);
+          if (res || res_z) t = __fadd_rn(t, rr[j]);
+          o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+        }
+        reinterpret_cast<float4*>(y)[(e + h * T4) / 4] = make_float4(o[0], o[1], o[2], o[3]);
+        if (QOUT) {
+          signed char qq[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            bad |= !isfinite(o[j]);
+            m = fmaxf(m, fabsf(o[j]));
+            qq[j] = static_cast<signed char>(quant_nearest(o[j], clip, s, inv_s));
+          }
+          reinterpret_cast<char4*>(q)[(e + h * T4) / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
+        }
+      }
     }
+  }
+  if (QOUT) {
+    if (bad) atomicOr(err, ERR_NONFINITE);
+    if (amax) {
+      __shared__ float sm[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h && !two) break;
-      const float4 v = h ? v1 : v0, r = h ? r1 : r0;
-      const float zz[4] = {v.x, v.y, v.z, v.w};
-      float rr[4] = {r.x, r.y, r.z, r.w};
-      if (res_z) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, sm[w]);
+        if (m > 0.0f) atomicMax(reinterpret_cast<int*>(amax), __float_as_int(m));
       }
-      float o[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float t = k.y(j, zz[j]);
-        if (res || res_z) t = __fadd_rn(t, rr[j]);
-        o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
-      }
-      reinterpret_cast<float4*>(y)[(e + h * T4) / 4] = make_float4(o[0], o[1], o[2], o[3]);
     }
   }
 }
@@ -495,10 +531,28 @@ int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double*
   if (rc) return rc;
   if (!cx || !bn || !gamma || !beta || !y || (res_z && (!res_bn || !res_gamma || !res_beta)))
     return set_error(I8T_EINVAL, "bn_act: bad arguments");
-  k_bn_act<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c), bn,
-                                                         gamma, beta, relu, res, res_z, res_bn, res_gamma, res_beta, y);
+  k_bn_act<false><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
+                                                                static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
+                                                                res_z, res_bn, res_gamma, res_beta, y, nullptr,
+                                                                nullptr, nullptr, nullptr);
   count_launch(1);
   return cuda_check("k_bn_act");
+}
+
+int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+                 const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
+                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !bn || !gamma || !beta || !y || !clip || !q || (res_z && (!res_bn || !res_gamma || !res_beta)))
+    return set_error(I8T_EINVAL, "bn_act_q: bad arguments");
+  k_bn_act<true><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
+                                                               static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
+                                                               res_z, res_bn, res_gamma, res_beta, y, clip, q, amax,
+                                                               cx->d_err);
+  count_launch(1);
+  return cuda_check("k_bn_act_q");
 }
 
 int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,

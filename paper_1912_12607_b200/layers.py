@@ -98,7 +98,10 @@ class LazyAct:
     def numel(self):
         return self.z.numel()
 
-    def materialize(self, res=None):
+    def materialize(self, res=None, quant_for=None, ctx=None):
+        """y = act(bn(z) [+ res]).  With quant_for = the conv that consumes y next
+        (and its clip known), the same pass also writes that conv's int8 input
+        (attached as y._i8t_q, picked up by Conv2d.forward)."""
         n, h, w, c = self.z.shape
         y = torch.empty_like(self.z)
         r, rz, rbn = (None, None, None)
@@ -106,9 +109,18 @@ class LazyAct:
             rz, rbn = res.z, res.bn
         elif res is not None:
             r = res
-        call("i8t_bn_act", ops.ctx(), ops._p(self.z), n * h * w, c, ops._p(self.bn.stats), ops._p(self.bn.gamma),
-             ops._p(self.bn.beta), int(self.relu), ops._p(r), ops._p(rz), ops._p(rbn.stats) if rbn else None,
-             ops._p(rbn.gamma) if rbn else None, ops._p(rbn.beta) if rbn else None, ops._p(y))
+        args = (ops.ctx(), ops._p(self.z), n * h * w, c, ops._p(self.bn.stats), ops._p(self.bn.gamma),
+                ops._p(self.bn.beta), int(self.relu), ops._p(r), ops._p(rz), ops._p(rbn.stats) if rbn else None,
+                ops._p(rbn.gamma) if rbn else None, ops._p(rbn.beta) if rbn else None, ops._p(y))
+        conv = quant_for
+        if conv is not None and ctx is not None and conv.takes_prequantized(c, ctx):
+            q = torch.empty((n, h, w, c), dtype=torch.int8, device=y.device)
+            qs = conv.qs
+            call("i8t_bn_act_q", *args, ops._p(qs.clip_a), ops._p(q),
+                 ops._p(qs.pending_amax) if ctx.track_amax else None)
+            y._i8t_q = (conv, q)
+        else:
+            call("i8t_bn_act", *args)
         return y
 
 
@@ -332,6 +344,11 @@ class Conv2d(Layer):
     def set_quantized(self, on):
         self.quantize_enabled = on
 
+    def takes_prequantized(self, c, ctx) -> bool:
+        """Can the producer of this conv's input quantise it (clip known, no channel padding)?"""
+        return (self.quantize_enabled and ctx.mode == Mode.INT8 and self.qs.clip_a_set and not self.depthwise
+                and self.c_pad == c == self.in_c)
+
     def params(self):
         return [ParamRef("weight", self.weight, self.grad_weight)]
 
@@ -393,7 +410,10 @@ class Conv2d(Layer):
         n, hh, ww, c = x.shape
         dev = x.z.device if fuse_in else x.device
         qa = torch.empty((n, hh, ww, self.c_pad), dtype=torch.int8, device=dev)
-        if fuse_in:  # BN-apply + ReLU + nearest quantise + amax in one pass over z
+        pre = getattr(x, "_i8t_q", None) if not fuse_in else None
+        if pre is not None and pre[0] is self:  # quantised by the producing block (i8t_bn_act_q)
+            qa = pre[1]
+        elif fuse_in:  # BN-apply + ReLU + nearest quantise + amax in one pass over z
             bn = x.bn
             call("i8t_bn_act_quant", h, ops._p(x.z), n * hh * ww, c, ops._p(bn.stats), ops._p(bn.gamma),
                  ops._p(bn.beta), int(x.relu), ops._p(qs.clip_a), ops._p(qa),
@@ -808,13 +828,14 @@ class ResidualBlock(Layer):
 
     def __init__(self, main: Sequential, shortcut: Sequential | None):
         self.main, self.shortcut, self.relu = main, shortcut, ReLU()
+        self.next_conv = None  # first conv of the next block: its int8 input is written with the block output
 
     def forward(self, x, ctx):
         x = dense(x)
         y = self.main.forward(x, ctx)
         sc = self.shortcut.forward(x, ctx) if self.shortcut else x
         if isinstance(y, LazyAct) and not y.relu:  # relu(bn3(z3) + shortcut) in one pass
-            out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc)
+            out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc, quant_for=self.next_conv, ctx=ctx)
             self._y, self._fused = out, True
             return out
         self._fused = False

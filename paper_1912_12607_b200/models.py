@@ -25,6 +25,16 @@ def _cbr(seq, name, cin, cout, k, s, p, gen, dev, relu=True, depthwise=False):
         seq.add(f"{name}_relu", ReLU())
 
 
+def _chain_blocks(net):
+    """Tell each ResidualBlock which conv consumes its output next (its int8
+    input is then written by the block's BN + residual + ReLU pass)."""
+    blocks = [layer for _, layer in net.children if isinstance(layer, ResidualBlock)]
+    for a, b in zip(blocks, blocks[1:]):
+        first = b.main.children[0][1] if b.main.children else None
+        if isinstance(first, Conv2d):
+            a.next_conv = first
+
+
 def resnet20(num_classes=10, seed=1, device="cuda") -> Model:
     gen = torch.Generator().manual_seed(seed)
     net = Sequential()
@@ -44,6 +54,7 @@ def resnet20(num_classes=10, seed=1, device="cuda") -> Model:
             cin = cout
     net.add("pool", GlobalAvgPool())
     net.add("fc", Dense(64, num_classes, gen, device))
+    _chain_blocks(net)
     return Model("resnet20", net, num_classes, (3, 32, 32))
 
 
@@ -68,6 +79,7 @@ def resnet50(num_classes=1000, seed=1, device="cuda") -> Model:
             cin = width * 4
     net.add("pool", GlobalAvgPool())
     net.add("fc", Dense(2048, num_classes, gen, device))
+    _chain_blocks(net)
     return Model("resnet50", net, num_classes, (3, 224, 224))
 
 
