@@ -320,6 +320,7 @@ def main():
     conv_ms, conv_gop = instrumented_conv_time(tr, x, y, it, total, model, a.batch)
     peak, peak_src = int8_peak_tops()
     achieved = conv_gop / (conv_ms / 1e3) / 1e3  # TOPS
+    att_ms = attainable_conv_ms(a.model, a.batch, peak)
     line = {
         "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
@@ -335,9 +336,13 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                      "nominal_peak": 4500.0, "frac_nominal": achieved / 4500.0,
-                     "kernel": "k_conv_tc (fwd+dgrad+wgrad, all ResNet-50 convs)",
+                     "kernel": "k_conv_tc + k_conv_sw (fwd+dgrad+wgrad, all ResNet-50 convs)",
                      "algorithmic_gop_per_step": conv_gop, "conv_ms_per_step": conv_ms,
-                     "conv_share_of_step": conv_ms / step_ms},
+                     "conv_share_of_step": conv_ms / step_ms,
+                     # per layer and direction max(ops / INT8 peak, compulsory bytes / HBM peak):
+                     # most ResNet-50 convs are bound by their fp32 output, not the tensor cores
+                     "attainable_ms_per_step": att_ms,
+                     "frac_attainable": (att_ms / conv_ms) if att_ms else None},
         "clocks": clk,
     }
     if rank == 0 and not a.no_cpu_baseline:
@@ -350,6 +355,20 @@ def main():
         dist.destroy_process_group()
 
 
+def attainable_conv_ms(model_name, batch, peak_tops):
+    """Roofline time of all ResNet-50 conv passes (tools/r50_roofline.py)."""
+    if model_name != "resnet50":
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from r50_roofline import layer_cost, r50_convs
+    bw = _peaks().get("hbm_gbs", 6555.2) * 1e9
+    tot = 0.0
+    for name, n, c, h, k, r, s, p in r50_convs(batch):
+        for _, (_, _, t) in layer_cost(n, c, h, k, r, s, p, peak_tops * 1e12, bw, skip_dgrad=(name == "stem")).items():
+            tot += t
+    return tot * 1e3
+
+
 def instrumented_conv_time(tr, x, y, it, total, model, batch):
     """Run one step with CUDA events around every tcgen05 conv / fc launch."""
     import torch
@@ -359,8 +378,8 @@ def instrumented_conv_time(tr, x, y, it, total, model, batch):
     orig = _lib.call
 
     def wrapped(name, *args):
-        if name in ("i8t_conv_fwd", "i8t_conv_dgrad", "i8t_conv_wgrad", "i8t_conv_dw_fwd", "i8t_conv_dw_dgrad",
-                    "i8t_conv_dw_wgrad"):
+        if name in ("i8t_conv_fwd", "i8t_conv_dgrad", "i8t_conv_dgrad_join", "i8t_conv_wgrad", "i8t_conv_dw_fwd",
+                    "i8t_conv_dw_dgrad", "i8t_conv_dw_wgrad"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             orig(name, *args)
