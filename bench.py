@@ -211,9 +211,13 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("I8T_DIST_BACKEND", "nccl")  # gloo: several ranks sharing one GPU (path test)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1912_12607_b200 import ops
     from paper_1912_12607_b200.layers import int8_replace, Mode
     from paper_1912_12607_b200.models import build_model, conv_gop_per_image
