@@ -95,7 +95,8 @@ uint64_t i8t_launch_count(void);
 /* Data parallel (8.e): the caller's gradient tensors are shard `rank` of
  * `world` equal contiguous batch shards.  Global DSGC statistics (max|g| and
  * the d_c / eps / g_hat sums) are combined by calling `fn` on device buffers
- * of doubles between kernel phases (op 0 = SUM, 1 = MAX; dtype 0 = f64), and
+ * of doubles between kernel phases (op 0 = SUM, 1 = MAX, 2 = MAX on element
+ * 0 and SUM on the rest, one collective per phase; dtype 0 = f64), and
  * the stochastic quantiser draws from the global stream at the shard's
  * offset, so every rank quantises exactly as one device would on the whole
  * batch.  fn == NULL restores single-device behaviour. */

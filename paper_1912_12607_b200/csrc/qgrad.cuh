@@ -189,11 +189,10 @@ inline int nblocks(int64_t n, int64_t multiple = 1, int64_t cap = 592) {
 inline int gcd_i(int64_t a, int64_t b) { return b == 0 ? static_cast<int>(a) : gcd_i(b, a % b); }
 
 // Global totals for data parallelism: totals[0] MAX, totals[1..nv) SUM.
+// One collective per phase: op 2 = MAX on element 0, SUM on the rest.
 inline int allreduce_totals(Ctx* c, int nv) {
   if (!c->allreduce) return I8T_OK;
-  int rc = ctx_allreduce(c, c->d_totals, 1, 1);
-  if (rc) return rc;
-  return ctx_allreduce(c, c->d_totals + 1, nv - 1, 0);
+  return ctx_allreduce(c, c->d_totals, nv, 2);
 }
 
 // K3 launcher over any input source.

@@ -47,6 +47,27 @@ def combine_totals(totals: torch.Tensor, group=None) -> torch.Tensor:
     return totals
 
 
+def combine_totals_gather(totals: torch.Tensor, group=None) -> torch.Tensor:
+    """combine_totals with one all_gather instead of two all_reduces (the
+    buffers are a few doubles: the collective is latency-bound).  The fold is
+    in rank order, so every rank computes identical totals."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return totals
+    world = dist.get_world_size(group)
+    rows = torch.empty((world, totals.numel()), dtype=totals.dtype, device=totals.device)
+    try:
+        dist.all_gather_into_tensor(rows, totals.contiguous(), group=group)
+    except (RuntimeError, NotImplementedError):  # backends without the fused all-gather
+        dist.all_gather(list(rows.unbind(0)), totals.contiguous(), group=group)
+    totals[:1] = rows[:, :1].max(dim=0).values
+    if totals.numel() > 1:
+        acc = rows[0, 1:].clone()
+        for r in range(1, world):
+            acc += rows[r, 1:]
+        totals[1:] = acc
+    return totals
+
+
 def allreduce_int64_(acc: torch.Tensor, group=None) -> torch.Tensor:
     """Exact sum of int64 weight-gradient accumulators across ranks."""
     assert acc.dtype == torch.int64

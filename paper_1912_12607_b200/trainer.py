@@ -84,7 +84,10 @@ class _DistHook:
     def _call(self, user, buf, count, dtype, op, stream):
         try:
             t = self._view(buf, count)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
+            if op == 2:  # [0] MAX, [1:] SUM in one collective: gather every rank's row, fold locally
+                dp.combine_totals_gather(t)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
             return 0
         except Exception:  # pragma: no cover - surfaced as I8T_ECUDA by the library
             return 1

@@ -37,7 +37,11 @@ def _worker(rank, world, port, out_dir):
         gl = dp.shard_batch(torch.from_numpy(g), rank, world).numpy()
         # global statistics: max|g| (MAX) + sum g^2 (SUM) as the device totals buffer would carry them
         tot = torch.tensor([float(np.abs(gl).max()), float((gl.astype(np.float64) ** 2).sum())], dtype=torch.float64)
+        tot2 = tot.clone()
         dp.combine_totals(tot)
+        dp.combine_totals_gather(tot2)  # the one-collective form the device hook uses (op 2)
+        assert float(tot2[0]) == float(tot[0])
+        assert abs(float(tot2[1]) - float(tot[1])) <= 1e-12 * abs(float(tot[1]))
         clip = float(np.float32(tot[0].item()) * np.float32(0.5))
         # stochastic draws from the global stream at this shard's offset
         seed = 1234
