@@ -326,11 +326,12 @@ def main():
     achieved = conv_gop / (conv_ms / 1e3) / 1e3  # TOPS
     att_ms = attainable_conv_ms(a.model, a.batch, peak)
     line = {
-        "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "metric": METRIC if a.model == "resnet50" else f"{a.model} INT8 train imgs/s", "value": value,
+        "unit": "imgs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
         "data": "synthetic (N(0,1) images, uniform labels, Kaiming weights)",
-        "config": {"workload": "resnet50_int8_train_step", "model": "resnet50", "global_batch": imgs,
-                   "per_gpu_batch": a.batch, "image": 224, "parallelism": f"dp{world}", "dsgc_period": 100,
+        "config": {"workload": f"{a.model}_int8_train_step", "model": a.model, "global_batch": imgs,
+                   "per_gpu_batch": a.batch, "image": model.in_shape[1], "parallelism": f"dp{world}", "dsgc_period": 100,
                    "l2": "inputs > L2 (154 MB/step)"},
         "value_no_search": imgs / (ms / a.steps / 1e3), "dsgc_search_step_ms": ms_search,
         "e2e": {"value": imgs / (step_ms_e2e / 1e3), "unit": "imgs/s",

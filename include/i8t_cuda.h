@@ -227,6 +227,9 @@ int i8t_conv_dw_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
                       const float* clip_g, const float* clip_w, float* ga, int32_t* acc);
 int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, const int8_t* a, int64_t c_pad,
                       const float* clip_g, const float* clip_a, int64_t* acc, float* gw);
+/* gw [C][kh*kw] = float(double(s_g)*double(s_a)*acc) from an (all-reduced) int64 accumulator. */
+int i8t_conv_dw_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t* acc, const float* clip_g,
+                               const float* clip_a, float* gw);
 /* gemm_i8 (gemm.cpp:18-40): C[m][n] = A[m][k] . B[k][n] exact int32
  * (row-major int8 operands; runs on the tcgen05 path as a 1x1 convolution). */
 int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64_t k, int64_t n, int32_t* c);

@@ -186,4 +186,14 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
   return cuda_check("k_dw_wgrad");
 }
 
+int i8t_conv_dw_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t* acc, const float* clip_g,
+                               const float* clip_a, float* gw) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !g || !acc || !clip_g || !clip_a || !gw) return set_error(I8T_EINVAL, "conv_dw_wgrad_finalize: null argument");
+  const int64_t n = g->c * g->kh * g->kw;
+  k_dw_wgrad_finalize<<<blocks_for(n), 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), n, clip_g, clip_a, gw);
+  count_launch(1);
+  return cuda_check("k_dw_wgrad_finalize");
+}
+
 }  // extern "C"

@@ -68,12 +68,15 @@ def combine_totals_gather(totals: torch.Tensor, group=None) -> torch.Tensor:
     return totals
 
 
-def allreduce_int64_(acc: torch.Tensor, group=None) -> torch.Tensor:
-    """Exact sum of int64 weight-gradient accumulators across ranks."""
+def allreduce_int64_(acc: torch.Tensor, group=None, async_op: bool = False):
+    """Exact sum of int64 weight-gradient accumulators across ranks (in place).
+    async_op: return the collective's work handle (None when there is nothing
+    to reduce) instead of waiting."""
     assert acc.dtype == torch.int64
+    work = None
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    return acc
+        work = dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    return work if async_op else acc
 
 
 def shard_batch(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:

@@ -55,7 +55,10 @@ class BackwardCtx:
     beta: float = 0.1
     form: str = "exp"
     lr_scaling_enabled: bool = True
-    wgrad_allreduce: object = None  # callable(int64 acc tensor) for data parallelism (exact sum)
+    wgrad_allreduce: object = None  # callable(int64 acc tensor) -> async work, data parallelism (exact sum)
+    # (work, finalize) pairs: the int64 weight-gradient allreduces run while the
+    # backward continues; the trainer waits on each and rescales before the update
+    deferred: list = field(default_factory=list)
 
 
 @dataclass
@@ -463,8 +466,16 @@ class Conv2d(Layer):
                      ops._p(self.qs.clip_w), ops._p(ga), None)
             if self.wgrad_acc is None:
                 self.wgrad_acc = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int64, device=gdev)
-            call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
-                 ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
+            if ctx.wgrad_allreduce is None:
+                call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
+                     ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight))
+            else:  # data parallel: exact int64 sum across ranks, rescaled after the allreduce
+                call("i8t_conv_dw_wgrad", h, C.byref(g), ops._p(qg), ops._p(self._qa), self.c_pad, ops._p(clip_g),
+                     ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), None)
+                acc, gw, clip_a, geo = self.wgrad_acc, self.grad_weight, self.qs.clip_a, g
+                ctx.deferred.append((ctx.wgrad_allreduce(acc), lambda: call(
+                    "i8t_conv_dw_wgrad_finalize", ops.ctx(), C.byref(geo), ops._p(acc), ops._p(clip_g), ops._p(clip_a),
+                    ops._p(gw))))
         else:
             join, self.dgrad_join, self.join_done = self.dgrad_join, None, False
             if self.need_input_grad and join is not None and g.c % 4 == 0:
@@ -482,12 +493,13 @@ class Conv2d(Layer):
             if ctx.wgrad_allreduce is None:
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
                      ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight), 1)
-            else:  # data parallel: exact int64 sum across ranks, then rescale
+            else:  # data parallel: exact int64 sum across ranks (async, overlapping the backward), then rescale
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
                      ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), None, 1)
-                ctx.wgrad_allreduce(self.wgrad_acc)
-                call("i8t_conv_wgrad_finalize", h, C.byref(g), ops._p(self.wgrad_acc), self.c_pad, ops._p(clip_g),
-                     ops._p(self.qs.clip_a), ops._p(self.grad_weight), 1)
+                acc, gw, clip_a, geo, c_pad = self.wgrad_acc, self.grad_weight, self.qs.clip_a, g, self.c_pad
+                ctx.deferred.append((ctx.wgrad_allreduce(acc), lambda: call(
+                    "i8t_conv_wgrad_finalize", ops.ctx(), C.byref(geo), ops._p(acc), c_pad, ops._p(clip_g),
+                    ops._p(clip_a), ops._p(gw), 1)))
         self._qa = None
         self._qg = qg if self.keep_qg else None
         return ga

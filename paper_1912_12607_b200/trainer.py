@@ -192,6 +192,10 @@ class Trainer:
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
                            self._wgrad_allreduce if self._hook is not None else None)
         self.model.net.backward(g_logits, bctx)
+        for work, finalize in bctx.deferred:  # int64 wgrad allreduces issued during the backward
+            if work is not None:
+                work.wait()
+            finalize()
         if self.world > 1:
             params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
             self._allreduce_fp32_grads(params)
@@ -219,7 +223,7 @@ class Trainer:
 
     # ---------------------------------------------------------------- data parallel
     def _wgrad_allreduce(self, acc: torch.Tensor):
-        dp.allreduce_int64_(acc)
+        return dp.allreduce_int64_(acc, async_op=True)
 
     def _allreduce_fp32_grads(self, params):
         flat = [p.grad for layer, p in params if not (layer.quantized and p.name == "weight")]
