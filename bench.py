@@ -325,6 +325,12 @@ def main():
     peak, peak_src = int8_peak_tops()
     achieved = conv_gop / (conv_ms / 1e3) / 1e3  # TOPS
     att_ms = attainable_conv_ms(a.model, a.batch, peak)
+    traffic = None  # DRAM bytes of all conv launches of one step, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_conv_dram_step.json")) as f:
+            traffic = json.load(f)["traffic_bytes_per_step"] if a.model == "resnet50" and a.batch == 256 else None
+    except Exception:
+        traffic = None
     line = {
         "metric": METRIC if a.model == "resnet50" else f"{a.model} INT8 train imgs/s", "value": value,
         "unit": "imgs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -339,7 +345,9 @@ def main():
                 "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": "DRAM bytes per step summed over the conv launches (profiles/r1_conv_dram_step.json)",
+                     "peak_source": peak_src,
                      "nominal_peak": 4500.0, "frac_nominal": achieved / 4500.0,
                      "kernel": "k_conv_tc + k_conv_sw (fwd+dgrad+wgrad, all ResNet-50 convs)",
                      "algorithmic_gop_per_step": conv_gop, "conv_ms_per_step": conv_ms,
