@@ -248,7 +248,8 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
  * Tensors are NHWC [m = N*H*W][c] fp32, c % 4 == 0.  bn: device doubles [6c]
  * (mean, invstd, s1/m, s2/m, gamma*invstd, ReLU-mask bounds), filled by the
  * calls below.  mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0,
- * 2 mask_y > 0.  With mask_mode 1, i8t_bn_bwd_reduce also stores per channel
+ * 2 mask_y > 0, 3 mask_y points at packed mask bits (uint32 words, see
+ * i8t_bn_act_q).  With mask_mode 1, i8t_bn_bwd_reduce also stores per channel
  * the float interval [lo, hi] with relu(bn(z)) > 0 <=> lo <= z <= hi (the map
  * z -> float(gamma*x_hat + beta) is monotone), which i8t_bn_bwd_apply and
  * i8t_quantize_gradient_bn then read: call them after i8t_bn_bwd_reduce. */
@@ -274,12 +275,16 @@ int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double*
                const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
                const float* res_gamma, const float* res_beta, float* y);
 /* BN backward reduction: dbeta = sum g_m, dgamma = sum g_m * x_hat. */
-/* i8t_bn_act plus q = quantize_nearest(y, clip) (NHWC int8, channel stride c)
- * with running max|y| -> *amax: the block output and the next conv's int8
- * input in one pass (layers.cpp:101, 108-109, 451-456). */
+/* i8t_bn_act with optional extra outputs of the same pass (NULL = skip):
+ *   q (+ clip, amax): quantize_nearest(y, clip) (NHWC int8, channel stride c)
+ *     with running max|y| -> *amax: the next conv's int8 input
+ *     (layers.cpp:101, 108-109, 451-456);
+ *   mask_bits: y > 0 packed one bit per element (word e/32, bit e%32, m*c/32
+ *     words rounded up): everything the backward needs of y (mask mode 3). */
 int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
                  const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
-                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax);
+                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax,
+                 uint32_t* mask_bits);
 int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,
                       const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* grad_gamma,
                       float* grad_beta);
@@ -294,6 +299,8 @@ int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const fl
                              uint32_t* lcg_state, int8_t* q);
 /* out = a + g * (y > 0) (ResidualBlock backward with an identity shortcut). */
 int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y, int64_t n, float* out);
+/* out = a + g * mask with the packed mask bits of i8t_bn_act_q. */
+int i8t_add_masked_bits(i8t_ctx* ctx, const float* a, const float* g, const uint32_t* bits, int64_t n, float* out);
 
 /* All parameters in one launch: w and grad are flat arenas; segment i covers
  * [seg_off[i], seg_off[i+1]) (multiples of 4, device int64) and uses the

@@ -24,6 +24,12 @@ namespace i8t_dev {
 
 constexpr int BN_GROUP = 128;  // channels per column-reduction block group
 
+// mask mode 3: the 4 mask bits of elements e..e+3 (e % 4 == 0) of a packed
+// ReLU mask (word e/32, bit e%32), as written by i8t_bn_act_q
+__device__ __forceinline__ uint32_t mask_nibble(const float* mask, uint64_t e) {
+  return (__ldg(reinterpret_cast<const uint32_t*>(mask) + (e >> 5)) >> (e & 31u)) & 0xFu;
+}
+
 struct ColArgs {
   const float* z;
   const float* g;       // MODE 1
@@ -32,7 +38,7 @@ struct ColArgs {
   const float* beta;
   double* bn;
   uint32_t m, c;
-  int mask_mode;        // 0 none, 1 relu(bn(z)) > 0, 2 mask_y > 0
+  int mask_mode;        // 0 none, 1 relu(bn(z)) > 0, 2 mask_y > 0, 3 packed mask bits (mask_y = uint32 words)
   double momentum, eps;
   float* running_mean;  // MODE 0
   float* running_var;
@@ -42,7 +48,7 @@ struct ColArgs {
 
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
-template <int MODE>
+template <int MODE, int MASK = 0>
 __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets) {
   const uint32_t c0 = blockIdx.y * BN_GROUP;
   const uint32_t gw = min(static_cast<uint32_t>(BN_GROUP), a.c - c0);  // group width (multiple of 4)
@@ -74,20 +80,22 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     // software pipeline: the U rows of the next trip are loaded before the
     // current trip's math, so U (x tensors) 16-byte loads are always in flight
     float4 zv[U], gv[U], yv[U], zn[U], gn[U], yn[U];
-    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd) {
+    uint32_t bv[U], bn_[U];  // MASK 3: raw mask words (the nibble is extracted at use: keeps the loads in flight)
+    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd, uint32_t* bd) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t ru = rr + u * row_step;
         const size_t off = static_cast<size_t>(ru < a.m ? ru : r) * a.c + ch;
         zd[u] = ldg_stream(a.z + off);
         if (MODE == 1) gd[u] = ldg_stream(a.g + off);
-        if (MODE == 1 && a.mask_mode == 2) yd[u] = ldg_stream(a.mask_y + off);
+        if (MODE == 1 && MASK == 2) yd[u] = ldg_stream(a.mask_y + off);
+        if (MODE == 1 && MASK == 3) bd[u] = __ldg(reinterpret_cast<const uint32_t*>(a.mask_y) + (off >> 5));
       }
     };
-    if (r < a.m) fetch(r, zv, gv, yv);
+    if (r < a.m) fetch(r, zv, gv, yv, bv);
     for (; r < a.m; r += U * row_step) {
       const uint32_t rn = r + U * row_step;
-      if (rn < a.m) fetch(rn, zn, gn, yn);
+      if (rn < a.m) fetch(rn, zn, gn, yn, bn_);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool valid = r + u * row_step < a.m;  // rows past the end re-read row r: not accumulated
@@ -108,8 +116,9 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
           for (int j = 0; j < 4; ++j) {
             xv[j] = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
             bool mk = valid;
-            if (a.mask_mode == 1) mk = mk && zz[j] >= lo[j] && zz[j] <= hi[j];
-            else if (a.mask_mode == 2) mk = mk && yy[j] > 0.0f;
+            if (MASK == 1) mk = mk && zz[j] >= lo[j] && zz[j] <= hi[j];
+            else if (MASK == 2) mk = mk && yy[j] > 0.0f;
+            else if (MASK == 3) mk = mk && ((bv[u] >> (((r + u * row_step) * a.c + ch + j) & 31u)) & 1u);
             gm[j] = mk ? static_cast<double>(gg[j]) : 0.0;
             xh[j] = rn24(xv[j], sub);
           }
@@ -129,7 +138,8 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
       for (int u = 0; u < U; ++u) {
         zv[u] = zn[u];
         if (MODE == 1) gv[u] = gn[u];
-        if (MODE == 1 && a.mask_mode == 2) yv[u] = yn[u];
+        if (MODE == 1 && MASK == 2) yv[u] = yn[u];
+        if (MODE == 1 && MASK == 3) bv[u] = bn_[u];
       }
     }
   }
@@ -275,70 +285,83 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
 
 // Forward: y = act(bn(z) [+ residual]); residual is fp32 `res` or a second BN
 // applied lazily to res_z (ResidualBlock, layers.cpp:451-456: float add, then ReLU).
-// QOUT: also q = quantize_nearest(y, clip) with running max|y| -- the next
-// conv's input quantiser (layers.cpp:101, 108-109) on the value just computed.
+// Optional extra outputs of the block-output pass (QOUT: any of them set):
+//   q     = quantize_nearest(y, clip) with running max|y| -- the next conv's
+//           input quantiser (layers.cpp:101, 108-109) on the value just computed;
+//   mbits = the ReLU mask y > 0 packed one bit per element (word e/32, bit e%32),
+//           all the backward needs of y (mask mode 3).
+// The loop is warp-uniform (a warp covers 128 consecutive elements per trip) so
+// the 4-bit nibbles of 8 lanes can be OR-ed into a word with shuffles.
 template <bool QOUT>
 __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
                                                 const float* gamma, const float* beta, int relu,
                                                 const float* __restrict__ res, const float* __restrict__ res_z,
                                                 const double* res_bn, const float* res_gamma, const float* res_beta,
                                                 float* __restrict__ y, const float* clip_p, int8_t* __restrict__ q,
-                                                float* amax, int* err) {
-  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+                                                uint32_t* __restrict__ mbits, float* amax, int* err) {
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;  // multiple of 128 and of c
+  const uint32_t lane = threadIdx.x & 31;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   float clip = 1.0f, s = 1.0f, inv_s = 1.0f, m = 0.0f;
   bool bad = false;
-  if (QOUT) {
+  if (QOUT && q) {
     clip = *clip_p;
     s = scale_of(clip);
     inv_s = 1.0f / s;
   }
-  if (e < n) {
-    BnQuad k, kr;
-    k.load(bn, gamma, beta, c, e % c);
-    if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
-    for (; e < n; e += 2 * T4) {  // two float4 loads (per input) in flight per thread
-      const bool two = e + T4 < n;
-      const uint32_t e1 = two ? e + T4 : e;
-      const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e)), v1 = __ldg(reinterpret_cast<const float4*>(z + e1));
-      float4 r0 = make_float4(0, 0, 0, 0), r1 = r0;
-      if (res || res_z) {
-        const float* rp = res ? res : res_z;
-        r0 = __ldg(reinterpret_cast<const float4*>(rp + e));
-        r1 = __ldg(reinterpret_cast<const float4*>(rp + e1));
+  BnQuad k, kr;
+  k.load(bn, gamma, beta, c, e % c);
+  if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
+  for (; e - lane * 4u < n; e += 2 * T4) {  // warp-uniform trips of two float4 per thread (loads first)
+    float4 v[2], r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t eh = e + h * T4;
+      const uint32_t ee = eh < n ? eh : 0u;
+      v[h] = __ldg(reinterpret_cast<const float4*>(z + ee));
+      r[h] = (res || res_z) ? __ldg(reinterpret_cast<const float4*>((res ? res : res_z) + ee))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t eh = e + h * T4;
+      const bool ok = eh < n;
+      const float zz[4] = {v[h].x, v[h].y, v[h].z, v[h].w};
+      float rr[4] = {r[h].x, r[h].y, r[h].z, r[h].w};
+      if (res_z) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
       }
+      float o[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h && !two) break;
-        const float4 v = h ? v1 : v0, r = h ? r1 : r0;
-        const float zz[4] = {v.x, v.y, v.z, v.w};
-        float rr[4] = {r.x, r.y, r.z, r.w};
-        if (res_z) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
-        }
-        float o[4];
+      for (int j = 0; j < 4; ++j) {
+        float t = k.y(j, zz[j]);
+        if (res || res_z) t = __fadd_rn(t, rr[j]);
+        o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+      }
+      if (ok) reinterpret_cast<float4*>(y)[eh / 4] = make_float4(o[0], o[1], o[2], o[3]);
+      if (QOUT && q && ok) {
+        signed char qq[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float t = k.y(j, zz[j]);
-          if (res || res_z) t = __fadd_rn(t, rr[j]);
-          o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
+          bad |= !isfinite(o[j]);
+          m = fmaxf(m, fabsf(o[j]));
+          qq[j] = static_cast<signed char>(quant_nearest(o[j], clip, s, inv_s));
         }
-        reinterpret_cast<float4*>(y)[(e + h * T4) / 4] = make_float4(o[0], o[1], o[2], o[3]);
-        if (QOUT) {
-          signed char qq[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            bad |= !isfinite(o[j]);
-            m = fmaxf(m, fabsf(o[j]));
-            qq[j] = static_cast<signed char>(quant_nearest(o[j], clip, s, inv_s));
-          }
-          reinterpret_cast<char4*>(q)[(e + h * T4) / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
-        }
+        reinterpret_cast<char4*>(q)[eh / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
+      }
+      if (QOUT && mbits) {  // eh - 4*lane is warp-uniform: all 32 lanes take part in the shuffles
+        uint32_t w = ok ? ((o[0] > 0.0f ? 1u : 0u) | (o[1] > 0.0f ? 2u : 0u) | (o[2] > 0.0f ? 4u : 0u) |
+                           (o[3] > 0.0f ? 8u : 0u)) << (4 * (lane & 7))
+                        : 0u;
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7) == 0 && ok) mbits[eh / 32] = w;
       }
     }
   }
-  if (QOUT) {
+  if (QOUT && q) {
     if (bad) atomicOr(err, ERR_NONFINITE);
     if (amax) {
       __shared__ float sm[8];
@@ -370,6 +393,7 @@ struct BnBwdSrc {
   float lo[4], hi[4];  // MASK 1: relu(bn(z)) > 0 <=> lo <= z <= hi
   struct Raw {
     float4 g, z, y;
+    uint32_t bits, shift;  // MASK 3: the mask word and this float4's bit offset in it
   };
   __device__ __forceinline__ void init(uint32_t c0) {
 #pragma unroll
@@ -391,6 +415,8 @@ struct BnBwdSrc {
     r.g = __ldg(reinterpret_cast<const float4*>(g) + e4);
     r.z = __ldg(reinterpret_cast<const float4*>(z) + e4);
     if (MASK == 2) r.y = __ldg(reinterpret_cast<const float4*>(mask_y) + e4);
+    if (MASK == 3) r.bits = __ldg(reinterpret_cast<const uint32_t*>(mask_y) + (e4 >> 3));
+    if (MASK == 3) r.shift = (e4 & 7u) * 4u;
     return r;
   }
   // exact (reference) value, and the fast one that flags float-subnormal x_hat
@@ -404,6 +430,7 @@ struct BnBwdSrc {
       bool mk = true;
       if (MASK == 1) mk = zz[j] >= lo[j] && zz[j] <= hi[j];
       if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
+      if (MASK == 3) mk = (r.bits >> (r.shift + j)) & 1u;
       const double gd = mk ? static_cast<double>(gg[j]) : 0.0;
       const double xh = FAST ? rn24(xv, slow) : static_cast<double>(static_cast<float>(xv));
       o[j] = static_cast<float>(k[j] * (gd - a[j] - xh * b[j]));
@@ -449,6 +476,22 @@ __global__ void k_bn_mask_bounds(double* bn, const float* gamma, const float* be
   reinterpret_cast<float2*>(bn + 5 * c)[ch] = bn_mask_bounds(bn[ch], bn[c + ch], gamma[ch], beta[ch]);
 }
 
+// out = a + g * mask (packed mask bits): the identity-shortcut join of mask mode 3.
+__global__ void __launch_bounds__(256) k_add_masked_bits(const float* __restrict__ a, const float* __restrict__ g,
+                                                         const float* __restrict__ bits, uint32_t n4,
+                                                         float* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const float4 av = __ldg(reinterpret_cast<const float4*>(a) + i), gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    const uint32_t b = mask_nibble(bits, 4ull * i);
+    float4 o;
+    o.x = __fadd_rn(av.x, (b & 1u) ? gv.x : 0.0f);
+    o.y = __fadd_rn(av.y, (b & 2u) ? gv.y : 0.0f);
+    o.z = __fadd_rn(av.z, (b & 4u) ? gv.z : 0.0f);
+    o.w = __fadd_rn(av.w, (b & 8u) ? gv.w : 0.0f);
+    reinterpret_cast<float4*>(out)[i] = o;
+  }
+}
+
 // ---------------------------------------------------------------- host
 static int ew_blocks(int64_t n, int64_t c) {
   // grid such that blocks*256*4 % c == 0 (fixed channel quad per thread)
@@ -480,7 +523,10 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   if (!p || !t) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
   if (mode == 0) k_bn_colsum<0><<<grid, 256, 0, c->stream>>>(a, p, t);
-  else k_bn_colsum<1><<<grid, 256, 0, c->stream>>>(a, p, t);
+  else if (a.mask_mode == 1) k_bn_colsum<1, 1><<<grid, 256, 0, c->stream>>>(a, p, t);
+  else if (a.mask_mode == 2) k_bn_colsum<1, 2><<<grid, 256, 0, c->stream>>>(a, p, t);
+  else if (a.mask_mode == 3) k_bn_colsum<1, 3><<<grid, 256, 0, c->stream>>>(a, p, t);
+  else k_bn_colsum<1, 0><<<grid, 256, 0, c->stream>>>(a, p, t);
   count_launch(1);
   return cuda_check("k_bn_colsum");
 }
@@ -534,23 +580,24 @@ int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double*
   k_bn_act<false><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
                                                                 static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
                                                                 res_z, res_bn, res_gamma, res_beta, y, nullptr,
-                                                                nullptr, nullptr, nullptr);
+                                                                nullptr, nullptr, nullptr, nullptr);
   count_launch(1);
   return cuda_check("k_bn_act");
 }
 
 int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
                  const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
-                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax) {
+                 const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q, float* amax,
+                 uint32_t* mask_bits) {
   Ctx* cx = CTX(ctx);
   int rc = bn_check(m, c, z);
   if (rc) return rc;
-  if (!cx || !bn || !gamma || !beta || !y || !clip || !q || (res_z && (!res_bn || !res_gamma || !res_beta)))
+  if (!cx || !bn || !gamma || !beta || !y || (q && !clip) || (res_z && (!res_bn || !res_gamma || !res_beta)))
     return set_error(I8T_EINVAL, "bn_act_q: bad arguments");
   k_bn_act<true><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
                                                                static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
-                                                               res_z, res_bn, res_gamma, res_beta, y, clip, q, amax,
-                                                               cx->d_err);
+                                                               res_z, res_bn, res_gamma, res_beta, y, clip, q,
+                                                               mask_bits, amax, cx->d_err);
   count_launch(1);
   return cuda_check("k_bn_act_q");
 }
@@ -561,8 +608,8 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
   Ctx* cx = CTX(ctx);
   int rc = bn_check(m, c, z);
   if (rc) return rc;
-  if (!cx || !g || !bn || !gamma || !beta || !grad_gamma || !grad_beta || mask_mode < 0 || mask_mode > 2 ||
-      (mask_mode == 2 && !mask_y))
+  if (!cx || !g || !bn || !gamma || !beta || !grad_gamma || !grad_beta || mask_mode < 0 || mask_mode > 3 ||
+      (mask_mode >= 2 && !mask_y))
     return set_error(I8T_EINVAL, "bn_bwd_reduce: bad arguments");
   ColArgs a{};
   a.z = z; a.g = g; a.mask_y = mask_y; a.gamma = gamma; a.beta = beta; a.bn = bn;
@@ -582,11 +629,13 @@ int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, in
   Ctx* cx = CTX(ctx);
   int rc = bn_check(m, c, z);
   if (rc) return rc;
-  if (!cx || !g || !bn || !gz || (mask_mode == 2 && !mask_y)) return set_error(I8T_EINVAL, "bn_bwd_apply: bad arguments");
+  if (!cx || !g || !bn || !gz || mask_mode < 0 || mask_mode > 3 || (mask_mode >= 2 && !mask_y))
+    return set_error(I8T_EINVAL, "bn_bwd_apply: bad arguments");
   const uint32_t un = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
   const int nb = ew_blocks(m * c, c);
   if (mask_mode == 1) k_bn_bwd_apply<1><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   else if (mask_mode == 2) k_bn_bwd_apply<2><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else if (mask_mode == 3) k_bn_bwd_apply<3><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<3>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   else k_bn_bwd_apply<0><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   count_launch(1);
   return cuda_check("k_bn_bwd_apply");
@@ -600,7 +649,8 @@ int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const fl
   DsgcState* st = reinterpret_cast<DsgcState*>(state);
   int rc = bn_check(n_img * hw, c, z);
   if (rc) return rc;
-  if (!cx || !st || !g || !bn || !gamma || !beta || !lcg_state || !q || (mask_mode == 2 && !mask_y))
+  if (!cx || !st || !g || !bn || !gamma || !beta || !lcg_state || !q || mask_mode < 0 || mask_mode > 3 ||
+      (mask_mode >= 2 && !mask_y))
     return set_error(I8T_EINVAL, "quantize_gradient_bn: bad arguments");
   if (lr_scaling_enabled && (!(alpha > 0.0) || !(beta_ > 0.0 && beta_ <= 1.0)))
     return set_error(I8T_EINVAL, "scale_factor: alpha must be > 0, beta in (0,1]");
@@ -610,7 +660,21 @@ int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const fl
     return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
   if (mask_mode == 2)
     return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
+  if (mask_mode == 3)
+    return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<3>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
   return launch_quant_grad_src(cx, st, nullptr, BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, n_img, c, hw, true, lcg_state, q, fin);
+}
+
+int i8t_add_masked_bits(i8t_ctx* ctx, const float* a, const float* g, const uint32_t* bits, int64_t n, float* out) {
+  Ctx* cx = CTX(ctx);
+  if (!cx || !a || !g || !bits || !out || n % 4 != 0) return set_error(I8T_EINVAL, "add_masked_bits: bad arguments");
+  if (!n) return I8T_OK;
+  int b = static_cast<int>((n / 4 + 255) / 256);
+  if (b > 148 * 8) b = 148 * 8;
+  k_add_masked_bits<<<b, 256, 0, cx->stream>>>(a, g, reinterpret_cast<const float*>(bits), static_cast<uint32_t>(n / 4),
+                                                out);
+  count_launch(1);
+  return cuda_check("k_add_masked_bits");
 }
 
 int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y, int64_t n, float* out) {

@@ -101,7 +101,7 @@ class LazyAct:
     def numel(self):
         return self.z.numel()
 
-    def materialize(self, res=None, quant_for=None, ctx=None):
+    def materialize(self, res=None, quant_for=None, ctx=None, mask_bits=None):
         """y = act(bn(z) [+ res]).  With quant_for = the conv that consumes y next
         (and its clip known), the same pass also writes that conv's int8 input
         (attached as y._i8t_q, picked up by Conv2d.forward)."""
@@ -116,12 +116,14 @@ class LazyAct:
                 ops._p(self.bn.beta), int(self.relu), ops._p(r), ops._p(rz), ops._p(rbn.stats) if rbn else None,
                 ops._p(rbn.gamma) if rbn else None, ops._p(rbn.beta) if rbn else None, ops._p(y))
         conv = quant_for
-        if conv is not None and ctx is not None and conv.takes_prequantized(c, ctx):
-            q = torch.empty((n, h, w, c), dtype=torch.int8, device=y.device)
-            qs = conv.qs
-            call("i8t_bn_act_q", *args, ops._p(qs.clip_a), ops._p(q),
-                 ops._p(qs.pending_amax) if ctx.track_amax else None)
-            y._i8t_q = (conv, q)
+        pre = conv is not None and ctx is not None and conv.takes_prequantized(c, ctx)
+        if pre or mask_bits is not None:
+            q = torch.empty((n, h, w, c), dtype=torch.int8, device=y.device) if pre else None
+            qs = conv.qs if pre else None
+            call("i8t_bn_act_q", *args, ops._p(qs.clip_a) if pre else None, ops._p(q),
+                 ops._p(qs.pending_amax) if pre and ctx.track_amax else None, ops._p(mask_bits))
+            if pre:
+                y._i8t_q = (conv, q)
         else:
             call("i8t_bn_act", *args)
         return y
@@ -147,6 +149,9 @@ class MaskedGrad:
     def materialize(self):
         if self.mode == 2:
             return torch.where(self.mask_y > 0, self.g, torch.zeros((), device=self.g.device))
+        if self.mode == 3:
+            return torch.where(unpack_mask(self.mask_y, self.g.numel()).view_as(self.g), self.g,
+                               torch.zeros((), device=self.g.device))
         y = LazyAct(self.bn._z, self.bn, relu=True).materialize()
         return torch.where(y > 0, self.g, torch.zeros((), device=self.g.device))
 
@@ -174,6 +179,12 @@ class BnGrad:
         call("i8t_bn_bwd_apply", ops.ctx(), ops._p(self.g), ops._p(self.bn._z), n * h * w, c, ops._p(self.bn.stats),
              ops._p(self.bn.gamma), ops._p(self.bn.beta), self.mode, ops._p(self.mask_y), ops._p(out))
         return out
+
+
+def unpack_mask(bits: torch.Tensor, n: int) -> torch.Tensor:
+    """Packed ReLU mask (int32 words, bit e%32 of word e/32) -> bool [n]."""
+    sh = torch.arange(32, device=bits.device, dtype=torch.int32)
+    return ((bits.view(-1, 1) >> sh) & 1).view(-1)[:n].bool()
 
 
 def dense(x):
@@ -847,8 +858,13 @@ class ResidualBlock(Layer):
         y = self.main.forward(x, ctx)
         sc = self.shortcut.forward(x, ctx) if self.shortcut else x
         if isinstance(y, LazyAct) and not y.relu:  # relu(bn3(z3) + shortcut) in one pass
-            out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc, quant_for=self.next_conv, ctx=ctx)
-            self._y, self._fused = out, True
+            bits = None
+            if ctx.training and y.z.numel() % 4 == 0:  # the backward keeps one bit of y per element
+                bits = torch.empty(((y.z.numel() + 31) // 32,), dtype=torch.int32, device=y.z.device)
+            out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc, quant_for=self.next_conv, ctx=ctx,
+                                                            mask_bits=bits)
+            self._bits, self._fused = bits, True
+            self._y = out if (bits is None or JOIN_FUSION) else None
             return out
         self._fused = False
         return self.relu.forward(dense(y) + dense(sc), ctx)
@@ -856,7 +872,7 @@ class ResidualBlock(Layer):
     def backward(self, g, ctx):
         g = dense_grad(g)
         if self._fused:
-            gl = MaskedGrad(g, 2, mask_y=self._y)
+            gl = MaskedGrad(g, 3, mask_y=self._bits) if self._bits is not None else MaskedGrad(g, 2, mask_y=self._y)
             first = self.main.children[0][1] if self.main.children else None
             joinable = isinstance(first, Conv2d) and not first.depthwise and JOIN_FUSION
             if joinable and not self.shortcut:  # identity: conv1's dgrad adds g * (y > 0)
@@ -874,7 +890,12 @@ class ResidualBlock(Layer):
                     return gs
                 return gm + gs
             out = torch.empty_like(gm)
-            call("i8t_add_masked", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._y), gm.numel(), ops._p(out))
+            if self._bits is not None:
+                call("i8t_add_masked_bits", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._bits), gm.numel(),
+                     ops._p(out))
+            else:
+                call("i8t_add_masked", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._y), gm.numel(), ops._p(out))
+            self._bits = self._y = None
             return out
         g = self.relu.backward(g, ctx)
         gm = dense_grad(self.main.backward(g, ctx))

@@ -214,6 +214,47 @@ def test_add_masked(ops):
     np.testing.assert_array_equal(out.cpu().numpy(), a + np.where(y > 0, g, 0).astype(np.float32))
 
 
+def _pack_bits(mask):
+    """bool [n] -> int32 words, bit e%32 of word e/32 (the i8t_bn_act_q layout)."""
+    flat = np.asarray(mask, bool).reshape(-1)
+    pad = (-flat.size) % 32
+    words = np.packbits(np.concatenate([flat, np.zeros(pad, bool)]).reshape(-1, 32)[:, ::-1], axis=1)
+    return np.ascontiguousarray(words).view(">u4").astype(np.uint32).view(np.int32).reshape(-1)
+
+
+def test_packed_mask_mode3_equals_mode2(ops):
+    """mask mode 3 (packed bits of y > 0, written by i8t_bn_act_q) gives the same
+    BN backward, fused gradient quantiser and residual join as mode 2 on y."""
+    m, c = 3136, 64
+    z, gamma, beta, g = _data(m, c, 21)
+    z2, g2, b2, _ = _data(m, c, 22)
+    zt, gt, bt, g_t = t(z), t(gamma), t(beta), t(g)
+    bn, bn2 = _stats(ops, zt, c), _stats(ops, t(z2), c)
+    # the block output y = relu(bn(z) + bn2(z2)) and its packed mask from the same pass
+    y = torch.empty_like(zt)
+    bits = torch.zeros(((m * c + 31) // 32,), dtype=torch.int32, device="cuda")
+    ops.call("i8t_bn_act_q", ops.ctx(), ops._p(zt), m, c, ops._p(bn), ops._p(gt), ops._p(bt), 1, None, ops._p(t(z2)),
+             ops._p(bn2), ops._p(t(g2)), ops._p(t(b2)), ops._p(y), None, None, None, ops._p(bits))
+    assert np.array_equal(bits.cpu().numpy(), _pack_bits(y.cpu().numpy() > 0))
+    outs = {}
+    for mode, mk in ((2, y), (3, bits)):
+        bnm = bn.clone()
+        gg, gb = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+        ops.call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bnm), ops._p(gt), ops._p(bt),
+                 mode, ops._p(mk), ops._p(gg), ops._p(gb))
+        gi = torch.empty_like(zt)
+        ops.call("i8t_bn_bwd_apply", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bnm), ops._p(gt), ops._p(bt),
+                 mode, ops._p(mk), ops._p(gi))
+        outs[mode] = (gg.clone(), gb.clone(), bnm.clone(), gi.clone())
+    for x2, x3 in zip(outs[2], outs[3]):
+        assert torch.equal(x2, x3)
+    a = torch.randn(m * c, device="cuda")
+    o2, o3 = torch.empty_like(a), torch.empty_like(a)
+    ops.call("i8t_add_masked", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(y), m * c, ops._p(o2))
+    ops.call("i8t_add_masked_bits", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(bits), m * c, ops._p(o3))
+    assert torch.equal(o2, o3)
+
+
 def test_bn_rejects_bad_shapes(ops):
     z = torch.zeros(10, 6, device="cuda")
     bn = torch.zeros(30, dtype=torch.float64, device="cuda")
