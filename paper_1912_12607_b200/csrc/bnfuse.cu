@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
 //           all the backward needs of y (mask mode 3).
 // The loop is warp-uniform (a warp covers 128 consecutive elements per trip) so
 // the 4-bit nibbles of 8 lanes can be OR-ed into a word with shuffles.
-template <bool QOUT>
+template <bool QOUT, int RES>  // RES: 0 none, 1 dense fp32 residual, 2 residual = bn'(res_z) (lazy)
 __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
                                                 const float* gamma, const float* beta, int relu,
                                                 const float* __restrict__ res, const float* __restrict__ res_z,
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
   }
   BnQuad k, kr;
   k.load(bn, gamma, beta, c, e % c);
-  if (res_z) kr.load(res_bn, res_gamma, res_beta, c, e % c);
+  if (RES == 2) kr.load(res_bn, res_gamma, res_beta, c, e % c);
   for (; e - lane * 4u < n; e += 2 * T4) {  // warp-uniform trips of two float4 per thread (loads first)
     float4 v[2], r[2];
 #pragma unroll
@@ -319,8 +319,8 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
       const uint32_t eh = e + h * T4;
       const uint32_t ee = eh < n ? eh : 0u;
       v[h] = __ldg(reinterpret_cast<const float4*>(z + ee));
-      r[h] = (res || res_z) ? __ldg(reinterpret_cast<const float4*>((res ? res : res_z) + ee))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      r[h] = RES ? __ldg(reinterpret_cast<const float4*>((RES == 1 ? res : res_z) + ee))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
       const bool ok = eh < n;
       const float zz[4] = {v[h].x, v[h].y, v[h].z, v[h].w};
       float rr[4] = {r[h].x, r[h].y, r[h].z, r[h].w};
-      if (res_z) {
+      if (RES == 2) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) rr[j] = kr.y(j, rr[j]);
       }
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float t = k.y(j, zz[j]);
-        if (res || res_z) t = __fadd_rn(t, rr[j]);
+        if (RES) t = __fadd_rn(t, rr[j]);
         o[j] = (relu && !(t > 0.0f)) ? 0.0f : t;
       }
       if (ok) reinterpret_cast<float4*>(y)[eh / 4] = make_float4(o[0], o[1], o[2], o[3]);
@@ -503,6 +503,24 @@ static int ew_blocks(int64_t n, int64_t c) {
   return static_cast<int>(b);
 }
 
+template <bool QOUT>
+static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,
+                          const float* beta, int relu, const float* res, const float* res_z, const double* res_bn,
+                          const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q,
+                          uint32_t* mbits, float* amax) {
+  const uint32_t n = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
+  const int nb = ew_blocks(m * c, c);
+  if (res_z)
+    k_bn_act<QOUT, 2><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, nullptr, res_z, res_bn, res_gamma,
+                                                  res_beta, y, clip, q, mbits, amax, cx->d_err);
+  else if (res)
+    k_bn_act<QOUT, 1><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, res, nullptr, nullptr, nullptr,
+                                                  nullptr, y, clip, q, mbits, amax, cx->d_err);
+  else
+    k_bn_act<QOUT, 0><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, nullptr, nullptr, nullptr, nullptr,
+                                                  nullptr, y, clip, q, mbits, amax, cx->d_err);
+}
+
 static unsigned* tickets(Ctx* c) {
   if (!c->d_tickets) {
     if (cudaMalloc(&c->d_tickets, 64 * sizeof(unsigned)) != cudaSuccess) return nullptr;
@@ -577,10 +595,8 @@ int i8t_bn_act(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double*
   if (rc) return rc;
   if (!cx || !bn || !gamma || !beta || !y || (res_z && (!res_bn || !res_gamma || !res_beta)))
     return set_error(I8T_EINVAL, "bn_act: bad arguments");
-  k_bn_act<false><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
-                                                                static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
-                                                                res_z, res_bn, res_gamma, res_beta, y, nullptr,
-                                                                nullptr, nullptr, nullptr, nullptr);
+  launch_bn_act<false>(cx, z, m, c, bn, gamma, beta, relu, res, res_z, res_bn, res_gamma, res_beta, y, nullptr,
+                       nullptr, nullptr, nullptr);
   count_launch(1);
   return cuda_check("k_bn_act");
 }
@@ -594,10 +610,8 @@ int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const doubl
   if (rc) return rc;
   if (!cx || !bn || !gamma || !beta || !y || (q && !clip) || (res_z && (!res_bn || !res_gamma || !res_beta)))
     return set_error(I8T_EINVAL, "bn_act_q: bad arguments");
-  k_bn_act<true><<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c),
-                                                               static_cast<uint32_t>(c), bn, gamma, beta, relu, res,
-                                                               res_z, res_bn, res_gamma, res_beta, y, clip, q,
-                                                               mask_bits, amax, cx->d_err);
+  launch_bn_act<true>(cx, z, m, c, bn, gamma, beta, relu, res, res_z, res_bn, res_gamma, res_beta, y, clip, q,
+                      mask_bits, amax);
   count_launch(1);
   return cuda_check("k_bn_act_q");
 }
