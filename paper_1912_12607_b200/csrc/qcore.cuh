@@ -51,14 +51,14 @@ __device__ __forceinline__ int quant_nearest(float x, float clip, float s, float
 // with the exact functions below.
 constexpr float QD = 0x1.0p-13f;
 
-// kNearest: round-half-away(|t|) with the sign of t.
+// kNearest: round-half-away(t).  t + RMAGIC keeps t's sign in the integer read
+// from the mantissa (|t| <= 127.0001 also needs no clamp: it rounds to <= 127);
+// ties (|t - rint(t)| = 1/2, where rint goes to even) and near-ties are slow.
 __device__ __forceinline__ int qn_fast(float t, bool& slow) {
-  const float at = fabsf(t);
-  const float kb = __fadd_rn(at, RMAGIC);
-  const float dn = __fsub_rn(at, __fsub_rn(kb, RMAGIC));  // in [-1/2, 1/2]
+  const float kb = __fadd_rn(t, RMAGIC);
+  const float dn = __fsub_rn(t, __fsub_rn(kb, RMAGIC));  // in [-1/2, 1/2]
   slow |= fabsf(dn) > 0.5f - QD;
-  const int ki = min(__float_as_int(kb) - RMAGIC_BITS, 127);
-  return t < 0.0f ? -ki : ki;
+  return __float_as_int(kb) - RMAGIC_BITS;
 }
 
 // kStochastic: floor(t) + (u < frac(t)) == ceil(t - u) for t = RN64(v/s)
