@@ -139,6 +139,20 @@ int i8t_quantize_stochastic(i8t_ctx* ctx, const float* x, int64_t n, const float
 int i8t_quantize_partitioned(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, uint32_t base_seed,
                              int partitions, int8_t* q);
 /* dequantize (quantize.cpp:81-87). */
+/* One layer of i8t_quantize_weights_multi (64 bytes, plain C layout): the
+ * arguments of i8t_quantize_weight for that layer (depthwise weights: k = C,
+ * c = 1, c_pad = 1, ld_krsc = kh*kw, q_crsk = NULL).  Padding bytes of the
+ * outputs are not written: zero them once when allocating. */
+typedef struct {
+  const float* w;
+  const float* clip;
+  int8_t* q_krsc;
+  int8_t* q_crsk;
+  int32_t k, c, rs, c_pad, ld_krsc, k_pad, ld_crsk, src_krsc;
+} i8t_wq_desc;
+/* i8t_quantize_weight for n_layers layers in one launch; dev_descs is a
+ * DEVICE array of descriptors (built once, the pointers stay valid). */
+int i8t_quantize_weights_multi(i8t_ctx* ctx, const i8t_wq_desc* dev_descs, int n_layers);
 int i8t_dequantize(i8t_ctx* ctx, const int8_t* q, int64_t n, const float* clip, float* out);
 /* Layout helpers for the drop-in path. */
 int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, int64_t hw, int64_t ld_src,

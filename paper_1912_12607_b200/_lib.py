@@ -28,6 +28,12 @@ class ConvGeom(C.Structure):
                 (self.w + 2 * self.pad_w - self.kw) // self.stride_w + 1)
 
 
+class WqDesc(C.Structure):
+    """i8t_wq_desc (include/i8t_cuda.h)."""
+    _fields_ = [("w", C.c_void_p), ("clip", C.c_void_p), ("q_krsc", C.c_void_p), ("q_crsk", C.c_void_p)] + \
+               [(n, C.c_int32) for n in ("k", "c", "rs", "c_pad", "ld_krsc", "k_pad", "ld_crsk", "src_krsc")]
+
+
 class DsgcView(C.Structure):
     _fields_ = [("clip", C.c_float), ("scale", C.c_float), ("max_abs", C.c_float), ("flags", C.c_uint32),
                 ("last_dc", C.c_double), ("lr_scale", C.c_double), ("eps_norm", C.c_double),

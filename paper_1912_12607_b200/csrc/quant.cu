@@ -80,6 +80,34 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
   if (amax) block_amax(m, amax);
 }
 
+// K2 over every quantised layer of a model in one launch (blockIdx.y = layer):
+// the per-layer launches cost more than their ~150 MB of traffic.  Padding
+// bytes of the outputs are never written (zeroed once at allocation).
+__global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* __restrict__ descs, int* err) {
+  const i8t_wq_desc d = descs[blockIdx.y];
+  const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s;
+  const uint32_t K = d.k, C = d.c, RS = d.rs, tot = K * C * RS;
+  bool bad = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    uint32_t k, c, rs;
+    if (d.src_krsc) {
+      c = i % C;
+      rs = (i / C) % RS;
+      k = i / (C * RS);
+    } else {
+      rs = i % RS;
+      c = (i / RS) % C;
+      k = i / (RS * C);
+    }
+    const float v = __ldg(d.w + i);
+    bad |= !isfinite(v);
+    const int8_t qv = static_cast<int8_t>(quant_nearest(v, clip, s, inv_s));
+    if (d.q_krsc) d.q_krsc[static_cast<size_t>(k) * d.ld_krsc + rs * d.c_pad + c] = qv;
+    if (d.q_crsk) d.q_crsk[static_cast<size_t>(c) * d.ld_crsk + rs * d.k_pad + k] = qv;
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+}
+
 // NCHW float -> NHWC int8 (channel stride c_pad) through a 32x32 smem transpose.
 __global__ void __launch_bounds__(256) k_quant_nearest_nchw(const float* __restrict__ x, uint32_t C, uint32_t HW,
                                                             const float* __restrict__ clip_p, int8_t* __restrict__ q,
@@ -332,6 +360,14 @@ int i8t_quantize_weight(i8t_ctx* ctx, const float* w, int src_krsc, int64_t k, i
       static_cast<uint32_t>(ld_crsk), amax, cx->d_err);
   count_launch(1);
   return cuda_check("k_quant_weight");
+}
+
+int i8t_quantize_weights_multi(i8t_ctx* ctx, const i8t_wq_desc* dev_descs, int n_layers) {
+  Ctx* cx = CTX(ctx);
+  if (!cx || !dev_descs || n_layers < 1 || n_layers > 65535) return set_error(I8T_EINVAL, "quantize_weights_multi: bad arguments");
+  k_quant_weight_multi<<<dim3(2 * 148, static_cast<unsigned>(n_layers)), 256, 0, cx->stream>>>(dev_descs, cx->d_err);
+  count_launch(1);
+  return cuda_check("k_quant_weight_multi");
 }
 
 int i8t_dequantize(i8t_ctx* ctx, const int8_t* q, int64_t n, const float* clip, float* out) {

@@ -39,6 +39,7 @@ class ForwardCtx:
     mode: Mode = Mode.INT8
     training: bool = True
     track_amax: bool = True
+    weights_quantized: bool = False  # the trainer already ran i8t_quantize_weights_multi for this step
 
 
 @dataclass
@@ -358,6 +359,17 @@ class Conv2d(Layer):
     def set_quantized(self, on):
         self.quantize_enabled = on
 
+    def wq_desc(self):
+        """(w, clip, q_krsc, q_crsk, k, c, rs, c_pad, ld_krsc, k_pad, ld_crsk, src_krsc) of
+        i8t_wq_desc once the buffers and clip exist, else None."""
+        if self._qw is None or not self.qs.clip_w_set:
+            return None
+        rs = self.kh * self.kw
+        if self.depthwise:
+            return (self.weight, self.qs.clip_w, self._qw, None, self.in_c, 1, rs, 1, rs, 0, 0, 0)
+        return (self.weight, self.qs.clip_w, self._qw, self._qwt, self.out_c, self.in_c, rs, self.c_pad, self.ld_w,
+                self.k_pad, self.ld_wt, 0)
+
     def takes_prequantized(self, c, ctx) -> bool:
         """Can the producer of this conv's input quantise it (clip known, no channel padding)?"""
         return (self.quantize_enabled and ctx.mode == Mode.INT8 and self.qs.clip_a_set and not self.depthwise
@@ -407,19 +419,21 @@ class Conv2d(Layer):
             call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.clip_a))
             qs.clip_a.clamp_(min=1e-12)
             qs.clip_a_set = True
-        # weights -> KRSC (fwd) + CRSK (dgrad) int8 in one pass
+        # weights -> KRSC (fwd) + CRSK (dgrad) int8 in one pass (or all layers at once, see wq_desc)
         if self.depthwise:
             if self._qw is None:
-                self._qw = torch.empty((self.in_c, self.kh * self.kw), dtype=torch.int8, device=x.device)
-            call("i8t_quantize_nearest", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w),
-                 ops._p(self._qw), None, 0)
+                self._qw = torch.zeros((self.in_c, self.kh * self.kw), dtype=torch.int8, device=x.device)
+            if not ctx.weights_quantized:
+                call("i8t_quantize_nearest", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w),
+                     ops._p(self._qw), None, 0)
         else:
-            if self._qw is None:
-                self._qw = torch.empty((self.out_c, self.ld_w), dtype=torch.int8, device=x.device)
-                self._qwt = torch.empty((self.in_c, self.ld_wt), dtype=torch.int8, device=x.device)
-            call("i8t_quantize_weight", h, ops._p(self.weight), 0, self.out_c, self.in_c, self.kh, self.kw,
-                 ops._p(qs.clip_w), ops._p(self._qw), self.c_pad, self.ld_w, ops._p(self._qwt), self.k_pad,
-                 self.ld_wt, None)
+            if self._qw is None:  # zeroed once: the padding bytes are never written
+                self._qw = torch.zeros((self.out_c, self.ld_w), dtype=torch.int8, device=x.device)
+                self._qwt = torch.zeros((self.in_c, self.ld_wt), dtype=torch.int8, device=x.device)
+            if not ctx.weights_quantized:
+                call("i8t_quantize_weight", h, ops._p(self.weight), 0, self.out_c, self.in_c, self.kh, self.kw,
+                     ops._p(qs.clip_w), ops._p(self._qw), self.c_pad, self.ld_w, ops._p(self._qwt), self.k_pad,
+                     self.ld_wt, None)
         # activations -> NHWC int8 (channel stride c_pad), pending_amax fused (layers.cpp:101)
         n, hh, ww, c = x.shape
         dev = x.z.device if fuse_in else x.device

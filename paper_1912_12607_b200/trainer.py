@@ -22,8 +22,9 @@ import torch
 import torch.distributed as dist
 
 from . import dp, ops
-from ._lib import DsgcView, call
-from .layers import (BackwardCtx, Dense, ForwardCtx, Mode, SoftmaxCrossEntropy, StateArena, int8_replace, leaves)
+from ._lib import DsgcView, WqDesc, call
+from .layers import (BackwardCtx, Conv2d, Dense, ForwardCtx, Mode, SoftmaxCrossEntropy, StateArena, int8_replace,
+                     leaves)
 
 
 @dataclass
@@ -117,6 +118,7 @@ class Trainer:
         if hasattr(first, "need_input_grad"):
             first.need_input_grad = False
         self.skip = torch.zeros(1, dtype=torch.int32, device=device)
+        self._wq_buf, self._wq_n = None, 0  # device i8t_wq_desc array (built at the second step)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
         self._build_param_arenas(device)
 
@@ -180,7 +182,8 @@ class Trainer:
         """Trainer::train_step (train.cpp:54-120).  images: NHWC float32 CUDA tensor."""
         cfg = self.cfg
         rep = StepReport(iter=it, base_lr_t=self.base_lr_at(it, total_iters))
-        logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8))
+        wq = cfg.mode == Mode.INT8 and self._quantize_weights_at_once()
+        logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8, wq))
         loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels)
         bad = (~torch.isfinite(loss)) | (~torch.isfinite(logits).all())
         # divergence check before backward (train.cpp:73-77): one host sync per step
@@ -209,6 +212,25 @@ class Trainer:
             rep.diverged = bool(self.skip.item())
             self._read_layer_stats(rep)
         return rep
+
+    def _quantize_weights_at_once(self) -> bool:
+        """Every quantised layer's weights in one launch (i8t_quantize_weights_multi)
+        once all layers have their buffers and clips (from the second step on)."""
+        if self._wq_buf is None:
+            convs = [getattr(layer, "conv", layer) for _, layer in self.quant_layers]
+            descs = [c.wq_desc() if isinstance(c, Conv2d) else None for c in convs]
+            if not descs or any(d is None for d in descs):
+                return False
+            arr = (WqDesc * len(descs))()
+            for a, d in zip(arr, descs):
+                ptr = [t.data_ptr() if t is not None else None for t in d[:4]]
+                a.w, a.clip, a.q_krsc, a.q_crsk = ptr
+                a.k, a.c, a.rs, a.c_pad, a.ld_krsc, a.k_pad, a.ld_crsk, a.src_krsc = d[4:]
+            raw = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8)
+            self._wq_buf = raw.to(self.skip.device)
+            self._wq_n = len(descs)
+        call("i8t_quantize_weights_multi", ops.ctx(), ops._p(self._wq_buf), self._wq_n)
+        return True
 
     def _read_layer_stats(self, rep: StepReport):
         views = self.arena.read_views()
