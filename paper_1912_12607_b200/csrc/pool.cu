@@ -95,6 +95,57 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ g
   }
 }
 
+// 3x3 / stride 2 / pad 1 with even H, W (the ResNet stem): a thread owns the
+// 2x2 input block (2p', 2q') .. (2p'+1, 2q'+1) and reads only the four windows
+// (p'..p'+1, q'..q'+1) that can reach it -- the same terms, in the same
+// (p, q) order, as k_maxpool_bwd.
+__global__ void __launch_bounds__(256) k_maxpool_bwd_s2k3(const float* __restrict__ gy, const uint8_t* __restrict__ idx,
+                                                          PoolGeom g, float* __restrict__ gx) {
+  const uint32_t c4n = g.C / 4;
+  const uint32_t tot = static_cast<uint32_t>(g.N) * g.P * g.Q * c4n;  // one 2x2 block per (n, p', q', quad)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const uint32_t c4 = i % c4n, blk = i / c4n;
+    const uint32_t q = blk % g.Q, np = blk / g.Q;
+    const uint32_t p = np % g.P, n = np / g.P;
+    const bool pn = p + 1 < static_cast<uint32_t>(g.P), qn = q + 1 < static_cast<uint32_t>(g.Q);
+    auto win = [&](uint32_t pp, uint32_t qq, uchar4& a, float4& v) {
+      const uint32_t o = ((n * g.P + pp) * g.Q + qq) * c4n + c4;
+      a = reinterpret_cast<const uchar4*>(idx)[o];
+      v = __ldg(reinterpret_cast<const float4*>(gy) + o);
+    };
+    uchar4 a00, a01 = make_uchar4(9, 9, 9, 9), a10 = a01, a11 = a01;
+    float4 g00, g01 = make_float4(0, 0, 0, 0), g10 = g01, g11 = g01;
+    win(p, q, a00, g00);
+    if (qn) win(p, q + 1, a01, g01);
+    if (pn) win(p + 1, q, a10, g10);
+    if (pn && qn) win(p + 1, q + 1, a11, g11);
+    const uint8_t s00[4] = {a00.x, a00.y, a00.z, a00.w}, s01[4] = {a01.x, a01.y, a01.z, a01.w},
+                  s10[4] = {a10.x, a10.y, a10.z, a10.w}, s11[4] = {a11.x, a11.y, a11.z, a11.w};
+    const float v00[4] = {g00.x, g00.y, g00.z, g00.w}, v01[4] = {g01.x, g01.y, g01.z, g01.w},
+                v10[4] = {g10.x, g10.y, g10.z, g10.w}, v11[4] = {g11.x, g11.y, g11.z, g11.w};
+    float o[4][4];  // [pixel of the 2x2 block][channel]
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      o[0][j] = s00[j] == 4 ? __fadd_rn(0.0f, v00[j]) : 0.0f;
+      float t = s00[j] == 5 ? __fadd_rn(0.0f, v00[j]) : 0.0f;
+      o[1][j] = s01[j] == 3 ? __fadd_rn(t, v01[j]) : t;
+      t = s00[j] == 7 ? __fadd_rn(0.0f, v00[j]) : 0.0f;
+      o[2][j] = s10[j] == 1 ? __fadd_rn(t, v10[j]) : t;
+      t = s00[j] == 8 ? __fadd_rn(0.0f, v00[j]) : 0.0f;
+      t = s01[j] == 6 ? __fadd_rn(t, v01[j]) : t;
+      t = s10[j] == 2 ? __fadd_rn(t, v10[j]) : t;
+      o[3][j] = s11[j] == 0 ? __fadd_rn(t, v11[j]) : t;
+    }
+    const uint32_t h = 2 * p, w = 2 * q;
+    float4* base = reinterpret_cast<float4*>(gx);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t hh = h + (k >> 1), ww = w + (k & 1);
+      base[((n * g.H + hh) * g.W + ww) * c4n + c4] = make_float4(o[k][0], o[k][1], o[k][2], o[k][3]);
+    }
+  }
+}
+
 static int pool_geom(int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int64_t s, int64_t pad, PoolGeom* g) {
   if (n < 1 || h < 1 || w < 1 || c < 4 || c % 4 != 0 || k < 1 || k > 15 || s < 1 || pad < 0 || 2 * pad > k)
     return set_error(I8T_EINVAL, "maxpool: bad geometry (needs c % 4 == 0, k <= 15, pad <= k/2)");
@@ -139,6 +190,12 @@ int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n
   int rc = pool_geom(n, h, w, c, k, s, pad, &g);
   if (rc) return rc;
   if (!cx || !gy || !idx || !gx) return set_error(I8T_EINVAL, "maxpool_bwd: bad arguments");
+  if (g.k == 3 && g.s == 2 && g.pad == 1 && g.H == 2 * g.P && g.W == 2 * g.Q) {
+    const int64_t blocks = static_cast<int64_t>(g.N) * g.P * g.Q * (g.C / 4);
+    k_maxpool_bwd_s2k3<<<grid_of(blocks), 256, 0, cx->stream>>>(gy, idx, g, gx);
+    count_launch(1);
+    return cuda_check("k_maxpool_bwd_s2k3");
+  }
   const int64_t tot = static_cast<int64_t>(g.N) * g.H * g.W * (g.C / 4);
   k_maxpool_bwd<<<grid_of(tot), 256, 0, cx->stream>>>(gy, idx, g, gx);
   count_launch(1);
