@@ -112,6 +112,208 @@ __global__ void k_dw_wgrad_finalize(const long long* __restrict__ acc, int64_t n
     gw[i] = static_cast<float>(rs * static_cast<double>(acc[i]));
 }
 
+// ------------------------------------------------------------------ channel-quad kernels
+// C % 4 == 0, c_pad == C (every MobileNetV2 depthwise layer): a thread owns 4
+// consecutive channels (one 32-bit load per tap, a warp reads 128 contiguous
+// bytes), the 4 x R*S int8 weights of its quad packed in R*S registers, 32-bit
+// index math, R, S and the stride as template constants.  Same integer sums
+// (exact) and the same FP64 rescale as the generic kernels above.
+__device__ __forceinline__ int sbyte(uint32_t v, int k) { return static_cast<int>(static_cast<int8_t>(v >> (8 * k))); }
+
+template <int R, int S>
+__device__ __forceinline__ void dw_load_wq(const int8_t* __restrict__ w, int c0, uint32_t (&wq)[R * S]) {
+#pragma unroll
+  for (int t = 0; t < R * S; ++t)
+    wq[t] = static_cast<uint32_t>(static_cast<uint8_t>(w[(c0 + 0) * R * S + t])) |
+            static_cast<uint32_t>(static_cast<uint8_t>(w[(c0 + 1) * R * S + t])) << 8 |
+            static_cast<uint32_t>(static_cast<uint8_t>(w[(c0 + 2) * R * S + t])) << 16 |
+            static_cast<uint32_t>(static_cast<uint8_t>(w[(c0 + 3) * R * S + t])) << 24;
+}
+
+__device__ __forceinline__ void dw_mac4(int (&s)[4], uint32_t a, uint32_t w) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s[k] += sbyte(a, k) * sbyte(w, k);
+}
+
+__device__ __forceinline__ void dw_store4(const int (&s)[4], double rs, float* out, int32_t* acc, uint32_t i4) {
+  if (out)
+    reinterpret_cast<float4*>(out)[i4] =
+        make_float4(static_cast<float>(rs * s[0]), static_cast<float>(rs * s[1]), static_cast<float>(rs * s[2]),
+                    static_cast<float>(rs * s[3]));
+  if (acc) reinterpret_cast<int4*>(acc)[i4] = make_int4(s[0], s[1], s[2], s[3]);
+}
+
+// grid-stride over (pixel, quad); T = threads in the grid is a multiple of C/4,
+// so the quad is fixed per thread and the pixel advances by T / (C/4)
+template <int R, int S, int SH>
+__global__ void __launch_bounds__(256) k_dw_fwd4(const DwArgs d, const uint32_t* __restrict__ a,
+                                                 const int8_t* __restrict__ w, const float* clip_a,
+                                                 const float* clip_w, float* z, int32_t* acc) {
+  const double rs = dw_rescale(clip_a, clip_w);
+  const uint32_t nq = d.C / 4, T = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t qd = tid % nq;
+  uint32_t wq[R * S];
+  dw_load_wq<R, S>(w, 4 * qd, wq);
+  const uint32_t tot = static_cast<uint32_t>(d.N) * d.P * d.Q * nq;
+  for (uint32_t i = tid; i < tot; i += T) {
+    const uint32_t pix = i / nq;
+    const uint32_t q = pix % d.Q, np = pix / d.Q, p = np % d.P, n = np / d.P;
+    const int y0 = static_cast<int>(p) * SH - d.ph, x0 = static_cast<int>(q) * SH - d.pw;
+    const uint32_t* img = a + static_cast<uint32_t>(n) * d.H * d.W * nq + qd;
+    int s[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int ih = y0 + r;
+      if (ih < 0 || ih >= d.H) continue;
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        const int iw = x0 + t;
+        if (iw < 0 || iw >= d.W) continue;
+        dw_mac4(s, __ldg(img + (static_cast<uint32_t>(ih) * d.W + iw) * nq), wq[r * S + t]);
+      }
+    }
+    dw_store4(s, rs, z, acc, i);
+  }
+}
+
+// ga[n,h,w,c] = sum over the taps with (h+ph-r) % SH == 0, (w+pw-s) % SH == 0
+template <int R, int S, int SH>
+__global__ void __launch_bounds__(256) k_dw_dgrad4(const DwArgs d, const uint32_t* __restrict__ g,
+                                                   const int8_t* __restrict__ w, const float* clip_g,
+                                                   const float* clip_w, float* ga, int32_t* acc) {
+  const double rs = dw_rescale(clip_g, clip_w);
+  const uint32_t nq = d.C / 4, T = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t qd = tid % nq;
+  uint32_t wq[R * S];
+  dw_load_wq<R, S>(w, 4 * qd, wq);
+  const uint32_t tot = static_cast<uint32_t>(d.N) * d.H * d.W * nq;
+  for (uint32_t i = tid; i < tot; i += T) {
+    const uint32_t pix = i / nq;
+    const uint32_t x = pix % d.W, ny = pix / d.W, y = ny % d.H, n = ny / d.H;
+    const uint32_t* img = g + static_cast<uint32_t>(n) * d.P * d.Q * nq + qd;
+    int s[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int pn = static_cast<int>(y) + d.ph - r;
+      if (pn < 0 || (SH > 1 && pn % SH)) continue;
+      const int p = pn / SH;
+      if (p >= d.P) continue;
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        const int qn = static_cast<int>(x) + d.pw - t;
+        if (qn < 0 || (SH > 1 && qn % SH)) continue;
+        const int qq = qn / SH;
+        if (qq >= d.Q) continue;
+        dw_mac4(s, __ldg(img + (static_cast<uint32_t>(p) * d.Q + qq) * nq), wq[r * S + t]);
+      }
+    }
+    dw_store4(s, rs, ga, acc, i);
+  }
+}
+
+// gw[c][r*S+s] = sum_{n,p,q} g[n,p,q,c] * a[n, p*SH-ph+r, q*SH-pw+s, c]:
+// a lane takes groups of 4 consecutive output pixels of one row for its channel
+// quad, transposes the 4 pixels x 4 channels byte blocks with PRMT and
+// accumulates each channel's 4-pixel dot product with one DP4A per tap.
+// block = 64 quads x 4 lanes over DW_GROUPS pixel groups (int32 partials stay
+// exact), the lanes folded in smem, one int64 atomic per (c, tap) per block.
+constexpr int DW_GROUPS = 512;
+
+__device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&c)[4]) {
+  const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
+  const uint32_t t2 = __byte_perm(w0, w1, 0x7362), t3 = __byte_perm(w2, w3, 0x7362);
+  c[0] = __byte_perm(t0, t1, 0x5410);
+  c[1] = __byte_perm(t0, t1, 0x7632);
+  c[2] = __byte_perm(t2, t3, 0x5410);
+  c[3] = __byte_perm(t2, t3, 0x7632);
+}
+
+template <int R, int S, int SH>
+__global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_t* __restrict__ g,
+                                                   const uint32_t* __restrict__ a, unsigned long long* acc) {
+  const uint32_t nq = d.C / 4;
+  const uint32_t qd = blockIdx.x * 64 + (threadIdx.x & 63);
+  const bool live = qd < nq;  // no early return: the block folds its lanes with a barrier
+  const uint32_t lane4 = threadIdx.x >> 6;
+  const uint32_t qgs = (d.Q + 3) / 4;  // pixel groups per output row
+  const uint32_t ngroups = static_cast<uint32_t>(d.N) * d.P * qgs;
+  const uint32_t lo = blockIdx.y * static_cast<uint32_t>(DW_GROUPS);
+  const uint32_t hi = min(lo + static_cast<uint32_t>(DW_GROUPS), ngroups);
+  int sum[R * S][4];
+#pragma unroll
+  for (int t = 0; t < R * S; ++t) sum[t][0] = sum[t][1] = sum[t][2] = sum[t][3] = 0;
+  for (uint32_t gi = lo + lane4; live && gi < hi; gi += 4) {
+    const uint32_t qg = gi % qgs, np = gi / qgs, p = np % d.P, n = np / d.P;
+    const uint32_t q0 = qg * 4;
+    const uint32_t* grow = g + ((static_cast<uint32_t>(n) * d.P + p) * d.Q) * nq + qd;
+    uint32_t gw[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gw[i] = (q0 + i < static_cast<uint32_t>(d.Q)) ? __ldg(grow + (q0 + i) * nq) : 0u;
+    if ((gw[0] | gw[1] | gw[2] | gw[3]) == 0u) continue;  // common: sparse quantised gradients
+    uint32_t gc[4];
+    transpose4x4(gw[0], gw[1], gw[2], gw[3], gc);
+    const uint32_t* img = a + static_cast<uint32_t>(n) * d.H * d.W * nq + qd;
+    const int y0 = static_cast<int>(p) * SH - d.ph, x0 = static_cast<int>(q0) * SH - d.pw;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int ih = y0 + r;
+      if (ih < 0 || ih >= d.H) continue;
+      const uint32_t* arow = img + static_cast<uint32_t>(ih) * d.W * nq;
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        uint32_t aw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int iw = x0 + i * SH + t;
+          aw[i] = (iw >= 0 && iw < d.W && q0 + i < static_cast<uint32_t>(d.Q)) ? __ldg(arow + iw * nq) : 0u;
+        }
+        uint32_t ac[4];
+        transpose4x4(aw[0], aw[1], aw[2], aw[3], ac);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sum[r * S + t][k] = __dp4a(static_cast<int>(gc[k]), static_cast<int>(ac[k]), sum[r * S + t][k]);
+      }
+    }
+  }
+  __shared__ int red[3][64][R * S * 4 + 1];  // lanes 1..3 (+1 pad: bank spread)
+  if (lane4) {
+#pragma unroll
+    for (int t = 0; t < R * S; ++t)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[lane4 - 1][threadIdx.x & 63][t * 4 + k] = sum[t][k];
+  }
+  __syncthreads();
+  if (lane4) return;
+#pragma unroll
+  for (int t = 0; t < R * S; ++t)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long v = static_cast<long long>(sum[t][k]) + red[0][threadIdx.x][t * 4 + k] +
+                          red[1][threadIdx.x][t * 4 + k] + red[2][threadIdx.x][t * 4 + k];
+      if (live && v) atomicAdd(acc + static_cast<int64_t>(4 * qd + k) * (R * S) + t, static_cast<unsigned long long>(v));
+    }
+}
+
+static bool dw_quad_ok(const DwArgs& d, const void* p0, const void* p1) {
+  return d.C % 4 == 0 && d.Cp == d.C && d.R == 3 && d.S == 3 && d.sh == d.sw && (d.sh == 1 || d.sh == 2) &&
+         (reinterpret_cast<uintptr_t>(p0) & 3u) == 0 && (reinterpret_cast<uintptr_t>(p1) & 3u) == 0 &&
+         static_cast<int64_t>(d.N) * d.H * d.W * d.C < (int64_t(1) << 32) &&
+         static_cast<int64_t>(d.N) * d.P * d.Q * d.C < (int64_t(1) << 32);
+}
+
+static int quad_grid(int64_t tot_quads, int nq) {
+  int64_t b = (tot_quads + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  // threads (b*256) a multiple of nq: the quad stays fixed per thread
+  int64_t g = 1, x = 256, y = nq;
+  while (y) { const int64_t t = x % y; x = y; y = t; }
+  g = nq / x;
+  return static_cast<int>((b + g - 1) / g * g);
+}
+
 static int dw_args(const i8t_conv_geom* g, int64_t c_pad, DwArgs& d) {
   if (!g || !g->depthwise || g->k != g->c) return set_error(I8T_EINVAL, "conv_dw: geometry must be depthwise with k == c");
   if (g->n < 1 || g->c < 1 || g->h < 1 || g->w < 1 || g->kh < 1 || g->kw < 1 || g->stride_h < 1 || g->stride_w < 1 ||
@@ -146,6 +348,14 @@ int i8t_conv_dw_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64
   int rc = dw_args(g, c_pad, d);
   if (rc) return rc;
   if (!c || !a || !w || !clip_a || !clip_w) return set_error(I8T_EINVAL, "conv_dw_fwd: null argument");
+  if (dw_quad_ok(d, a, z ? static_cast<const void*>(z) : static_cast<const void*>(acc))) {
+    const int nq = d.C / 4, grid = quad_grid(static_cast<int64_t>(d.N) * d.P * d.Q * nq, nq);
+    const uint32_t* a4 = reinterpret_cast<const uint32_t*>(a);
+    if (d.sh == 1) k_dw_fwd4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, a4, w, clip_a, clip_w, z, acc);
+    else k_dw_fwd4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, a4, w, clip_a, clip_w, z, acc);
+    count_launch(1);
+    return cuda_check("k_dw_fwd4");
+  }
   k_dw_fwd<<<blocks_for((int64_t)d.N * d.P * d.Q * d.C), 256, 0, c->stream>>>(d, a, w, clip_a, clip_w, z, acc);
   count_launch(1);
   return cuda_check("k_dw_fwd");
@@ -158,6 +368,14 @@ int i8t_conv_dw_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   int rc = dw_args(g, c_pad, d);
   if (rc) return rc;
   if (!c || !gz || !w || !clip_g || !clip_w) return set_error(I8T_EINVAL, "conv_dw_dgrad: null argument");
+  if (dw_quad_ok(d, gz, ga ? static_cast<const void*>(ga) : static_cast<const void*>(acc))) {
+    const int nq = d.C / 4, grid = quad_grid(static_cast<int64_t>(d.N) * d.H * d.W * nq, nq);
+    const uint32_t* g4 = reinterpret_cast<const uint32_t*>(gz);
+    if (d.sh == 1) k_dw_dgrad4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, g4, w, clip_g, clip_w, ga, acc);
+    else k_dw_dgrad4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, g4, w, clip_g, clip_w, ga, acc);
+    count_launch(1);
+    return cuda_check("k_dw_dgrad4");
+  }
   k_dw_dgrad<<<blocks_for((int64_t)d.N * d.H * d.W * d.C), 256, 0, c->stream>>>(d, gz, w, clip_g, clip_w, ga, acc);
   count_launch(1);
   return cuda_check("k_dw_dgrad");
@@ -172,6 +390,23 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
   if (!c || !gz || !a || !clip_g || !clip_a || !acc) return set_error(I8T_EINVAL, "conv_dw_wgrad: null argument");
   const int64_t RS = (int64_t)d.R * d.S, npq = (int64_t)d.N * d.P * d.Q;
   cudaMemsetAsync(acc, 0, sizeof(int64_t) * d.C * RS, c->stream);
+  if (dw_quad_ok(d, gz, a)) {
+    const int nq = d.C / 4;
+    const int64_t ngroups = static_cast<int64_t>(d.N) * d.P * ((d.Q + 3) / 4);
+    const dim3 grid((nq + 63) / 64, static_cast<unsigned>((ngroups + DW_GROUPS - 1) / DW_GROUPS));
+    const uint32_t *g4 = reinterpret_cast<const uint32_t*>(gz), *a4 = reinterpret_cast<const uint32_t*>(a);
+    unsigned long long* acc_u = reinterpret_cast<unsigned long long*>(acc);
+    if (d.sh == 1) k_dw_wgrad4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, g4, a4, acc_u);
+    else k_dw_wgrad4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, g4, a4, acc_u);
+    count_launch(1);
+    if ((rc = cuda_check("k_dw_wgrad4"))) return rc;
+    if (gw) {
+      k_dw_wgrad_finalize<<<blocks_for(d.C * RS), 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), d.C * RS,
+                                                                     clip_g, clip_a, gw);
+      count_launch(1);
+    }
+    return cuda_check("k_dw_wgrad_finalize");
+  }
   const int cblk = (d.C + 63) / 64;
   int64_t ysplit = (4 * 148 + cblk - 1) / cblk;
   int64_t per = (npq + ysplit - 1) / ysplit;

@@ -51,6 +51,9 @@ GEOMS = [
     (1, 16, 13, 13, 128, 7, 7, 2, 3, None, None, False),  # 7x7 s2 p3
     (3, 8, 6, 6, 8, 3, 3, 1, 1, None, None, True),       # depthwise
     (2, 40, 9, 9, 40, 3, 3, 2, 1, None, None, True),     # depthwise stride 2
+    (4, 96, 28, 28, 96, 3, 3, 1, 1, None, None, True),   # depthwise, channel-quad kernels
+    (3, 144, 29, 31, 144, 3, 3, 2, 1, None, None, True),  # depthwise stride 2, odd sizes
+    (2, 6, 7, 7, 6, 3, 3, 1, 1, None, None, True),       # depthwise C % 4 != 0 (generic kernels)
 ]
 
 
