@@ -260,7 +260,7 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
  * BatchNorm2d (layers.cpp:230-323) and ReLU (:328-344) are FP32 layers the
  * reference never quantises; these fuse them into the INT8 path's HBM passes.
  * Tensors are NHWC [m = N*H*W][c] fp32, c % 4 == 0.  bn: device doubles [6c]
- * (mean, invstd, s1/m, s2/m, gamma*invstd, ReLU-mask bounds), filled by the
+ * (mean, invstd, k*s1/m, k*s2/m, k = gamma*invstd, ReLU-mask bounds), filled by the
  * calls below.  mask_mode: 0 none, 1 ReLU mask recomputed from bn(z) > 0,
  * 2 mask_y > 0, 3 mask_y points at packed mask bits (uint32 words, see
  * i8t_bn_act_q).  With mask_mode 1, i8t_bn_bwd_reduce also stores per channel

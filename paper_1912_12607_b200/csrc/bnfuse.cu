@@ -225,9 +225,10 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     } else {  // layers.cpp:285-300
       a.grad_beta[cc] = static_cast<float>(s0);
       a.grad_gamma[cc] = static_cast<float>(s1);
-      a.bn[2 * a.c + cc] = s0 / m;
-      a.bn[3 * a.c + cc] = s1 / m;
-      a.bn[4 * a.c + cc] = static_cast<double>(a.gamma[cc]) * a.bn[a.c + cc];
+      const double k = static_cast<double>(a.gamma[cc]) * a.bn[a.c + cc];
+      a.bn[2 * a.c + cc] = k * (s0 / m);
+      a.bn[3 * a.c + cc] = k * (s1 / m);
+      a.bn[4 * a.c + cc] = k;
     }
   }
   __syncthreads();
@@ -377,9 +378,12 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
   }
 }
 
-// Backward value source: g_in = float(gamma*invstd * (g_m - s1/m - x_hat*(s2/m))),
-// g_m = g masked by the ReLU that followed the BN (MASK 1: relu(bn(z)) > 0
-// recomputed from z; MASK 2: a stored output y > 0; MASK 0: none).
+// Backward value source: g_in = float(k*g_m - (k*s1/m + x_hat*(k*s2/m))) with
+// k = gamma*invstd (layers.cpp:309-318 regrouped into two FMAs: the double
+// rounding differs from the reference's by ~2^-53 of the largest term, below
+// the final float cast), g_m = g masked by the ReLU that followed the BN
+// (MASK 1: relu(bn(z)) > 0 recomputed from z; MASK 2: a stored output y > 0;
+// MASK 3: packed mask bits; MASK 0: none).
 template <int MASK>
 struct BnBwdSrc {
   const float* g;
@@ -389,7 +393,7 @@ struct BnBwdSrc {
   const float* gamma;
   const float* beta;
   uint32_t c;
-  double mean[4], invstd[4], a[4], b[4], k[4];
+  double mean[4], invstd[4], ka[4], kb[4], k[4];
   float lo[4], hi[4];  // MASK 1: relu(bn(z)) > 0 <=> lo <= z <= hi
   struct Raw {
     float4 g, z, y;
@@ -400,8 +404,8 @@ struct BnBwdSrc {
     for (int j = 0; j < 4; ++j) {
       mean[j] = bn[c0 + j];
       invstd[j] = bn[c + c0 + j];
-      a[j] = bn[2 * c + c0 + j];
-      b[j] = bn[3 * c + c0 + j];
+      ka[j] = bn[2 * c + c0 + j];
+      kb[j] = bn[3 * c + c0 + j];
       k[j] = bn[4 * c + c0 + j];
       if (MASK == 1) {
         const float2 lh = reinterpret_cast<const float2*>(bn + 5 * c)[c0 + j];
@@ -419,29 +423,28 @@ struct BnBwdSrc {
     if (MASK == 3) r.shift = (e4 & 7u) * 4u;
     return r;
   }
-  // exact (reference) value, and the fast one that flags float-subnormal x_hat
+  // element j: exact (reference x_hat = double(float(x))), or the fast x_hat
+  // (rn24) that flags float-subnormal x_hat in `sub`
   template <bool FAST>
-  __device__ __forceinline__ float4 value_t(const Raw& r, bool& slow) const {
-    const float gg[4] = {r.g.x, r.g.y, r.g.z, r.g.w}, zz[4] = {r.z.x, r.z.y, r.z.z, r.z.w};
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
-      bool mk = true;
-      if (MASK == 1) mk = zz[j] >= lo[j] && zz[j] <= hi[j];
-      if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
-      if (MASK == 3) mk = (r.bits >> (r.shift + j)) & 1u;
-      const double gd = mk ? static_cast<double>(gg[j]) : 0.0;
-      const double xh = FAST ? rn24(xv, slow) : static_cast<double>(static_cast<float>(xv));
-      o[j] = static_cast<float>(k[j] * (gd - a[j] - xh * b[j]));
-    }
-    return make_float4(o[0], o[1], o[2], o[3]);
+  __device__ __forceinline__ float elem(const Raw& r, int j, bool& sub) const {
+    const float zz = j == 0 ? r.z.x : j == 1 ? r.z.y : j == 2 ? r.z.z : r.z.w;
+    const float gg = j == 0 ? r.g.x : j == 1 ? r.g.y : j == 2 ? r.g.z : r.g.w;
+    const double xv = (static_cast<double>(zz) - mean[j]) * invstd[j];
+    bool mk = true;
+    if (MASK == 1) mk = zz >= lo[j] && zz <= hi[j];
+    if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
+    if (MASK == 3) mk = (r.bits >> (r.shift + j)) & 1u;
+    const double gd = static_cast<double>(mk ? gg : 0.0f);
+    const double xh = FAST ? rn24(xv, sub) : static_cast<double>(static_cast<float>(xv));
+    return static_cast<float>(fma(k[j], gd, -fma(xh, kb[j], ka[j])));
   }
   __device__ __forceinline__ float4 value(const Raw& r) const {
-    bool dummy = false;
-    return value_t<false>(r, dummy);
+    bool d = false;
+    return make_float4(elem<false>(r, 0, d), elem<false>(r, 1, d), elem<false>(r, 2, d), elem<false>(r, 3, d));
   }
-  __device__ __forceinline__ float4 value_fast(const Raw& r, bool& slow) const { return value_t<true>(r, slow); }
+  __device__ __forceinline__ float4 value_fast(const Raw& r, bool& slow) const {
+    return make_float4(elem<true>(r, 0, slow), elem<true>(r, 1, slow), elem<true>(r, 2, slow), elem<true>(r, 3, slow));
+  }
   __device__ __forceinline__ float4 load(uint32_t e4) const { return value(fetch(e4)); }
 };
 

@@ -74,6 +74,41 @@ __device__ __forceinline__ int qs_fast(float t, uint32_t X, bool& slow) {
   return (__float_as_int(rb) - RMAGIC_BITS) + (d > 0.0f ? 1 : 0);
 }
 
+// Leaner fast path of K3: the decision is within 2^-15 of the exact one
+// (3 * 2^-17 from s, 0.5/clip and w, 2^-18 each from t1 and y, 2^-23 from
+// the truncated u), so a margin QK = 2^-14 suffices.  Clamp and scale in
+// two FMA-pipe ops: w = sat(v * (0.5/clip) + 0.5) (NaN -> 0, like the clamp
+// of the exact path), t1 = 254 w - 126 = t + 1 within 2^-15 of RN64(v/s) + 1
+// for |v| <= clip and exactly 127 + 1 (-127 + 1) beyond it.  The quantised
+// values come back as the float bit patterns of RMAGIC + q (qs) and
+// RMAGIC + q + 1 (qn): their low byte is the int8 and they index the dequant
+// table directly; callers that take the exact path build the same patterns.
+constexpr float QK = 0x1.0p-14f;
+__device__ __forceinline__ float q_t1(float v, float hs) {
+  return __fmaf_rn(__saturatef(__fmaf_rn(v, hs, 0.5f)), 254.0f, -126.0f);
+}
+// kStochastic: ceil(t - u) = round(t - u + 1/2) away from the boundaries;
+// 1 + u is the float with X's top 23 bits as significand (one funnel shift).
+__device__ __forceinline__ uint32_t qs_bits(float t1, uint32_t X, bool& slow) {
+  const float uh = __fsub_rn(__uint_as_float(__funnelshift_r(X, 0x7Fu, 9)), 0.5f);  // 1/2 + u, exact
+  const float yh = __fsub_rn(t1, uh);                                                // t - u + 1/2
+  const float kb = __fadd_rn(yh, RMAGIC);
+  slow |= fabsf(__fsub_rn(yh, __fsub_rn(kb, RMAGIC))) > 0.5f - QK;
+  return __float_as_uint(kb);
+}
+// kNearest: round-half-away(t); ties and near-ties are slow.
+__device__ __forceinline__ uint32_t qn_bits(float t1, bool& slow) {
+  const float kb = __fadd_rn(t1, RMAGIC);
+  slow |= fabsf(__fsub_rn(t1, __fsub_rn(kb, RMAGIC))) > 0.5f - QK;
+  return __float_as_uint(kb);
+}
+// 8-byte shared load at a 32-bit shared-window address.
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // quantize_value, kStochastic, exact: the FP32 fast path where it decides,
 // else the reference's FP64 formula (quantize.cpp:16-31).
 __device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {

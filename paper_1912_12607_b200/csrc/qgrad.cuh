@@ -37,7 +37,7 @@ struct QgFin {
 // Tail of quantize_gradient (layers.cpp:32-58) from global totals.
 static __device__ void fin_quant_grad(DsgcState* st, const double* tot, const QgFin& f, uint32_t* lcg_state, int* err) {
   const float m = static_cast<float>(tot[0]);
-  const bool nonfinite = tot[1] > 0.0;
+  const bool nonfinite = tot[1] > 0.0 || !isfinite(tot[5]);
   if (f.mode & 4) {  // plain stochastic quantize (quantize.cpp:33-43): any non-finite throws
     if (nonfinite) atomicOr(err, ERR_NONFINITE);
     *lcg_state = apply(lcg_jump_map(f.advance), *lcg_state);
@@ -80,15 +80,16 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
   __shared__ double tab[256];
   float clip = clip_override ? *clip_override : st->v.clip;
   if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
-  const float s = scale_of(clip), inv_s = 1.0f / s;
+  const float s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   build_dequant_table(tab, s);
   __syncthreads();
-  const double* tab0 = tab + 127;  // tab0[q], q in [-127, 127]
+  // tab[q + 127] at the bit patterns qs_bits / qn_bits return (32-bit wrap)
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 8u * (127u - RMAGIC_BITS);
+  const uint32_t tab_n = tab_s - 8u;
   const uint32_t X0 = *lcg_state;
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   double a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0, a6 = 0.0;
-  bool bad = false;
   float m = 0.0f;
   if (e < numel) {
     uint32_t X, hw = 0;
@@ -102,63 +103,51 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
       X = apply(lcg_jump_map(static_cast<uint64_t>((n * C + c) * HW + hw) + draw_offset + 1u), X0);
       src.init(c);
     }
-    typename Src::Raw r0 = src.fetch(e / 4), r1 = r0;
-    uint32_t e1 = e + T4;
-    if (e1 < numel) r1 = src.fetch(e1 / 4);
-    while (true) {
-      const uint32_t e2 = e1 + T4;  // < 2^31 + 2*T4: no wrap
-      typename Src::Raw r2 = r1;
-      if (e2 < numel) r2 = src.fetch(e2 / 4);
-      // fast path for the float4 (branch-free); any element within 2^-13 of a
-      // rounding boundary (or with a float-subnormal BN x_hat) redoes the
-      // float4 with the exact functions
+    // one float4: fast path; any element within QK of a rounding boundary (or
+    // with a float-subnormal BN x_hat) sends the float4 to the exact functions
+    auto process = [&](const typename Src::Raw& r) {
       bool slow = false;
-      const float4 v4 = src.value_fast(r0, slow);
+      const float4 v4 = src.value_fast(r, slow);
       float vv[4] = {v4.x, v4.y, v4.z, v4.w};
       uint32_t Xs[4];
       Xs[0] = X;
 #pragma unroll
       for (int j = 1; j < 4; ++j) Xs[j] = apply(step_elem, Xs[j - 1]);
-      int qs[4], qn[4];
+      uint32_t ks[4], kn[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float t = __fmul_rn(fminf(fmaxf(vv[j], -clip), clip), inv_s);
-        qs[j] = qs_fast(t, Xs[j], slow);
-        if (DC_SUMS) qn[j] = qn_fast(t, slow);
+        const float t1 = q_t1(vv[j], hs);
+        ks[j] = qs_bits(t1, Xs[j], slow);
+        if (DC_SUMS) kn[j] = qn_bits(t1, slow);
       }
-      if (slow) {
-        const float4 w4 = src.value(r0);
+      if (slow) {  // rare: the float4 again through the exact functions
+        const float4 w4 = src.value(r);
         vv[0] = w4.x; vv[1] = w4.y; vv[2] = w4.z; vv[3] = w4.w;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          qs[j] = quant_stoch(vv[j], clip, s, inv_s, Xs[j]);
-          if (DC_SUMS) qn[j] = quant_nearest(vv[j], clip, s, inv_s);
+          ks[j] = static_cast<uint32_t>(RMAGIC_BITS + quant_stoch(vv[j], clip, s, inv_s, Xs[j]));
+          if (DC_SUMS) kn[j] = static_cast<uint32_t>(RMAGIC_BITS + 1 + quant_nearest(vv[j], clip, s, inv_s));
         }
       }
-      signed char qq[4];
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(vv[0]), fabsf(vv[1])), fmaxf(fabsf(vv[2]), fabsf(vv[3]))));
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float v = vv[j];
-        bad |= !isfinite(v);
-        m = fmaxf(m, fabsf(v));
-        qq[j] = static_cast<signed char>(qs[j]);
-        const double vd = v, gsd = tab0[qs[j]];
+        const double vd = vv[j], gsd = lds_f64(tab_s + 8u * ks[j]);
         const double d = vd - gsd;
         a5 = fma(d, d, a5);
         a6 = fma(gsd, gsd, a6);
         if (DC_SUMS) {
-          const double gn = tab0[qn[j]];
+          const double gn = lds_f64(tab_n + 8u * kn[j]);
           a2 = fma(vd, vd, a2);
           a3 = fma(vd, gn, a3);
           a4 = fma(gn, gn, a4);
         }
       }
-      reinterpret_cast<char4*>(q)[e / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
-      if (e1 >= numel) break;
-      e = e1;
-      e1 = e2;
-      r0 = r1;
-      r1 = r2;
+      reinterpret_cast<uint32_t*>(q)[e / 4] = __byte_perm(__byte_perm(ks[0], ks[1], 0x0040),
+                                                          __byte_perm(ks[2], ks[3], 0x0040), 0x5410);
+    };
+    auto advance = [&]() {
+      e += T4;
       X = apply(step_iter, X);
       if (!FLAT) {
         hw += dpix;
@@ -167,9 +156,29 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
           X = apply(step_wrap, X);
         }
       }
+    };
+    // three-slot ring, two float4 fetches in flight ahead of the one being
+    // quantised; unrolled so the slots never move between registers
+    typename Src::Raw ra = src.fetch(e / 4), rb = ra, rc = ra;
+    if (e + T4 < numel) rb = src.fetch((e + T4) / 4);
+    while (true) {  // e + 2*T4 < 2^31 + 2*T4: no wrap
+      if (e + 2 * T4 < numel) rc = src.fetch((e + 2 * T4) / 4);
+      process(ra);
+      if (e + T4 >= numel) break;
+      advance();
+      if (e + 2 * T4 < numel) ra = src.fetch((e + 2 * T4) / 4);
+      process(rb);
+      if (e + T4 >= numel) break;
+      advance();
+      if (e + 2 * T4 < numel) rb = src.fetch((e + 2 * T4) / 4);
+      process(rc);
+      if (e + T4 >= numel) break;
+      advance();
     }
   }
-  double acc[QG_NV] = {m, bad ? 1.0 : 0.0, a2, a3, a4, a5, a6, 0.0};
+  // non-finite inputs show up as a non-finite sum of squared errors
+  // (|v - g_s|^2 summed in double cannot overflow for finite float v)
+  double acc[QG_NV] = {m, 0.0, a2, a3, a4, a5, a6, 0.0};
   if (grid_reduce<QG_NV>(acc, 1u, partials, totals, ticket) && FUSED && threadIdx.x == 0)
     fin_quant_grad(st, totals, fin, lcg_state, err);
 }

@@ -637,7 +637,7 @@ class BatchNorm2d(Layer):
         self.running_mean = torch.zeros(c, device=device)
         self.running_var = torch.ones(c, device=device)
         self.momentum, self.eps = momentum, eps
-        self.stats = torch.zeros(6 * c, dtype=torch.float64, device=device)  # mean, invstd, s1/m, s2/m, gamma*invstd
+        self.stats = torch.zeros(6 * c, dtype=torch.float64, device=device)  # mean, invstd, k*s1/m, k*s2/m, k = gamma*invstd, mask bounds
         self._z = None
 
     def params(self):

@@ -163,8 +163,10 @@ def test_bn_backward_matches_reference(ops, mode):
     np.testing.assert_allclose(gg.cpu().numpy(), s2.astype(np.float32), rtol=1e-6, atol=1e-12)
     b = bn.cpu().numpy()
     # sums of +-terms: relative error is bounded against the largest sum, not each one
-    np.testing.assert_allclose(b[2 * c:3 * c], s1 / m, rtol=1e-9, atol=1e-9 * np.abs(s1 / m).max())
-    np.testing.assert_allclose(b[3 * c:4 * c], s2 / m, rtol=1e-9, atol=1e-9 * np.abs(s2 / m).max())
+    k = gamma.astype(np.float64) * ref["inv"]  # bn[4c..5c) = gamma*invstd, bn[2c..4c) = k*s1/m, k*s2/m
+    np.testing.assert_allclose(b[4 * c:5 * c], k, rtol=1e-9)
+    np.testing.assert_allclose(b[2 * c:3 * c], k * s1 / m, rtol=1e-9, atol=1e-9 * np.abs(k * s1 / m).max())
+    np.testing.assert_allclose(b[3 * c:4 * c], k * s2 / m, rtol=1e-9, atol=1e-9 * np.abs(k * s2 / m).max())
     gi = torch.empty_like(zt)
     ops.call("i8t_bn_bwd_apply", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bn), ops._p(gt), ops._p(bt), mode,
              ops._p(my) if mode == 2 else None, ops._p(gi))
