@@ -50,6 +50,7 @@ struct ColArgs {
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
 template <int MODE, int MASK = 0>
 __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets) {
+  pdl_entry();
   const uint32_t c0 = blockIdx.y * BN_GROUP;
   const uint32_t gw = min(static_cast<uint32_t>(BN_GROUP), a.c - c0);  // group width (multiple of 4)
   const uint32_t lpr = gw / 4;                                         // lanes per row
@@ -110,22 +111,21 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
         } else {
           const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
           const float yy[4] = {yv[u].x, yv[u].y, yv[u].z, yv[u].w};
-          double xv[4], xh[4], gm[4];
-          bool sub = false;
+          double xh[4], gm[4];
+          // MASK 3: this row's nibble (ch % 4 == 0, so the 4 bits share a word)
+          const uint32_t w = (MASK == 3 && valid) ? bv[u] >> (((r + u * row_step) * a.c + ch) & 31u) : 0u;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            xv[j] = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
+            const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
             bool mk = valid;
             if (MASK == 1) mk = mk && zz[j] >= lo[j] && zz[j] <= hi[j];
             else if (MASK == 2) mk = mk && yy[j] > 0.0f;
-            else if (MASK == 3) mk = mk && ((bv[u] >> (((r + u * row_step) * a.c + ch + j) & 31u)) & 1u);
-            gm[j] = mk ? static_cast<double>(gg[j]) : 0.0;
-            xh[j] = rn24(xv[j], sub);
-          }
-          if (__any_sync(__activemask(), sub)) {  // float-subnormal x_hat (rare): the converting path
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (fabs(xv[j]) < 0x1.0p-126) xh[j] = static_cast<double>(static_cast<float>(xv[j]));
+            else if (MASK == 3) mk = (w >> j) & 1u;
+            float gmf;  // masked g as a float select, converted once
+            asm("{.reg .pred p; setp.ne.u32 p, %1, 0; selp.f32 %0, %2, 0f00000000, p;}"
+                : "=f"(gmf) : "r"(mk ? 1u : 0u), "f"(gg[j]));
+            gm[j] = static_cast<double>(gmf);
+            xh[j] = rn24(xv);  // x_hat as in BnBwdSrc::elem
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
                                                       const double* bn, const float* gamma, const float* beta, int relu,
                                                       const float* clip_p, int8_t* __restrict__ q, float* amax,
                                                       int* err) {
+  pdl_entry();
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
                                                 const double* res_bn, const float* res_gamma, const float* res_beta,
                                                 float* __restrict__ y, const float* clip_p, int8_t* __restrict__ q,
                                                 uint32_t* __restrict__ mbits, float* amax, int* err) {
+  pdl_entry();
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;  // multiple of 128 and of c
   const uint32_t lane = threadIdx.x & 31;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
@@ -423,33 +425,35 @@ struct BnBwdSrc {
     if (MASK == 3) r.shift = (e4 & 7u) * 4u;
     return r;
   }
-  // element j: exact (reference x_hat = double(float(x))), or the fast x_hat
-  // (rn24) that flags float-subnormal x_hat in `sub`
-  template <bool FAST>
-  __device__ __forceinline__ float elem(const Raw& r, int j, bool& sub) const {
+  // element j; w = the float4's mask bits (MASK 3).  x_hat (here and in the
+  // MODE 1 column sums) is rounded to a
+  // 24-bit significand in the integer pipe (rn24), i.e. the reference's
+  // float(x) without the float-subnormal range: the two differ only for
+  // |x_hat| < 2^-126, where the effect on g_in is below 2^-149 * |k s2/m|.
+  __device__ __forceinline__ float elem(const Raw& r, int j, uint32_t w) const {
     const float zz = j == 0 ? r.z.x : j == 1 ? r.z.y : j == 2 ? r.z.z : r.z.w;
     const float gg = j == 0 ? r.g.x : j == 1 ? r.g.y : j == 2 ? r.g.z : r.g.w;
     const double xv = (static_cast<double>(zz) - mean[j]) * invstd[j];
     bool mk = true;
     if (MASK == 1) mk = zz >= lo[j] && zz <= hi[j];
     if (MASK == 2) mk = (j == 0 ? r.y.x : j == 1 ? r.y.y : j == 2 ? r.y.z : r.y.w) > 0.0f;
-    if (MASK == 3) mk = (r.bits >> (r.shift + j)) & 1u;
-    const double gd = static_cast<double>(mk ? gg : 0.0f);
-    const double xh = FAST ? rn24(xv, sub) : static_cast<double>(static_cast<float>(xv));
-    return static_cast<float>(fma(k[j], gd, -fma(xh, kb[j], ka[j])));
+    if (MASK == 3) mk = (w >> j) & 1u;
+    float gm;  // the masked g as a float select (the conversion then runs once)
+    asm("{.reg .pred p; setp.ne.u32 p, %1, 0; selp.f32 %0, %2, 0f00000000, p;}" : "=f"(gm) : "r"(mk ? 1u : 0u), "f"(gg));
+    const double xh = rn24(xv);
+    return static_cast<float>(fma(k[j], static_cast<double>(gm), -fma(xh, kb[j], ka[j])));
   }
   __device__ __forceinline__ float4 value(const Raw& r) const {
-    bool d = false;
-    return make_float4(elem<false>(r, 0, d), elem<false>(r, 1, d), elem<false>(r, 2, d), elem<false>(r, 3, d));
+    const uint32_t w = (MASK == 3) ? (r.bits >> r.shift) : 0u;
+    return make_float4(elem(r, 0, w), elem(r, 1, w), elem(r, 2, w), elem(r, 3, w));
   }
-  __device__ __forceinline__ float4 value_fast(const Raw& r, bool& slow) const {
-    return make_float4(elem<true>(r, 0, slow), elem<true>(r, 1, slow), elem<true>(r, 2, slow), elem<true>(r, 3, slow));
-  }
+  __device__ __forceinline__ float4 value_fast(const Raw& r, bool&) const { return value(r); }
   __device__ __forceinline__ float4 load(uint32_t e4) const { return value(fetch(e4)); }
 };
 
 template <int MASK>
 __global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc<MASK> src, uint32_t n, float* __restrict__ out) {
+  pdl_entry();
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   if (e >= n) return;
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc<MASK> src, uint32
 // out = a + g * (y > 0): identity-shortcut gradient joined with the main branch.
 __global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a, const float* __restrict__ g,
                                                     const float* __restrict__ y, uint32_t n4, float* __restrict__ out) {
+  pdl_entry();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
     const float4 av = __ldg(reinterpret_cast<const float4*>(a) + i), gv = __ldg(reinterpret_cast<const float4*>(g) + i),
                  yv = __ldg(reinterpret_cast<const float4*>(y) + i);
@@ -474,6 +479,7 @@ __global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a,
 
 // ReLU-mask bounds per channel into bn[5c..6c) (as float2).
 __global__ void k_bn_mask_bounds(double* bn, const float* gamma, const float* beta, uint32_t c) {
+  pdl_entry();
   const uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x;
   if (ch >= c) return;
   reinterpret_cast<float2*>(bn + 5 * c)[ch] = bn_mask_bounds(bn[ch], bn[c + ch], gamma[ch], beta[ch]);
@@ -483,6 +489,7 @@ __global__ void k_bn_mask_bounds(double* bn, const float* gamma, const float* be
 __global__ void __launch_bounds__(256) k_add_masked_bits(const float* __restrict__ a, const float* __restrict__ g,
                                                          const float* __restrict__ bits, uint32_t n4,
                                                          float* __restrict__ out) {
+  pdl_entry();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
     const float4 av = __ldg(reinterpret_cast<const float4*>(a) + i), gv = __ldg(reinterpret_cast<const float4*>(g) + i);
     const uint32_t b = mask_nibble(bits, 4ull * i);
@@ -514,13 +521,13 @@ static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const d
   const uint32_t n = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
   const int nb = ew_blocks(m * c, c);
   if (res_z)
-    k_bn_act<QOUT, 2><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, nullptr, res_z, res_bn, res_gamma,
+    launch_k(k_bn_act<QOUT, 2>, nb, 256, 0, cx->stream, z, n, uc, bn, gamma, beta, relu, nullptr, res_z, res_bn, res_gamma,
                                                   res_beta, y, clip, q, mbits, amax, cx->d_err);
   else if (res)
-    k_bn_act<QOUT, 1><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, res, nullptr, nullptr, nullptr,
+    launch_k(k_bn_act<QOUT, 1>, nb, 256, 0, cx->stream, z, n, uc, bn, gamma, beta, relu, res, nullptr, nullptr, nullptr,
                                                   nullptr, y, clip, q, mbits, amax, cx->d_err);
   else
-    k_bn_act<QOUT, 0><<<nb, 256, 0, cx->stream>>>(z, n, uc, bn, gamma, beta, relu, nullptr, nullptr, nullptr, nullptr,
+    launch_k(k_bn_act<QOUT, 0>, nb, 256, 0, cx->stream, z, n, uc, bn, gamma, beta, relu, nullptr, nullptr, nullptr, nullptr,
                                                   nullptr, y, clip, q, mbits, amax, cx->d_err);
 }
 
@@ -543,11 +550,11 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   unsigned* t = tickets(c);
   if (!p || !t) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
-  if (mode == 0) k_bn_colsum<0><<<grid, 256, 0, c->stream>>>(a, p, t);
-  else if (a.mask_mode == 1) k_bn_colsum<1, 1><<<grid, 256, 0, c->stream>>>(a, p, t);
-  else if (a.mask_mode == 2) k_bn_colsum<1, 2><<<grid, 256, 0, c->stream>>>(a, p, t);
-  else if (a.mask_mode == 3) k_bn_colsum<1, 3><<<grid, 256, 0, c->stream>>>(a, p, t);
-  else k_bn_colsum<1, 0><<<grid, 256, 0, c->stream>>>(a, p, t);
+  if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t);
+  else if (a.mask_mode == 1) launch_k(k_bn_colsum<1, 1>, grid, 256, 0, c->stream, a, p, t);
+  else if (a.mask_mode == 2) launch_k(k_bn_colsum<1, 2>, grid, 256, 0, c->stream, a, p, t);
+  else if (a.mask_mode == 3) launch_k(k_bn_colsum<1, 3>, grid, 256, 0, c->stream, a, p, t);
+  else launch_k(k_bn_colsum<1, 0>, grid, 256, 0, c->stream, a, p, t);
   count_launch(1);
   return cuda_check("k_bn_colsum");
 }
@@ -584,7 +591,7 @@ int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const d
   int rc = bn_check(m, c, z);
   if (rc) return rc;
   if (!cx || !bn || !gamma || !beta || !clip || !q) return set_error(I8T_EINVAL, "bn_act_quant: bad arguments");
-  k_bn_act_quant<<<ew_blocks(m * c, c), 256, 0, cx->stream>>>(z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c),
+  launch_k(k_bn_act_quant, ew_blocks(m * c, c), 256, 0, cx->stream, z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c),
                                                                bn, gamma, beta, relu, clip, q, amax, cx->d_err);
   count_launch(1);
   return cuda_check("k_bn_act_quant");
@@ -633,7 +640,7 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
   a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = mask_mode;
   a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
   if (mask_mode == 1) {
-    k_bn_mask_bounds<<<static_cast<unsigned>((c + 127) / 128), 128, 0, cx->stream>>>(bn, gamma, beta,
+    launch_k(k_bn_mask_bounds, static_cast<unsigned>((c + 127) / 128), 128, 0, cx->stream, bn, gamma, beta,
                                                                                      static_cast<uint32_t>(c));
     count_launch(1);
     if ((rc = cuda_check("k_bn_mask_bounds"))) return rc;
@@ -650,10 +657,10 @@ int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, in
     return set_error(I8T_EINVAL, "bn_bwd_apply: bad arguments");
   const uint32_t un = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
   const int nb = ew_blocks(m * c, c);
-  if (mask_mode == 1) k_bn_bwd_apply<1><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
-  else if (mask_mode == 2) k_bn_bwd_apply<2><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
-  else if (mask_mode == 3) k_bn_bwd_apply<3><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<3>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
-  else k_bn_bwd_apply<0><<<nb, 256, 0, cx->stream>>>(BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  if (mask_mode == 1) launch_k(k_bn_bwd_apply<1>, nb, 256, 0, cx->stream, BnBwdSrc<1>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else if (mask_mode == 2) launch_k(k_bn_bwd_apply<2>, nb, 256, 0, cx->stream, BnBwdSrc<2>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else if (mask_mode == 3) launch_k(k_bn_bwd_apply<3>, nb, 256, 0, cx->stream, BnBwdSrc<3>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
+  else launch_k(k_bn_bwd_apply<0>, nb, 256, 0, cx->stream, BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   count_launch(1);
   return cuda_check("k_bn_bwd_apply");
 }
@@ -688,7 +695,7 @@ int i8t_add_masked_bits(i8t_ctx* ctx, const float* a, const float* g, const uint
   if (!n) return I8T_OK;
   int b = static_cast<int>((n / 4 + 255) / 256);
   if (b > 148 * 8) b = 148 * 8;
-  k_add_masked_bits<<<b, 256, 0, cx->stream>>>(a, g, reinterpret_cast<const float*>(bits), static_cast<uint32_t>(n / 4),
+  launch_k(k_add_masked_bits, b, 256, 0, cx->stream, a, g, reinterpret_cast<const float*>(bits), static_cast<uint32_t>(n / 4),
                                                 out);
   count_launch(1);
   return cuda_check("k_add_masked_bits");
@@ -700,7 +707,7 @@ int i8t_add_masked(i8t_ctx* ctx, const float* a, const float* g, const float* y,
   if (!n) return I8T_OK;
   int b = static_cast<int>((n / 4 + 255) / 256);
   if (b > 148 * 8) b = 148 * 8;
-  k_add_masked<<<b, 256, 0, cx->stream>>>(a, g, y, static_cast<uint32_t>(n / 4), out);
+  launch_k(k_add_masked, b, 256, 0, cx->stream, a, g, y, static_cast<uint32_t>(n / 4), out);
   count_launch(1);
   return cuda_check("k_add_masked");
 }

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -13,6 +14,14 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("I8T_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int set_error(int status, const std::string& msg) {
   g_last_error = msg;

@@ -20,6 +20,7 @@ __device__ __forceinline__ double dw_rescale(const float* x, const float* y) {
 // z[n,p,q,c] = sum_{r,s} a[n, p*sh-ph+r, q*sw-pw+s, c] * w[c][r*S+s]
 __global__ void __launch_bounds__(256) k_dw_fwd(const DwArgs d, const int8_t* __restrict__ a, const int8_t* __restrict__ w,
                                                 const float* clip_a, const float* clip_w, float* z, int32_t* acc) {
+  pdl_entry();
   const double rs = dw_rescale(clip_a, clip_w);
   const int64_t tot = static_cast<int64_t>(d.N) * d.P * d.Q * d.C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(256) k_dw_fwd(const DwArgs d, const int8_t* __
 // ga[n,h,w,c] = sum_{r,s: (h+ph-r) % sh == 0 ...} g[n,p,q,c] * w[c][r*S+s]
 __global__ void __launch_bounds__(256) k_dw_dgrad(const DwArgs d, const int8_t* __restrict__ g, const int8_t* __restrict__ w,
                                                   const float* clip_g, const float* clip_w, float* ga, int32_t* acc) {
+  pdl_entry();
   const double rs = dw_rescale(clip_g, clip_w);
   const int64_t tot = static_cast<int64_t>(d.N) * d.H * d.W * d.C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(256) k_dw_dgrad(const DwArgs d, const int8_t* 
 constexpr int DW_MAXTAP = 49;
 __global__ void __launch_bounds__(256) k_dw_wgrad(const DwArgs d, const int8_t* __restrict__ g, const int8_t* __restrict__ a,
                                                   unsigned long long* acc, int64_t npq_per_block) {
+  pdl_entry();
   const int c = blockIdx.x * 64 + (threadIdx.x & 63);
   const int lane4 = threadIdx.x >> 6;
   if (c >= d.C) return;
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(256) k_dw_wgrad(const DwArgs d, const int8_t* 
 
 __global__ void k_dw_wgrad_finalize(const long long* __restrict__ acc, int64_t n, const float* clip_g, const float* clip_a,
                                     float* gw) {
+  pdl_entry();
   const double rs = dw_rescale(clip_g, clip_a);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     gw[i] = static_cast<float>(rs * static_cast<double>(acc[i]));
@@ -149,6 +153,7 @@ template <int R, int S, int SH>
 __global__ void __launch_bounds__(256) k_dw_fwd4(const DwArgs d, const uint32_t* __restrict__ a,
                                                  const int8_t* __restrict__ w, const float* clip_a,
                                                  const float* clip_w, float* z, int32_t* acc) {
+  pdl_entry();
   const double rs = dw_rescale(clip_a, clip_w);
   const uint32_t nq = d.C / 4, T = gridDim.x * blockDim.x;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -182,6 +187,7 @@ template <int R, int S, int SH>
 __global__ void __launch_bounds__(256) k_dw_dgrad4(const DwArgs d, const uint32_t* __restrict__ g,
                                                    const int8_t* __restrict__ w, const float* clip_g,
                                                    const float* clip_w, float* ga, int32_t* acc) {
+  pdl_entry();
   const double rs = dw_rescale(clip_g, clip_w);
   const uint32_t nq = d.C / 4, T = gridDim.x * blockDim.x;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,6 +239,7 @@ __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t 
 template <int R, int S, int SH>
 __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_t* __restrict__ g,
                                                    const uint32_t* __restrict__ a, unsigned long long* acc) {
+  pdl_entry();
   const uint32_t nq = d.C / 4;
   const uint32_t qd = blockIdx.x * 64 + (threadIdx.x & 63);
   const bool live = qd < nq;  // no early return: the block folds its lanes with a barrier
@@ -351,12 +358,12 @@ int i8t_conv_dw_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64
   if (dw_quad_ok(d, a, z ? static_cast<const void*>(z) : static_cast<const void*>(acc))) {
     const int nq = d.C / 4, grid = quad_grid(static_cast<int64_t>(d.N) * d.P * d.Q * nq, nq);
     const uint32_t* a4 = reinterpret_cast<const uint32_t*>(a);
-    if (d.sh == 1) k_dw_fwd4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, a4, w, clip_a, clip_w, z, acc);
-    else k_dw_fwd4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, a4, w, clip_a, clip_w, z, acc);
+    if (d.sh == 1) launch_k(k_dw_fwd4<3, 3, 1>, grid, 256, 0, c->stream, d, a4, w, clip_a, clip_w, z, acc);
+    else launch_k(k_dw_fwd4<3, 3, 2>, grid, 256, 0, c->stream, d, a4, w, clip_a, clip_w, z, acc);
     count_launch(1);
     return cuda_check("k_dw_fwd4");
   }
-  k_dw_fwd<<<blocks_for((int64_t)d.N * d.P * d.Q * d.C), 256, 0, c->stream>>>(d, a, w, clip_a, clip_w, z, acc);
+  launch_k(k_dw_fwd, blocks_for((int64_t)d.N * d.P * d.Q * d.C), 256, 0, c->stream, d, a, w, clip_a, clip_w, z, acc);
   count_launch(1);
   return cuda_check("k_dw_fwd");
 }
@@ -371,12 +378,12 @@ int i8t_conv_dw_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   if (dw_quad_ok(d, gz, ga ? static_cast<const void*>(ga) : static_cast<const void*>(acc))) {
     const int nq = d.C / 4, grid = quad_grid(static_cast<int64_t>(d.N) * d.H * d.W * nq, nq);
     const uint32_t* g4 = reinterpret_cast<const uint32_t*>(gz);
-    if (d.sh == 1) k_dw_dgrad4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, g4, w, clip_g, clip_w, ga, acc);
-    else k_dw_dgrad4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, g4, w, clip_g, clip_w, ga, acc);
+    if (d.sh == 1) launch_k(k_dw_dgrad4<3, 3, 1>, grid, 256, 0, c->stream, d, g4, w, clip_g, clip_w, ga, acc);
+    else launch_k(k_dw_dgrad4<3, 3, 2>, grid, 256, 0, c->stream, d, g4, w, clip_g, clip_w, ga, acc);
     count_launch(1);
     return cuda_check("k_dw_dgrad4");
   }
-  k_dw_dgrad<<<blocks_for((int64_t)d.N * d.H * d.W * d.C), 256, 0, c->stream>>>(d, gz, w, clip_g, clip_w, ga, acc);
+  launch_k(k_dw_dgrad, blocks_for((int64_t)d.N * d.H * d.W * d.C), 256, 0, c->stream, d, gz, w, clip_g, clip_w, ga, acc);
   count_launch(1);
   return cuda_check("k_dw_dgrad");
 }
@@ -396,12 +403,12 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
     const dim3 grid((nq + 63) / 64, static_cast<unsigned>((ngroups + DW_GROUPS - 1) / DW_GROUPS));
     const uint32_t *g4 = reinterpret_cast<const uint32_t*>(gz), *a4 = reinterpret_cast<const uint32_t*>(a);
     unsigned long long* acc_u = reinterpret_cast<unsigned long long*>(acc);
-    if (d.sh == 1) k_dw_wgrad4<3, 3, 1><<<grid, 256, 0, c->stream>>>(d, g4, a4, acc_u);
-    else k_dw_wgrad4<3, 3, 2><<<grid, 256, 0, c->stream>>>(d, g4, a4, acc_u);
+    if (d.sh == 1) launch_k(k_dw_wgrad4<3, 3, 1>, grid, 256, 0, c->stream, d, g4, a4, acc_u);
+    else launch_k(k_dw_wgrad4<3, 3, 2>, grid, 256, 0, c->stream, d, g4, a4, acc_u);
     count_launch(1);
     if ((rc = cuda_check("k_dw_wgrad4"))) return rc;
     if (gw) {
-      k_dw_wgrad_finalize<<<blocks_for(d.C * RS), 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), d.C * RS,
+      launch_k(k_dw_wgrad_finalize, blocks_for(d.C * RS), 256, 0, c->stream, reinterpret_cast<const long long*>(acc), d.C * RS,
                                                                      clip_g, clip_a, gw);
       count_launch(1);
     }
@@ -412,10 +419,10 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
   int64_t per = (npq + ysplit - 1) / ysplit;
   if (per < 256) per = 256;
   ysplit = (npq + per - 1) / per;
-  k_dw_wgrad<<<dim3((unsigned)cblk, (unsigned)ysplit), 256, 0, c->stream>>>(d, gz, a, reinterpret_cast<unsigned long long*>(acc), per);
+  launch_k(k_dw_wgrad, dim3((unsigned)cblk, (unsigned)ysplit), 256, 0, c->stream, d, gz, a, reinterpret_cast<unsigned long long*>(acc), per);
   count_launch(1);
   if (gw) {
-    k_dw_wgrad_finalize<<<blocks_for(d.C * RS), 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), d.C * RS, clip_g, clip_a, gw);
+    launch_k(k_dw_wgrad_finalize, blocks_for(d.C * RS), 256, 0, c->stream, reinterpret_cast<const long long*>(acc), d.C * RS, clip_g, clip_a, gw);
     count_launch(1);
   }
   return cuda_check("k_dw_wgrad");
@@ -426,7 +433,7 @@ int i8t_conv_dw_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !g || !acc || !clip_g || !clip_a || !gw) return set_error(I8T_EINVAL, "conv_dw_wgrad_finalize: null argument");
   const int64_t n = g->c * g->kh * g->kw;
-  k_dw_wgrad_finalize<<<blocks_for(n), 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), n, clip_g, clip_a, gw);
+  launch_k(k_dw_wgrad_finalize, blocks_for(n), 256, 0, c->stream, reinterpret_cast<const long long*>(acc), n, clip_g, clip_a, gw);
   count_launch(1);
   return cuda_check("k_dw_wgrad_finalize");
 }

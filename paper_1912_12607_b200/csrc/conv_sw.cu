@@ -74,6 +74,7 @@ template <int BN, int R, int S, bool MIRROR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_sw(const Args a, const __grid_constant__ CUtensorMap tm_in,
                                                          const __grid_constant__ CUtensorMap tm_w,
                                                          const __grid_constant__ CUtensorMap tm_out) {
+  pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sHalo = smem;
@@ -301,7 +302,7 @@ static int launch(cudaStream_t st, const Args& a, const CUtensorMap& ti, const C
   const int total = a.N * a.tiles_h * a.tiles_w * a.n_tiles;
   int grid = std::min(total, num_sms());
   grid = grid / a.n_tiles * a.n_tiles;
-  k_conv_sw<BN, R, S, MIRROR><<<grid, NTHREADS, smem, st>>>(a, ti, tw, to);
+  launch_k(k_conv_sw<BN, R, S, MIRROR>, grid, NTHREADS, smem, st, a, ti, tw, to);
   count_launch(1);
   return cuda_check("k_conv_sw");
 }

@@ -149,6 +149,7 @@ template <int MODE, int BN, int VA, int VB>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
                                                           const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
+  pdl_entry();
   using C = Cfg<MODE, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
 // WGRAD finalize: int64 acc [(r,s,c_pad)][K] -> float KCRS or KRSC, reference rescale.
 __global__ void k_wgrad_finalize(const long long* __restrict__ acc, int K, int C, int Cp, int RS,
                                  const float* clip_g, const float* clip_a, float* __restrict__ gw, int out_kcrs) {
+  pdl_entry();
   const double rescale =
       static_cast<double>(__fdiv_rn(*clip_g, 127.0f)) * static_cast<double>(__fdiv_rn(*clip_a, 127.0f));
   const int64_t tot = static_cast<int64_t>(K) * C * RS;
@@ -568,6 +570,7 @@ __global__ void k_wgrad_finalize(const long long* __restrict__ acc, int K, int C
 __global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int m_pad, int Kp, int M, int K, int C,
                                int Cp, int RS, long long* __restrict__ acc, const float* clip_g, const float* clip_a,
                                float* __restrict__ gw, int out_kcrs) {
+  pdl_entry();
   const double rescale =
       static_cast<double>(__fdiv_rn(*clip_g, 127.0f)) * static_cast<double>(__fdiv_rn(*clip_a, 127.0f));
   const int64_t tot = static_cast<int64_t>(M) * K;
@@ -594,6 +597,7 @@ __global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int
 // is the original KRSC order, so the weight rows only gain 4 zero bytes per r.
 __global__ void k_fold_taps(const int8_t* __restrict__ x, int64_t NH, int W, int Q, int kw, int sw, int pw,
                             int8_t* __restrict__ xf) {
+  pdl_entry();
   const int64_t tot = NH * Q;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t nh = i / Q;
@@ -613,6 +617,7 @@ __global__ void k_fold_taps(const int8_t* __restrict__ x, int64_t NH, int W, int
 
 // KRSC [K][ldw] (c_pad 4) -> [K][R*32]: each r's kw*4 bytes, zero padded to 32.
 __global__ void k_fold_weights(const int8_t* __restrict__ w, int64_t ldw, int K, int R, int kw, int8_t* __restrict__ wf) {
+  pdl_entry();
   const int tot = K * R * 32;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
     const int k = i / (R * 32), rem = i - k * R * 32, r = rem / 32, j = rem - r * 32;
@@ -622,6 +627,7 @@ __global__ void k_fold_weights(const int8_t* __restrict__ w, int64_t ldw, int K,
 
 // folded wgrad accumulator [R*32][K] -> original [(r*kw + s)*4 + c][K]
 __global__ void k_unfold_wacc(const long long* __restrict__ accf, int R, int kw, int K, long long* __restrict__ acc) {
+  pdl_entry();
   const int tot = R * kw * 4 * K;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
     const int m = i / K, k = i - m * K;
@@ -655,7 +661,7 @@ static int8_t* fold_input(Ctx* c, const i8t_conv_geom* g, int64_t Q, const int8_
   if (!buf) return nullptr;
   const int64_t tot = g->n * g->h * Q;
   const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
-  k_fold_taps<<<blocks, 256, 0, c->stream>>>(a, g->n * g->h, (int)g->w, (int)Q, (int)g->kw, (int)g->stride_w,
+  launch_k(k_fold_taps, blocks, 256, 0, c->stream, a, g->n * g->h, (int)g->w, (int)Q, (int)g->kw, (int)g->stride_w,
                                              (int)g->pad_w, buf);
   count_launch(1);
   *extra_out = buf + ((xbytes + 255) / 256) * 256;
@@ -664,6 +670,7 @@ static int8_t* fold_input(Ctx* c, const i8t_conv_geom* g, int64_t Q, const int8_
 
 // DGRAD phase with no taps (e.g. 1x1 stride 2, odd pixels): rows are zero.
 __global__ void k_zero_phase(ConvArgs a) {
+  pdl_entry();
   const int64_t rows = static_cast<int64_t>(a.N) * a.Hq * a.Wq;
   const int c4 = a.Ng / 4;  // Ng % 4 == 0 on this path
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -687,6 +694,7 @@ __global__ void k_zero_phase(ConvArgs a) {
 
 __global__ void k_transpose_i8(const int8_t* __restrict__ src, int64_t rows, int64_t cols, int8_t* __restrict__ dst,
                                int64_t ld_dst) {
+  pdl_entry();
   const int64_t tot = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / cols, c = i - r * cols;
@@ -696,6 +704,7 @@ __global__ void k_transpose_i8(const int8_t* __restrict__ src, int64_t rows, int
 
 __global__ void k_pad_rows_i8(const int8_t* __restrict__ src, int64_t rows, int64_t cols, int8_t* __restrict__ dst,
                               int64_t ld_dst) {
+  pdl_entry();
   const int64_t tot = rows * ld_dst;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / ld_dst, c = i - r * ld_dst;
@@ -779,7 +788,7 @@ static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& ama
   }
   const int tiles = a.m_tiles * a.n_tiles * a.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k_conv_tc<MODE, BN, VA, VB><<<grid, NTHREADS, C::SMEM, st>>>(a, amap, map, omap);
+  launch_k(k_conv_tc<MODE, BN, VA, VB>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
 }
@@ -886,7 +895,7 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.use_tma_out = 0;
       if (nr == 0 || x.ns == 0) {
         const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
-        k_zero_phase<<<blocks, 256, 0, c->stream>>>(x);
+        launch_k(k_zero_phase, blocks, 256, 0, c->stream, x);
         count_launch(1);
         int rc = cuda_check("k_zero_phase");
         if (rc) return rc;
@@ -929,7 +938,7 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
     const int8_t* xf = fold_input(c, g, Q, a, static_cast<size_t>(g->k) * g->kh * 32, &wf);
     if (!xf) return set_error(I8T_ECUDA, "conv_fwd: fold buffer alloc failed");
     const int tot = (int)(g->k * g->kh * 32);
-    k_fold_weights<<<(tot + 255) / 256, 256, 0, c->stream>>>(w, ld_w, (int)g->k, (int)g->kh, (int)g->kw, wf);
+    launch_k(k_fold_weights, (tot + 255) / 256, 256, 0, c->stream, w, ld_w, (int)g->k, (int)g->kh, (int)g->kw, wf);
     count_launch(1);
     if ((rc = cuda_check("k_fold"))) return rc;
     const i8t_conv_geom f = folded_geom(g, Q);
@@ -1041,7 +1050,7 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
     const i8t_conv_geom f = folded_geom(g, Q);
     if ((rc = i8t_conv_wgrad(ctx, &f, gz, k_pad, xf, 32, clip_g, clip_a, accf, nullptr, out_kcrs))) return rc;
     const int tot = (int)(g->kh * g->kw * 4 * g->k);
-    k_unfold_wacc<<<(tot + 255) / 256, 256, 0, c->stream>>>(reinterpret_cast<const long long*>(accf), (int)g->kh,
+    launch_k(k_unfold_wacc, (tot + 255) / 256, 256, 0, c->stream, reinterpret_cast<const long long*>(accf), (int)g->kh,
                                                             (int)g->kw, (int)g->k, reinterpret_cast<long long*>(acc));
     count_launch(1);
     if ((rc = cuda_check("k_unfold_wacc"))) return rc;
@@ -1102,7 +1111,7 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   const int64_t tot = x.M * g->k;
   int blocks = (int)((tot + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_wgrad_reduce<<<blocks, 256, 0, c->stream>>>(part, (int)splits, x.m_pad, (int)k_pad, (int)x.M, (int)g->k, (int)g->c,
+  launch_k(k_wgrad_reduce, blocks, 256, 0, c->stream, part, (int)splits, x.m_pad, (int)k_pad, (int)x.M, (int)g->k, (int)g->c,
                                                  (int)c_pad, (int)(g->kh * g->kw), reinterpret_cast<long long*>(acc),
                                                  clip_g, clip_a, gw, out_kcrs);
   count_launch(1);
@@ -1119,7 +1128,7 @@ int i8t_conv_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64_t*
   const int64_t tot = g->k * g->c * g->kh * g->kw;
   int blocks = (int)((tot + 255) / 256);
   if (blocks > 4096) blocks = 4096;
-  k_wgrad_finalize<<<blocks, 256, 0, c->stream>>>(reinterpret_cast<const long long*>(acc), (int)g->k, (int)g->c,
+  launch_k(k_wgrad_finalize, blocks, 256, 0, c->stream, reinterpret_cast<const long long*>(acc), (int)g->k, (int)g->c,
                                                    (int)c_pad, (int)(g->kh * g->kw), clip_g, clip_a, gw, out_kcrs);
   count_launch(1);
   return cuda_check("k_wgrad_finalize");
@@ -1141,10 +1150,10 @@ int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64
   const float h127[2] = {127.0f, 127.0f};
   cudaMemcpyAsync(ones, h127, sizeof(h127), cudaMemcpyHostToDevice, c->stream);
   cudaMemsetAsync(bt, 0, need_b, c->stream);
-  k_transpose_i8<<<(unsigned)std::min<int64_t>((k * n + 255) / 256, 4096), 256, 0, c->stream>>>(b, k, n, bt, ldw);
+  launch_k(k_transpose_i8, (unsigned)std::min<int64_t>((k * n + 255) / 256, 4096), 256, 0, c->stream, b, k, n, bt, ldw);
   count_launch(1);
   if (ap) {
-    k_pad_rows_i8<<<(unsigned)std::min<int64_t>((m * kp + 255) / 256, 4096), 256, 0, c->stream>>>(a, m, k, ap, kp);
+    launch_k(k_pad_rows_i8, (unsigned)std::min<int64_t>((m * kp + 255) / 256, 4096), 256, 0, c->stream, a, m, k, ap, kp);
     count_launch(1);
   }
   i8t_conv_geom g{m, kp, 1, 1, n, 1, 1, 1, 1, 0, 0, 0, 1};

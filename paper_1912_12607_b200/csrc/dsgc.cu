@@ -31,6 +31,7 @@ template <int NC>
 __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restrict__ g, uint32_t n,
                                                           const float* __restrict__ cands, const int32_t* active,
                                                           double* partials, double* totals, unsigned* ticket) {
+  pdl_entry();
   constexpr int NV = 3 + 2 * NC;
   if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
   // per-candidate dequantisation tables double(float(q) * s_j) in dynamic smem
@@ -104,6 +105,7 @@ constexpr double kInvPhi = 0.6180339887498949;
 
 // After the k_dc_stats<0> pass: m, non-finite, sum g^2 (clip.cpp:32-34).
 __global__ void k_search_begin(DsgcState* st, const double* tot, int R, float prev_clip, int prev_from_state, int* err) {
+  pdl_entry();
   if (threadIdx.x) return;
   if (prev_from_state) prev_clip = st->v.clip;
   st->m = static_cast<float>(tot[0]);
@@ -127,6 +129,7 @@ __global__ void k_search_begin(DsgcState* st, const double* tot, int R, float pr
 
 // After a k_dc_stats<nc> pass over st->cand.
 __global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, int rounds) {
+  pdl_entry();
   if (threadIdx.x || st->active == 0) return;
   double dcs[32];
   for (int j = 0; j < nc; ++j) dcs[j] = cosine_from(tot[3 + 2 * j], st->sq_g, tot[4 + 2 * j]);
@@ -194,6 +197,7 @@ __global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, i
 
 // End of maybe_update's search branch (clip.cpp:84-88) or a raw search_clip.
 __global__ void k_search_end(DsgcState* st, int64_t iter, int update_state, float* clip_out, double* dc_out) {
+  pdl_entry();
   if (threadIdx.x) return;
   const float c = st->best_clip;
   const double dc = st->best_dc;
@@ -208,6 +212,7 @@ __global__ void k_search_end(DsgcState* st, int64_t iter, int update_state, floa
 
 // Search-disabled branch of quantize_gradient (layers.cpp:27-36): clip = max_abs.
 __global__ void k_clip_from_max(DsgcState* st, const double* tot, int64_t iter) {
+  pdl_entry();
   if (threadIdx.x) return;
   const float mf = static_cast<float>(tot[0]);
   if (mf > 0.0f) st->v.clip = mf;
@@ -216,6 +221,7 @@ __global__ void k_clip_from_max(DsgcState* st, const double* tot, int64_t iter) 
 
 // Non-search branch of maybe_update: last_dc = max_abs == 0 ? 0 : measure_dc.
 __global__ void k_fin_maybe_dc(DsgcState* st, const double* tot, int* err) {
+  pdl_entry();
   if (threadIdx.x) return;
   const float m = static_cast<float>(tot[0]);
   st->v.max_abs = m;
@@ -228,6 +234,7 @@ __global__ void k_fin_maybe_dc(DsgcState* st, const double* tot, int* err) {
 }
 
 __global__ void k_fin_scalar(const double* tot, int which, float* out_f, double* out_d, int32_t* out_i) {
+  pdl_entry();
   if (threadIdx.x) return;
   const double v = tot[which];
   if (out_f) *out_f = static_cast<float>(v);
@@ -236,6 +243,7 @@ __global__ void k_fin_scalar(const double* tot, int which, float* out_f, double*
 }
 
 __global__ void k_fin_measure_dc(const double* tot, double* out, int* err) {
+  pdl_entry();
   if (threadIdx.x) return;
   if (tot[1] > 0.0) atomicOr(err, ERR_NONFINITE);
   *out = cosine_from(tot[3], tot[2], tot[4]);
@@ -244,6 +252,7 @@ __global__ void k_fin_measure_dc(const double* tot, double* out, int* err) {
 // dot / cosine totals: [0] sum a*b [1] sum a^2 [2] sum b^2
 __global__ void __launch_bounds__(RED_THREADS) k_dot3(const float* __restrict__ a, const float* __restrict__ b,
                                                       uint32_t n, double* partials, double* totals, unsigned* ticket) {
+  pdl_entry();
   double acc[3] = {0, 0, 0};
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double x = a[i], y = b[i];
@@ -255,6 +264,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dot3(const float* __restrict__ 
 }
 
 __global__ void k_fin_cosine(const double* tot, double* dot_out, double* cos_out) {
+  pdl_entry();
   if (threadIdx.x) return;
   if (dot_out) *dot_out = tot[0];
   if (cos_out) *cos_out = cosine_from(tot[0], tot[1], tot[2]);
@@ -267,7 +277,7 @@ static int stats_pass0(Ctx* c, const float* x, int64_t n) {
   const int nb = nblocks(n);
   double* p = ensure_partials(c, static_cast<size_t>(nb) * 3);
   if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
-  k_dc_stats<0><<<nb, RED_THREADS, 0, c->stream>>>(x, static_cast<uint32_t>(n), nullptr, nullptr, p, c->d_totals,
+  launch_k(k_dc_stats<0>, nb, RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), nullptr, nullptr, p, c->d_totals,
                                                     c->d_ticket);
   count_launch(1);
   return cuda_check("k_dc_stats<0>");
@@ -281,7 +291,7 @@ static void dc_pass(Ctx* c, const float* g, int64_t n, const float* cands, const
     cudaFuncSetAttribute(k_dc_stats<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
-  k_dc_stats<NC><<<nb, RED_THREADS, smem, c->stream>>>(g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
+  launch_k(k_dc_stats<NC>, nb, RED_THREADS, smem, c->stream, g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
                                                      c->d_ticket);
 }
 
@@ -306,7 +316,7 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
                       int prev_from_state) {
   int rc = stats_pass0(c, g, n);
   if (rc || (rc = allreduce_totals(c, 3))) return rc;
-  k_search_begin<<<1, 32, 0, c->stream>>>(st, c->d_totals, R, prev_clip, prev_from_state, c->d_err);
+  launch_k(k_search_begin, 1, 32, 0, c->stream, st, c->d_totals, R, prev_clip, prev_from_state, c->d_err);
   count_launch(1);
   // The device decides whether the search short-circuits (st->active); under
   // data parallelism every rank takes the same branch (global totals), and a
@@ -315,7 +325,7 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
     if (c->allreduce) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * nc), c->stream);
     int r = dc_pass_n(c, g, n, st->cand, &st->active, nc);
     if (r || (r = allreduce_totals(c, 3 + 2 * nc))) return r;
-    k_search_step<<<1, 32, 0, c->stream>>>(st, c->d_totals, nc, R, rounds);
+    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, nc, R, rounds);
     count_launch(1);
     return cuda_check("k_search_step");
   };
@@ -347,7 +357,7 @@ int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out) {
   if (!c || !x || !out) return set_error(I8T_EINVAL, "max_abs: bad arguments");
   int rc = stats_pass0(c, x, n);
   if (rc) return rc;
-  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 0, out, nullptr, nullptr);
+  launch_k(k_fin_scalar, 1, 32, 0, c->stream, c->d_totals, 0, out, nullptr, nullptr);
   count_launch(1);
   return cuda_check("k_fin_scalar");
 }
@@ -357,7 +367,7 @@ int i8t_sq_l2_norm(i8t_ctx* ctx, const float* x, int64_t n, double* out) {
   if (!c || !x || !out) return set_error(I8T_EINVAL, "sq_l2_norm: bad arguments");
   int rc = stats_pass0(c, x, n);
   if (rc) return rc;
-  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 2, nullptr, out, nullptr);
+  launch_k(k_fin_scalar, 1, 32, 0, c->stream, c->d_totals, 2, nullptr, out, nullptr);
   count_launch(1);
   return cuda_check("k_fin_scalar");
 }
@@ -367,7 +377,7 @@ int i8t_has_nonfinite(i8t_ctx* ctx, const float* x, int64_t n, int32_t* out) {
   if (!c || !x || !out) return set_error(I8T_EINVAL, "has_nonfinite: bad arguments");
   int rc = stats_pass0(c, x, n);
   if (rc) return rc;
-  k_fin_scalar<<<1, 32, 0, c->stream>>>(c->d_totals, 1, nullptr, nullptr, out);
+  launch_k(k_fin_scalar, 1, 32, 0, c->stream, c->d_totals, 1, nullptr, nullptr, out);
   count_launch(1);
   return cuda_check("k_fin_scalar");
 }
@@ -376,8 +386,8 @@ static int dot_like(Ctx* c, const float* a, const float* b, int64_t n, double* d
   const int nb = nblocks(n);
   double* p = ensure_partials(c, static_cast<size_t>(nb) * 3);
   if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
-  k_dot3<<<nb, RED_THREADS, 0, c->stream>>>(a, b, static_cast<uint32_t>(n), p, c->d_totals, c->d_ticket);
-  k_fin_cosine<<<1, 32, 0, c->stream>>>(c->d_totals, dot_out, cos_out);
+  launch_k(k_dot3, nb, RED_THREADS, 0, c->stream, a, b, static_cast<uint32_t>(n), p, c->d_totals, c->d_ticket);
+  launch_k(k_fin_cosine, 1, 32, 0, c->stream, c->d_totals, dot_out, cos_out);
   count_launch(2);
   return cuda_check("k_dot3");
 }
@@ -403,7 +413,7 @@ int i8t_measure_dc(i8t_ctx* ctx, const float* g, int64_t n, float clip, double* 
   cudaMemcpyAsync(dclip, &clip, sizeof(float), cudaMemcpyHostToDevice, c->stream);
   int rc = dc_pass_n(c, g, n, dclip, nullptr, 1);
   if (rc) return rc;
-  k_fin_measure_dc<<<1, 32, 0, c->stream>>>(c->d_totals, out, c->d_err);
+  launch_k(k_fin_measure_dc, 1, 32, 0, c->stream, c->d_totals, out, c->d_err);
   count_launch(1);
   cudaStreamSynchronize(c->stream);  // `clip` lives on the caller's stack
   return cuda_check("measure_dc");
@@ -418,7 +428,7 @@ int i8t_search_clip(i8t_ctx* ctx, const float* g, int64_t n, int grid, int round
   if (!st) return set_error(I8T_ECUDA, "scratch alloc failed");
   int rc = run_search(c, st, g, n, grid, rounds, prev_clip, 0);
   if (rc) return rc;
-  k_search_end<<<1, 32, 0, c->stream>>>(st, 0, 0, clip_out, dc_out);
+  launch_k(k_search_end, 1, 32, 0, c->stream, st, 0, 0, clip_out, dc_out);
   count_launch(1);
   return cuda_check("k_search_end");
 }
@@ -461,12 +471,12 @@ int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64
   int rc;
   if (due) {
     if ((rc = run_search(c, st, g, n, grid, rounds, 0.0f, 1))) return rc;
-    k_search_end<<<1, 32, 0, c->stream>>>(st, iter, 1, nullptr, nullptr);
+    launch_k(k_search_end, 1, 32, 0, c->stream, st, iter, 1, nullptr, nullptr);
     count_launch(1);
     return cuda_check("maybe_update");
   }
   if ((rc = dc_pass_n(c, g, n, &st->v.clip, nullptr, 1)) || (rc = allreduce_totals(c, 5))) return rc;
-  k_fin_maybe_dc<<<1, 32, 0, c->stream>>>(st, c->d_totals, c->d_err);
+  launch_k(k_fin_maybe_dc, 1, 32, 0, c->stream, st, c->d_totals, c->d_err);
   count_launch(1);
   return cuda_check("maybe_update");
 }
@@ -490,7 +500,7 @@ int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_i
     if (grid < 8) return set_error(I8T_EINVAL, "search_clip: grid resolution must be >= 8");
     if (due) {
       if ((rc = run_search(c, st, g, numel, grid, rounds, 0.0f, 1))) return rc;
-      k_search_end<<<1, 32, 0, c->stream>>>(st, iter, 1, nullptr, nullptr);
+      launch_k(k_search_end, 1, 32, 0, c->stream, st, iter, 1, nullptr, nullptr);
       count_launch(1);
       dc_sums = false;
     } else {
@@ -498,7 +508,7 @@ int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_i
     }
   } else {
     if ((rc = stats_pass0(c, g, numel)) || (rc = allreduce_totals(c, 3))) return rc;
-    k_clip_from_max<<<1, 32, 0, c->stream>>>(st, c->d_totals, iter);
+    launch_k(k_clip_from_max, 1, 32, 0, c->stream, st, c->d_totals, iter);
     count_launch(1);
     dc_sums = true;
   }

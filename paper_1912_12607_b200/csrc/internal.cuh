@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "../../include/i8t_cuda.h"
 
@@ -86,6 +87,39 @@ void* ensure_wgrad(Ctx* c, size_t bytes);
 void* ensure_fold(Ctx* c, size_t bytes);
 
 void count_launch(int n = 1);
+
+// Programmatic dependent launch: every kernel of this library starts with
+// pdl_entry() (wait until the preceding grid of the stream has completed and
+// its writes are visible), and launch_k() sets the programmatic-serialization
+// attribute, so a grid is launched and its blocks scheduled while its
+// predecessor drains instead of after it.  No kernel triggers early
+// (griddepcontrol.launch_dependents): the dependents of a persistent grid then
+// land on SMs as they free up and lose their one-wave balance, which measured
+// slower than the implicit trigger at grid completion.  I8T_PDL=0 turns the
+// attribute off.
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_entry() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // shifted-window stride-1 convolution (conv_sw.cu)
 bool conv_sw_eligible(const i8t_conv_geom* g, int64_t Cred, int Ng, int OH, int OW, const void* in, const void* out,

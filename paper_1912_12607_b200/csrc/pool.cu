@@ -24,6 +24,7 @@ template <bool BN>
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x, PoolGeom g, const double* bn,
                                                      const float* gamma, const float* beta, int relu,
                                                      float* __restrict__ y, uint8_t* __restrict__ idx) {
+  pdl_entry();
   const uint32_t c4n = g.C / 4;
   const uint32_t tot = static_cast<uint32_t>(g.N) * g.P * g.Q * c4n;  // < 2^31 (host check)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x
 
 __global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ gy, const uint8_t* __restrict__ idx,
                                                      PoolGeom g, float* __restrict__ gx) {
+  pdl_entry();
   const uint32_t c4n = g.C / 4;
   const uint32_t tot = static_cast<uint32_t>(g.N) * g.H * g.W * c4n;  // < 2^31 (host check)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(const float* __restrict__ g
 // (p, q) order, as k_maxpool_bwd.
 __global__ void __launch_bounds__(256) k_maxpool_bwd_s2k3(const float* __restrict__ gy, const uint8_t* __restrict__ idx,
                                                           PoolGeom g, float* __restrict__ gx) {
+  pdl_entry();
   const uint32_t c4n = g.C / 4;
   const uint32_t tot = static_cast<uint32_t>(g.N) * g.P * g.Q * c4n;  // one 2x2 block per (n, p', q', quad)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
@@ -177,8 +180,8 @@ int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t 
   if (rc) return rc;
   if (!cx || !x || !y || !idx || (bn && (!gamma || !beta))) return set_error(I8T_EINVAL, "maxpool_fwd: bad arguments");
   const int64_t tot = static_cast<int64_t>(g.N) * g.P * g.Q * (g.C / 4);
-  if (bn) k_maxpool_fwd<true><<<grid_of(tot), 256, 0, cx->stream>>>(x, g, bn, gamma, beta, relu, y, idx);
-  else k_maxpool_fwd<false><<<grid_of(tot), 256, 0, cx->stream>>>(x, g, nullptr, nullptr, nullptr, 0, y, idx);
+  if (bn) launch_k(k_maxpool_fwd<true>, grid_of(tot), 256, 0, cx->stream, x, g, bn, gamma, beta, relu, y, idx);
+  else launch_k(k_maxpool_fwd<false>, grid_of(tot), 256, 0, cx->stream, x, g, nullptr, nullptr, nullptr, 0, y, idx);
   count_launch(1);
   return cuda_check("k_maxpool_fwd");
 }
@@ -192,12 +195,12 @@ int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n
   if (!cx || !gy || !idx || !gx) return set_error(I8T_EINVAL, "maxpool_bwd: bad arguments");
   if (g.k == 3 && g.s == 2 && g.pad == 1 && g.H == 2 * g.P && g.W == 2 * g.Q) {
     const int64_t blocks = static_cast<int64_t>(g.N) * g.P * g.Q * (g.C / 4);
-    k_maxpool_bwd_s2k3<<<grid_of(blocks), 256, 0, cx->stream>>>(gy, idx, g, gx);
+    launch_k(k_maxpool_bwd_s2k3, grid_of(blocks), 256, 0, cx->stream, gy, idx, g, gx);
     count_launch(1);
     return cuda_check("k_maxpool_bwd_s2k3");
   }
   const int64_t tot = static_cast<int64_t>(g.N) * g.H * g.W * (g.C / 4);
-  k_maxpool_bwd<<<grid_of(tot), 256, 0, cx->stream>>>(gy, idx, g, gx);
+  launch_k(k_maxpool_bwd, grid_of(tot), 256, 0, cx->stream, gy, idx, g, gx);
   count_launch(1);
   return cuda_check("k_maxpool_bwd");
 }

@@ -125,14 +125,13 @@ __device__ __forceinline__ int quant_stoch(float x, float clip, float s, float i
   return max(-127, min(127, q));
 }
 
-// double(float(x)) without the two XU conversions: round the 53-bit
-// significand to 24 bits (nearest-even) in the integer pipe.  Exact for
-// |x| >= 2^-126 (float normal range); smaller |x| (incl. 0) raise `slow`.
-__device__ __forceinline__ double rn24(double x, bool& slow) {
+// x rounded to a 24-bit significand (nearest-even) in the integer pipe: the
+// value of double(float(x)) without the two XU conversions for float-normal
+// |x| in [2^-126, 2^128); zero, inf and NaN map to themselves.
+__device__ __forceinline__ double rn24(double x) {
   long long b = __double_as_longlong(x);
   b += 0x0FFFFFFFLL + ((b >> 29) & 1);
   b &= ~0x1FFFFFFFLL;
-  slow |= fabs(x) < 0x1.0p-126;
   return __longlong_as_double(b);
 }
 

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
                                                             uint32_t* lcg_state, int8_t* __restrict__ q,
                                                             double* partials, double* totals, unsigned* ticket, QgFin fin,
                                                             int* err) {
+  pdl_entry();
   __shared__ double tab[256];
   float clip = clip_override ? *clip_override : st->v.clip;
   if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
 }
 
 static __global__ void k_fin_quant_grad(DsgcState* st, const double* totals, QgFin fin, uint32_t* lcg_state, int* err) {
+  pdl_entry();
   if (threadIdx.x == 0) fin_quant_grad(st, totals, fin, lcg_state, err);
 }
 
@@ -235,11 +237,9 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
   const bool fused = (c->allreduce == nullptr);
   const uint32_t un = static_cast<uint32_t>(numel), uc = static_cast<uint32_t>(flat ? 1 : C),
                  uhw = static_cast<uint32_t>(flat ? numel : HW);
-#define LAUNCH(F, D, U)                                                                                               \
-  k_quant_grad<Src, F, D, U><<<nb, RED_THREADS, 0, c->stream>>>(src, un, uc, uhw, draw_offset, step_iter,          \
-                                                                step_elem,                                      \
-                                                           step_wrap, dpix, clip_override, st, lcg, q, p,           \
-                                                           c->d_totals, c->d_ticket, fin, c->d_err)
+#define LAUNCH(F, D, U)                                                                                  \
+  launch_k(k_quant_grad<Src, F, D, U>, nb, RED_THREADS, 0, c->stream, src, un, uc, uhw, draw_offset, step_iter,     \
+           step_elem, step_wrap, dpix, clip_override, st, lcg, q, p, c->d_totals, c->d_ticket, fin, c->d_err)
   if (flat) {
     if (dc_sums) { if (fused) LAUNCH(true, true, true); else LAUNCH(true, true, false); }
     else { if (fused) LAUNCH(true, false, true); else LAUNCH(true, false, false); }
@@ -252,7 +252,7 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
   int rc = cuda_check("k_quant_grad");
   if (rc || fused) return rc;
   if ((rc = allreduce_totals(c, QG_NV))) return rc;
-  k_fin_quant_grad<<<1, 32, 0, c->stream>>>(st, c->d_totals, fin, lcg, c->d_err);
+  launch_k(k_fin_quant_grad, 1, 32, 0, c->stream, st, c->d_totals, fin, lcg, c->d_err);
   count_launch(1);
   return cuda_check("k_fin_quant_grad");
 }

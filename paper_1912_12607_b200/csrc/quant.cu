@@ -31,6 +31,7 @@ __device__ __forceinline__ void block_amax(float m, float* amax) {
 __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_flat(const float* __restrict__ x, uint32_t n,
                                                                     const float* __restrict__ clip_p,
                                                                     int8_t* __restrict__ q, float* amax, int* err) {
+  pdl_entry();
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   float m = 0.0f;
   bool bad = false;
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
                                                                     uint32_t cols, const float* __restrict__ clip_p,
                                                                     int8_t* __restrict__ q, uint32_t ld_q, float* amax,
                                                                     int* err) {
+  pdl_entry();
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   float m = 0.0f;
   bool bad = false;
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
 // the per-layer launches cost more than their ~150 MB of traffic.  Padding
 // bytes of the outputs are never written (zeroed once at allocation).
 __global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* __restrict__ descs, int* err) {
+  pdl_entry();
   const i8t_wq_desc d = descs[blockIdx.y];
   const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s;
   const uint32_t K = d.k, C = d.c, RS = d.rs, tot = K * C * RS;
@@ -112,6 +115,7 @@ __global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* _
 __global__ void __launch_bounds__(256) k_quant_nearest_nchw(const float* __restrict__ x, uint32_t C, uint32_t HW,
                                                             const float* __restrict__ clip_p, int8_t* __restrict__ q,
                                                             uint32_t c_pad, float* amax, int* err) {
+  pdl_entry();
   __shared__ float tile[32][33];
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   const size_t n = blockIdx.z;
@@ -144,6 +148,7 @@ __global__ void __launch_bounds__(256) k_quant_weight(const float* __restrict__ 
                                                       uint32_t RS, const float* __restrict__ clip_p, int8_t* q_krsc,
                                                       uint32_t c_pad, uint32_t ld_krsc, int8_t* q_crsk, uint32_t k_pad,
                                                       uint32_t ld_crsk, float* amax, int* err) {
+  pdl_entry();
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   const uint32_t tot = K * C * RS;
   float m = 0.0f;
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(256) k_quant_weight(const float* __restrict__ 
 
 __global__ void k_dequantize(const int8_t* __restrict__ q, uint32_t n, const float* __restrict__ clip_p,
                              float* __restrict__ out) {
+  pdl_entry();
   const float s = scale_of(*clip_p);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = __fmul_rn(static_cast<float>(q[i]), s);
@@ -180,6 +186,7 @@ __global__ void k_dequantize(const int8_t* __restrict__ q, uint32_t n, const flo
 // quantize_partitioned (quantize.cpp:45-79): chunk k = [n*k/P, n*(k+1)/P) draws from LcgStream(base+k).
 __global__ void k_quant_partitioned(const float* __restrict__ x, int64_t n, const float* __restrict__ clip_p,
                                     uint32_t base_seed, int parts, int8_t* __restrict__ q, int* err) {
+  pdl_entry();
   const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -198,6 +205,7 @@ __global__ void k_quant_partitioned(const float* __restrict__ x, int64_t n, cons
 // SGD step (train.cpp:97-117, momentum 0): w -= float(lr * g), lr = base_lr * phi.
 __global__ void __launch_bounds__(256) k_sgd_dclr(float* __restrict__ w, const float* __restrict__ grad, uint32_t n,
                                                   double base_lr, const DsgcState* st, const int32_t* skip) {
+  pdl_entry();
   if (skip && *skip) return;
   const double lr = st ? base_lr * st->v.lr_scale : base_lr;
   const uint32_t n4 = n / 4, stride = gridDim.x * blockDim.x;
@@ -221,6 +229,7 @@ __global__ void __launch_bounds__(256) k_sgd_dclr_multi(float* __restrict__ w, c
                                                         int nseg, const int64_t* __restrict__ seg_off,
                                                         const void* const* __restrict__ seg_state, double base_lr,
                                                         const int32_t* skip) {
+  pdl_entry();
   if (skip && *skip) return;
   const int64_t n4 = seg_off[nseg] / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -244,6 +253,7 @@ __global__ void __launch_bounds__(256) k_sgd_dclr_multi(float* __restrict__ w, c
 }
 
 __global__ void __launch_bounds__(256) k_nonfinite_flag(const float* __restrict__ x, int64_t n, int32_t* flag) {
+  pdl_entry();
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
@@ -257,6 +267,7 @@ __global__ void __launch_bounds__(256) k_nonfinite_flag(const float* __restrict_
 // ---- layout helpers
 __global__ void k_nhwc_to_nchw_f32(const float* __restrict__ src, uint32_t C, uint32_t HW, uint32_t ld,
                                    float* __restrict__ dst) {
+  pdl_entry();
   __shared__ float tile[32][33];
   const size_t n = blockIdx.z;
   const uint32_t c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
@@ -274,6 +285,7 @@ __global__ void k_nhwc_to_nchw_f32(const float* __restrict__ src, uint32_t C, ui
 
 __global__ void k_nchw_to_nhwc_i8(const int8_t* __restrict__ src, uint32_t C, uint32_t HW, int8_t* __restrict__ dst,
                                   uint32_t c_pad) {
+  pdl_entry();
   const size_t n = blockIdx.z;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < HW * c_pad; i += gridDim.x * blockDim.x) {
     const uint32_t p = i / c_pad, c = i - p * c_pad;
@@ -283,6 +295,7 @@ __global__ void k_nchw_to_nhwc_i8(const int8_t* __restrict__ src, uint32_t C, ui
 
 __global__ void k_kcrs_relayout_i8(const int8_t* __restrict__ src, uint32_t K, uint32_t C, uint32_t RS, int8_t* dst,
                                    uint32_t pad, uint32_t ld, int to_crsk) {
+  pdl_entry();
   const uint32_t tot = K * C * RS;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
     const uint32_t rs = i % RS, c = (i / RS) % C, k = i / (RS * C);
@@ -316,10 +329,10 @@ int i8t_quantize_nearest_rows(i8t_ctx* ctx, const float* x, int64_t rows, int64_
   if (amax && !accumulate_amax) cudaMemsetAsync(amax, 0, sizeof(float), c->stream);
   if (ld_q == cols) {
     const int64_t n = rows * cols;
-    k_quant_nearest_flat<<<grid_for(n / 4 + 1), RED_THREADS, 0, c->stream>>>(x, static_cast<uint32_t>(n), clip, q, amax,
+    launch_k(k_quant_nearest_flat, grid_for(n / 4 + 1), RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), clip, q, amax,
                                                                               c->d_err);
   } else {
-    k_quant_nearest_rows<<<grid_for(rows * ld_q), RED_THREADS, 0, c->stream>>>(
+    launch_k(k_quant_nearest_rows, grid_for(rows * ld_q), RED_THREADS, 0, c->stream, 
         x, static_cast<uint32_t>(rows), static_cast<uint32_t>(cols), clip, q, static_cast<uint32_t>(ld_q), amax, c->d_err);
   }
   count_launch(1);
@@ -338,7 +351,7 @@ int i8t_quantize_nearest_nchw_to_nhwc(i8t_ctx* ctx, const float* x, int64_t n, i
   if (n * c * hw == 0) return I8T_OK;
   if (amax && !accumulate_amax) cudaMemsetAsync(amax, 0, sizeof(float), cx->stream);
   dim3 grid(static_cast<unsigned>((hw + 31) / 32), static_cast<unsigned>((c_pad + 31) / 32), static_cast<unsigned>(n));
-  k_quant_nearest_nchw<<<grid, 256, 0, cx->stream>>>(x, static_cast<uint32_t>(c), static_cast<uint32_t>(hw), clip, q,
+  launch_k(k_quant_nearest_nchw, grid, 256, 0, cx->stream, x, static_cast<uint32_t>(c), static_cast<uint32_t>(hw), clip, q,
                                                       static_cast<uint32_t>(c_pad), amax, cx->d_err);
   count_launch(1);
   return cuda_check("k_quant_nearest_nchw");
@@ -354,7 +367,7 @@ int i8t_quantize_weight(i8t_ctx* ctx, const float* w, int src_krsc, int64_t k, i
   if (q_krsc && (c_pad != c || ld_krsc != kh * kw * c_pad)) cudaMemsetAsync(q_krsc, 0, k * ld_krsc, cx->stream);
   if (q_crsk && (k_pad != k || ld_crsk != kh * kw * k_pad)) cudaMemsetAsync(q_crsk, 0, c * ld_crsk, cx->stream);
   if (amax) cudaMemsetAsync(amax, 0, sizeof(float), cx->stream);
-  k_quant_weight<<<grid_for(k * c * kh * kw), 256, 0, cx->stream>>>(
+  launch_k(k_quant_weight, grid_for(k * c * kh * kw), 256, 0, cx->stream, 
       w, src_krsc, static_cast<uint32_t>(k), static_cast<uint32_t>(c), static_cast<uint32_t>(kh * kw), clip, q_krsc,
       static_cast<uint32_t>(c_pad), static_cast<uint32_t>(ld_krsc), q_crsk, static_cast<uint32_t>(k_pad),
       static_cast<uint32_t>(ld_crsk), amax, cx->d_err);
@@ -365,7 +378,7 @@ int i8t_quantize_weight(i8t_ctx* ctx, const float* w, int src_krsc, int64_t k, i
 int i8t_quantize_weights_multi(i8t_ctx* ctx, const i8t_wq_desc* dev_descs, int n_layers) {
   Ctx* cx = CTX(ctx);
   if (!cx || !dev_descs || n_layers < 1 || n_layers > 65535) return set_error(I8T_EINVAL, "quantize_weights_multi: bad arguments");
-  k_quant_weight_multi<<<dim3(2 * 148, static_cast<unsigned>(n_layers)), 256, 0, cx->stream>>>(dev_descs, cx->d_err);
+  launch_k(k_quant_weight_multi, dim3(2 * 148, static_cast<unsigned>(n_layers)), 256, 0, cx->stream, dev_descs, cx->d_err);
   count_launch(1);
   return cuda_check("k_quant_weight_multi");
 }
@@ -374,7 +387,7 @@ int i8t_dequantize(i8t_ctx* ctx, const int8_t* q, int64_t n, const float* clip, 
   Ctx* c = CTX(ctx);
   if (!c || !q || !clip || !out) return set_error(I8T_EINVAL, "dequantize: bad arguments");
   if (!n) return I8T_OK;
-  k_dequantize<<<grid_for(n), 256, 0, c->stream>>>(q, static_cast<uint32_t>(n), clip, out);
+  launch_k(k_dequantize, grid_for(n), 256, 0, c->stream, q, static_cast<uint32_t>(n), clip, out);
   count_launch(1);
   return cuda_check("k_dequantize");
 }
@@ -385,7 +398,7 @@ int i8t_quantize_partitioned(i8t_ctx* ctx, const float* x, int64_t n, const floa
   if (!c || !x || !clip || !q) return set_error(I8T_EINVAL, "quantize_partitioned: bad arguments");
   if (parts < 1) return set_error(I8T_EINVAL, "quantize_partitioned: partitions must be >= 1");
   if (n == 0) return I8T_OK;
-  k_quant_partitioned<<<grid_for(n), 256, 0, c->stream>>>(x, n, clip, base_seed, parts, q, c->d_err);
+  launch_k(k_quant_partitioned, grid_for(n), 256, 0, c->stream, x, n, clip, base_seed, parts, q, c->d_err);
   count_launch(1);
   return cuda_check("k_quant_partitioned");
 }
@@ -397,7 +410,7 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
   if (!n) return I8T_OK;
   if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(grad)) & 15u)
     return set_error(I8T_EUNSUPPORTED, "sgd: pointers must be 16-byte aligned");
-  k_sgd_dclr<<<grid_for(n / 4 + 1), 256, 0, c->stream>>>(w, grad, static_cast<uint32_t>(n), base_lr,
+  launch_k(k_sgd_dclr, grid_for(n / 4 + 1), 256, 0, c->stream, w, grad, static_cast<uint32_t>(n), base_lr,
                                                           reinterpret_cast<const DsgcState*>(state), skip);
   count_launch(1);
   return cuda_check("k_sgd_dclr");
@@ -409,7 +422,7 @@ int i8t_sgd_dclr_multi(i8t_ctx* ctx, float* w, const float* grad, int nseg, cons
   if (!c || !w || !grad || nseg < 1 || !seg_off || !seg_state) return set_error(I8T_EINVAL, "sgd_multi: bad arguments");
   if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(grad)) & 15u)
     return set_error(I8T_EUNSUPPORTED, "sgd_multi: arenas must be 16-byte aligned");
-  k_sgd_dclr_multi<<<148 * 8, 256, 0, c->stream>>>(w, grad, nseg, seg_off, seg_state, base_lr, skip);
+  launch_k(k_sgd_dclr_multi, 148 * 8, 256, 0, c->stream, w, grad, nseg, seg_off, seg_state, base_lr, skip);
   count_launch(1);
   return cuda_check("k_sgd_dclr_multi");
 }
@@ -419,7 +432,7 @@ int i8t_nonfinite_flag(i8t_ctx* ctx, const float* x, int64_t n, int32_t* flag) {
   if (!c || !x || !flag) return set_error(I8T_EINVAL, "nonfinite_flag: bad arguments");
   if (reinterpret_cast<uintptr_t>(x) & 15u) return set_error(I8T_EUNSUPPORTED, "nonfinite_flag: 16-byte alignment");
   cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream);
-  k_nonfinite_flag<<<148 * 4, 256, 0, c->stream>>>(x, n, flag);
+  launch_k(k_nonfinite_flag, 148 * 4, 256, 0, c->stream, x, n, flag);
   count_launch(1);
   return cuda_check("k_nonfinite_flag");
 }
@@ -429,7 +442,7 @@ int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, i
   if (!cx || !src || !dst || ld < c) return set_error(I8T_EINVAL, "nhwc_to_nchw: bad arguments");
   if (n * c * hw == 0) return I8T_OK;
   dim3 grid(static_cast<unsigned>((hw + 31) / 32), static_cast<unsigned>((c + 31) / 32), static_cast<unsigned>(n));
-  k_nhwc_to_nchw_f32<<<grid, 256, 0, cx->stream>>>(src, static_cast<uint32_t>(c), static_cast<uint32_t>(hw),
+  launch_k(k_nhwc_to_nchw_f32, grid, 256, 0, cx->stream, src, static_cast<uint32_t>(c), static_cast<uint32_t>(hw),
                                                     static_cast<uint32_t>(ld), dst);
   count_launch(1);
   return cuda_check("k_nhwc_to_nchw_f32");
@@ -440,7 +453,7 @@ int i8t_nchw_to_nhwc_i8(i8t_ctx* ctx, const int8_t* src, int64_t n, int64_t c, i
   if (!cx || !src || !dst || c_pad < c) return set_error(I8T_EINVAL, "nchw_to_nhwc: bad arguments");
   if (!n) return I8T_OK;
   dim3 grid(static_cast<unsigned>(grid_for(hw * c_pad, 256, 1024)), 1, static_cast<unsigned>(n));
-  k_nchw_to_nhwc_i8<<<grid, 256, 0, cx->stream>>>(src, static_cast<uint32_t>(c), static_cast<uint32_t>(hw), dst,
+  launch_k(k_nchw_to_nhwc_i8, grid, 256, 0, cx->stream, src, static_cast<uint32_t>(c), static_cast<uint32_t>(hw), dst,
                                                    static_cast<uint32_t>(c_pad));
   count_launch(1);
   return cuda_check("k_nchw_to_nhwc_i8");
@@ -451,7 +464,7 @@ int i8t_kcrs_to_krsc_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, i
   Ctx* cx = CTX(ctx);
   if (!cx || !src || !dst || c_pad < c || ld < kh * kw * c_pad) return set_error(I8T_EINVAL, "kcrs_to_krsc: bad arguments");
   cudaMemsetAsync(dst, 0, k * ld, cx->stream);
-  k_kcrs_relayout_i8<<<grid_for(k * c * kh * kw), 256, 0, cx->stream>>>(
+  launch_k(k_kcrs_relayout_i8, grid_for(k * c * kh * kw), 256, 0, cx->stream, 
       src, static_cast<uint32_t>(k), static_cast<uint32_t>(c), static_cast<uint32_t>(kh * kw), dst,
       static_cast<uint32_t>(c_pad), static_cast<uint32_t>(ld), 0);
   count_launch(1);
@@ -463,7 +476,7 @@ int i8t_kcrs_to_crsk_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, i
   Ctx* cx = CTX(ctx);
   if (!cx || !src || !dst || k_pad < k || ld < kh * kw * k_pad) return set_error(I8T_EINVAL, "kcrs_to_crsk: bad arguments");
   cudaMemsetAsync(dst, 0, c * ld, cx->stream);
-  k_kcrs_relayout_i8<<<grid_for(k * c * kh * kw), 256, 0, cx->stream>>>(
+  launch_k(k_kcrs_relayout_i8, grid_for(k * c * kh * kw), 256, 0, cx->stream, 
       src, static_cast<uint32_t>(k), static_cast<uint32_t>(c), static_cast<uint32_t>(kh * kw), dst,
       static_cast<uint32_t>(k_pad), static_cast<uint32_t>(ld), 1);
   count_launch(1);
