@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
                                                       const float* clip_p, int8_t* __restrict__ q, float* amax,
                                                       int* err) {
   pdl_entry();
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   float m = 0.0f;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
           if (relu) y = y > 0.0f ? y : 0.0f;
           bad |= !isfinite(y);
           m = fmaxf(m, fabsf(y));
-          qq[j] = static_cast<signed char>(quant_nearest(y, clip, s, inv_s));
+          qq[j] = static_cast<signed char>(quant_nearest_fast(y, clip, hs, s, inv_s));
         }
         reinterpret_cast<char4*>(q)[(e + h * T4) / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
       }
@@ -305,12 +305,13 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
   const uint32_t T4 = gridDim.x * blockDim.x * 4u;  // multiple of 128 and of c
   const uint32_t lane = threadIdx.x & 31;
   uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
-  float clip = 1.0f, s = 1.0f, inv_s = 1.0f, m = 0.0f;
+  float clip = 1.0f, s = 1.0f, inv_s = 1.0f, hs = 0.5f, m = 0.0f;
   bool bad = false;
   if (QOUT && q) {
     clip = *clip_p;
     s = scale_of(clip);
     inv_s = 1.0f / s;
+    hs = __fdiv_rn(0.5f, clip);
   }
   BnQuad k, kr;
   k.load(bn, gamma, beta, c, e % c);
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
         for (int j = 0; j < 4; ++j) {
           bad |= !isfinite(o[j]);
           m = fmaxf(m, fabsf(o[j]));
-          qq[j] = static_cast<signed char>(quant_nearest(o[j], clip, s, inv_s));
+          qq[j] = static_cast<signed char>(quant_nearest_fast(o[j], clip, hs, s, inv_s));
         }
         reinterpret_cast<char4*>(q)[eh / 4] = make_char4(qq[0], qq[1], qq[2], qq[3]);
       }

@@ -102,6 +102,14 @@ __device__ __forceinline__ uint32_t qn_bits(float t1, bool& slow) {
   slow |= fabsf(__fsub_rn(t1, __fsub_rn(kb, RMAGIC))) > 0.5f - QK;
   return __float_as_uint(kb);
 }
+// quantize_value kNearest through the fast path, the exact function only near
+// a rounding tie (hs = 0.5 / clip).
+__device__ __forceinline__ int quant_nearest_fast(float v, float clip, float hs, float s, float inv_s) {
+  bool slow = false;
+  const uint32_t kb = qn_bits(q_t1(v, hs), slow);
+  if (slow) return quant_nearest(v, clip, s, inv_s);
+  return static_cast<int>(kb) - (RMAGIC_BITS + 1);
+}
 // 8-byte shared load at a 32-bit shared-window address.
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
   double v;

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_flat(const float*
                                                                     const float* __restrict__ clip_p,
                                                                     int8_t* __restrict__ q, float* amax, int* err) {
   pdl_entry();
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   float m = 0.0f;
   bool bad = false;
   const uint32_t n4 = n / 4, stride = gridDim.x * blockDim.x;
@@ -42,16 +42,16 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_flat(const float*
     const float4 v = __ldg(x4 + i);
     bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
     m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-    q4[i] = make_char4(static_cast<signed char>(quant_nearest(v.x, clip, s, inv_s)),
-                       static_cast<signed char>(quant_nearest(v.y, clip, s, inv_s)),
-                       static_cast<signed char>(quant_nearest(v.z, clip, s, inv_s)),
-                       static_cast<signed char>(quant_nearest(v.w, clip, s, inv_s)));
+    q4[i] = make_char4(static_cast<signed char>(quant_nearest_fast(v.x, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.y, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.z, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.w, clip, hs, s, inv_s)));
   }
   for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const float v = x[i];
     bad |= !isfinite(v);
     m = fmaxf(m, fabsf(v));
-    q[i] = static_cast<int8_t>(quant_nearest(v, clip, s, inv_s));
+    q[i] = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
   }
   if (bad) atomicOr(err, ERR_NONFINITE);
   if (amax) block_amax(m, amax);
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
                                                                     int8_t* __restrict__ q, uint32_t ld_q, float* amax,
                                                                     int* err) {
   pdl_entry();
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   float m = 0.0f;
   bool bad = false;
   const uint32_t tot = rows * ld_q;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
       const float v = x[static_cast<size_t>(r) * cols + c];
       bad |= !isfinite(v);
       m = fmaxf(m, fabsf(v));
-      o = static_cast<int8_t>(quant_nearest(v, clip, s, inv_s));
+      o = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
     }
     q[i] = o;
   }
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
 __global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* __restrict__ descs, int* err) {
   pdl_entry();
   const i8t_wq_desc d = descs[blockIdx.y];
-  const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   const uint32_t K = d.k, C = d.c, RS = d.rs, tot = K * C * RS;
   bool bad = false;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* _
     }
     const float v = __ldg(d.w + i);
     bad |= !isfinite(v);
-    const int8_t qv = static_cast<int8_t>(quant_nearest(v, clip, s, inv_s));
+    const int8_t qv = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
     if (d.q_krsc) d.q_krsc[static_cast<size_t>(k) * d.ld_krsc + rs * d.c_pad + c] = qv;
     if (d.q_crsk) d.q_crsk[static_cast<size_t>(c) * d.ld_crsk + rs * d.k_pad + k] = qv;
   }
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_quant_nearest_nchw(const float* __restr
                                                             uint32_t c_pad, float* amax, int* err) {
   pdl_entry();
   __shared__ float tile[32][33];
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   const size_t n = blockIdx.z;
   const uint32_t c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_quant_nearest_nchw(const float* __restr
   for (int r = ty; r < 32; r += 8) {
     const uint32_t p = p0 + r, c = c0 + tx;
     if (p < HW && c < c_pad)
-      q[(n * HW + p) * c_pad + c] = (c < C) ? static_cast<int8_t>(quant_nearest(tile[tx][r], clip, s, inv_s)) : 0;
+      q[(n * HW + p) * c_pad + c] = (c < C) ? static_cast<int8_t>(quant_nearest_fast(tile[tx][r], clip, hs, s, inv_s)) : 0;
   }
   if (bad) atomicOr(err, ERR_NONFINITE);
   if (amax) block_amax(m, amax);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) k_quant_weight(const float* __restrict__ 
                                                       uint32_t c_pad, uint32_t ld_krsc, int8_t* q_crsk, uint32_t k_pad,
                                                       uint32_t ld_crsk, float* amax, int* err) {
   pdl_entry();
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   const uint32_t tot = K * C * RS;
   float m = 0.0f;
   bool bad = false;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) k_quant_weight(const float* __restrict__ 
     const float v = w[i];
     bad |= !isfinite(v);
     m = fmaxf(m, fabsf(v));
-    const int8_t qv = static_cast<int8_t>(quant_nearest(v, clip, s, inv_s));
+    const int8_t qv = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
     if (q_krsc) q_krsc[static_cast<size_t>(k) * ld_krsc + rs * c_pad + c] = qv;
     if (q_crsk) q_crsk[static_cast<size_t>(c) * ld_crsk + rs * k_pad + k] = qv;
   }
@@ -187,7 +187,7 @@ __global__ void k_dequantize(const int8_t* __restrict__ q, uint32_t n, const flo
 __global__ void k_quant_partitioned(const float* __restrict__ x, int64_t n, const float* __restrict__ clip_p,
                                     uint32_t base_seed, int parts, int8_t* __restrict__ q, int* err) {
   pdl_entry();
-  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s;
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t k = (i * parts) / n;
