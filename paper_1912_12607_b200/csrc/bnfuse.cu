@@ -532,7 +532,7 @@ static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const d
                                                   nullptr, y, clip, q, mbits, amax, cx->d_err);
 }
 
-static unsigned* tickets(Ctx* c) {
+unsigned* group_tickets(Ctx* c) {
   if (!c->d_tickets) {
     if (cudaMalloc(&c->d_tickets, 64 * sizeof(unsigned)) != cudaSuccess) return nullptr;
     cudaMemset(c->d_tickets, 0, 64 * sizeof(unsigned));
@@ -548,7 +548,7 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
   double* p = ensure_partials(c, static_cast<size_t>(bx) * groups * 2 * BN_GROUP);
-  unsigned* t = tickets(c);
+  unsigned* t = group_tickets(c);
   if (!p || !t) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
   if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t);

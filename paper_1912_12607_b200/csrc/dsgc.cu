@@ -27,27 +27,11 @@
 namespace i8t_dev {
 
 // K4.  totals: [0] max|g|, [1] nonfinite, [2] sum g^2, [3+2j] sum g*gh_j, [4+2j] sum gh_j^2.
-template <int NC>
-__global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restrict__ g, uint32_t n,
-                                                          const float* __restrict__ cands, const int32_t* active,
-                                                          double* partials, double* totals, unsigned* ticket) {
+// NC == 0: the first three only.
+__global__ void __launch_bounds__(RED_THREADS) k_dc_stats0(const float* __restrict__ g, uint32_t n, double* partials,
+                                                           double* totals, unsigned* ticket) {
   pdl_entry();
-  constexpr int NV = 3 + 2 * NC;
-  if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
-  // per-candidate dequantisation tables double(float(q) * s_j) in dynamic smem
-  extern __shared__ double dq_tab[];
-  float cl[NC > 0 ? NC : 1], sc[NC > 0 ? NC : 1], is[NC > 0 ? NC : 1];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    cl[j] = cands[j];
-    sc[j] = scale_of(cl[j]);
-    is[j] = 1.0f / sc[j];
-    build_dequant_table(dq_tab + j * 256, sc[j]);
-  }
-  if (NC > 0) __syncthreads();
-  double acc[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+  double acc[3] = {0.0, 0.0, 0.0};
   float m = 0.0f;
   bool bad = false;
   auto body = [&](float v) {
@@ -55,15 +39,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
     m = fmaxf(m, fabsf(v));
     const double vd = v;
     acc[2] = fma(vd, vd, acc[2]);
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const double gh = dq_tab[j * 256 + 127 + quant_nearest(v, cl[j], sc[j], is[j])];
-      acc[3 + 2 * j] = fma(vd, gh, acc[3 + 2 * j]);
-      acc[4 + 2 * j] = fma(gh, gh, acc[4 + 2 * j]);
-    }
   };
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t n4 = n / 4;
+  const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n4; f += stride) {
     const float4 v = __ldg(g4 + f);
@@ -75,7 +52,82 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
   for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) body(g[i]);
   acc[0] = m;
   acc[1] = bad ? 1.0 : 0.0;
-  grid_reduce<NV>(acc, 1u, partials, totals, ticket);
+  grid_reduce<3>(acc, 1u, partials, totals, ticket);
+}
+
+// Candidates in groups of NG per blockIdx.y (every group streams g once): the
+// per-element work is NG nearest quantisations (FMA-pipe fast path, the exact
+// function for an element near a tie of any of its candidates), NG table
+// lookups and 2*NG FMAs, in registers small enough for three blocks per SM.
+// Group y reduces over blockIdx.x into its own partials / ticket, and its last
+// block scatters the candidate sums (and, for y == 0, [0..2]) into totals.
+template <int NG>
+__global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restrict__ g, uint32_t n,
+                                                          const float* __restrict__ cands, int nc,
+                                                          const int32_t* active, double* partials, double* gtot,
+                                                          double* totals, unsigned* tickets) {
+  pdl_entry();
+  constexpr int NV = 3 + 2 * NG;
+  if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
+  __shared__ double dq_tab[NG * 256];
+  const int j0 = blockIdx.y * NG;
+  float hs[NG];
+  uint32_t tab_n[NG];  // dq_tab[j][q + 127] at the qn_bits pattern RMAGIC + q + 1 (32-bit wrap)
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    const float cl = cands[min(j0 + j, nc - 1)];  // past nc: a duplicate, never scattered
+    hs[j] = __fdiv_rn(0.5f, cl);
+    build_dequant_table(dq_tab + j * 256, scale_of(cl));
+    tab_n[j] = static_cast<uint32_t>(__cvta_generic_to_shared(dq_tab + j * 256)) + 8u * (126u - RMAGIC_BITS);
+  }
+  __syncthreads();
+  double acc[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+  float m = 0.0f;
+  bool bad = false;
+  auto body = [&](float v) {
+    bad |= !isfinite(v);
+    m = fmaxf(m, fabsf(v));
+    const double vd = v;
+    acc[2] = fma(vd, vd, acc[2]);
+    uint32_t kb[NG];
+    bool slow = false;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) kb[j] = qn_bits(q_t1(v, hs[j]), slow);
+    if (slow) {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        const float cl = cands[min(j0 + j, nc - 1)], sc = scale_of(cl);
+        kb[j] = static_cast<uint32_t>(RMAGIC_BITS + 1 + quant_nearest(v, cl, sc, 1.0f / sc));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const double gh = lds_f64(tab_n[j] + 8u * kb[j]);
+      acc[3 + 2 * j] = fma(vd, gh, acc[3 + 2 * j]);
+      acc[4 + 2 * j] = fma(gh, gh, acc[4 + 2 * j]);
+    }
+  };
+  const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n4; f += stride) {
+    const float4 v = __ldg(g4 + f);
+    body(v.x);
+    body(v.y);
+    body(v.z);
+    body(v.w);
+  }
+  for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) body(g[i]);
+  acc[0] = m;
+  acc[1] = bad ? 1.0 : 0.0;
+  double* gt = gtot + blockIdx.y * NV;
+  if (!grid_reduce<NV>(acc, 1u, partials + static_cast<size_t>(blockIdx.y) * gridDim.x * NV, gt,
+                       tickets + blockIdx.y))
+    return;
+  const int ncg = min(NG, nc - j0);
+  for (int t = threadIdx.x; t < 2 * ncg; t += blockDim.x) totals[3 + 2 * j0 + t] = __ldcg(gt + 3 + t);
+  if (blockIdx.y == 0 && threadIdx.x < 3) totals[threadIdx.x] = __ldcg(gt + threadIdx.x);
 }
 
 // ---- DSGC search state machine (clip.cpp:30-78), one thread, on totals.
@@ -272,42 +324,32 @@ __global__ void k_fin_cosine(const double* tot, double* dot_out, double* cos_out
 
 // ---------------------------------------------------------------- host side
 
-// Ensure partials for nblk blocks x nv values, and run kernel K.
 static int stats_pass0(Ctx* c, const float* x, int64_t n) {
   const int nb = nblocks(n);
   double* p = ensure_partials(c, static_cast<size_t>(nb) * 3);
   if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
-  launch_k(k_dc_stats<0>, nb, RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), nullptr, nullptr, p, c->d_totals,
-                                                    c->d_ticket);
+  launch_k(k_dc_stats0, nb, RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), p, c->d_totals, c->d_ticket);
   count_launch(1);
-  return cuda_check("k_dc_stats<0>");
+  return cuda_check("k_dc_stats0");
 }
 
-template <int NC>
-static void dc_pass(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nb, double* p) {
-  constexpr int smem = NC * 256 * static_cast<int>(sizeof(double));
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_dc_stats<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  launch_k(k_dc_stats<NC>, nb, RED_THREADS, smem, c->stream, g, static_cast<uint32_t>(n), cands, active, p, c->d_totals,
-                                                     c->d_ticket);
-}
-
+// K4 over nc <= 32 candidates: groups of 8 (or one group of 1 / 2 for the
+// golden-section rounds).
 static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nc) {
-  const int nb = nblocks(n);
-  double* p = ensure_partials(c, static_cast<size_t>(nb) * (3 + 2 * 32));
-  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
-  switch (nc) {
-#define CASE(K) \
-  case K: dc_pass<K>(c, g, n, cands, active, nb, p); break;
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
-    CASE(14) CASE(15) CASE(16) CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24) CASE(25)
-    CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
-#undef CASE
-    default: return set_error(I8T_EINVAL, "dc pass: bad candidate count");
-  }
+  if (nc < 1 || nc > 32) return set_error(I8T_EINVAL, "dc pass: bad candidate count");
+  const int ng = nc <= 1 ? 1 : nc <= 2 ? 2 : 8;
+  const int groups = (nc + ng - 1) / ng;
+  const int nb = nblocks(n, 1, 3 * 148);
+  const int nv = 3 + 2 * ng;
+  double* p = ensure_partials(c, static_cast<size_t>(nb) * groups * nv + static_cast<size_t>(groups) * nv);
+  unsigned* t = group_tickets(c);
+  if (!p || !t) return set_error(I8T_ECUDA, "partials alloc failed");
+  double* gt = p + static_cast<size_t>(nb) * groups * nv;
+  const dim3 grid(nb, groups);
+  const uint32_t un = static_cast<uint32_t>(n);
+  if (ng == 1) launch_k(k_dc_stats<1>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
+  else if (ng == 2) launch_k(k_dc_stats<2>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
+  else launch_k(k_dc_stats<8>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
   count_launch(1);
   return cuda_check("k_dc_stats");
 }

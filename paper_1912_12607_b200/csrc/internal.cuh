@@ -87,6 +87,8 @@ void* ensure_wgrad(Ctx* c, size_t bytes);
 void* ensure_fold(Ctx* c, size_t bytes);
 
 void count_launch(int n = 1);
+// 64 self-resetting tickets: [0, 32) BN column-sum groups, [32, 64) K4 candidate groups
+unsigned* group_tickets(Ctx* c);
 
 // Programmatic dependent launch: every kernel of this library starts with
 // pdl_entry() (wait until the preceding grid of the stream has completed and
