@@ -223,6 +223,12 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
 int i8t_conv_dgrad_join(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
                         int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
                         const float* add_y);
+/* The same join with the block ReLU mask as packed bits (bit e % 32 of word
+ * e / 32 for the flat NHWC index e, as i8t_bn_act_q writes them):
+ *   ga = dgrad + add_g * bit           (add_bits == NULL: no mask) */
+int i8t_conv_dgrad_join_bits(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                             int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
+                             const uint32_t* add_bits);
 /* Backward-weight (conv.cpp:186-195), int64 accumulation (no depth bound):
  *   acc : int64 workspace [kh*kw*c_pad][K] (zeroed by the call)
  *   gw  : float weights, KCRS when out_kcrs != 0 else KRSC (may be NULL) */

@@ -68,6 +68,7 @@ struct ConvArgs {
   // result equals the separate join bit for bit)
   const float* add_g;
   const float* add_y;
+  const uint32_t* add_bits;  // instead of add_y: packed mask (bit e of word e/32 for flat NHWC index e)
 };
 
 // residual addend of output row `orow`, columns c0..c0+3
@@ -80,9 +81,16 @@ __device__ __forceinline__ float4 join_addend(const ConvArgs& a, int64_t orow, i
     g.y = y.y > 0.0f ? g.y : 0.0f;
     g.z = y.z > 0.0f ? g.z : 0.0f;
     g.w = y.w > 0.0f ? g.w : 0.0f;
+  } else if (a.add_bits) {
+    const uint32_t w = __ldg(a.add_bits + (o >> 5)) >> (o & 31);  // o % 4 == 0: one word
+    g.x = (w & 1u) ? g.x : 0.0f;
+    g.y = (w & 2u) ? g.y : 0.0f;
+    g.z = (w & 4u) ? g.z : 0.0f;
+    g.w = (w & 8u) ? g.w : 0.0f;
   }
   return g;
 }
+
 
 // exact int32 -> double on the FP64 pipe (no XU conversion): 2^52 + (x + 2^31) - (2^52 + 2^31)
 __device__ __forceinline__ double i32_to_f64(uint32_t x) {
@@ -101,6 +109,7 @@ __device__ __forceinline__ int64_t out_row_of(const ConvArgs& a, int64_t m) {
   const int hh = rem / a.Wq, ww = rem - hh * a.Wq;
   return (static_cast<int64_t>(n) * a.H + hh * a.sh + a.fh) * a.W + ww * a.sw + a.fw;
 }
+
 
 constexpr int BM = 128;
 constexpr int BKB = 128;  // bytes of reduction per stage (4 MMAs of K=32)
@@ -512,8 +521,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                     float o = dequant_acc(rescale, v[i]);
                     if (MODE == MODE_DGRAD && args.add_g) {
                       const int64_t ai = out_row_of(args, m) * args.ldo + gc0 + i;
-                      const float ad = (!args.add_y || args.add_y[ai] > 0.0f) ? args.add_g[ai] : 0.0f;
-                      o = __fadd_rn(o, ad);
+                      const bool mk = args.add_y ? args.add_y[ai] > 0.0f
+                                                 : !args.add_bits || ((args.add_bits[ai >> 5] >> (ai & 31)) & 1u);
+                      o = __fadd_rn(o, mk ? args.add_g[ai] : 0.0f);
                     }
                     dst[i] = o;
                   }
@@ -872,7 +882,7 @@ static void fill_geom(ConvArgs& x, const i8t_conv_geom* g, int64_t P, int64_t Q)
 // runs on the zero-stuffed positions of the reference's col2im (conv.cpp:60-84).
 static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, const int8_t* gz, int64_t k_pad,
                         const int8_t* wt, int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga,
-                        int32_t* acc, const float* add_g, const float* add_y) {
+                        int32_t* acc, const float* add_g, const float* add_y, const uint32_t* add_bits) {
   const int sh = (int)g->stride_h, sw = (int)g->stride_w;
   for (int fh = 0; fh < sh; ++fh) {
     for (int fw = 0; fw < sw; ++fw) {
@@ -891,7 +901,7 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.dw = (int)((fw + g->pad_w - x.s0) / sw);
       x.M = g->n * x.Hq * x.Wq; x.Ng = (int)g->c;
       x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
-      x.add_g = add_g; x.add_y = add_y;
+      x.add_g = add_g; x.add_y = add_y; x.add_bits = add_bits;
       x.use_tma_out = 0;
       if (nr == 0 || x.ns == 0) {
         const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
@@ -970,7 +980,7 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
 
 static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
                       int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc,
-                      const float* add_g, const float* add_y);
+                      const float* add_g, const float* add_y, const uint32_t* add_bits = nullptr);
 
 int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt, int64_t ld_wt,
                    const float* clip_g, const float* clip_w, float* ga, int32_t* acc) {
@@ -986,11 +996,20 @@ int i8t_conv_dgrad_join(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, 
   return dgrad_impl(ctx, g, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, nullptr, add_g, add_y);
 }
 
+int i8t_conv_dgrad_join_bits(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
+                             int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
+                             const uint32_t* add_bits) {
+  if (!ga || !add_g) return set_error(I8T_EINVAL, "conv_dgrad_join_bits: null output or addend");
+  if ((reinterpret_cast<uintptr_t>(add_g) & 15u) || (g && g->c % 4))
+    return set_error(I8T_EUNSUPPORTED, "conv_dgrad_join_bits: addend must be 16-byte aligned with c % 4 == 0");
+  return dgrad_impl(ctx, g, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, nullptr, add_g, nullptr, add_bits);
+}
+
 }  // extern "C"
 
 static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
                       int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, int32_t* acc,
-                      const float* add_g, const float* add_y) {
+                      const float* add_g, const float* add_y, const uint32_t* add_bits) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   int64_t P, Q;
   int rc = geom_common(g, P, Q);
@@ -1004,7 +1023,7 @@ static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   if (g->k * g->kh * g->kw > 133000) return set_error(I8T_EUNSUPPORTED, "conv_dgrad: int32 accumulator bound");
   if ((g->stride_h > 1 || g->stride_w > 1) && k_pad % 128 == 0 && g->c % 4 == 0 && (ld_wt % 16) == 0) {
     static const bool off = getenv("I8T_NO_DGRAD_PHASE") != nullptr;
-    if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc, add_g, add_y);
+    if (!off) return dgrad_phases(c, g, P, Q, gz, k_pad, wt, ld_wt, clip_g, clip_w, ga, acc, add_g, add_y, add_bits);
   }
   if (!add_g && conv_sw_eligible(g, k_pad, (int)g->c, (int)g->h, (int)g->w, gz, ga, ld_wt))
     return conv_sw_run(c, true, g, gz, k_pad, (int)P, (int)Q, wt, ld_wt, (int)g->c, (int)g->h, (int)g->w, clip_g,
@@ -1015,7 +1034,7 @@ static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   x.M = g->n * g->h * g->w; x.Ng = (int)g->c; x.Kd = Kd;
   x.k_tiles = (int)((Kd + BKB - 1) / BKB);
   x.clip_x = clip_g; x.clip_y = clip_w; x.out = ga; x.ldo = g->c; x.acc32 = acc;
-  x.add_g = add_g; x.add_y = add_y;
+  x.add_g = add_g; x.add_y = add_y; x.add_bits = add_bits;
   x.m_tiles = (int)((x.M + BM - 1) / BM);
   const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;

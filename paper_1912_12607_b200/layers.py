@@ -79,9 +79,10 @@ class ParamRef:
 # value materialised at once (bit-identical results, used to test the
 # plumbing); "torch": torch's fp32 batch norm.
 BN_IMPL = os.environ.get("I8T_BN", "fused")
-# residual joins inside the dgrad epilogue (I8T_JOIN=1).  Off by default: the
-# addend loads sit on the epilogue's critical path and measured slower (7.2 ms
-# vs 2.1 + 3.0 ms for dgrad + separate joins per ResNet-50 step, B200).
+# residual joins inside the dgrad epilogue (I8T_JOIN=1; identity joins take the
+# block ReLU mask as packed bits).  Off by default: the addend loads sit on the
+# epilogue's critical path (its 96-register budget leaves no room to prefetch
+# them) and measured slower: 37.7 vs 35.7 ms per ResNet-50 b256 step (B200).
 JOIN_FUSION = os.environ.get("I8T_JOIN", "0") == "1"
 
 
@@ -504,10 +505,15 @@ class Conv2d(Layer):
         else:
             join, self.dgrad_join, self.join_done = self.dgrad_join, None, False
             if self.need_input_grad and join is not None and g.c % 4 == 0:
-                add_g, add_y = join
-                call("i8t_conv_dgrad_join", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
-                     ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), ops._p(add_g.contiguous()),
-                     ops._p(add_y.contiguous() if add_y is not None else None))
+                add_g, add_y, add_bits = join
+                if add_bits is not None:  # identity shortcut through the block ReLU, mask as packed bits
+                    call("i8t_conv_dgrad_join_bits", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt),
+                         self.ld_wt, ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), ops._p(add_g.contiguous()),
+                         ops._p(add_bits))
+                else:
+                    call("i8t_conv_dgrad_join", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
+                         ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), ops._p(add_g.contiguous()),
+                         ops._p(add_y.contiguous() if add_y is not None else None))
                 self.join_done = True
             elif self.need_input_grad:
                 call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
@@ -878,7 +884,7 @@ class ResidualBlock(Layer):
             out = LazyAct(y.z, y.bn, relu=True).materialize(res=sc, quant_for=self.next_conv, ctx=ctx,
                                                             mask_bits=bits)
             self._bits, self._fused = bits, True
-            self._y = out if (bits is None or JOIN_FUSION) else None
+            self._y = out if bits is None else None
             return out
         self._fused = False
         return self.relu.forward(dense(y) + dense(sc), ctx)
@@ -890,7 +896,7 @@ class ResidualBlock(Layer):
             first = self.main.children[0][1] if self.main.children else None
             joinable = isinstance(first, Conv2d) and not first.depthwise and JOIN_FUSION
             if joinable and not self.shortcut:  # identity: conv1's dgrad adds g * (y > 0)
-                first.dgrad_join = (g, self._y)
+                first.dgrad_join = (g, self._y, self._bits)
             gm = dense_grad(self.main.backward(gl, ctx))
             if joinable and not self.shortcut and first.join_done:
                 return gm
@@ -898,7 +904,7 @@ class ResidualBlock(Layer):
                 sc = self.shortcut.children[0][1] if self.shortcut.children else None
                 sc_join = isinstance(sc, Conv2d) and not sc.depthwise and JOIN_FUSION
                 if sc_join:  # projection: the downsample conv's dgrad adds the main-branch gradient
-                    sc.dgrad_join = (gm, None)
+                    sc.dgrad_join = (gm, None, None)
                 gs = dense_grad(self.shortcut.backward(gl, ctx))
                 if sc_join and sc.join_done:
                     return gs
