@@ -797,7 +797,12 @@ static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& ama
     configured = true;
   }
   const int tiles = a.m_tiles * a.n_tiles * a.splits;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  static const int cap = [] {
+    const char* e = getenv("I8T_CONV_GRID");  // tuning experiments: fewer persistent CTAs
+    return e ? atoi(e) : 0;
+  }();
+  const int sms = cap > 0 && cap < num_sms() ? cap : num_sms();
+  const int grid = tiles < sms ? tiles : sms;
   launch_k(k_conv_tc<MODE, BN, VA, VB>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
@@ -838,17 +843,18 @@ static int dispatch(cudaStream_t st, const ConvArgs& a, int bn, const CUtensorMa
 
 static int pick_bn(int64_t ng) { return ng <= 64 ? 64 : (ng <= 128 ? 128 : 256); }
 
-// Tile width for FWD / DGRAD: the widest tile unless that leaves the persistent
-// queue badly quantised (tiles per SM small and fractional); then halve it.
+// Tile width for FWD / DGRAD.
 static int pick_bn_balanced(int64_t ng, int64_t m_tiles, int sms) {
+  static const int force = [] {
+    const char* e = getenv("I8T_FORCE_BN");  // tuning experiments: 64 / 128 / 256
+    return e ? atoi(e) : 0;
+  }();
+  if (force == 64 || force == 128 || force == 256) return force;
+  // A CTA's k-stage costs about the same whatever the tile width (the operand
+  // loads, not the MMA, set its pace: B200 measurements), so a narrower tile
+  // only pays when the wide one would leave most SMs idle.
   int bn = pick_bn(ng);
-  while (bn > 64) {
-    const int64_t tiles = m_tiles * ((ng + bn - 1) / bn);
-    const double per = static_cast<double>(tiles) / sms;
-    const double waste = (static_cast<double>((tiles + sms - 1) / sms) - per) / static_cast<double>((tiles + sms - 1) / sms);
-    if (per >= 8.0 || waste <= 0.12) break;
-    bn /= 2;
-  }
+  while (bn > 64 && m_tiles * ((ng + bn - 1) / bn) * 2 < sms) bn /= 2;
   return bn;
 }
 
