@@ -230,7 +230,8 @@ int i8t_conv_dgrad_join_bits(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t*
                              int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
                              const uint32_t* add_bits);
 /* Backward-weight (conv.cpp:186-195), int64 accumulation (no depth bound):
- *   acc : int64 workspace [kh*kw*c_pad][K] (zeroed by the call)
+ *   acc : int64 accumulator [kh*kw*c_pad][K] (written by the call; may be NULL
+ *         when gw is given: single device, the accumulator is not kept)
  *   gw  : float weights, KCRS when out_kcrs != 0 else KRSC (may be NULL) */
 int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* a,
                    int64_t c_pad, const float* clip_g, const float* clip_a, int64_t* acc, float* gw, int out_kcrs);

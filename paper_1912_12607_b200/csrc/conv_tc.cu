@@ -576,7 +576,7 @@ __global__ void k_wgrad_finalize(const long long* __restrict__ acc, int K, int C
 }
 
 // WGRAD split reduction: acc[m][k] = sum_s part[s][m][k] (int64, exact, fixed order),
-// optionally rescaled into float weights (KCRS or KRSC).
+// optionally rescaled into float weights (KCRS or KRSC); acc may be NULL.
 __global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int m_pad, int Kp, int M, int K, int C,
                                int Cp, int RS, long long* __restrict__ acc, const float* clip_g, const float* clip_a,
                                float* __restrict__ gw, int out_kcrs) {
@@ -1063,7 +1063,7 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   int64_t P, Q;
   int rc = geom_common(g, P, Q);
   if (rc) return rc;
-  if (!c || !gz || !a || !clip_g || !clip_a || !acc) return set_error(I8T_EINVAL, "conv_wgrad: null argument");
+  if (!c || !gz || !a || !clip_g || !clip_a || (!acc && !gw)) return set_error(I8T_EINVAL, "conv_wgrad: null argument");
   if (g->depthwise) return set_error(I8T_EINVAL, "conv_wgrad: use i8t_conv_dw_wgrad for depthwise");
   if (c_pad < g->c || c_pad % 4 != 0 || k_pad < g->k || k_pad % 4 != 0)
     return set_error(I8T_EUNSUPPORTED, "conv_wgrad: channel strides must be multiples of 4");
@@ -1075,6 +1075,8 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
     const i8t_conv_geom f = folded_geom(g, Q);
     if ((rc = i8t_conv_wgrad(ctx, &f, gz, k_pad, xf, 32, clip_g, clip_a, accf, nullptr, out_kcrs))) return rc;
     const int tot = (int)(g->kh * g->kw * 4 * g->k);
+    if (!acc) acc = reinterpret_cast<int64_t*>(ensure_scratch(c, sizeof(long long) * static_cast<size_t>(tot)));
+    if (!acc) return set_error(I8T_ECUDA, "conv_wgrad: scratch alloc failed");
     launch_k(k_unfold_wacc, (tot + 255) / 256, 256, 0, c->stream, reinterpret_cast<const long long*>(accf), (int)g->kh,
                                                             (int)g->kw, (int)g->k, reinterpret_cast<long long*>(acc));
     count_launch(1);

@@ -518,12 +518,12 @@ class Conv2d(Layer):
             elif self.need_input_grad:
                 call("i8t_conv_dgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt), self.ld_wt,
                      ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), None)
-            if self.wgrad_acc is None:
+            if self.wgrad_acc is None and ctx.wgrad_allreduce is not None:
                 self.wgrad_acc = torch.empty((self.kh * self.kw * self.c_pad, self.out_c), dtype=torch.int64,
                                              device=gdev)
-            if ctx.wgrad_allreduce is None:
+            if ctx.wgrad_allreduce is None:  # single device: weights straight from the partials, no int64 copy
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
-                     ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), ops._p(self.grad_weight), 1)
+                     ops._p(clip_g), ops._p(self.qs.clip_a), None, ops._p(self.grad_weight), 1)
             else:  # data parallel: exact int64 sum across ranks (async, overlapping the backward), then rescale
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
                      ops._p(clip_g), ops._p(self.qs.clip_a), ops._p(self.wgrad_acc), None, 1)
