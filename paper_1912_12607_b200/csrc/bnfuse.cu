@@ -249,10 +249,15 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
   if (e < n) {
     BnQuad k;
     k.load(bn, gamma, beta, c, e % c);
-    for (; e < n; e += 2 * T4) {  // two float4 loads in flight per thread
+    // software pipeline: the next trip's two float4 are in flight while this
+    // trip's two are converted (four 16-byte loads outstanding per thread)
+    float4 n0 = __ldg(reinterpret_cast<const float4*>(z + e)), n1 = n0;
+    if (e + T4 < n) n1 = __ldg(reinterpret_cast<const float4*>(z + e + T4));
+    for (; e < n; e += 2 * T4) {
       const bool two = e + T4 < n;
-      const float4 v0 = __ldg(reinterpret_cast<const float4*>(z + e));
-      const float4 v1 = two ? __ldg(reinterpret_cast<const float4*>(z + e + T4)) : v0;
+      const float4 v0 = n0, v1 = n1;
+      if (e + 2 * T4 < n) n0 = __ldg(reinterpret_cast<const float4*>(z + e + 2 * T4));
+      if (e + 3 * T4 < n) n1 = __ldg(reinterpret_cast<const float4*>(z + e + 3 * T4));
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (h && !two) break;
@@ -316,16 +321,23 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
   BnQuad k, kr;
   k.load(bn, gamma, beta, c, e % c);
   if (RES == 2) kr.load(res_bn, res_gamma, res_beta, c, e % c);
-  for (; e - lane * 4u < n; e += 2 * T4) {  // warp-uniform trips of two float4 per thread (loads first)
-    float4 v[2], r[2];
+  // warp-uniform trips of two float4 per thread, software-pipelined: the next
+  // trip's loads are issued before this trip's math
+  float4 nv[2], nr[2];
+  auto fetch = [&](uint32_t eb) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const uint32_t eh = e + h * T4;
+      const uint32_t eh = eb + h * T4;
       const uint32_t ee = eh < n ? eh : 0u;
-      v[h] = __ldg(reinterpret_cast<const float4*>(z + ee));
-      r[h] = RES ? __ldg(reinterpret_cast<const float4*>((RES == 1 ? res : res_z) + ee))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      nv[h] = __ldg(reinterpret_cast<const float4*>(z + ee));
+      nr[h] = RES ? __ldg(reinterpret_cast<const float4*>((RES == 1 ? res : res_z) + ee))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  if (e - lane * 4u < n) fetch(e);
+  for (; e - lane * 4u < n; e += 2 * T4) {
+    float4 v[2] = {nv[0], nv[1]}, r[2] = {nr[0], nr[1]};
+    if (e + 2 * T4 - lane * 4u < n) fetch(e + 2 * T4);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t eh = e + h * T4;
