@@ -169,6 +169,13 @@ int i8t_kcrs_to_crsk_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, i
  * written to device scalars.  Sums are double, deterministic for a given n. */
 int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out);
 int i8t_sq_l2_norm(i8t_ctx* ctx, const float* x, int64_t n, double* out);
+/* Histogram (stats.hpp:11-23, `make_histogram`; declared by the reference
+ * without an implementation): `bins` (1..8192) uniform bins over [-m, m],
+ * m = max|x| over the finite samples ([-1, 1] when m == 0); bin =
+ * floor((v - lo) / (hi - lo) * bins)
+ * in double, clamped to [0, bins - 1]; non-finite samples are not counted.
+ * counts: device int64[bins]; lo_hi: device double[2] (may be NULL). */
+int i8t_histogram(i8t_ctx* ctx, const float* x, int64_t n, int bins, int64_t* counts, double* lo_hi);
 int i8t_dot(i8t_ctx* ctx, const float* a, const float* b, int64_t n, double* out);
 int i8t_has_nonfinite(i8t_ctx* ctx, const float* x, int64_t n, int32_t* out);
 

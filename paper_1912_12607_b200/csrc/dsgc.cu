@@ -322,6 +322,49 @@ __global__ void k_fin_cosine(const double* tot, double* dot_out, double* cos_out
   if (cos_out) *cos_out = cosine_from(tot[0], tot[1], tot[2]);
 }
 
+// max|x| over the finite samples (the histogram range) into totals[0].
+__global__ void __launch_bounds__(RED_THREADS) k_finite_absmax(const float* __restrict__ x, uint32_t n,
+                                                               double* partials, double* totals, unsigned* ticket) {
+  pdl_entry();
+  float m = 0.0f;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float a = fabsf(__ldg(x + i));
+    if (a < __uint_as_float(0x7F800000u)) m = fmaxf(m, a);  // NaN and inf fail the compare
+  }
+  double acc[1] = {m};
+  grid_reduce<1>(acc, 1u, partials, totals, ticket);
+}
+
+// Histogram of x over `bins` uniform bins of [-m, m], m = max|x| over the
+// finite samples (k_finite_absmax); [-1, 1] when m == 0 (stats.hpp:11-20,
+// declared there without an implementation).  Bin of v: floor((v - lo) /
+// (hi - lo) * bins) in double, clamped to [0, bins - 1]; non-finite samples
+// are not counted.  Per-block smem counts, one 64-bit atomic per bin per block.
+__global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, uint32_t n, const double* totals,
+                                                   int bins, unsigned long long* counts, double* lo_hi) {
+  pdl_entry();
+  extern __shared__ unsigned int hcount[];
+  for (int b = threadIdx.x; b < bins; b += blockDim.x) hcount[b] = 0u;
+  const double m = static_cast<double>(static_cast<float>(totals[0]));
+  const double lo = m > 0.0 ? -m : -1.0, hi = m > 0.0 ? m : 1.0;
+  const double scale = static_cast<double>(bins) / (hi - lo);
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float v = __ldg(x + i);
+    if (!isfinite(v)) continue;
+    int b = static_cast<int>(floor((static_cast<double>(v) - lo) * scale));
+    b = b < 0 ? 0 : (b >= bins ? bins - 1 : b);
+    atomicAdd(&hcount[b], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < bins; b += blockDim.x)
+    if (hcount[b]) atomicAdd(counts + b, static_cast<unsigned long long>(hcount[b]));
+  if (blockIdx.x == 0 && threadIdx.x == 0 && lo_hi) {
+    lo_hi[0] = lo;
+    lo_hi[1] = hi;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 static int stats_pass0(Ctx* c, const float* x, int64_t n) {
@@ -402,6 +445,26 @@ int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out) {
   launch_k(k_fin_scalar, 1, 32, 0, c->stream, c->d_totals, 0, out, nullptr, nullptr);
   count_launch(1);
   return cuda_check("k_fin_scalar");
+}
+
+int i8t_histogram(i8t_ctx* ctx, const float* x, int64_t n, int bins, int64_t* counts, double* lo_hi) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !counts || bins < 1 || bins > 8192 || n < 0) return set_error(I8T_EINVAL, "histogram: bad arguments");
+  if (n >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "histogram: tensor >= 2^31 elements");
+  cudaMemsetAsync(counts, 0, sizeof(int64_t) * static_cast<size_t>(bins), c->stream);
+  int nb = nblocks(n);
+  double* p = ensure_partials(c, static_cast<size_t>(nb));
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+  launch_k(k_finite_absmax, nb, RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), p, c->d_totals, c->d_ticket);
+  count_launch(1);
+  int rc = cuda_check("k_finite_absmax");
+  if (rc) return rc;
+  nb = nblocks(n, 1, 4 * 148);
+  launch_k(k_histogram, nb, 256, sizeof(unsigned int) * static_cast<size_t>(bins), c->stream, x,
+           static_cast<uint32_t>(n), static_cast<const double*>(c->d_totals), bins,
+           reinterpret_cast<unsigned long long*>(counts), lo_hi);
+  count_launch(1);
+  return cuda_check("k_histogram");
 }
 
 int i8t_sq_l2_norm(i8t_ctx* ctx, const float* x, int64_t n, double* out) {
