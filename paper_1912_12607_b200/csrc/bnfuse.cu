@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
       }
     }
   }
+  pdl_trigger();
   if (bad) atomicOr(err, ERR_NONFINITE);
   if (amax) {
     __shared__ float sm[8];
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uin
       }
     }
   }
+  pdl_trigger();
   if (QOUT && q) {
     if (bad) atomicOr(err, ERR_NONFINITE);
     if (amax) {

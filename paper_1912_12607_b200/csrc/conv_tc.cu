@@ -158,7 +158,6 @@ template <int MODE, int BN, int VA, int VB>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
                                                           const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
-  pdl_entry();
   using C = Cfg<MODE, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -198,6 +197,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the prologue above (barriers, descriptor prefetch, TMEM) touches no global
+  // data: it overlaps the predecessor grid's tail under programmatic launch
+  pdl_entry();
 
   if (warp < MMA_WARP && args.tma_a) {
     // ================================================= TMA producer (thread 0)

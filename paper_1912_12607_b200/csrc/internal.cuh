@@ -94,16 +94,24 @@ unsigned* group_tickets(Ctx* c);
 // pdl_entry() (wait until the preceding grid of the stream has completed and
 // its writes are visible), and launch_k() sets the programmatic-serialization
 // attribute, so a grid is launched and its blocks scheduled while its
-// predecessor drains instead of after it.  No kernel triggers early
-// (griddepcontrol.launch_dependents): the dependents of a persistent grid then
-// land on SMs as they free up and lose their one-wave balance, which measured
-// slower than the implicit trigger at grid completion.  I8T_PDL=0 turns the
-// attribute off.
+// predecessor drains instead of after it.  Most kernels do not trigger early
+// (griddepcontrol.launch_dependents): the dependents of a persistent
+// multi-block-per-SM grid would land on the SMs that free up first and lose
+// their one-wave balance (measured slower).  I8T_PDL=0 turns the attribute off.
 bool pdl_enabled();
 
 __device__ __forceinline__ void pdl_entry() {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+// Early trigger, only in kernels whose successor is a conv grid (one CTA per
+// SM by its shared memory, so it cannot pile onto the SMs that free up first):
+// the gradient quantiser before its grid reduction, the BN-apply passes after
+// their main loops.  The conv kernels wait after their prologue.
+__device__ __forceinline__ void pdl_trigger() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
 

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
   // non-finite inputs show up as a non-finite sum of squared errors
   // (|v - g_s|^2 summed in double cannot overflow for finite float v)
   double acc[QG_NV] = {m, 0.0, a2, a3, a4, a5, a6, 0.0};
+  pdl_trigger();  // only the grid reduction remains: let a dependent conv grid start its prologue
   if (grid_reduce<QG_NV>(acc, 1u, partials, totals, ticket) && FUSED && threadIdx.x == 0)
     fin_quant_grad(st, totals, fin, lcg_state, err);
 }
