@@ -62,15 +62,31 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
   double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0};
   float lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+  if (MODE == 1 && MASK == 1) {
+    // ReLU-mask bounds of this block's channel group, bisected in the prologue
+    // (redundantly per block: cheaper than a launch); block x == 0 stores them
+    // in bn[5c..6c) for the gradient quantiser.
+    __shared__ float2 sbound[BN_GROUP];
+    if (threadIdx.x < gw) {
+      const uint32_t cc = c0 + threadIdx.x;
+      const float2 b = bn_mask_bounds(a.bn[cc], a.bn[a.c + cc], a.gamma[cc], a.beta[cc]);
+      sbound[threadIdx.x] = b;
+      if (blockIdx.x == 0) reinterpret_cast<float2*>(a.bn + 5 * a.c)[cc] = b;
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] = sbound[quad * 4 + j].x;
+        hi[j] = sbound[quad * 4 + j].y;
+      }
+    }
+  }
   if (MODE == 1 && active) {
-    const float2* bounds = reinterpret_cast<const float2*>(a.bn + 5 * a.c);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       mean[j] = a.bn[ch + j];
       invstd[j] = a.bn[a.c + ch + j];
-      const float2 lh = bounds[ch + j];
-      lo[j] = lh.x;
-      hi[j] = lh.y;
     }
   }
   if (active) {
@@ -492,14 +508,6 @@ __global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a,
   }
 }
 
-// ReLU-mask bounds per channel into bn[5c..6c) (as float2).
-__global__ void k_bn_mask_bounds(double* bn, const float* gamma, const float* beta, uint32_t c) {
-  pdl_entry();
-  const uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= c) return;
-  reinterpret_cast<float2*>(bn + 5 * c)[ch] = bn_mask_bounds(bn[ch], bn[c + ch], gamma[ch], beta[ch]);
-}
-
 // out = a + g * mask (packed mask bits): the identity-shortcut join of mask mode 3.
 __global__ void __launch_bounds__(256) k_add_masked_bits(const float* __restrict__ a, const float* __restrict__ g,
                                                          const float* __restrict__ bits, uint32_t n4,
@@ -654,12 +662,8 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
   a.z = z; a.g = g; a.mask_y = mask_y; a.gamma = gamma; a.beta = beta; a.bn = bn;
   a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = mask_mode;
   a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
-  if (mask_mode == 1) {
-    launch_k(k_bn_mask_bounds, static_cast<unsigned>((c + 127) / 128), 128, 0, cx->stream, bn, gamma, beta,
-                                                                                     static_cast<uint32_t>(c));
-    count_launch(1);
-    if ((rc = cuda_check("k_bn_mask_bounds"))) return rc;
-  }
+  // mask_mode 1: the column-sum kernel bisects the ReLU-mask bounds in its
+  // prologue and stores them in bn[5c..6c)
   return colsum(cx, a, 1);
 }
 
