@@ -119,11 +119,12 @@ constexpr int EPI_WARP0 = 9;
 constexpr int NEPI = 256;                    // 8 epilogue warps: 2 per TMEM lane quadrant
 constexpr int NTHREADS = NPROD + 32 + NEPI;  // 544
 
-template <int MODE, int BN>
+template <int MODE, int BN, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BKB;  // 16 KB
   static constexpr int B_SUB = (BN + 127) / 128;
-  static constexpr int B_BYTES = (MODE == MODE_WGRAD) ? 128 * 128 * B_SUB : BN * BKB;
+  // CG == 2 (CTA pair): each CTA holds half of the B tile's N rows
+  static constexpr int B_BYTES = (MODE == MODE_WGRAD) ? 128 * 128 * B_SUB : (BN / CG) * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = 8 * 32 * 128;  // per epilogue warp: one [32 rows x 128 B] staging tile
   static constexpr int BUDGET = 232448 - EPI_BYTES - 1024 - 256;
@@ -154,11 +155,16 @@ __device__ __forceinline__ int tile_nk(const ConvArgs& a, int split) {
   return n < a.k_tiles ? n : a.k_tiles;
 }
 
-template <int MODE, int BN, int VA, int VB>
+// CG == 2: a CTA pair (cluster of 2) runs 256-row tiles with
+// tcgen05.mma.cta_group::2 -- each CTA loads its 128 A rows and half of the B
+// rows (TMA, completion counted on the leader's barrier), the leader issues
+// the M = 256 MMAs and multicasts their commits; TMA-operand path only.
+template <int MODE, int BN, int VA, int VB, int CG = 1>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
                                                           const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
-  using C = Cfg<MODE, BN>;
+  using C = Cfg<MODE, BN, CG>;
+  constexpr bool PAIR = CG == 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -173,6 +179,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int total_tiles = args.m_tiles * args.n_tiles * args.splits;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const int cta0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);  // tile-queue slot
+  const int ncta = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const int row_base = PAIR ? static_cast<int>(crank) * 128 : 0;  // this CTA's rows inside a tile
+  constexpr int TM = PAIR ? 2 * BM : BM;                          // tile rows
 
   if (warp == MMA_WARP) {
     if (lane == 0) {
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], NEPI);
+        mbar_init(&tempty[a], PAIR ? 2 * (NEPI / 32) : NEPI);  // PAIR: one arrival per epilogue warp of both CTAs
       }
       fence_mbar_init();
       if (C::TMA_B || args.tma_a || args.tma_b) tma_prefetch(&tmap_b);
@@ -190,11 +201,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       if (args.use_tma_out) tma_prefetch(&tmap_out);
     }
     __syncwarp();
-    tmem_alloc(tmem_slot, C::TMEM_COLS);
-    tmem_relinquish();
+    if constexpr (PAIR) {
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // the prologue above (barriers, descriptor prefetch, TMEM) touches no global
@@ -205,9 +222,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     // ================================================= TMA producer (thread 0)
     if (tid == 0) {
       int kc = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cta0; t < total_tiles; t += ncta) {
         const TileCoord tc = tile_of(args, t);
-        const int m0 = tc.m_tile * BM, n0 = tc.n_tile * BN;
+        const int m0 = tc.m_tile * TM + row_base, n0 = tc.n_tile * BN;
         const int kt0 = tc.split * args.k_tiles;
         const int nk = tile_nk(args, tc.split);
         for (int kt = 0; kt < nk; ++kt, ++kc) {
@@ -216,6 +233,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           const uint32_t a_st = smem_u32(sA + s * C::A_BYTES);
           const uint32_t b_st = smem_u32(sB + s * C::B_BYTES);
           const int kb = (kt0 + kt) * BKB;
+          if constexpr (PAIR) {
+            // both CTAs' A and B halves complete on the leader's barrier
+            if (crank == 0) mbar_arrive_expect_tx_cluster(&full[s], 2 * (C::A_BYTES + C::B_BYTES));
+            const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+            tma_load_2d_pair(a_st, &tmap_a, lbar, kb, m0);
+            tma_load_2d_pair(b_st, &tmap_b, lbar, kb, n0 + static_cast<int>(crank) * (BN / 2));
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
           if constexpr (MODE == MODE_WGRAD) {
             tma_load_2d(a_st, &tmap_a, &full[s], m0, kb);  // [128 npq rows][128 channels], MN-major
@@ -236,6 +261,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     const int ja = tid % PPR_A, ra0 = tid / PPR_A;
     const int adv_p = BKB / args.Q, adv_q = BKB - adv_p * args.Q;  // WGRAD: 128 pixels = adv_p rows + adv_q
     int kc = 0;  // global stage counter across tiles
+    if constexpr (PAIR) __trap();  // CTA pairs take the TMA-operand path only
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       const TileCoord tc = tile_of(args, t);
       const int64_t m0 = static_cast<int64_t>(tc.m_tile) * BM;
@@ -396,12 +422,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     cp_async_wait<0>();
   } else if (warp == MMA_WARP) {
     // ================================================= MMA issuer (one thread)
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       constexpr bool MN = (MODE == MODE_WGRAD);
-      constexpr uint32_t idesc = make_idesc_i8(BM, BN, MN, MN);
+      constexpr uint32_t idesc = make_idesc_i8(TM, BN, MN, MN);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int kc = 0, it = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      for (int t = cta0; t < total_tiles; t += ncta, ++it) {
         const TileCoord tc = tile_of(args, t);
         const int nk = tile_nk(args, tc.split);
         const int acc = it & 1;
@@ -425,11 +451,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 32, 16, 1024);
               bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 32, 16, 1024);
             }
-            mma_i8(d_tmem, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
+            if constexpr (PAIR) mma_i8_pair(d_tmem, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
+            else mma_i8(d_tmem, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
+          if constexpr (PAIR) mma_commit_pair(&empty[s], 3);
+          else mma_commit(&empty[s]);
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR) mma_commit_pair(&tfull[acc], 3);
+        else mma_commit(&tfull[acc]);
       }
     }
     __syncwarp();
@@ -445,9 +474,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     constexpr int HALF = BN / 2 < 32 ? 32 : BN / 2;
     constexpr int NCH = HALF / 32;  // 32-column chunks per epilogue warp per tile
     const int c_begin0 = half * HALF;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+    // PAIR: the epilogue warps of both CTAs hand the accumulator back to the leader
+    const uint32_t tempty_leader = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+    auto release_acc = [&](int acc) {
+      tc_fence_before();
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + 8u * static_cast<uint32_t>(acc));
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
+    };
+    for (int t = cta0; t < total_tiles; t += ncta, ++it) {
       const TileCoord tc = tile_of(args, t);
-      const int64_t m = static_cast<int64_t>(tc.m_tile) * BM + row;
+      const int64_t m = static_cast<int64_t>(tc.m_tile) * TM + row_base + row;
       const int n0 = tc.n_tile * BN;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -455,8 +495,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int c_begin = c_begin0, c_end = (half + 1) * HALF < BN ? (half + 1) * HALF : BN;
       if (c_begin >= c_end) {  // BN == 32 would leave the second half idle
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release_acc(acc);
         continue;
       }
       auto chunk = [&](const int ci) {
@@ -464,10 +503,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         uint32_t v[32];
         tmem_ld32(t_row + static_cast<uint32_t>(col), v);
         tmem_ld_wait();
-        if (col + 32 >= c_end) {  // last read of this accumulator: hand it back to the MMA warp
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-        }
+        if (col + 32 >= c_end) release_acc(acc);  // last read of this accumulator: hand it back to the MMA warp
         const int gc0 = n0 + col;
         if (args.use_tma_out) {
           // 32x32 sub-tile -> swizzled smem staging -> one TMA bulk store
@@ -493,7 +529,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * BM + quad * 32;
+            const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * TM + row_base + quad * 32;
             tma_store_2d(&tmap_out, buf_s, gc0, r0);
             bulk_commit();
           }
@@ -548,9 +584,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no remote arrival or multicast targets an exited CTA
   if (warp == MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -789,6 +827,35 @@ static int num_sms() {
   return n;
 }
 
+// CTA-pair launch (TMA-operand path, 256-row tiles): a.m_tiles counts 256-row tiles.
+template <int MODE, int BN>
+static int launch_pair(cudaStream_t st, const ConvArgs& a, const CUtensorMap& amap, const CUtensorMap& map,
+                       const CUtensorMap& omap) {
+  using C = Cfg<MODE, BN, 2>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_conv_tc<MODE, BN, 16, 16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    configured = true;
+  }
+  const int tiles = a.m_tiles * a.n_tiles * a.splits;
+  const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  launch_k_cluster(k_conv_tc<MODE, BN, 16, 16, 2>, 2 * pairs, NTHREADS, C::SMEM, st, 2u, a, amap, map, omap);
+  count_launch(1);
+  return cuda_check("k_conv_tc<pair>");
+}
+
+// Opt-in (I8T_CONV_PAIR=1): correct (tests/test_gpu_conv_pair.py) but, as
+// measured on B200, slower than the single-CTA kernel on the 1x1 shapes it
+// covers (e.g. 1024 -> 256 at 14x14: 28.7 -> 40 us) -- kept as the base for
+// the CTA-pair work.
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("I8T_CONV_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int MODE, int BN, int VA, int VB>
 static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& amap, const CUtensorMap& map,
                       const CUtensorMap& omap) {
@@ -975,13 +1042,18 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   const int bn = pick_bn_balanced(g->k, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
   CUtensorMap amap{}, map, omap{};
-  if ((rc = make_weight_map(&map, w, g->k, ld_w, bn))) return rc;
+  const bool pair = pair_enabled() && bn == 256 && plain_1x1(g, a, c_pad);
+  if ((rc = make_weight_map(&map, w, g->k, ld_w, pair ? bn / 2 : bn))) return rc;
   if (plain_1x1(g, a, c_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, a, x.M, c_pad, BM))) return rc;
   }
   x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;
+  if (pair) {
+    x.m_tiles = (int)((x.M + 2 * BM - 1) / (2 * BM));
+    return launch_pair<MODE_FWD, 256>(c->stream, x, amap, map, omap);
+  }
   return dispatch<MODE_FWD>(c->stream, x, bn, amap, map, omap, vec_of(c_pad), 16);
 }
 
@@ -1047,13 +1119,18 @@ static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
   CUtensorMap amap{}, map, omap{};
-  if ((rc = make_weight_map(&map, wt, g->c, ld_wt, bn))) return rc;
+  const bool pair = pair_enabled() && bn == 256 && plain_1x1(g, gz, k_pad) && !add_g;
+  if ((rc = make_weight_map(&map, wt, g->c, ld_wt, pair ? bn / 2 : bn))) return rc;
   if (plain_1x1(g, gz, k_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, gz, x.M, k_pad, BM))) return rc;
   }
   x.use_tma_out = tma_out_ok(ga, g->c) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, ga, g->c, x.M, g->c, false))) return rc;
+  if (pair) {
+    x.m_tiles = (int)((x.M + 2 * BM - 1) / (2 * BM));
+    return launch_pair<MODE_DGRAD, 256>(c->stream, x, amap, map, omap);
+  }
   return dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16);
 }
 
