@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           const int kb = (kt0 + kt) * BKB;
           if constexpr (PAIR) {
             // both CTAs' A and B halves complete on the leader's barrier
-            if (crank == 0) mbar_arrive_expect_tx_cluster(&full[s], 2 * (C::A_BYTES + C::B_BYTES));
+            if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_BYTES));
             const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
             tma_load_2d_pair(a_st, &tmap_a, lbar, kb, m0);
             tma_load_2d_pair(b_st, &tmap_b, lbar, kb, n0 + static_cast<int>(crank) * (BN / 2));
@@ -844,10 +844,10 @@ static int launch_pair(cudaStream_t st, const ConvArgs& a, const CUtensorMap& am
   return cuda_check("k_conv_tc<pair>");
 }
 
-// Opt-in (I8T_CONV_PAIR=1): correct (tests/test_gpu_conv_pair.py) but, as
-// measured on B200, slower than the single-CTA kernel on the 1x1 shapes it
-// covers (e.g. 1024 -> 256 at 14x14: 28.7 -> 40 us) -- kept as the base for
-// the CTA-pair work.
+// Opt-in (I8T_CONV_PAIR=1): correct (tests/test_gpu_conv_pair.py); on the 1x1
+// shapes it covers it runs within +-5 % of the single-CTA kernel (those are
+// bound by the fp32 output and the epilogue, not the operand loads) -- kept as
+// the base for pairing the gathered 3x3 path.
 static bool pair_enabled() {
   static const bool on = [] {
     const char* e = getenv("I8T_CONV_PAIR");
