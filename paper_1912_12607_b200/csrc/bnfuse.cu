@@ -13,6 +13,8 @@
 // mean, invstd, s1/m, s2/m, gamma*invstd.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <cmath>
 
 #include "internal.cuh"
@@ -49,7 +51,8 @@ struct ColArgs {
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
 template <int MODE, int MASK = 0>
-__global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets) {
+__global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets,
+                                                   unsigned* set_tickets) {
   pdl_entry();
   const uint32_t c0 = blockIdx.y * BN_GROUP;
   const uint32_t gw = min(static_cast<uint32_t>(BN_GROUP), a.c - c0);  // group width (multiple of 4)
@@ -179,53 +182,61 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     p[threadIdx.x] = s0;
     p[BN_GROUP + threadIdx.x] = s1;
   }
+  // two-level fixed-order reduction of the per-block partials: the last block
+  // of each set of COL_SET blocks folds its set (in block order), the last set
+  // finisher folds the set sums (in set order) -- a single finisher reading
+  // every partial was the fixed cost of the small layers' launches
+  constexpr uint32_t COL_SET = 16;
+  const uint32_t gx = gridDim.x, set = blockIdx.x / COL_SET, nsets = (gx + COL_SET - 1) / COL_SET;
+  const uint32_t set_lo = set * COL_SET, set_n = min(COL_SET, gx - set_lo);
+  double* const level2 = partials + static_cast<size_t>(gridDim.y) * gx * (2 * BN_GROUP);
   __threadfence();
   __syncthreads();
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.y], 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&set_tickets[blockIdx.y * 32 + set], 1u) == set_n - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last block: tpc threads per column fold the per-block partials (block
-  // b -> part b % tpc, fixed order), then a fixed-order sum over the parts
-  const uint32_t tpc = blockDim.x / gw;
-  double s0 = 0.0, s1 = 0.0;
-  if (threadIdx.x < gw * tpc) {
-    const uint32_t col = threadIdx.x % gw, part = threadIdx.x / gw;
-    // 8 independent load/add chains (latency-bound L2 reads), combined in a fixed order
-    double a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const double* base = partials + static_cast<size_t>(blockIdx.y) * gridDim.x * (2 * BN_GROUP) + col;
-    uint32_t b = part;
-    for (; b + 7 * tpc < gridDim.x; b += 8 * tpc) {
+  if (threadIdx.x < 2 * gw) {  // thread t: column t % gw, sum t / gw
+    const uint32_t col = threadIdx.x % gw, which = threadIdx.x / gw;
+    const double* base = partials + (static_cast<size_t>(blockIdx.y) * gx + set_lo) * (2 * BN_GROUP) +
+                         which * BN_GROUP + col;
+    double v[COL_SET];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double* p = base + static_cast<size_t>(b + k * tpc) * (2 * BN_GROUP);
-        a0[k] += __ldcg(p);
-        a1[k] += __ldcg(p + BN_GROUP);
-      }
-    }
-    for (int k = 0; b < gridDim.x; b += tpc, ++k) {
-      const double* p = base + static_cast<size_t>(b) * (2 * BN_GROUP);
-      a0[k] += __ldcg(p);
-      a1[k] += __ldcg(p + BN_GROUP);
-    }
+    for (uint32_t k = 0; k < COL_SET; ++k) v[k] = k < set_n ? __ldcg(base + static_cast<size_t>(k) * (2 * BN_GROUP)) : 0.0;
+    double sum = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      s0 += a0[k];
-      s1 += a1[k];
-    }
+    for (uint32_t k = 0; k < COL_SET; ++k) sum += v[k];
+    level2[(static_cast<size_t>(blockIdx.y) * nsets + set) * (2 * BN_GROUP) + which * BN_GROUP + col] = sum;
   }
-  __shared__ double fold[2][256];
-  fold[0][threadIdx.x] = s0;
-  fold[1][threadIdx.x] = s1;
+  if (threadIdx.x == 0) set_tickets[blockIdx.y * 32 + set] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.y], 1u) == nsets - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s0 = 0.0, s1 = 0.0;
+  if (threadIdx.x < 2 * gw) {
+    const uint32_t col = threadIdx.x % gw, which = threadIdx.x / gw;
+    const double* base = level2 + static_cast<size_t>(blockIdx.y) * nsets * (2 * BN_GROUP) + which * BN_GROUP + col;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains, combined in a fixed order
+    uint32_t k = 0;
+    for (; k + 3 < nsets; k += 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += __ldcg(base + static_cast<size_t>(k + j) * (2 * BN_GROUP));
+    }
+    for (int j = 0; k < nsets; ++k, ++j) acc[j] += __ldcg(base + static_cast<size_t>(k) * (2 * BN_GROUP));
+    const double t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (which == 0) s0 = t; else s1 = t;
+  }
+  __shared__ double fold[2][BN_GROUP];
+  if (threadIdx.x < gw) fold[0][threadIdx.x] = s0;
+  else if (threadIdx.x < 2 * gw) fold[1][threadIdx.x - gw] = s1;
   __syncthreads();
   if (threadIdx.x < gw) {
-    s0 = 0.0;
-    s1 = 0.0;
-    for (uint32_t part = 0; part < tpc; ++part) {
-      s0 += fold[0][part * gw + threadIdx.x];
-      s1 += fold[1][part * gw + threadIdx.x];
-    }
+    s0 = fold[0][threadIdx.x];
+    s1 = fold[1][threadIdx.x];
     const uint32_t cc = c0 + threadIdx.x;
     const double m = static_cast<double>(a.m);
     if (MODE == 0) {  // layers.cpp:260-268
@@ -554,6 +565,18 @@ static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const d
                                                   nullptr, y, clip, q, mbits, amax, cx->d_err);
 }
 
+// per-(group, set) tickets of the two-level column-sum reduction: 64 groups x 32 sets
+// (self-resetting; one array per process: column sums of one stream run in order)
+static unsigned* set_tickets(Ctx*) {
+  static unsigned* t = [] {
+    unsigned* p = nullptr;
+    if (cudaMalloc(&p, 64 * 32 * sizeof(unsigned)) != cudaSuccess) return static_cast<unsigned*>(nullptr);
+    cudaMemset(p, 0, 64 * 32 * sizeof(unsigned));
+    return p;
+  }();
+  return t;
+}
+
 unsigned* group_tickets(Ctx* c) {
   if (!c->d_tickets) {
     if (cudaMalloc(&c->d_tickets, 64 * sizeof(unsigned)) != cudaSuccess) return nullptr;
@@ -565,19 +588,26 @@ unsigned* group_tickets(Ctx* c) {
 static int colsum(Ctx* c, const ColArgs& a, int mode) {
   const int groups = static_cast<int>((a.c + BN_GROUP - 1) / BN_GROUP);
   if (groups > 64) return set_error(I8T_EUNSUPPORTED, "bn: more than 8192 channels");
-  int bx = static_cast<int>((a.m + 8 * 64 - 1) / (8 * 64));
-  const int cap = (148 * 2 + groups - 1) / groups;  // one resident wave (~100-128 registers)
+  // >= 128 rows per block; the grid is one resident wave (2 blocks of ~100
+  // registers per SM), two for >= 2048 channels, where a group's rows are few
+  // and the trips per warp many (tools/bn_bench.py on B200)
+  int bx = static_cast<int>((a.m + 127) / 128);
+  const int waves = groups >= 16 ? 4 : 2;
+  const int cap = (148 * waves + groups - 1) / groups;
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
-  double* p = ensure_partials(c, static_cast<size_t>(bx) * groups * 2 * BN_GROUP);
+  if (bx > 32 * 16) bx = 32 * 16;  // <= 32 sets of 16 blocks per group
+  const int nsets = (bx + 15) / 16;
+  double* p = ensure_partials(c, static_cast<size_t>(bx + nsets) * groups * 2 * BN_GROUP);
   unsigned* t = group_tickets(c);
-  if (!p || !t) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
+  unsigned* st = set_tickets(c);
+  if (!p || !t || !st) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
-  if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t);
-  else if (a.mask_mode == 1) launch_k(k_bn_colsum<1, 1>, grid, 256, 0, c->stream, a, p, t);
-  else if (a.mask_mode == 2) launch_k(k_bn_colsum<1, 2>, grid, 256, 0, c->stream, a, p, t);
-  else if (a.mask_mode == 3) launch_k(k_bn_colsum<1, 3>, grid, 256, 0, c->stream, a, p, t);
-  else launch_k(k_bn_colsum<1, 0>, grid, 256, 0, c->stream, a, p, t);
+  if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t, st);
+  else if (a.mask_mode == 1) launch_k(k_bn_colsum<1, 1>, grid, 256, 0, c->stream, a, p, t, st);
+  else if (a.mask_mode == 2) launch_k(k_bn_colsum<1, 2>, grid, 256, 0, c->stream, a, p, t, st);
+  else if (a.mask_mode == 3) launch_k(k_bn_colsum<1, 3>, grid, 256, 0, c->stream, a, p, t, st);
+  else launch_k(k_bn_colsum<1, 0>, grid, 256, 0, c->stream, a, p, t, st);
   count_launch(1);
   return cuda_check("k_bn_colsum");
 }
