@@ -1,0 +1,48 @@
+"""Gradient quantiser with the fused BN backward (i8t_quantize_gradient_bn, K3)
+on ResNet-50 shapes (batch 256): time per launch back to back (CUDA events),
+fixed cost vs bandwidth."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1912_12607_b200 import ops  # noqa: E402
+
+res = []
+for n, hw, c in [(256, 3136, 64), (256, 3136, 256), (256, 784, 128), (256, 784, 512), (256, 196, 256),
+                 (256, 196, 1024), (256, 49, 512), (256, 49, 2048)]:
+    m = n * hw
+    z = torch.randn(m, c, device="cuda")
+    g = torch.randn(m, c, device="cuda") * 1e-3
+    gamma, beta = torch.ones(c, device="cuda"), torch.zeros(c, device="cuda")
+    bn = torch.zeros(6 * c, dtype=torch.float64, device="cuda")
+    gg, gb = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+    ops.call("i8t_bn_fwd_stats", ops.ctx(), ops._p(z), m, c, C.c_double(0.1), C.c_double(1e-5), ops._p(bn), None, None)
+    ops.call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(z), m, c, ops._p(bn), ops._p(gamma), ops._p(beta), 1,
+             None, ops._p(gg), ops._p(gb))
+    st = ops.DsgcState(period=1000)
+    lcg = ops.new_lcg_state(1)
+    q = torch.empty((m, c), dtype=torch.int8, device="cuda")
+    f = lambda: ops.call("i8t_quantize_gradient_bn", ops.ctx(), st.ptr, ops._p(g), ops._p(z), n, c, hw, ops._p(bn),
+                         ops._p(gamma), ops._p(beta), 1, None, 1, C.c_double(20.0), C.c_double(0.1),
+                         ops.FORMS["exp"], ops._p(lcg), ops._p(q))
+    f()  # iteration-0 search happens inside the first call's state machine? (period 1000: state searched once)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        f()
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 10 * 1e3
+    b = 9 * m * c
+    res.append((b, t))
+    print(f"m={m:8d} c={c:5d} {t:8.1f} us  {b / t / 1e6:6.0f} GB/s", flush=True)
+A = np.array([[1.0, b] for b, _ in res])
+coef = np.linalg.lstsq(A, np.array([t for _, t in res]), rcond=None)[0]
+print(f"fit: fixed {coef[0]:.1f} us, marginal {1e-6 / coef[1]:.0f} GB/s")
