@@ -42,7 +42,7 @@ for n, hw, c in [(256, 3136, 64), (256, 3136, 256), (256, 784, 128), (256, 784, 
     t = s.elapsed_time(e) / 10 * 1e3
     b = 9 * m * c
     res.append((b, t))
-    print(f"m={m:8d} c={c:5d} {t:8.1f} us  {b / t / 1e6:6.0f} GB/s", flush=True)
+    print(f"m={m:8d} c={c:5d} {t:8.1f} us  {b / t / 1e3:6.0f} GB/s", flush=True)
 A = np.array([[1.0, b] for b, _ in res])
 coef = np.linalg.lstsq(A, np.array([t for _, t in res]), rcond=None)[0]
-print(f"fit: fixed {coef[0]:.1f} us, marginal {1e-6 / coef[1]:.0f} GB/s")
+print(f"fit: fixed {coef[0]:.1f} us, marginal {1e-3 / coef[1]:.0f} GB/s")
