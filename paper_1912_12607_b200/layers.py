@@ -84,6 +84,10 @@ BN_IMPL = os.environ.get("I8T_BN", "fused")
 # epilogue's critical path (its 96-register budget leaves no room to prefetch
 # them) and measured slower: 37.7 vs 35.7 ms per ResNet-50 b256 step (B200).
 JOIN_FUSION = os.environ.get("I8T_JOIN", "0") == "1"
+# The projection-shortcut join (the downsample conv's dgrad adds the
+# main-branch gradient; 4 ResNet-50 blocks) pays off: 35.01 -> 34.90 ms per
+# step.  I8T_JOIN_PROJ=0 turns it off.
+JOIN_PROJ = os.environ.get("I8T_JOIN_PROJ", "1") == "1" or JOIN_FUSION
 
 
 class LazyAct:
@@ -902,7 +906,7 @@ class ResidualBlock(Layer):
                 return gm
             if self.shortcut:
                 sc = self.shortcut.children[0][1] if self.shortcut.children else None
-                sc_join = isinstance(sc, Conv2d) and not sc.depthwise and JOIN_FUSION
+                sc_join = isinstance(sc, Conv2d) and not sc.depthwise and JOIN_PROJ
                 if sc_join:  # projection: the downsample conv's dgrad adds the main-branch gradient
                     sc.dgrad_join = (gm, None, None)
                 gs = dense_grad(self.shortcut.backward(gl, ctx))

@@ -269,8 +269,8 @@ def _train(impl, name="resnet20", batch=16, steps=3, mode=None, join=True):
     from paper_1912_12607_b200 import layers as L
     from paper_1912_12607_b200.models import build_model
     from paper_1912_12607_b200.trainer import TrainConfig, Trainer, synthetic_batch
-    old, old_join = L.BN_IMPL, L.JOIN_FUSION
-    L.BN_IMPL, L.JOIN_FUSION = impl, join
+    old, old_join, old_proj = L.BN_IMPL, L.JOIN_FUSION, L.JOIN_PROJ
+    L.BN_IMPL, L.JOIN_FUSION, L.JOIN_PROJ = impl, join, join
     try:
         m = build_model(name, seed=3)
         L.int8_replace(m.net)
@@ -281,7 +281,7 @@ def _train(impl, name="resnet20", batch=16, steps=3, mode=None, join=True):
         x, y = synthetic_batch(m, batch, 5)
         return tr, [tr.train_step(x, y, it, 100) for it in range(steps)]
     finally:
-        L.BN_IMPL, L.JOIN_FUSION = old, old_join
+        L.BN_IMPL, L.JOIN_FUSION, L.JOIN_PROJ = old, old_join, old_proj
 
 
 @pytest.mark.parametrize("name,batch", [("resnet20", 16), ("resnet50", 2), ("mobilenet_v2", 4), ("inception_v3", 2)])
