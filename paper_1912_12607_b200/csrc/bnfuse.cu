@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ 
 // The loop is warp-uniform (a warp covers 128 consecutive elements per trip) so
 // the 4-bit nibbles of 8 lanes can be OR-ed into a word with shuffles.
 template <bool QOUT, int RES>  // RES: 0 none, 1 dense fp32 residual, 2 residual = bn'(res_z) (lazy)
-__global__ void __launch_bounds__(256) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
+__global__ void __launch_bounds__(256, RES == 2 ? 2 : 3) k_bn_act(const float* __restrict__ z, uint32_t n, uint32_t c, const double* bn,
                                                 const float* gamma, const float* beta, int relu,
                                                 const float* __restrict__ res, const float* __restrict__ res_z,
                                                 const double* res_bn, const float* res_gamma, const float* res_beta,
