@@ -296,7 +296,9 @@ def main():
             assert torch.isfinite(loss_host).all(), "non-finite loss in the e2e run"
         return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() - launches0
 
-    if os.environ.get("I8T_PROFILE_STEP"):  # ncu --profile-from-start off: capture exactly one normal step
+    if os.environ.get("I8T_PROFILE_STEP"):  # ncu --profile-from-start off: capture exactly one step
+        if os.environ.get("I8T_PROFILE_STEP") == "search":  # ... the DSGC search step (Periodic Update)
+            it = ((it // cfg.clip_period) + 1) * cfg.clip_period
         barrier()
         torch.cuda.cudart().cudaProfilerStart()
         tr.train_step(x, y, it, total, read_stats=False)
