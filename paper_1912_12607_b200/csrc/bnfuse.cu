@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   }
   if (active) {
     // U rows per thread per trip: all loads of a trip are issued before any math
-    constexpr int U = MODE == 0 ? 8 : 4;
+    constexpr int U = MODE == 0 ? 10 : 4;
     const uint32_t row_step = gridDim.x * 8 * rpw;
     uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub;
     // software pipeline: the U rows of the next trip are loaded before the
