@@ -393,8 +393,8 @@ def instrumented_conv_time(tr, x, y, it, total, model, batch):
     orig = _lib.call
 
     def wrapped(name, *args):
-        if name in ("i8t_conv_fwd", "i8t_conv_dgrad", "i8t_conv_dgrad_join", "i8t_conv_wgrad", "i8t_conv_dw_fwd",
-                    "i8t_conv_dw_dgrad", "i8t_conv_dw_wgrad"):
+        if name in ("i8t_conv_fwd", "i8t_conv_dgrad", "i8t_conv_dgrad_join", "i8t_conv_dgrad_join_bits",
+                    "i8t_conv_wgrad", "i8t_conv_dw_fwd", "i8t_conv_dw_dgrad", "i8t_conv_dw_wgrad"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             orig(name, *args)
