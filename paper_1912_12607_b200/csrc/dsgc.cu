@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats0(const float* __restri
 // Group y reduces over blockIdx.x into its own partials / ticket, and its last
 // block scatters the candidate sums (and, for y == 0, [0..2]) into totals.
 template <int NG>
-__global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restrict__ g, uint32_t n,
+__global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __restrict__ g, uint32_t n,
                                                           const float* __restrict__ cands, int nc,
                                                           const int32_t* active, double* partials, double* gtot,
                                                           double* totals, unsigned* tickets) {
@@ -72,11 +72,13 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
   __shared__ double dq_tab[NG * 256];
   const int j0 = blockIdx.y * NG;
   float hs[NG];
+  bool tiny = false;  // a subnormal candidate scale: the exact function for every element
   uint32_t tab_n[NG];  // dq_tab[j][q + 127] at the qn_bits pattern RMAGIC + q + 1 (32-bit wrap)
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
     const float cl = cands[min(j0 + j, nc - 1)];  // past nc: a duplicate, never scattered
     hs[j] = __fdiv_rn(0.5f, cl);
+    tiny |= !(scale_of(cl) >= 0x1p-126f);
     build_dequant_table(dq_tab + j * 256, scale_of(cl));
     tab_n[j] = static_cast<uint32_t>(__cvta_generic_to_shared(dq_tab + j * 256)) + 8u * (126u - RMAGIC_BITS);
   }
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats(const float* __restric
     const double vd = v;
     acc[2] = fma(vd, vd, acc[2]);
     uint32_t kb[NG];
-    bool slow = false;
+    bool slow = tiny;
 #pragma unroll
     for (int j = 0; j < NG; ++j) kb[j] = qn_bits(q_t1(v, hs[j]), slow);
     if (slow) {

@@ -35,7 +35,12 @@ constexpr int RMAGIC_BITS = 0x4B400000;
 // test a >= s*(k+1/2) is decided exactly by the sign of one FMA.
 __device__ __forceinline__ int quant_nearest(float x, float clip, float s, float inv_s) {
   const float v = fminf(fmaxf(x, -clip), clip);
-  const float a = fabsf(v);
+  float a = fabsf(v);
+  if (!(s >= 0x1p-126f)) {  // subnormal scale (clip < 127 * FLT_MIN): a and s scaled by 2^64, exactly
+    a *= 0x1p64f;
+    s *= 0x1p64f;
+    inv_s = __frcp_rn(s);
+  }
   const float kb = __fadd_rn(__fmul_rn(a, inv_s), RMAGIC);
   const float k = __fsub_rn(kb, RMAGIC);
   int ki = __float_as_int(kb) - RMAGIC_BITS;
@@ -105,7 +110,7 @@ __device__ __forceinline__ uint32_t qn_bits(float t1, bool& slow) {
 // quantize_value kNearest through the fast path, the exact function only near
 // a rounding tie (hs = 0.5 / clip).
 __device__ __forceinline__ int quant_nearest_fast(float v, float clip, float hs, float s, float inv_s) {
-  bool slow = false;
+  bool slow = !(s >= 0x1p-126f);  // the fast paths assume a normal scale
   const uint32_t kb = qn_bits(q_t1(v, hs), slow);
   if (slow) return quant_nearest(v, clip, s, inv_s);
   return static_cast<int>(kb) - (RMAGIC_BITS + 1);
@@ -121,7 +126,7 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 // else the reference's FP64 formula (quantize.cpp:16-31).
 __device__ __forceinline__ int quant_stoch(float x, float clip, float s, float inv_s, uint32_t X) {
   const float v = fminf(fmaxf(x, -clip), clip);
-  bool slow = false;
+  bool slow = !(s >= 0x1p-126f);
   const int qf = qs_fast(__fmul_rn(v, inv_s), X, slow);
   if (!slow) return qf;
   double td = static_cast<double>(v) / static_cast<double>(s);

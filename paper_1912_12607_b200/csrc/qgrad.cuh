@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
   float clip = clip_override ? *clip_override : st->v.clip;
   if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
   const float s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
+  const bool tiny = !(s >= 0x1p-126f);  // subnormal scale: every element through the exact functions
   build_dequant_table(tab, s);
   __syncthreads();
   // tab[q + 127] at the bit patterns qs_bits / qn_bits return (32-bit wrap)
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t
     // one float4: fast path; any element within QK of a rounding boundary (or
     // with a float-subnormal BN x_hat) sends the float4 to the exact functions
     auto process = [&](const typename Src::Raw& r) {
-      bool slow = false;
+      bool slow = tiny;
       const float4 v4 = src.value_fast(r, slow);
       float vv[4] = {v4.x, v4.y, v4.z, v4.w};
       uint32_t Xs[4];

@@ -94,6 +94,21 @@ def test_quantize_stochastic_adversarial(ops, clip):
     assert ops.lcg_value(st) == st_ref
 
 
+@pytest.mark.parametrize("clip", [1e-37, 4e-39, 2e-41])
+def test_quantize_subnormal_scale(ops, clip):
+    """clip < 127 * FLT_MIN makes s = float(clip / 127) subnormal: the FP32 fast
+    paths do not hold there and the kernels take the FP64 formula."""
+    rng = np.random.default_rng(int(clip * 1e45) % 1000)
+    x = (rng.standard_normal(30_000) * clip * 0.6).astype(np.float32)
+    x[:4] = [clip, -clip, 3 * clip, 0.0]
+    ref, _ = O.quantize(x, clip)
+    np.testing.assert_array_equal(ops.quantize(t(x), clip).cpu().numpy(), ref)
+    ref, st_ref = O.quantize(x, clip, True, 7)
+    st = ops.new_lcg_state(7)
+    np.testing.assert_array_equal(ops.quantize(t(x), clip, stochastic=True, stream_state=st).cpu().numpy(), ref)
+    assert ops.lcg_value(st) == st_ref
+
+
 def test_quantize_stochastic_odd_length(ops):
     x = np.linspace(-1, 1, 1001).astype(np.float32)
     ref, st_ref = O.quantize(x, 0.9, True, 77)
@@ -194,6 +209,22 @@ def test_search_clip_refined(seed, ops):
     assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
 
 
+@pytest.mark.parametrize("mag", [1e-37, 3e-39, 1e37, 3e38])
+def test_search_clip_extreme_magnitudes(mag, ops):
+    """The candidate pass rebuilds the double x̂ from the float bits with
+    power-of-two scalings; scales below FLT_MIN (subnormal x̂) take the multiply
+    path, and the largest finite g still scales without overflow."""
+    g = O.gradient_like((20_000,), 3, 1e-4, 0.02)
+    g = (g / np.abs(g).max() * np.float32(mag)).astype(np.float32)
+    assert np.isfinite(g).all() and np.abs(g).max() > 0
+    ref = O.search_clip(g, 32, 0)
+    got = ops.search_clip(t(g), 32, 0)
+    assert got[0] == ref[0]
+    assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
+    for clip in (ref[0], float(np.abs(g).max()) / 7):
+        assert ops.measure_dc(t(g), clip) == pytest.approx(O.measure_dc(g, clip), abs=DC_ABS)
+
+
 def test_search_clip_kats(ops):
     s = 0.01
     g = (np.arange(-127, 128) * np.float32(s)).astype(np.float32)
@@ -274,6 +305,11 @@ def test_quantize_gradient_flat_and_search_disabled(ops):
 def test_quantize_gradient_zero_skip_consumes_no_draws(ops):
     gs = [O.gradient_like((2, 8, 4, 4), 6, 1e-3, 0.0), np.zeros((2, 8, 4, 4), np.float32)]
     _qg_compare(ops, gs, 4)
+
+
+def test_quantize_gradient_subnormal_scale(ops):
+    gs = [O.gradient_like((2, 8, 6, 6), s, 1e-3, 0.01) * np.float32(1e-37) for s in (7, 8)]
+    _qg_compare(ops, gs, 3)
 
 
 def test_quantize_gradient_config1_full(ops):
