@@ -94,13 +94,14 @@ def test_quantize_stochastic_adversarial(ops, clip):
     assert ops.lcg_value(st) == st_ref
 
 
-@pytest.mark.parametrize("clip", [1e-37, 4e-39, 2e-41])
+@pytest.mark.parametrize("clip", [1e-37, 4e-39, 2e-41, 3e38])
 def test_quantize_subnormal_scale(ops, clip):
     """clip < 127 * FLT_MIN makes s = float(clip / 127) subnormal: the FP32 fast
     paths do not hold there and the kernels take the FP64 formula."""
-    rng = np.random.default_rng(int(clip * 1e45) % 1000)
-    x = (rng.standard_normal(30_000) * clip * 0.6).astype(np.float32)
-    x[:4] = [clip, -clip, 3 * clip, 0.0]
+    rng = np.random.default_rng(int(np.log2(clip)) % 1000)
+    big = float(np.finfo(np.float32).max)
+    x = np.clip(rng.standard_normal(30_000) * clip * 0.6, -big, big).astype(np.float32)
+    x[:4] = [clip, -clip, min(3 * clip, big), 0.0]
     ref, _ = O.quantize(x, clip)
     np.testing.assert_array_equal(ops.quantize(t(x), clip).cpu().numpy(), ref)
     ref, st_ref = O.quantize(x, clip, True, 7)
@@ -308,8 +309,9 @@ def test_quantize_gradient_zero_skip_consumes_no_draws(ops):
 
 
 def test_quantize_gradient_subnormal_scale(ops):
-    gs = [O.gradient_like((2, 8, 6, 6), s, 1e-3, 0.01) * np.float32(1e-37) for s in (7, 8)]
-    _qg_compare(ops, gs, 3)
+    for mag in (1e-37, 1e35):
+        gs = [(O.gradient_like((2, 8, 6, 6), s, 1e-3, 0.01) * np.float32(mag)).astype(np.float32) for s in (7, 8)]
+        _qg_compare(ops, gs, 3)
 
 
 def test_quantize_gradient_config1_full(ops):
