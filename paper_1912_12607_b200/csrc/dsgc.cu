@@ -42,7 +42,22 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats0(const float* __restri
   };
   const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n4; f += stride) {
+  constexpr int U = 4;  // float4 loads in flight per thread (HBM-bound passes)
+  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (U > 1)
+  for (; f + (U - 1) * stride < n4; f += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(g4 + f + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      body(v[u].x);
+      body(v[u].y);
+      body(v[u].z);
+      body(v[u].w);
+    }
+  }
+  for (; f < n4; f += stride) {
     const float4 v = __ldg(g4 + f);
     body(v.x);
     body(v.y);
@@ -113,7 +128,22 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
   };
   const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n4; f += stride) {
+  constexpr int U = NG <= 2 ? 4 : 1;  // float4 loads in flight per thread (HBM-bound passes)
+  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (U > 1)
+  for (; f + (U - 1) * stride < n4; f += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(g4 + f + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      body(v[u].x);
+      body(v[u].y);
+      body(v[u].z);
+      body(v[u].w);
+    }
+  }
+  for (; f < n4; f += stride) {
     const float4 v = __ldg(g4 + f);
     body(v.x);
     body(v.y);
