@@ -639,6 +639,47 @@ __global__ void k_wgrad_reduce(const int32_t* __restrict__ part, int splits, int
   }
 }
 
+// Few outputs, many splits (the deep layers' wgrads: M*K of a few thousand,
+// ~100 splits): P split phases per output, 256/P consecutive outputs per block
+// (coalesced per warp), the phases summed through shared memory.  Integer sums,
+// so the result is the same whatever the order.
+template <int P>
+__global__ void __launch_bounds__(256) k_wgrad_reduce_split(const int32_t* __restrict__ part, int splits, int m_pad,
+                                                            int Kp, int M, int K, int C, int Cp, int RS,
+                                                            long long* __restrict__ acc, const float* clip_g,
+                                                            const float* clip_a, float* __restrict__ gw, int out_kcrs) {
+  pdl_entry();
+  constexpr int W = 256 / P;
+  __shared__ long long red[P][W];
+  const double rescale =
+      static_cast<double>(__fdiv_rn(*clip_g, 127.0f)) * static_cast<double>(__fdiv_rn(*clip_a, 127.0f));
+  const int64_t tot = static_cast<int64_t>(M) * K;
+  const int lo = threadIdx.x % W, ph = threadIdx.x / W;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * W; base < tot; base += static_cast<int64_t>(gridDim.x) * W) {
+    const int64_t i = base + lo;
+    const int m = static_cast<int>(i / K), k = static_cast<int>(i - static_cast<int64_t>(m) * K);
+    long long sum = 0;
+    if (i < tot)
+      for (int sp = ph; sp < splits; sp += P) sum += __ldg(part + (static_cast<int64_t>(sp) * m_pad + m) * Kp + k);
+    red[ph][lo] = sum;
+    __syncthreads();
+    if (ph == 0 && i < tot) {
+#pragma unroll
+      for (int p = 1; p < P; ++p) sum += red[p][lo];
+      if (acc) acc[i] = sum;
+      if (gw) {
+        const int rs = m / Cp, c = m - rs * Cp;
+        if (c < C) {
+          const int64_t o =
+              out_kcrs ? (static_cast<int64_t>(k) * C + c) * RS + rs : (static_cast<int64_t>(k) * RS + rs) * C + c;
+          gw[o] = static_cast<float>(rescale * static_cast<double>(sum));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Narrow-channel convolutions (c_pad == 4, e.g. the RGB stem): fold the kw
 // horizontal taps into the channel dimension,
 //   X'[n][h][q][s*4 + c] = X[n][h][q*sw + s - pw][c]  (zero outside; bytes 4*kw..31 zero),
@@ -1215,6 +1256,15 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   rc = dispatch<MODE_WGRAD>(c->stream, x, bn, amap, map, omap, vec_of(c_pad), vec_of(k_pad));
   if (rc) return rc;
   const int64_t tot = x.M * g->k;
+  if (tot < 148 * 256 * 2 && splits >= 8) {  // too few outputs to fill the GPU one per thread
+    int blocks = (int)((tot + 31) / 32);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    launch_k(k_wgrad_reduce_split<8>, blocks, 256, 0, c->stream, part, (int)splits, x.m_pad, (int)k_pad, (int)x.M,
+             (int)g->k, (int)g->c, (int)c_pad, (int)(g->kh * g->kw), reinterpret_cast<long long*>(acc), clip_g, clip_a,
+             gw, out_kcrs);
+    count_launch(1);
+    return cuda_check("k_wgrad_reduce_split");
+  }
   int blocks = (int)((tot + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   launch_k(k_wgrad_reduce, blocks, 256, 0, c->stream, part, (int)splits, x.m_pad, (int)k_pad, (int)x.M, (int)g->k, (int)g->c,
