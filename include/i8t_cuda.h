@@ -333,9 +333,14 @@ int i8t_add_masked_bits(i8t_ctx* ctx, const float* a, const float* g, const uint
 /* All parameters in one launch: w and grad are flat arenas; segment i covers
  * [seg_off[i], seg_off[i+1]) (multiples of 4, device int64) and uses the
  * DCLR factor of device state seg_state[i] (device array of pointers; NULL
- * entry = phi 1).  Same arithmetic as i8t_sgd_dclr per element. */
+ * entry = phi 1).  Same arithmetic as i8t_sgd_dclr per element.
+ * lr_dev (device double, may be NULL): when given, replaces base_lr (so a
+ * captured CUDA graph reads the step's cosine LR from device memory).
+ * mom (flat arena like w, may be NULL): the reference's momentum update
+ * (train.cpp:106-111) buf = float(momentum*buf + g), w -= float(lr*buf). */
 int i8t_sgd_dclr_multi(i8t_ctx* ctx, float* w, const float* grad, int nseg, const int64_t* seg_off,
-                       const void* const* seg_state, double base_lr, const int32_t* skip);
+                       const void* const* seg_state, double base_lr, const double* lr_dev, const int32_t* skip,
+                       float* mom, double momentum);
 /* Non-finite scan of a flat gradient arena: *flag = 1 if any element is
  * NaN/Inf (has_nonfinite, tensor.cpp:96-101, over every parameter gradient). */
 int i8t_nonfinite_flag(i8t_ctx* ctx, const float* x, int64_t n, int32_t* flag);

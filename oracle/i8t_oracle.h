@@ -102,6 +102,23 @@ int or_quantize_gradient(or_clip_state* st, const float* g, int64_t n, int64_t i
 /* ---- SGD with DCLR factor (train.cpp:97-117, momentum 0) ---- */
 void or_sgd_update(float* w, const float* g, int64_t n, double lr);
 
+/* ---- FP32 layers (layers.cpp:230-529), NCHW ---- */
+void or_bn_forward_train(const float* x, int64_t n, int64_t c, int64_t hw, const float* gamma, const float* beta,
+                         float* running_mean, float* running_var, double momentum, double eps, float* y,
+                         float* xhat, double* invstd_out);
+void or_bn_forward_eval(const float* x, int64_t n, int64_t c, int64_t hw, const float* gamma, const float* beta,
+                        const float* running_mean, const float* running_var, double eps, float* y);
+void or_bn_backward(const float* g_out, const float* xhat, const double* invstd, int64_t n, int64_t c, int64_t hw,
+                    const float* gamma, float* g_in, float* grad_gamma, float* grad_beta);
+int or_pool_forward(const float* x, int64_t n, int64_t c, int64_t h, int64_t w, int kind, int64_t k, int64_t s,
+                    int64_t pad, float* y, int64_t* argmax);
+int or_pool_backward(const float* g_out, const int64_t* argmax, int64_t n, int64_t c, int64_t h, int64_t w, int kind,
+                     int64_t k, int64_t s, int64_t pad, float* g_in);
+double or_softmax_ce(const float* logits, int64_t n, int64_t classes, const int32_t* labels, float* g_logits,
+                     int* status);
+int or_conv_fwd_f32(const float* x, const float* w, const or_geom* g, float* z);
+void or_sgd_momentum_update(float* w, const float* g, float* buf, int64_t n, double lr, double momentum);
+
 /* ---- synthetic inputs (rng.hpp:13-50 SplitMix64 + Box-Muller) ---- */
 void or_fill_gaussian(float* x, int64_t n, uint64_t seed, double stddev, int relu);
 void or_fill_gradient_like(float* x, int64_t n, uint64_t seed, double scale, double outlier_rate);

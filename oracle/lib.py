@@ -88,6 +88,24 @@ def lib():
         L.or_fill_gaussian.restype = None
         L.or_fill_gradient_like.argtypes = [P_F32, C.c_int64, C.c_uint64, C.c_double, C.c_double]
         L.or_fill_gradient_like.restype = None
+        P_F64 = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.or_bn_forward_train.argtypes = [P_F32, C.c_int64, C.c_int64, C.c_int64, P_F32, P_F32, P_F32, P_F32,
+                                          C.c_double, C.c_double, P_F32, P_F32, P_F64]
+        L.or_bn_forward_train.restype = None
+        L.or_bn_forward_eval.argtypes = [P_F32, C.c_int64, C.c_int64, C.c_int64, P_F32, P_F32, P_F32, P_F32,
+                                         C.c_double, P_F32]
+        L.or_bn_forward_eval.restype = None
+        L.or_bn_backward.argtypes = [P_F32, P_F32, P_F64, C.c_int64, C.c_int64, C.c_int64, P_F32, P_F32, P_F32,
+                                     P_F32]
+        L.or_bn_backward.restype = None
+        L.or_pool_forward.argtypes = [P_F32] + [C.c_int64] * 4 + [C.c_int] + [C.c_int64] * 3 + [P_F32, C.c_void_p]
+        L.or_pool_backward.argtypes = [P_F32, C.c_void_p] + [C.c_int64] * 4 + [C.c_int] + [C.c_int64] * 3 + [P_F32]
+        L.or_softmax_ce.argtypes = [P_F32, C.c_int64, C.c_int64, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                    P_F32, C.POINTER(C.c_int)]
+        L.or_softmax_ce.restype = C.c_double
+        L.or_sgd_momentum_update.argtypes = [P_F32, P_F32, P_F32, C.c_int64, C.c_double, C.c_double]
+        L.or_sgd_momentum_update.restype = None
+        L.or_conv_fwd_f32.argtypes = [P_F32, P_F32, C.POINTER(Geom), P_F32]
         _lib = L
     return _lib
 

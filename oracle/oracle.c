@@ -578,3 +578,221 @@ void or_fill_gradient_like(float* x, int64_t n, uint64_t seed, double scale, dou
     x[i] = (float)v;
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* FP32 layers around the INT8 convolutions (layers.cpp:230-529), NCHW.      */
+/* Sequential double sums in the reference's loop order; expressions are     */
+/* written in the reference's form so GCC's FP contraction treats them alike */
+/* (pinned against the compiled reference Trainer, tests/test_oracle_model). */
+
+/* BatchNorm2d::forward, training (layers.cpp:262-291).  xhat (float, the
+ * reference's cached_xhat_) and invstd (double per channel) are outputs for
+ * the backward; running stats are updated in place. */
+void or_bn_forward_train(const float* x, int64_t n, int64_t c, int64_t hw, const float* gamma, const float* beta,
+                         float* running_mean, float* running_var, double momentum, double eps, float* y,
+                         float* xhat, double* invstd_out) {
+  const int64_t m = n * hw;
+  for (int64_t ch = 0; ch < c; ++ch) {
+    double sum = 0.0, sq = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const float* px = x + (i * c + ch) * hw;
+      for (int64_t p = 0; p < hw; ++p) {
+        sum += px[p];
+        sq += (double)px[p] * (double)px[p];
+      }
+    }
+    const double mean = sum / m;
+    const double v0 = sq / m - mean * mean;
+    const double var = v0 > 0.0 ? v0 : 0.0;
+    const double invstd = 1.0 / sqrt(var + eps);
+    invstd_out[ch] = invstd;
+    running_mean[ch] = (float)((1.0 - momentum) * running_mean[ch] + momentum * mean);
+    running_var[ch] = (float)((1.0 - momentum) * running_var[ch] + momentum * var);
+    const double g = gamma[ch], b = beta[ch];
+    for (int64_t i = 0; i < n; ++i) {
+      const float* px = x + (i * c + ch) * hw;
+      float* ph = xhat + (i * c + ch) * hw;
+      float* py = y + (i * c + ch) * hw;
+      for (int64_t p = 0; p < hw; ++p) {
+        const double xv = ((double)px[p] - mean) * invstd;
+        ph[p] = (float)xv;
+        py[p] = (float)(g * xv + b);
+      }
+    }
+  }
+}
+
+/* BatchNorm2d::forward, inference (layers.cpp:247-259). */
+void or_bn_forward_eval(const float* x, int64_t n, int64_t c, int64_t hw, const float* gamma, const float* beta,
+                        const float* running_mean, const float* running_var, double eps, float* y) {
+  for (int64_t ch = 0; ch < c; ++ch) {
+    const double invstd = 1.0 / sqrt((double)running_var[ch] + eps);
+    const double mean = running_mean[ch];
+    const double g = gamma[ch], b = beta[ch];
+    for (int64_t i = 0; i < n; ++i) {
+      const float* px = x + (i * c + ch) * hw;
+      float* py = y + (i * c + ch) * hw;
+      for (int64_t p = 0; p < hw; ++p) py[p] = (float)(g * (((double)px[p] - mean) * invstd) + b);
+    }
+  }
+}
+
+/* BatchNorm2d::backward (layers.cpp:295-323). */
+void or_bn_backward(const float* g_out, const float* xhat, const double* invstd, int64_t n, int64_t c, int64_t hw,
+                    const float* gamma, float* g_in, float* grad_gamma, float* grad_beta) {
+  const int64_t m = n * hw;
+  for (int64_t ch = 0; ch < c; ++ch) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const float* pg = g_out + (i * c + ch) * hw;
+      const float* ph = xhat + (i * c + ch) * hw;
+      for (int64_t p = 0; p < hw; ++p) {
+        s1 += pg[p];
+        s2 += (double)pg[p] * (double)ph[p];
+      }
+    }
+    grad_beta[ch] = (float)s1;
+    grad_gamma[ch] = (float)s2;
+    const double coeff = (double)gamma[ch] * invstd[ch];
+    for (int64_t i = 0; i < n; ++i) {
+      const float* pg = g_out + (i * c + ch) * hw;
+      const float* ph = xhat + (i * c + ch) * hw;
+      float* pi = g_in + (i * c + ch) * hw;
+      for (int64_t p = 0; p < hw; ++p)
+        pi[p] = (float)(coeff * ((double)pg[p] - s1 / m - (double)ph[p] * s2 / m));
+    }
+  }
+}
+
+/* Pool2d::forward (layers.cpp:349-391) with EXT zero-cost padding for max
+ * pooling (padded taps never win; the reference Pool2d has no padding,
+ * SURVEY.md A.3-5).  kind 0 = max (strict '>' keeps the first maximum; argmax
+ * is the flat index h*W+w inside the (n,c) plane), 1 = average (double sum
+ * over the window in (ki,kj) order / (k*k)).  floor-mode output size. */
+int or_pool_forward(const float* x, int64_t n, int64_t c, int64_t h, int64_t w, int kind, int64_t k, int64_t s,
+                    int64_t pad, float* y, int64_t* argmax) {
+  if (k < 1 || s < 1 || pad < 0 || h + 2 * pad < k || w + 2 * pad < k || (kind == 1 && pad)) return OR_EINVAL;
+  const int64_t oh = (h + 2 * pad - k) / s + 1, ow = (w + 2 * pad - k) / s + 1;
+  for (int64_t i = 0; i < n * c; ++i) {
+    const float* px = x + i * h * w;
+    float* py = y + i * oh * ow;
+    for (int64_t a = 0; a < oh; ++a)
+      for (int64_t b = 0; b < ow; ++b) {
+        if (kind == 0) {
+          float best = -INFINITY;
+          int64_t best_idx = 0;
+          for (int64_t ki = 0; ki < k; ++ki)
+            for (int64_t kj = 0; kj < k; ++kj) {
+              const int64_t ih = a * s + ki - pad, iw = b * s + kj - pad;
+              if (ih < 0 || ih >= h || iw < 0 || iw >= w) continue;
+              const int64_t idx = ih * w + iw;
+              if (px[idx] > best) {
+                best = px[idx];
+                best_idx = idx;
+              }
+            }
+          py[a * ow + b] = best;
+          if (argmax) argmax[i * oh * ow + a * ow + b] = best_idx;
+        } else {
+          double acc = 0.0;
+          for (int64_t ki = 0; ki < k; ++ki)
+            for (int64_t kj = 0; kj < k; ++kj) acc += px[(a * s + ki) * w + (b * s + kj)];
+          py[a * ow + b] = (float)(acc / (double)(k * k));
+        }
+      }
+  }
+  return OR_OK;
+}
+
+/* Pool2d::backward (layers.cpp:393-415): float scatter-add in loop order. */
+int or_pool_backward(const float* g_out, const int64_t* argmax, int64_t n, int64_t c, int64_t h, int64_t w, int kind,
+                     int64_t k, int64_t s, int64_t pad, float* g_in) {
+  if (k < 1 || s < 1 || pad < 0 || h + 2 * pad < k || w + 2 * pad < k || (kind == 1 && pad)) return OR_EINVAL;
+  const int64_t oh = (h + 2 * pad - k) / s + 1, ow = (w + 2 * pad - k) / s + 1;
+  memset(g_in, 0, sizeof(float) * (size_t)(n * c * h * w));
+  for (int64_t i = 0; i < n * c; ++i) {
+    const float* pg = g_out + i * oh * ow;
+    float* pi = g_in + i * h * w;
+    for (int64_t a = 0; a < oh; ++a)
+      for (int64_t b = 0; b < ow; ++b) {
+        if (kind == 0) {
+          pi[argmax[i * oh * ow + a * ow + b]] += pg[a * ow + b];
+        } else {
+          const float share = pg[a * ow + b] / (float)(k * k);
+          for (int64_t ki = 0; ki < k; ++ki)
+            for (int64_t kj = 0; kj < k; ++kj) pi[(a * s + ki) * w + (b * s + kj)] += share;
+        }
+      }
+  }
+  return OR_OK;
+}
+
+/* SoftmaxCrossEntropy::loss_and_grad (layers.cpp:507-529): per row max, a
+ * sequential double sum of exp, log_z, g = float((p - y)/n).  Returns the
+ * mean loss; OR_EINVAL via *status for a label out of range. */
+double or_softmax_ce(const float* logits, int64_t n, int64_t classes, const int32_t* labels, float* g_logits,
+                     int* status) {
+  double total = 0.0;
+  *status = OR_OK;
+  for (int64_t i = 0; i < n; ++i) {
+    if (labels[i] < 0 || labels[i] >= classes) {
+      *status = OR_EINVAL;
+      return 0.0;
+    }
+    const float* row = logits + i * classes;
+    double mx = row[0];
+    for (int64_t c = 1; c < classes; ++c) mx = mx > (double)row[c] ? mx : (double)row[c];
+    double sum = 0.0;
+    for (int64_t c = 0; c < classes; ++c) sum += exp((double)row[c] - mx);
+    const double log_z = mx + log(sum);
+    total += log_z - (double)row[labels[i]];
+    for (int64_t c = 0; c < classes; ++c) {
+      const double p = exp((double)row[c] - log_z);
+      const double yv = (c == labels[i]) ? 1.0 : 0.0;
+      g_logits[i * classes + c] = (float)((p - yv) / (double)n);
+    }
+  }
+  return total / (double)n;
+}
+
+/* Trainer::train_step momentum update (train.cpp:106-111):
+ * buf = float(m*buf + g); w -= float(lr*buf). */
+void or_sgd_momentum_update(float* w, const float* g, float* buf, int64_t n, double lr, double momentum) {
+  for (int64_t i = 0; i < n; ++i) {
+    buf[i] = (float)(momentum * buf[i] + g[i]);
+    w[i] -= (float)(lr * buf[i]);
+  }
+}
+
+/* conv2d_f32 forward (conv.cpp:206-236 through gemm_f32, gemm.cpp:66-82):
+ * per output a double accumulator over r = (c, i, j) ascending (products of
+ * two floats are exact in double, so contraction cannot change the sum);
+ * padding taps contribute +-0.  Used for the FP32 calibration forwards
+ * (train.cpp:29-32).  EXT geometry. */
+int or_conv_fwd_f32(const float* x, const float* w, const or_geom* g, float* z) {
+  int st = or_geom_validate(g);
+  if (st) return st;
+  const int64_t oh = or_out_h(g), ow = or_out_w(g);
+  const int64_t kout = g->depthwise ? g->c : g->k;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < g->n; ++n)
+    for (int64_t ko = 0; ko < kout; ++ko)
+      for (int64_t p = 0; p < oh; ++p)
+        for (int64_t q = 0; q < ow; ++q) {
+          double acc = 0.0;
+          const int64_t c_lo = g->depthwise ? ko : 0, c_hi = g->depthwise ? ko + 1 : g->c;
+          for (int64_t c = c_lo; c < c_hi; ++c)
+            for (int64_t i = 0; i < g->kh; ++i)
+              for (int64_t j = 0; j < g->kw; ++j) {
+                const int64_t ih = p * g->stride_h + i - g->pad_h, iw = q * g->stride_w + j - g->pad_w;
+                if (ih < 0 || ih >= g->h || iw < 0 || iw >= g->w) continue;
+                const int64_t widx = g->depthwise ? (ko * g->kh + i) * g->kw + j
+                                                  : ((ko * g->c + c) * g->kh + i) * g->kw + j;
+                const double a = w[widx];
+                if (a == 0.0) continue;
+                acc += a * (double)x[((n * g->c + c) * g->h + ih) * g->w + iw];
+              }
+          z[((n * kout + ko) * oh + p) * ow + q] = (float)acc;
+        }
+  return OR_OK;
+}

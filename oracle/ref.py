@@ -67,6 +67,26 @@ def lib():
                                           C.POINTER(C.c_uint32), C.POINTER(ClipState), P_F32, P_F32, P_F32, P_F64]
         L.ref_fill_gaussian.argtypes = [P_F32, C.c_int64, C.c_uint64, C.c_double]
         L.ref_fill_gaussian.restype = None
+        VP = C.c_void_p
+        L.ref_model_new.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.POINTER(VP)]
+        L.ref_model_free.argtypes = [VP]
+        L.ref_model_free.restype = None
+        L.ref_model_ntensors.argtypes = [VP]
+        L.ref_model_tensor_info.argtypes = [VP, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int), P_I64]
+        L.ref_model_tensor_get.argtypes = [VP, C.c_int, P_F32]
+        L.ref_model_tensor_set.argtypes = [VP, C.c_int, P_F32]
+        L.ref_model_int8_replace.argtypes = [VP]
+        L.ref_trainer_new.argtypes = [VP, P_F64, P_I64, C.POINTER(VP)]
+        L.ref_trainer_free.argtypes = [VP]
+        L.ref_trainer_free.restype = None
+        L.ref_trainer_calibrate.argtypes = [VP, VP, P_F32, C.c_int64]
+        L.ref_trainer_finish_calibration.argtypes = [VP]
+        L.ref_trainer_refresh.argtypes = [VP]
+        L.ref_train_step.argtypes = [VP, VP, P_F32, C.c_int64, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                     C.c_int64, C.c_int64, P_F64, P_F64]
+        L.ref_trainer_quant_state.argtypes = [VP, C.c_int, P_F32, C.POINTER(ClipState)]
+        L.ref_save_checkpoint.argtypes = [VP, C.c_char_p]
+        L.ref_load_checkpoint.argtypes = [VP, C.c_char_p]
         _lib = L
     return _lib
 
@@ -159,3 +179,91 @@ def conv_layer_step(gv, weight, x, g_out, it, stream, cs: ClipState, period=100,
                                      grid, rounds, C.byref(s), C.byref(cs), z.reshape(-1), gw.reshape(-1),
                                      ga.reshape(-1), stats))
     return z, gw, ga, s.value, stats
+
+
+# ---------------------------------------------------------------- Model / Trainer / checkpoint (train.cpp)
+FORMS = {"exp": 0, "linear": 1, "quadratic": 2}
+
+
+class RefModel:
+    """A reference Model (models.cpp, or the probe's res_s1 / mbv2_s1)."""
+
+    def __init__(self, name, seed=1, side=32, classes=10):
+        self.h = C.c_void_p()
+        _check(lib().ref_model_new(name.encode(), seed, side, classes, C.byref(self.h)))
+        self.name, self.side, self.classes = name, side, classes
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_model_free(self.h)
+
+    def tensors(self) -> dict:
+        out = {}
+        L = lib()
+        for i in range(L.ref_model_ntensors(self.h)):
+            nb = C.create_string_buffer(256)
+            rank = C.c_int()
+            dims = np.zeros(8, np.int64)
+            _check(L.ref_model_tensor_info(self.h, i, nb, 256, C.byref(rank), dims))
+            t = np.empty(tuple(int(d) for d in dims[:rank.value]), np.float32)
+            _check(L.ref_model_tensor_get(self.h, i, t.reshape(-1)))
+            out[nb.value.decode()] = t
+        return out
+
+    def set_tensors(self, values: dict):
+        L = lib()
+        names = list(self.tensors().keys())
+        for i, name in enumerate(names):
+            if name in values:
+                _check(L.ref_model_tensor_set(self.h, i, f32(values[name]).reshape(-1)))
+
+    def int8_replace(self) -> int:
+        return lib().ref_model_int8_replace(self.h)
+
+    def save(self, path):
+        _check(lib().ref_save_checkpoint(self.h, path.encode()))
+
+    def load(self, path):
+        rc = lib().ref_load_checkpoint(self.h, path.encode())
+        if rc:
+            raise RuntimeError("reference load_checkpoint failed")
+
+
+class RefTrainer:
+    """The reference Trainer (train.cpp:12-120) on a RefModel."""
+
+    def __init__(self, model: RefModel, base_lr=0.1, momentum=0.0, alpha=20.0, beta=0.1, mode="int8",
+                 schedule="cosine", lr_scaling=True, clip_enabled=True, clip_period=100, seed=1, grid=32, rounds=2,
+                 form="exp"):
+        self.model = model
+        self.h = C.c_void_p()
+        cfg = np.array([base_lr, momentum, alpha, beta], np.float64)
+        icfg = np.array([int(mode == "int8"), int(schedule == "constant"), int(lr_scaling), int(clip_enabled),
+                         clip_period, seed, grid, rounds, FORMS[form]], np.int64)
+        _check(lib().ref_trainer_new(model.h, cfg, icfg, C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_trainer_free(self.h)
+
+    def calibrate(self, images):
+        _check(lib().ref_trainer_calibrate(self.h, self.model.h, f32(images).reshape(-1), images.shape[0]))
+
+    def finish_calibration(self):
+        _check(lib().ref_trainer_finish_calibration(self.h))
+
+    def refresh_wa_clips(self):
+        _check(lib().ref_trainer_refresh(self.h))
+
+    def train_step(self, images, labels, it, total, n_quant):
+        out = np.zeros(3, np.float64)
+        st = np.zeros(5 * max(n_quant, 1), np.float64)
+        _check(lib().ref_train_step(self.h, self.model.h, f32(images).reshape(-1), images.shape[0],
+                                    np.ascontiguousarray(labels, np.int32), it, total, out, st))
+        return dict(loss=out[0], diverged=bool(out[1]), base_lr_t=out[2], layers=st.reshape(-1, 5)[:n_quant])
+
+    def quant_state(self, i):
+        f = np.zeros(3, np.float32)
+        cs = ClipState()
+        _check(lib().ref_trainer_quant_state(self.h, i, f, C.byref(cs)))
+        return f, cs

@@ -8,13 +8,21 @@
 // for bench.py's cpu_baseline / --impl reference arm.  No reference source is
 // copied into this repo; this file only calls the reference's public API.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
 #include <vector>
 
+#include <memory>
+#include <string>
+
+#include "i8t/checkpoint.hpp"
 #include "i8t/clip.hpp"
 #include "i8t/conv.hpp"
+#include "i8t/dataset.hpp"
+#include "i8t/models.hpp"
+#include "i8t/train.hpp"
 #include "i8t/gemm.hpp"
 #include "i8t/layers.hpp"
 #include "i8t/lr_scale.hpp"
@@ -260,4 +268,181 @@ void ref_fill_gaussian(float* x, int64_t n, uint64_t seed, double stddev) {
   for (int64_t i = 0; i < n; ++i) x[i] = static_cast<float>(r.next_gaussian() * stddev);
 }
 
+
+// ---------------------------------------------------------------------------
+// Model / Trainer / checkpoint probe over the reference's own classes
+// (models.cpp, train.cpp, checkpoint.cpp).  Models: the reference's
+// build_model names, plus two nets composed here from the reference's public
+// Layer classes with only the geometry the reference accepts (stride 1):
+//   "res_s1"  stem conv3x3(3->8) bn relu, ResidualBlock(8,8,1),
+//             ResidualBlock(8,16,1) (projection shortcut), gap, fc(16)
+//   "mbv2_s1" stem conv3x3(3->8) bn relu, InvertedResidual(8,12,1,2),
+//             InvertedResidual(12,12,1,2), head conv1x1(12->16) bn relu, gap, fc(16)
+// gap = Pool2d(avg, side, side) over the (side x side) input plane.
+
+int ref_model_new(const char* name, uint64_t seed, int side, int classes, void** out) {
+  return guard([&] {
+    std::string nm(name);
+    auto m = std::make_unique<Model>();
+    if (nm == "res_s1" || nm == "mbv2_s1") {
+      InitRng rng(seed);
+      m->name = nm;
+      m->input_shape = Shape{3, side, side};
+      m->num_classes = classes;
+      m->net = std::make_unique<Sequential>();
+      m->net->add("stem", std::make_unique<Conv2d>(3, 8, 3, 1, 1, false, rng));
+      m->net->add("stem_bn", std::make_unique<BatchNorm2d>(8));
+      m->net->add("stem_relu", std::make_unique<ReLU>());
+      int64_t last = 16;
+      if (nm == "res_s1") {
+        m->net->add("block1", std::make_unique<ResidualBlock>(8, 8, 1, rng));
+        m->net->add("block2", std::make_unique<ResidualBlock>(8, 16, 1, rng));
+      } else {
+        m->net->add("block1", std::make_unique<InvertedResidual>(8, 12, 1, 2, rng));
+        m->net->add("block2", std::make_unique<InvertedResidual>(12, 12, 1, 2, rng));
+        m->net->add("head", std::make_unique<Conv2d>(12, 16, 1, 1, 0, false, rng));
+        m->net->add("head_bn", std::make_unique<BatchNorm2d>(16));
+        m->net->add("head_relu", std::make_unique<ReLU>());
+      }
+      m->net->add("gap", std::make_unique<Pool2d>(PoolKind::kAvg, side, side));
+      m->net->add("fc", std::make_unique<Dense>(last, classes, rng));
+    } else {
+      *m = build_model(nm, seed, 3 * 32 * 32, classes);
+    }
+    *out = m.release();
+  });
+}
+
+void ref_model_free(void* m) { delete static_cast<Model*>(m); }
+
+namespace {
+std::vector<std::pair<std::string, Tensor*>> model_tensors(Model* m) {
+  std::vector<std::pair<std::string, Tensor*>> out;
+  for (auto& [path, layer] : m->leaves()) {
+    for (ParamRef p : layer->params()) out.emplace_back(path + "." + p.name, p.value);
+    for (ParamRef p : layer->buffers()) out.emplace_back(path + "." + p.name, p.value);
+  }
+  return out;
+}
+}  // namespace
+
+int ref_model_ntensors(void* m) { return static_cast<int>(model_tensors(static_cast<Model*>(m)).size()); }
+
+// name (NUL-terminated, truncated to cap), rank and dims[<=4] of tensor i
+int ref_model_tensor_info(void* m, int i, char* name, int cap, int* rank, int64_t* dims) {
+  return guard([&] {
+    auto t = model_tensors(static_cast<Model*>(m)).at(static_cast<size_t>(i));
+    std::snprintf(name, static_cast<size_t>(cap), "%s", t.first.c_str());
+    *rank = t.second->shape().rank();
+    for (int d = 0; d < *rank; ++d) dims[d] = t.second->shape()[d];
+  });
+}
+
+int ref_model_tensor_get(void* m, int i, float* out) {
+  return guard([&] {
+    Tensor* t = model_tensors(static_cast<Model*>(m)).at(static_cast<size_t>(i)).second;
+    std::memcpy(out, t->data(), sizeof(float) * static_cast<size_t>(t->numel()));
+  });
+}
+
+int ref_model_tensor_set(void* m, int i, const float* in) {
+  return guard([&] {
+    Tensor* t = model_tensors(static_cast<Model*>(m)).at(static_cast<size_t>(i)).second;
+    std::memcpy(t->data(), in, sizeof(float) * static_cast<size_t>(t->numel()));
+  });
+}
+
+int ref_model_int8_replace(void* m) { return int8_replace(*static_cast<Model*>(m)->net); }
+
+// cfg = {base_lr, momentum, alpha, beta}; icfg = {mode(0 fp32/1 int8), constant schedule, lr_scaling_enabled,
+//        clip_enabled, clip_period, seed, grid, rounds, form}
+int ref_trainer_new(void* m, const double* cfg, const int64_t* icfg, void** out) {
+  return guard([&] {
+    TrainConfig tc;
+    tc.base_lr = cfg[0];
+    tc.momentum = cfg[1];
+    tc.lr_scale.alpha = cfg[2];
+    tc.lr_scale.beta = cfg[3];
+    tc.mode = icfg[0] ? Mode::kInt8 : Mode::kFp32;
+    tc.schedule = icfg[1] ? LrSchedule::kConstant : LrSchedule::kCosine;
+    tc.lr_scaling_enabled = icfg[2] != 0;
+    tc.clip_enabled = icfg[3] != 0;
+    tc.clip_period = icfg[4];
+    tc.seed = static_cast<uint64_t>(icfg[5]);
+    tc.clip_search.grid_resolution = static_cast<int>(icfg[6]);
+    tc.clip_search.refine_rounds = static_cast<int>(icfg[7]);
+    tc.lr_scale.form = static_cast<ScaleForm>(icfg[8]);
+    tc.threads = 0;
+    *out = new Trainer(*static_cast<Model*>(m), tc);
+  });
+}
+
+void ref_trainer_free(void* t) { delete static_cast<Trainer*>(t); }
+
+int ref_trainer_calibrate(void* t, void* m, const float* images, int64_t n) {
+  return guard([&] {
+    Model* mm = static_cast<Model*>(m);
+    Shape s{n, mm->input_shape[0], mm->input_shape[1], mm->input_shape[2]};
+    static_cast<Trainer*>(t)->calibrate(shaped(images, s));
+  });
+}
+
+int ref_trainer_finish_calibration(void* t) { return guard([&] { static_cast<Trainer*>(t)->finish_calibration(); }); }
+int ref_trainer_refresh(void* t) { return guard([&] { static_cast<Trainer*>(t)->refresh_wa_clips(); }); }
+
+// one Trainer::train_step; out = {loss, diverged, base_lr_t}; layer_stats[5*L] = {dc, clip, lr_scale, eps, ghat2}
+int ref_train_step(void* t, void* m, const float* images, int64_t n, const int32_t* labels, int64_t iter,
+                   int64_t total, double* out, double* layer_stats) {
+  return guard([&] {
+    Model* mm = static_cast<Model*>(m);
+    Shape s{n, mm->input_shape[0], mm->input_shape[1], mm->input_shape[2]};
+    std::vector<int32_t> lab(labels, labels + n);
+    StepReport r = static_cast<Trainer*>(t)->train_step(shaped(images, s), lab, iter, total);
+    out[0] = r.loss;
+    out[1] = r.diverged ? 1.0 : 0.0;
+    out[2] = r.base_lr_t;
+    for (size_t i = 0; i < r.layers.size(); ++i) {
+      layer_stats[5 * i + 0] = r.layers[i].dc;
+      layer_stats[5 * i + 1] = r.layers[i].clip;
+      layer_stats[5 * i + 2] = r.layers[i].lr_scale;
+      layer_stats[5 * i + 3] = r.layers[i].eps_norm;
+      layer_stats[5 * i + 4] = r.layers[i].ghat_sqnorm;
+    }
+  });
+}
+
+// QuantState of quantised layer i: f = {clip_w, clip_a, pending_amax}, clip state
+int ref_trainer_quant_state(void* t, int i, float* f, RefClipState* cs) {
+  return guard([&] {
+    Layer* l = static_cast<Trainer*>(t)->quant_layers().at(static_cast<size_t>(i)).second;
+    QuantState* qs = l->quant_state();
+    f[0] = qs->clip_w;
+    f[1] = qs->clip_a;
+    f[2] = qs->pending_amax;
+    cs->clip = qs->clip_state.clip;
+    cs->last_dc = qs->clip_state.last_dc;
+    cs->iter_of_last_update = qs->clip_state.iter_of_last_update;
+    cs->period = qs->clip_state.period;
+  });
+}
+
+int ref_save_checkpoint(void* m, const char* path) {
+  return guard([&] { save_checkpoint(*static_cast<Model*>(m), path); });
+}
+int ref_load_checkpoint(void* m, const char* path) {
+  return guard([&] { load_checkpoint(*static_cast<Model*>(m), path); });
+}
+
 }  // extern "C"
+
+// dataset.cpp does not compile, and the probe never loads a
+// dataset; train.cpp's run_training/evaluate reference these two members, so
+// the probe defines them (its own code) to fail loudly if ever reached.
+namespace i8t {
+Tensor Dataset::gather(const std::vector<int64_t>&) const {
+  throw std::logic_error("ref_capi: datasets are outside the probe");
+}
+std::vector<int32_t> Dataset::gather_labels(const std::vector<int64_t>&) const {
+  throw std::logic_error("ref_capi: datasets are outside the probe");
+}
+}  // namespace i8t

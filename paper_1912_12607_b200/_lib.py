@@ -108,5 +108,11 @@ def check(rc: int, what: str = ""):
     raise I8tError(f"{what}: status {rc}: {msg}")
 
 
+def _arg(a):
+    # device tensors are passed by their data pointer; the caller's argument
+    # tuple owns them until the call (and the launch it enqueues) has returned
+    return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else a
+
+
 def call(name: str, *args):
-    check(getattr(lib(), name)(*args), name)
+    check(getattr(lib(), name)(*(_arg(a) for a in args)), name)

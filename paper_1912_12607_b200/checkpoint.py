@@ -4,9 +4,13 @@
   u32 n_tensors, u32 n_clip; tensor records (name, rank, u32 dims, f32
   payload) for every parameter and buffer of every leaf, sorted by name;
   clip records (name, f32 clip, f64 last_dc, i64 iter_of_last_update, i64
-  period, f32 clip_w, f32 clip_a).  Version 1 is the reference's layout.
-  Version 2 (default) appends what exact resume needs and v1 lacks: the LCG
-  gradient-stream state and the iteration counter.
+  period, f32 clip_w, f32 clip_a).  Version 1 (default) is the reference's
+  layout byte for byte (Dense weights are [out, in] like layers.cpp:132), so
+  either side loads the other's files.  What exact resume needs and v1
+  lacks -- the LCG gradient-stream state, the iteration counter and the
+  momentum buffers -- goes to a sidecar file "<path>.resume" (or, with
+  version=2, after the clip records of the same file; the reference rejects
+  version 2).
 * Trace CSV (csv.cpp:8-27): header row, one row per iteration
   per quantised layer: run_id, iter, layer, loss, dc, clip, lr_scale,
   eps_norm, ghat_sqnorm; floats with 9 significant digits, LF endings.
@@ -32,7 +36,19 @@ def _tensors(trainer):
     return dict(sorted(out.items(), key=lambda kv: kv[0].encode()))
 
 
-def save_checkpoint(trainer, path: str, iteration: int = 0, version: int = 2):
+RESUME_MAGIC = b"I8RS"
+
+
+def _resume_blob(trainer, iteration):
+    mom = trainer.mflat
+    head = struct.pack("<Iq", int(trainer.grad_stream.item()) & 0xFFFFFFFF, iteration)
+    body = struct.pack("<q", 0 if mom is None else mom.numel())
+    if mom is not None:
+        body += mom.cpu().numpy().tobytes()
+    return head, body
+
+
+def save_checkpoint(trainer, path: str, iteration: int = 0, version: int = 1, resume: bool = True):
     tensors = _tensors(trainer)
     views = trainer.arena.read_views()
     with open(path, "wb") as f:
@@ -49,13 +65,18 @@ def save_checkpoint(trainer, path: str, iteration: int = 0, version: int = 2):
             f.write(struct.pack("<I", len(nb)) + nb)
             f.write(struct.pack("<fdqqff", v.clip, v.last_dc, v.iter_of_last_update, v.period,
                                 float(qs.clip_w.item()), float(qs.clip_a.item())))
+        head, body = _resume_blob(trainer, iteration)
         if version >= 2:
-            f.write(struct.pack("<Iq", int(trainer.grad_stream.item()) & 0xFFFFFFFF, iteration))
+            f.write(head)
+    if version == 1 and resume:
+        with open(path + ".resume", "wb") as r:
+            r.write(RESUME_MAGIC + head + body)
 
 
 def load_checkpoint(trainer, path: str) -> int:
-    """Restores parameters, buffers, clip states (and for v2 the LCG state);
-    returns the saved iteration (0 for v1)."""
+    """Restores parameters, buffers, clip states (and for v2, or a v1 file
+    with its .resume sidecar, the LCG state and momentum); returns the saved
+    iteration (0 for a bare v1 file, e.g. one the reference wrote)."""
     tensors = _tensors(trainer)
     by_layer = {p: l for p, l in trainer.quant_layers}
     idx = {p: i for i, (p, _) in enumerate(trainer.quant_layers)}
@@ -96,6 +117,19 @@ def load_checkpoint(trainer, path: str) -> int:
         if version >= 2:
             state, it = struct.unpack("<Iq", f.read(12))
             trainer.grad_stream.fill_(struct.unpack("<i", struct.pack("<I", state))[0])
+    side = path + ".resume"
+    import os
+    if version == 1 and os.path.exists(side):
+        with open(side, "rb") as r:
+            if r.read(4) != RESUME_MAGIC:
+                raise RuntimeError("checkpoint: bad resume sidecar")
+            state, it = struct.unpack("<Iq", r.read(12))
+            trainer.grad_stream.fill_(struct.unpack("<i", struct.pack("<I", state))[0])
+            (nm,) = struct.unpack("<q", r.read(8))
+            if nm:
+                if trainer.mflat is None or trainer.mflat.numel() != nm:
+                    raise RuntimeError("checkpoint: momentum buffer does not match the trainer")
+                trainer.mflat.copy_(torch.frombuffer(bytearray(r.read(4 * nm)), dtype=torch.float32))
     return it
 
 

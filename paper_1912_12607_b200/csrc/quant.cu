@@ -225,12 +225,26 @@ __global__ void __launch_bounds__(256) k_sgd_dclr(float* __restrict__ w, const f
 }
 
 // Segmented SGD+DCLR over flat arenas: one launch for every parameter.
+// lr = base_lr (or *lr_dev) * phi_layer; momentum (train.cpp:106-111):
+//   buf = float(m*buf + g)  (the reference's GNU build contracts m*buf + g to one FMA)
+//   w  -= float(lr*buf)
+__device__ __forceinline__ float sgd_elem(float w, float g, float* buf, double lr, double m) {
+  if (buf) {
+    const float b = static_cast<float>(fma(m, static_cast<double>(*buf), static_cast<double>(g)));
+    *buf = b;
+    g = b;
+  }
+  return w - static_cast<float>(lr * static_cast<double>(g));
+}
+
 __global__ void __launch_bounds__(256) k_sgd_dclr_multi(float* __restrict__ w, const float* __restrict__ grad,
                                                         int nseg, const int64_t* __restrict__ seg_off,
                                                         const void* const* __restrict__ seg_state, double base_lr,
-                                                        const int32_t* skip) {
+                                                        const double* __restrict__ lr_dev, const int32_t* skip,
+                                                        float* __restrict__ mom, double momentum) {
   pdl_entry();
   if (skip && *skip) return;
+  if (lr_dev) base_lr = *lr_dev;
   const int64_t n4 = seg_off[nseg] / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 4;
@@ -244,10 +258,19 @@ __global__ void __launch_bounds__(256) k_sgd_dclr_multi(float* __restrict__ w, c
     const double lr = st ? base_lr * st->v.lr_scale : base_lr;
     float4 a = reinterpret_cast<float4*>(w)[i];
     const float4 g = __ldg(reinterpret_cast<const float4*>(grad) + i);
-    a.x -= static_cast<float>(lr * static_cast<double>(g.x));
-    a.y -= static_cast<float>(lr * static_cast<double>(g.y));
-    a.z -= static_cast<float>(lr * static_cast<double>(g.z));
-    a.w -= static_cast<float>(lr * static_cast<double>(g.w));
+    if (mom) {
+      float4 b = reinterpret_cast<float4*>(mom)[i];
+      a.x = sgd_elem(a.x, g.x, &b.x, lr, momentum);
+      a.y = sgd_elem(a.y, g.y, &b.y, lr, momentum);
+      a.z = sgd_elem(a.z, g.z, &b.z, lr, momentum);
+      a.w = sgd_elem(a.w, g.w, &b.w, lr, momentum);
+      reinterpret_cast<float4*>(mom)[i] = b;
+    } else {
+      a.x = sgd_elem(a.x, g.x, nullptr, lr, 0.0);
+      a.y = sgd_elem(a.y, g.y, nullptr, lr, 0.0);
+      a.z = sgd_elem(a.z, g.z, nullptr, lr, 0.0);
+      a.w = sgd_elem(a.w, g.w, nullptr, lr, 0.0);
+    }
     reinterpret_cast<float4*>(w)[i] = a;
   }
 }
@@ -417,12 +440,15 @@ int i8t_sgd_dclr(i8t_ctx* ctx, float* w, const float* grad, int64_t n, double ba
 }
 
 int i8t_sgd_dclr_multi(i8t_ctx* ctx, float* w, const float* grad, int nseg, const int64_t* seg_off,
-                       const void* const* seg_state, double base_lr, const int32_t* skip) {
+                       const void* const* seg_state, double base_lr, const double* lr_dev, const int32_t* skip,
+                       float* mom, double momentum) {
   Ctx* c = CTX(ctx);
   if (!c || !w || !grad || nseg < 1 || !seg_off || !seg_state) return set_error(I8T_EINVAL, "sgd_multi: bad arguments");
   if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(grad)) & 15u)
     return set_error(I8T_EUNSUPPORTED, "sgd_multi: arenas must be 16-byte aligned");
-  launch_k(k_sgd_dclr_multi, 148 * 8, 256, 0, c->stream, w, grad, nseg, seg_off, seg_state, base_lr, skip);
+  if (reinterpret_cast<uintptr_t>(mom) & 15u) return set_error(I8T_EUNSUPPORTED, "sgd_multi: momentum arena must be 16-byte aligned");
+  launch_k(k_sgd_dclr_multi, 148 * 8, 256, 0, c->stream, w, grad, nseg, seg_off, seg_state, base_lr, lr_dev, skip,
+           mom, momentum);
   count_launch(1);
   return cuda_check("k_sgd_dclr_multi");
 }

@@ -320,6 +320,13 @@ class Layer:
         fn(prefix, self)
 
 
+def _dp_max_(t: torch.Tensor):
+    """MAX all-reduce across data-parallel ranks (no-op on one process)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+
+
 def _kaiming(shape, fan_in, gen, device):
     return (torch.randn(shape, generator=gen, device="cpu") * math.sqrt(2.0 / fan_in)).to(device)
 
@@ -415,14 +422,17 @@ class Conv2d(Layer):
             y = F.conv2d(xc, self.weight, None, (self.sh, self.sw), (self.ph, self.pw),
                          groups=self.in_c if self.depthwise else 1)
             return y.permute(0, 2, 3, 1).contiguous()
-        # lazy clip init: clip = max(max_abs(t), 1e-12) (layers.cpp:106-107)
+        # lazy clip init: clip = max(max_abs(t), 1e-12) (layers.cpp:106-107); under data
+        # parallelism the max is over the global batch, so every rank quantises with one scale
         if not qs.clip_w_set:
             call("i8t_max_abs", h, ops._p(self.weight), self.weight.numel(), ops._p(qs.clip_w))
             qs.clip_w.clamp_(min=1e-12)
+            _dp_max_(qs.clip_w)
             qs.clip_w_set = True
         if not qs.clip_a_set and not fuse_in:
             call("i8t_max_abs", h, ops._p(x), x.numel(), ops._p(qs.clip_a))
             qs.clip_a.clamp_(min=1e-12)
+            _dp_max_(qs.clip_a)
             qs.clip_a_set = True
         # weights -> KRSC (fwd) + CRSK (dgrad) int8 in one pass (or all layers at once, see wq_desc)
         if self.depthwise:
@@ -603,7 +613,10 @@ class Dense(Layer):
         self.conv.set_quantized(on)
 
     def params(self):
-        return [ParamRef("weight", self.conv.weight, self.conv.grad_weight), ParamRef("bias", self.bias, self.grad_bias)]
+        # [out, in] like the reference's Dense weight (layers.cpp:132): checkpoints interoperate
+        return [ParamRef("weight", self.conv.weight.view(self.out_f, self.in_f),
+                         self.conv.grad_weight.view(self.out_f, self.in_f)),
+                ParamRef("bias", self.bias, self.grad_bias)]
 
     def param_attrs(self):
         return [(self.conv, "weight", "grad_weight"), (self, "bias", "grad_bias")]
@@ -961,13 +974,14 @@ class SoftmaxCrossEntropy:
     loss as a 0-d CUDA double tensor and g_logits = float((p - y) / N)."""
 
     @staticmethod
-    def loss_and_grad(logits: torch.Tensor, labels: torch.Tensor):
-        n = logits.shape[0]
+    def loss_and_grad(logits: torch.Tensor, labels: torch.Tensor, total_n: int | None = None):
+        """total_n: the global batch under data parallelism (default: local)."""
+        n = logits.shape[0] if total_n is None else total_n
         ld = logits.double()
         logz = torch.logsumexp(ld, dim=1)
         loss = (logz - ld.gather(1, labels.view(-1, 1)).squeeze(1)).sum() / n
         p = torch.exp(ld - logz.view(-1, 1))
-        p[torch.arange(n, device=logits.device), labels] -= 1.0
+        p[torch.arange(logits.shape[0], device=logits.device), labels] -= 1.0
         return loss, (p / n).float()
 
 

@@ -52,20 +52,13 @@ def launch_count() -> int:
     return int(lib().i8t_launch_count())
 
 
-_KEEP: list = [None] * 256  # ring keeping pointer-donor tensors alive until their call is enqueued
-_KEEP_I = 0
-
-
 def _p(t: torch.Tensor | None):
-    """Device pointer of t.  Temporaries created inline in a call expression
-    (e.g. _p(_dev_f32(clip))) would otherwise be freed -- and their block
-    reused by the next temporary -- before the C call runs."""
-    global _KEEP_I
-    if t is None:
-        return None
-    _KEEP[_KEEP_I] = t
-    _KEEP_I = (_KEEP_I + 1) % len(_KEEP)
-    return C.c_void_p(t.data_ptr())
+    """A device-pointer argument of `call`: the tensor itself (None = NULL).
+    `call` converts it to its data pointer while its own argument tuple keeps
+    the tensor alive, so temporaries created inline (``_p(_dev_f32(clip))``)
+    live until the launch they feed has been enqueued; the stream-ordered
+    caching allocator makes any later reuse safe."""
+    return t
 
 
 def _dev_f32(v, device=None) -> torch.Tensor:

@@ -45,7 +45,7 @@ class TrainConfig:
     batch_size: int = 64
     epochs: int = 5
     calibration_batches: int = 2
-    momentum: float = 0.0
+    momentum: float = 0.0  # SGD momentum (train.cpp:106-111), one flat device buffer per trainer
 
 
 @dataclass
@@ -120,7 +120,10 @@ class Trainer:
         self.skip = torch.zeros(1, dtype=torch.int32, device=device)
         self._wq_buf, self._wq_n = None, 0  # device i8t_wq_desc array (built at the second step)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
+        self.lr_dev = torch.zeros(1, dtype=torch.float64, device=device)
         self._build_param_arenas(device)
+        if self.world > 1:  # identical initial parameters on every rank (seeded alike; made certain)
+            dist.broadcast(self.pflat, 0)
 
     def _build_param_arenas(self, device):
         """Every parameter / gradient becomes a view into one flat arena
@@ -147,6 +150,8 @@ class Trainer:
         self.seg_off = torch.tensor(offs, dtype=torch.int64, device=device)
         self.seg_state = torch.tensor(states, dtype=torch.int64, device=device)
         self.nseg = len(segs)
+        # Trainer::momentum_ (train.cpp:22-26): zero-initialised, one buffer per parameter
+        self.mflat = torch.zeros(total, dtype=torch.float32, device=device) if cfg.momentum != 0.0 else None
 
     # ---------------------------------------------------------------- clips
     def calibrate(self, images):
@@ -157,7 +162,11 @@ class Trainer:
         self.refresh_wa_clips()
 
     def refresh_wa_clips(self):
-        """clip_w = max_abs(W), clip_a = running max of batch maxima (train.cpp:36-46), on the device."""
+        """clip_w = max_abs(W) if > 0, clip_a = running max of batch maxima if >
+        0, pending_amax reset (train.cpp:36-46), on the device.  A clip left at
+        0 (all-zero weights, no calibration batch) keeps its flag clear so the
+        forward's lazy max(max_abs, 1e-12) initialisation (layers.cpp:106-107)
+        still runs.  One host read for all layers decides the flags."""
         h = ops.ctx()
         for _, layer in self.quant_layers:
             qs = layer.qs
@@ -168,8 +177,11 @@ class Trainer:
             qs.clip_w.copy_(torch.where(qs.tmp > 0, qs.tmp, qs.clip_w))
             qs.clip_a.copy_(torch.where(qs.pending_amax > 0, qs.pending_amax, qs.clip_a))
             qs.pending_amax.zero_()
-            qs.clip_w_set = True
-            qs.clip_a_set = qs.clip_a_set or True
+        if self.quant_layers:
+            clips = torch.stack([torch.cat([l.qs.clip_w, l.qs.clip_a]) for _, l in self.quant_layers]).cpu()
+            for (_, layer), (cw, ca) in zip(self.quant_layers, clips.tolist()):
+                layer.qs.clip_w_set = cw > 0
+                layer.qs.clip_a_set = ca > 0
 
     def base_lr_at(self, it, total):
         """cosine schedule (train.cpp:48-52)."""
@@ -184,8 +196,13 @@ class Trainer:
         rep = StepReport(iter=it, base_lr_t=self.base_lr_at(it, total_iters))
         wq = cfg.mode == Mode.INT8 and self._quantize_weights_at_once()
         logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8, wq))
-        loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels)
+        # data parallel: the mean is over the GLOBAL batch (loss summed across ranks when read)
+        loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels, logits.shape[0] * self.world)
         bad = (~torch.isfinite(loss)) | (~torch.isfinite(logits).all())
+        if self.world > 1:  # every rank takes the same branch
+            bad = bad.to(torch.int32)
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            bad = bad.bool()
         # divergence check before backward (train.cpp:73-77): one host sync per step
         if bool(bad.item()):
             rep.loss, rep.diverged = float(loss.item()), True
@@ -205,9 +222,13 @@ class Trainer:
         # bad-gradient check (train.cpp:87-95) stays on the device and gates the update
         h = ops.ctx()
         call("i8t_nonfinite_flag", h, ops._p(self.gflat), self.gflat.numel(), ops._p(self.skip))
+        self.lr_dev.fill_(rep.base_lr_t)
         call("i8t_sgd_dclr_multi", h, ops._p(self.pflat), ops._p(self.gflat), self.nseg, ops._p(self.seg_off),
-             ops._p(self.seg_state), C.c_double(rep.base_lr_t), ops._p(self.skip))
+             ops._p(self.seg_state), C.c_double(rep.base_lr_t), self.lr_dev, ops._p(self.skip), self.mflat,
+             C.c_double(cfg.momentum))
         if read_stats:
+            if self.world > 1:
+                dist.all_reduce(self.loss_dev, op=dist.ReduceOp.SUM)
             rep.loss = float(self.loss_dev.item())
             rep.diverged = bool(self.skip.item())
             self._read_layer_stats(rep)
