@@ -37,6 +37,9 @@ class ForwardCtx:
     mode: str = "int8"
     training: bool = True
     track_amax: bool = True
+    # teacher(layer, "x", x) -> the input the INT8 layer really sees (teacher
+    # forcing with the GPU's values, tests/test_gpu_step_parity.py); None = own value
+    teacher: object = None
 
 
 @dataclass
@@ -53,6 +56,7 @@ class BackwardCtx:
     form: str = "exp"
     lr_scaling_enabled: bool = True
     hook: object = None  # optional callback(layer, event, **tensors) -- teacher forcing / capture
+    teacher: object = None  # teacher(layer, "g", g) -> the gradient the INT8 layer really sees
 
 
 class QuantState:
@@ -131,6 +135,8 @@ class Conv2d(Layer):
                       int(self.depthwise), 1)
 
     def forward(self, x, ctx: ForwardCtx, hook=None):
+        if ctx.teacher:
+            x = ctx.teacher(self, "x", x)
         g = self.geom(x)
         self._g = g
         use_int8 = self.quantize_enabled and ctx.mode == "int8"
@@ -153,6 +159,8 @@ class Conv2d(Layer):
         return z
 
     def backward(self, g_out, ctx: BackwardCtx):
+        if ctx.teacher:
+            g_out = ctx.teacher(self, "g", g_out)
         qs = self.qs
         stream_in = ctx.stream[0]
         qg, s_g = quantize_gradient(qs, g_out, ctx)
@@ -193,6 +201,8 @@ class Dense(Layer):
         self._in_shape = x.shape
         n = x.shape[0]
         flat = np.ascontiguousarray(x.reshape(n, -1), F32)
+        if ctx.teacher:
+            flat = ctx.teacher(self, "x", flat)
         if flat.shape[1] != self.in_f:
             raise ValueError("Dense: input does not flatten to expected features")
         use_int8 = self.quantize_enabled and ctx.mode == "int8"
@@ -218,6 +228,8 @@ class Dense(Layer):
         return (z + self.bias).astype(F32)
 
     def backward(self, g_out, ctx: BackwardCtx):
+        if ctx.teacher:
+            g_out = ctx.teacher(self, "g", g_out)
         qs = self.qs
         n = g_out.shape[0]
         stream_in = ctx.stream[0]
@@ -488,12 +500,16 @@ class Trainer:
             return self.cfg.base_lr
         return self.cfg.base_lr * 0.5 * (1.0 + math.cos(math.pi * (it / total)))
 
-    def train_step(self, images, labels, it, total, fhook=None, bhook=None):
-        """Returns {loss, diverged, base_lr_t, layers: [(path, dc, clip, lr_scale, eps, ghat2)], g_logits, logits}."""
+    def train_step(self, images, labels, it, total, fhook=None, bhook=None, teacher=None):
+        """Returns {loss, diverged, base_lr_t, layers: [(path, dc, clip, lr_scale, eps, ghat2)], g_logits, logits}.
+        teacher: optional teacher-forcing callback (layer, "x" | "g", value) -> value fed to each
+        INT8 layer's forward / backward, and (None, "g_logits", g) for the loss gradient."""
         cfg = self.cfg
         rep = dict(iter=it, base_lr_t=self.base_lr_at(it, total), diverged=False)
-        logits = self.net.forward(O.f32(images), ForwardCtx(cfg.mode, True, cfg.mode == "int8"), fhook)
+        logits = self.net.forward(O.f32(images), ForwardCtx(cfg.mode, True, cfg.mode == "int8", teacher), fhook)
         loss, g_logits = softmax_ce(logits, labels)
+        if teacher:
+            g_logits = teacher(None, "g_logits", g_logits)
         rep.update(loss=loss, logits=logits, g_logits=g_logits)
 
         def stats():
@@ -504,7 +520,7 @@ class Trainer:
             rep["diverged"] = True
             return stats()
         bctx = BackwardCtx(cfg.mode, it, self.stream, cfg.grid, cfg.rounds, cfg.clip_enabled, cfg.clip_period,
-                           cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled, bhook)
+                           cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled, bhook, teacher)
         self.net.backward(g_logits, bctx)
         for _, l in self.leaves:
             for _, _, gv in l.params():

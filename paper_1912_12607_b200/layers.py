@@ -88,6 +88,11 @@ JOIN_FUSION = os.environ.get("I8T_JOIN", "0") == "1"
 # main-branch gradient; 4 ResNet-50 blocks) pays off: 35.01 -> 34.90 ms per
 # step.  I8T_JOIN_PROJ=0 turns it off.
 JOIN_PROJ = os.environ.get("I8T_JOIN_PROJ", "1") == "1" or JOIN_FUSION
+# Test instrumentation: when set, TRACE(conv, event, **tensors) is called at the
+# end of every INT8 Conv2d forward ("fwd") and backward ("bwd") -- the step-level
+# parity test (tests/test_gpu_step_parity.py) teacher-forces the CPU oracle with
+# these values.  None in production (one attribute test per call).
+TRACE = None
 
 
 class LazyAct:
@@ -472,6 +477,8 @@ class Conv2d(Layer):
         else:
             call("i8t_conv_fwd", h, C.byref(g), ops._p(qa), self.c_pad, ops._p(self._qw), self.ld_w,
                  ops._p(qs.clip_a), ops._p(qs.clip_w), ops._p(z), None)
+        if TRACE is not None:
+            TRACE(self, "fwd", x=None if fuse_in else x, qa=qa, qw=self._qw, z=z, w=self.weight)
         return z
 
     # -- backward (layers.cpp:113-126)
@@ -492,6 +499,7 @@ class Conv2d(Layer):
                                                                (self.ph, self.pw), groups=groups))
             return gi.permute(0, 2, 3, 1).contiguous()
         h = ops.ctx()
+        stream_in = ctx.grad_stream.clone() if TRACE is not None else None
         if fuse_g:  # BN backward computed on the fly inside the stochastic quantiser
             qg = quantize_gradient_bn_layer(self.qs, gz, ctx)
         else:
@@ -547,6 +555,9 @@ class Conv2d(Layer):
                     ops._p(clip_a), ops._p(gw), 1)))
         self._qa = None
         self._qg = qg if self.keep_qg else None
+        if TRACE is not None:
+            TRACE(self, "bwd", g=None if fuse_g else gz, qg=qg, stream_in=stream_in, stream_out=ctx.grad_stream,
+                  ga=ga, gw=self.grad_weight if ctx.wgrad_allreduce is None else None)
         return ga
 
 

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from ._lib import ConvGeom, DsgcView, call, lib
+from ._lib import ConvGeom, DsgcView, I8tError, call, lib  # noqa: F401 (I8tError re-exported)
 
 # --------------------------------------------------------------------------- context
 _ctx = {}

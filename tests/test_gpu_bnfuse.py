@@ -260,7 +260,7 @@ def test_packed_mask_mode3_equals_mode2(ops):
 def test_bn_rejects_bad_shapes(ops):
     z = torch.zeros(10, 6, device="cuda")
     bn = torch.zeros(30, dtype=torch.float64, device="cuda")
-    with pytest.raises(ValueError):
+    with pytest.raises(ops.I8tError, match="c % 4"):  # I8T_EUNSUPPORTED: outside the kernels' envelope
         ops.call("i8t_bn_fwd_stats", ops.ctx(), z, 10, 6, C.c_double(0.1), C.c_double(1e-5), bn, None, None)
 
 
