@@ -853,12 +853,18 @@ class Concat(Layer):
 
 
 class GlobalAvgPool(Layer):
+    """Pool2d(kAvg) over the whole map (layers.cpp:383-388): the window sum is
+    accumulated in double and divided once, float(sum / (h*w)), like the
+    reference.  Its summation order differs from the reference's sequential
+    one only in the last double bits (exact unless the window spans > 2^23 in
+    magnitude), far below the final float rounding."""
     kind = "avgpool"
 
     def forward(self, x, ctx):
         x = dense(x)
         self._shape = x.shape
-        return x.mean(dim=(1, 2))
+        n, h, w, c = x.shape
+        return (torch.sum(x, dim=(1, 2), dtype=torch.float64) / (h * w)).float()
 
     def backward(self, g, ctx):
         g = dense_grad(g)
