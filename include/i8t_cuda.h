@@ -157,6 +157,11 @@ int i8t_dequantize(i8t_ctx* ctx, const int8_t* q, int64_t n, const float* clip, 
 /* Layout helpers for the drop-in path. */
 int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, int64_t hw, int64_t ld_src,
                          float* dst);
+/* im2col_i8 / im2col_channel_i8 (conv.cpp:23-47, 98-106) for channels
+ * [c_lo, c_hi): NCHW int8 x -> col [(c-c_lo)*kh*kw + i*kw + j][n*oh*ow + p*ow + q],
+ * zero padding (the reference's explicit-GEMM operand; the convolutions here
+ * never materialise it -- this is the API function). */
+int i8t_im2col_s8(i8t_ctx* ctx, const int8_t* x, const i8t_conv_geom* g, int64_t c_lo, int64_t c_hi, int8_t* col);
 int i8t_nchw_to_nhwc_i8(i8t_ctx* ctx, const int8_t* src, int64_t n, int64_t c, int64_t hw, int8_t* dst,
                         int64_t c_pad);
 int i8t_kcrs_to_krsc_i8(i8t_ctx* ctx, const int8_t* src, int64_t k, int64_t c, int64_t kh, int64_t kw, int8_t* dst,
@@ -261,6 +266,11 @@ int i8t_conv_dw_wgrad_finalize(i8t_ctx* ctx, const i8t_conv_geom* g, const int64
 /* gemm_i8 (gemm.cpp:18-40): C[m][n] = A[m][k] . B[k][n] exact int32
  * (row-major int8 operands; runs on the tcgen05 path as a 1x1 convolution). */
 int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64_t k, int64_t n, int32_t* c);
+/* gemm_i8_fused_lhs (gemm.cpp:49-64): C = quantize(A, from_clip(*clip), mode
+ * [, stream]) . B on the device, A fp32 row-major (m x k); stochastic draws in
+ * row-major order from *lcg_state (device), advanced by m*k. */
+int i8t_gemm_s8_fused_lhs(i8t_ctx* ctx, const float* a, int64_t m, int64_t k, const float* clip, int stochastic,
+                          uint32_t* lcg_state, const int8_t* b, int64_t n, int32_t* c);
 
 /* ------------------------------------------------------------ optimiser */
 /* SGD step of Trainer::train_step (train.cpp:97-117), momentum 0:

@@ -1318,4 +1318,25 @@ int i8t_gemm_s8(i8t_ctx* ctx, const int8_t* a, const int8_t* b, int64_t m, int64
   return rc;
 }
 
+// gemm_i8_fused_lhs (gemm.cpp:49-64): quantise the fp32 lhs on the device --
+// nearest, or stochastic with the draws in row-major order from the device
+// LCG state (advanced by m*k) -- straight into the GEMM's A operand (an int8
+// copy of m*k bytes that stays in L2 for the GEMM that follows), then the
+// tcgen05 GEMM.  Bit-identical to quantize() + gemm_i8() incl. the stream.
+int i8t_gemm_s8_fused_lhs(i8t_ctx* ctx, const float* a, int64_t m, int64_t k, const float* clip, int stochastic,
+                          uint32_t* lcg_state, const int8_t* b, int64_t n, int32_t* cout) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !a || !b || !cout || !clip || m < 1 || k < 1 || n < 1 || (stochastic && !lcg_state))
+    return set_error(I8T_EINVAL, "gemm_i8_fused_lhs: bad arguments");
+  if (k > 130000) return set_error(I8T_EINVAL, "gemm_i8: depth exceeds i32 overflow bound");
+  int8_t* qa = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&qa), (size_t)(m * k), c->stream) != cudaSuccess)
+    return set_error(I8T_ECUDA, "gemm_i8_fused_lhs: alloc failed");
+  int rc = stochastic ? i8t_quantize_stochastic(ctx, a, m * k, clip, lcg_state, qa)
+                      : i8t_quantize_nearest(ctx, a, m * k, clip, qa, nullptr, 0);
+  if (rc == I8T_OK) rc = i8t_gemm_s8(ctx, qa, b, m, k, n, cout);
+  cudaFreeAsync(qa, c->stream);
+  return rc;
+}
+
 }  // extern "C"

@@ -467,6 +467,12 @@ static int launch_quant_grad(Ctx* c, DsgcState* st, const float* clip_override, 
 using namespace i8t_dev;
 #define CTX(c) reinterpret_cast<Ctx*>(c)
 
+// state <- state advanced by k draws (k mod 2^32; 2^32 - d steps back by d)
+static __global__ void k_lcg_jump(uint32_t* state, uint64_t k) {
+  pdl_entry();
+  *state = apply(lcg_jump_map(k), *state);
+}
+
 extern "C" {
 
 int i8t_max_abs(i8t_ctx* ctx, const float* x, int64_t n, float* out) {
@@ -657,11 +663,31 @@ int i8t_quantize_stochastic(i8t_ctx* ctx, const float* x, int64_t n, const float
   Ctx* c = CTX(ctx);
   if (!c || !x || !clip || !lcg_state || !q) return set_error(I8T_EINVAL, "quantize: stream required iff mode is stochastic");
   if (n == 0) return I8T_OK;
-  if (n % 4 != 0) return set_error(I8T_EUNSUPPORTED, "quantize_stochastic: numel % 4 != 0 (pad on the host)");
   DsgcState* st = reinterpret_cast<DsgcState*>(ensure_scratch(c, sizeof(DsgcState)));
   if (!st) return set_error(I8T_ECUDA, "scratch alloc failed");
   QgFin fin{4, 0.0, 0.0, 0, 0u};
-  return launch_quant_grad(c, st, clip, x, 1, 1, n, false, lcg_state, q, fin);
+  if (n % 4 == 0) return launch_quant_grad(c, st, clip, x, 1, 1, n, false, lcg_state, q, fin);
+  // ragged length: quantise a zero-padded copy (the kernel reads float4s), keep
+  // the first n bytes, then step the stream back over the pad's draws (the LCG
+  // has period 2^32, so a jump of 2^32 - d is d steps back): one draw per element
+  const int64_t np = (n + 3) / 4 * 4;
+  float* xp = nullptr;
+  int8_t* qp = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&xp), sizeof(float) * np, c->stream) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&qp), np, c->stream) != cudaSuccess)
+    return set_error(I8T_ECUDA, "quantize_stochastic: alloc failed");
+  cudaMemcpyAsync(xp, x, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemsetAsync(xp + n, 0, sizeof(float) * (np - n), c->stream);
+  int rc = launch_quant_grad(c, st, clip, xp, 1, 1, np, false, lcg_state, qp, fin);
+  if (rc == I8T_OK) {
+    cudaMemcpyAsync(q, qp, n, cudaMemcpyDeviceToDevice, c->stream);
+    launch_k(k_lcg_jump, 1, 1, 0, c->stream, lcg_state, (uint64_t)((uint64_t(1) << 32) - uint64_t(np - n)));
+    count_launch(1);
+    rc = cuda_check("k_lcg_jump");
+  }
+  cudaFreeAsync(xp, c->stream);
+  cudaFreeAsync(qp, c->stream);
+  return rc;
 }
 
 }  // extern "C"

@@ -263,18 +263,31 @@ Int8Matrix transpose(const Int8Matrix& m) {
   return t;
 }
 
-// Row-at-a-time quantisation draws in the same row-major order as quantizing
-// the whole matrix, so fusing changes nothing (gemm.cpp:49-64).
+// gemm_i8_fused_lhs (gemm.cpp:49-64): the lhs is quantised on the device
+// straight into the GEMM's A operand (i8t_gemm_s8_fused_lhs); stochastic draws
+// run in row-major order from the caller's stream, which is advanced by m*k --
+// bit-identical to quantize() followed by gemm_i8().
 Int32Matrix gemm_i8_fused_lhs(const Tensor& a_rowmajor, const QuantParams& pa, RoundingMode mode, LcgStream* stream,
                               const Int8Matrix& b) {
   if (a_rowmajor.shape().rank() != 2) throw std::invalid_argument("gemm_i8_fused_lhs: lhs must be 2-D");
+  if ((mode == RoundingMode::kStochastic) != (stream != nullptr))
+    throw std::invalid_argument("quantize: stream required iff mode is stochastic");
   const int64_t m = a_rowmajor.shape()[0], k = a_rowmajor.shape()[1];
   if (k != b.rows) throw std::invalid_argument("gemm_i8: inner dimensions do not match");
   if (k > kMaxGemmDepth) throw std::invalid_argument("gemm_i8: depth exceeds i32 overflow bound");
-  QuantizedTensor q = quantize(a_rowmajor, pa, mode, stream);
-  Int8Matrix qa(m, k);
-  qa.data = std::move(q.q);
-  return gemm_i8(qa, b);
+  Int32Matrix c(m, b.cols);
+  if (m == 0 || b.cols == 0 || k == 0) return c;
+  Dev ad(a_rowmajor.data(), sizeof(float) * m * k), bd(b.data.data(), b.data.size()),
+      cd(sizeof(int32_t) * c.data.size());
+  Dev clip = dev_scalar(pa.clip);
+  const uint32_t s0 = stream ? stream->state() : 0u;
+  Dev st(&s0, sizeof(s0));
+  ok(i8t_gemm_s8_fused_lhs(ctx(), ad.as<float>(), m, k, clip.as<float>(), stream ? 1 : 0,
+                           stream ? st.as<uint32_t>() : nullptr, bd.as<int8_t>(), b.cols, cd.as<int32_t>()));
+  sync();
+  cd.to_host(c.data.data(), sizeof(int32_t) * c.data.size());
+  if (stream) stream->seek(read_scalar<uint32_t>(st));
+  return c;
 }
 
 // ================================================================ conv.hpp
@@ -287,21 +300,6 @@ void ConvGeometry::validate() const {
 }
 
 namespace {
-void im2col_range(const int8_t* x, const ConvGeometry& g, int64_t c_lo, int64_t c_hi, int8_t* out) {
-  const int64_t oh = g.out_h(), ow = g.out_w(), cols = g.n * oh * ow;
-  int64_t r = 0;
-  for (int64_t c = c_lo; c < c_hi; ++c)
-    for (int64_t i = 0; i < g.kh; ++i)
-      for (int64_t j = 0; j < g.kw; ++j, ++r)
-        for (int64_t n = 0; n < g.n; ++n)
-          for (int64_t p = 0; p < oh; ++p)
-            for (int64_t q = 0; q < ow; ++q) {
-              const int64_t y = p * g.stride + i - g.pad, xx = q * g.stride + j - g.pad;
-              out[r * cols + (n * oh + p) * ow + q] =
-                  (y >= 0 && y < g.h && xx >= 0 && xx < g.w) ? x[((n * g.c + c) * g.h + y) * g.w + xx] : int8_t(0);
-            }
-}
-
 void check_conv_operands(const QuantizedTensor& a, const QuantizedTensor& w, const ConvGeometry& g) {
   g.validate();
   if (!(a.shape == g.input_shape())) throw std::invalid_argument("conv2d_q: activation shape mismatch");
@@ -321,13 +319,22 @@ std::unique_ptr<Dev> to_nhwc(const std::vector<int8_t>& q, int64_t n, int64_t c,
 }
 }  // namespace
 
-void im2col_i8(const int8_t* x, const ConvGeometry& g, int8_t* out) {
+// im2col (conv.cpp:23-47, 98-106) on the device: host buffers in and out, as
+// the reference's raw-pointer signature requires.
+static void im2col_device(const int8_t* x, const ConvGeometry& g, int64_t c_lo, int64_t c_hi, int8_t* out) {
   g.validate();
-  im2col_range(x, g, 0, g.c, out);
+  if (c_lo < 0 || c_hi > g.c) throw std::invalid_argument("im2col_channel_i8: channel out of range");
+  const int64_t in_bytes = g.n * g.c * g.h * g.w, rows = (c_hi - c_lo) * g.kh * g.kw;
+  const int64_t out_bytes = rows * g.n * g.out_h() * g.out_w();
+  Dev xd(x, static_cast<size_t>(in_bytes)), od(static_cast<size_t>(out_bytes));
+  const i8t_conv_geom cg = cgeom(g);
+  ok(i8t_im2col_s8(ctx(), xd.as<int8_t>(), &cg, c_lo, c_hi, od.as<int8_t>()));
+  sync();
+  od.to_host(out, static_cast<size_t>(out_bytes));
 }
+void im2col_i8(const int8_t* x, const ConvGeometry& g, int8_t* out) { im2col_device(x, g, 0, g.c, out); }
 void im2col_channel_i8(const int8_t* x, const ConvGeometry& g, int64_t channel, int8_t* out) {
-  g.validate();
-  im2col_range(x, g, channel, channel + 1, out);
+  im2col_device(x, g, channel, channel + 1, out);
 }
 
 Tensor conv2d_q(const QuantizedTensor& a, const QuantizedTensor& w, const ConvGeometry& g, int /*threads*/) {

@@ -474,6 +474,34 @@ int i8t_nhwc_to_nchw_f32(i8t_ctx* ctx, const float* src, int64_t n, int64_t c, i
   return cuda_check("k_nhwc_to_nchw_f32");
 }
 
+// im2col_i8 / im2col_channel_i8 (conv.cpp:23-47, 98-106): channels [c_lo,
+// c_hi) of an NCHW int8 tensor -> col[((c-c_lo)*kh + i)*kw + j][(n*oh + p)*ow + q],
+// zero where the tap falls into the padding.  One thread per output byte,
+// consecutive threads along q: the col row writes are coalesced.
+static __global__ void k_im2col_i8(const int8_t* __restrict__ x, i8t_conv_geom g, int64_t oh, int64_t ow, int64_t c_lo,
+                                   int64_t rows, int8_t* __restrict__ col) {
+  pdl_entry();
+  const int64_t cols = g.n * oh * ow, total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, m = e - r * cols;
+    const int64_t j = r % g.kw, i = (r / g.kw) % g.kh, c = c_lo + r / (g.kw * g.kh);
+    const int64_t q = m % ow, p = (m / ow) % oh, n = m / (ow * oh);
+    const int64_t y = p * g.stride_h + i - g.pad_h, xx = q * g.stride_w + j - g.pad_w;
+    col[e] = (y >= 0 && y < g.h && xx >= 0 && xx < g.w) ? x[((n * g.c + c) * g.h + y) * g.w + xx] : int8_t(0);
+  }
+}
+
+int i8t_im2col_s8(i8t_ctx* ctx, const int8_t* x, const i8t_conv_geom* g, int64_t c_lo, int64_t c_hi, int8_t* col) {
+  Ctx* cx = CTX(ctx);
+  if (!cx || !x || !g || !col || c_lo < 0 || c_hi > g->c || c_lo >= c_hi) return set_error(I8T_EINVAL, "im2col: bad arguments");
+  const int64_t oh = (g->h + 2 * g->pad_h - g->kh) / g->stride_h + 1, ow = (g->w + 2 * g->pad_w - g->kw) / g->stride_w + 1;
+  if (oh < 1 || ow < 1) return set_error(I8T_EINVAL, "im2col: empty output");
+  const int64_t rows = (c_hi - c_lo) * g->kh * g->kw;
+  launch_k(k_im2col_i8, grid_for(rows * g->n * oh * ow), 256, 0, cx->stream, x, *g, oh, ow, c_lo, rows, col);
+  count_launch(1);
+  return cuda_check("k_im2col_i8");
+}
+
 int i8t_nchw_to_nhwc_i8(i8t_ctx* ctx, const int8_t* src, int64_t n, int64_t c, int64_t hw, int8_t* dst, int64_t c_pad) {
   Ctx* cx = CTX(ctx);
   if (!cx || !src || !dst || c_pad < c) return set_error(I8T_EINVAL, "nchw_to_nhwc: bad arguments");

@@ -104,21 +104,8 @@ def quantize(x: torch.Tensor, clip, stochastic: bool = False, stream_state: torc
     q = torch.empty(x.shape, dtype=torch.int8, device=x.device)
     d_clip = _dev_f32(clip, x.device)
     h = ctx()
-    if stochastic:
-        n = x.numel()
-        if n % 4:
-            xp = torch.zeros(n + (4 - n % 4), dtype=torch.float32, device=x.device)
-            xp[:n] = x.reshape(-1)
-            qp = torch.empty(xp.numel(), dtype=torch.int8, device=x.device)
-            # extra padded draws must not advance the stream: quantize padded, then rewind by re-jumping
-            before = stream_state.clone()
-            call("i8t_quantize_stochastic", h, _p(xp), xp.numel(), _p(d_clip), _p(stream_state), _p(qp))
-            q.view(-1).copy_(qp[:n])
-            st = C.c_uint32()
-            call("i8t_lcg_jump_host", C.c_uint32(int(before.item()) & 0xFFFFFFFF), C.c_uint64(n), C.byref(st))
-            stream_state.fill_(C.c_int32(st.value).value)
-        else:
-            call("i8t_quantize_stochastic", h, _p(x), n, _p(d_clip), _p(stream_state), _p(q))
+    if stochastic:  # any length: the library pads a ragged tail and rewinds the stream over it
+        call("i8t_quantize_stochastic", h, _p(x), x.numel(), _p(d_clip), _p(stream_state), _p(q))
     else:
         call("i8t_quantize_nearest", h, _p(x), x.numel(), _p(d_clip), _p(q), _p(amax), int(accumulate_amax))
     return q
@@ -388,6 +375,36 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     c = torch.empty((m, n), dtype=torch.int32, device=a.device)
     call("i8t_gemm_s8", ctx(), _p(a.contiguous()), _p(b.contiguous()), m, k, n, _p(c))
     return c
+
+
+def gemm_i8_fused_lhs(a: torch.Tensor, clip, stochastic: bool, stream_state: torch.Tensor | None,
+                      b: torch.Tensor) -> torch.Tensor:
+    """gemm_i8_fused_lhs (gemm.cpp:49-64): C = quantize(A fp32, from_clip(clip), mode[, stream]) . B,
+    quantised on the device into the GEMM's operand; bit-identical to quantize() + gemm_i8()
+    incl. the stream state (advanced by m*k when stochastic)."""
+    if stochastic != (stream_state is not None):
+        raise ValueError("quantize: stream required iff mode is stochastic")
+    if a.dim() != 2:
+        raise ValueError("gemm_i8_fused_lhs: lhs must be 2-D")
+    _check_clip(clip)
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2:
+        raise ValueError("gemm_i8: inner dimensions do not match")
+    c = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    call("i8t_gemm_s8_fused_lhs", ctx(), _p(a.contiguous().float()), m, k, _p(_dev_f32(clip, a.device)),
+         int(stochastic), _p(stream_state), _p(b.contiguous()), n, _p(c))
+    return c
+
+
+def im2col_i8(x: torch.Tensor, g: ConvGeom, channel: int | None = None) -> torch.Tensor:
+    """im2col_i8 / im2col_channel_i8 (conv.cpp:23-47, 98-106): NCHW int8 ->
+    col [C*kh*kw (or kh*kw), N*P*Q] int8, zero padding."""
+    p, q = g.out_hw()
+    c_lo, c_hi = (0, g.c) if channel is None else (channel, channel + 1)
+    col = torch.empty(((c_hi - c_lo) * g.kh * g.kw, g.n * p * q), dtype=torch.int8, device=x.device)
+    call("i8t_im2col_s8", ctx(), _p(x.contiguous()), C.byref(g), c_lo, c_hi, _p(col))
+    return col
 
 
 def geom(n, c, h, w, k, kh, kw=None, stride=1, pad=0, depthwise=False, floor_mode=True, stride_w=None,

@@ -7,6 +7,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "i8t/clip.hpp"
@@ -192,6 +193,77 @@ static void test_gemm_conv() {
   CHECK(throws<std::invalid_argument>([&] { bad.validate(); }));
 }
 
+// fused quantize-GEMM == unfused composition bit-exactly, incl. the stream
+// (test_kernels.cpp:120-142); a ragged m*k (not a multiple of 4) as well
+static void test_fused_lhs() {
+  Rng r{31};
+  for (auto [m, k, n] : {std::tuple<int64_t, int64_t, int64_t>{9, 40, 13}, {7, 41, 5}, {130, 300, 70}}) {
+    Tensor a(Shape{m, k});
+    for (int64_t i = 0; i < a.numel(); ++i) a[i] = static_cast<float>(2.0 * r.uniform() - 1.0) * 3.0f;
+    Int8Matrix b(k, n);
+    for (auto& v : b.data) v = r.i8();
+    QuantParams pa = QuantParams::from_clip(max_abs(a));
+    LcgStream s1(555), s2(555);
+    auto q = quantize(a, pa, RoundingMode::kStochastic, &s1);
+    Int8Matrix qa(m, k);
+    qa.data = q.q;
+    auto unfused = gemm_i8(qa, b);
+    auto fused = gemm_i8_fused_lhs(a, pa, RoundingMode::kStochastic, &s2, b);
+    CHECK(unfused.data == fused.data);
+    CHECK(s1.state() == s2.state());
+    auto fused_nearest = gemm_i8_fused_lhs(a, pa, RoundingMode::kNearest, nullptr, b);
+    Int8Matrix qn(m, k);
+    qn.data = quantize(a, pa, RoundingMode::kNearest).q;
+    CHECK(fused_nearest.data == gemm_i8(qn, b).data);
+  }
+  CHECK(throws<std::invalid_argument>([] {
+    LcgStream s(1);
+    gemm_i8_fused_lhs(Tensor(Shape{2, 3}), QuantParams::from_clip(1.0f), RoundingMode::kNearest, &s, Int8Matrix(3, 1));
+  }));
+  Tensor bad(Shape{1, 4}, {1.0f, NAN, 0.0f, 2.0f});
+  CHECK(throws<std::domain_error>([&] {
+    gemm_i8_fused_lhs(bad, QuantParams::from_clip(1.0f), RoundingMode::kNearest, nullptr, Int8Matrix(4, 2));
+  }));
+}
+
+// im2col known layouts (test_kernels.cpp:144-161) + a padded strided case vs a direct gather
+static void test_im2col() {
+  ConvGeometry g{.n = 1, .c = 1, .h = 3, .w = 3, .k = 1, .kh = 2, .kw = 2};
+  std::vector<int8_t> x = {1, 2, 3, 4, 5, 6, 7, 8, 9};
+  std::vector<int8_t> col(4 * 4);
+  im2col_i8(x.data(), g, col.data());
+  CHECK(col[0 * 4 + 0] == 1);
+  CHECK(col[1 * 4 + 0] == 2);
+  CHECK(col[2 * 4 + 0] == 4);
+  CHECK(col[3 * 4 + 0] == 5);
+  ConvGeometry g2{.n = 1, .c = 1, .h = 3, .w = 3, .k = 1, .kh = 3, .kw = 3};
+  std::vector<int8_t> col2(9);
+  im2col_i8(x.data(), g2, col2.data());
+  CHECK(col2 == x);
+  Rng r{7};
+  ConvGeometry g3{.n = 2, .c = 3, .h = 7, .w = 7, .k = 4, .kh = 3, .kw = 3, .stride = 2, .pad = 1};
+  std::vector<int8_t> x3(2 * 3 * 7 * 7);
+  for (auto& v : x3) v = r.i8();
+  const int64_t oh = g3.out_h(), ow = g3.out_w(), cols = g3.n * oh * ow;
+  std::vector<int8_t> c3(static_cast<size_t>(3 * 9 * cols)), ch1(static_cast<size_t>(9 * cols));
+  im2col_i8(x3.data(), g3, c3.data());
+  im2col_channel_i8(x3.data(), g3, 1, ch1.data());
+  bool same = true;
+  for (int64_t c = 0; c < 3; ++c)
+    for (int64_t i = 0; i < 3; ++i)
+      for (int64_t j = 0; j < 3; ++j)
+        for (int64_t n = 0; n < 2; ++n)
+          for (int64_t p = 0; p < oh; ++p)
+            for (int64_t q = 0; q < ow; ++q) {
+              const int64_t y = p * 2 + i - 1, xx = q * 2 + j - 1, row = (c * 3 + i) * 3 + j;
+              const int8_t want = (y >= 0 && y < 7 && xx >= 0 && xx < 7) ? x3[((n * 3 + c) * 7 + y) * 7 + xx] : 0;
+              const int64_t m = (n * oh + p) * ow + q;
+              same = same && c3[row * cols + m] == want;
+              if (c == 1) same = same && ch1[(i * 3 + j) * cols + m] == want;
+            }
+  CHECK(same);
+}
+
 static void test_clip_lr() {
   CHECK(std::fabs(cosine_distance(Tensor({3}, {0.5f, -1.0f, 2.0f}), Tensor({3}, {0.5f, -1.0f, 2.0f}))) < 1e-12);
   CHECK(cosine_distance(Tensor({2}, {1, 0}), Tensor({2}, {0, 0})) == 1.0);
@@ -221,7 +293,8 @@ static void test_clip_lr() {
 
 int main() {
   std::vector<std::pair<const char*, std::function<void()>>> suites = {
-      {"quantize", test_quantize}, {"gemm_conv", test_gemm_conv}, {"clip_lr", test_clip_lr}};
+      {"quantize", test_quantize}, {"gemm_conv", test_gemm_conv}, {"fused_lhs", test_fused_lhs},
+      {"im2col", test_im2col},     {"clip_lr", test_clip_lr}};
   for (auto& [name, fn] : suites) {
     try {
       fn();
