@@ -332,6 +332,13 @@ def _dp_max_(t: torch.Tensor):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
 
+def _fp32_exact():
+    """FP32-mode convolutions (calibration, the FP32 baseline; conv2d_f32 in the
+    reference) in IEEE fp32, not TF32: cuDNN's default TF32 inputs would shift
+    the activation maxima the calibration hands to the INT8 clips."""
+    return torch.backends.cudnn.flags(enabled=True, benchmark=False, deterministic=False, allow_tf32=False)
+
+
 def _kaiming(shape, fan_in, gen, device):
     return (torch.randn(shape, generator=gen, device="cpu") * math.sqrt(2.0 / fan_in)).to(device)
 
@@ -424,8 +431,9 @@ class Conv2d(Layer):
             if ctx.training:
                 self._x = x
             xc = x.permute(0, 3, 1, 2)
-            y = F.conv2d(xc, self.weight, None, (self.sh, self.sw), (self.ph, self.pw),
-                         groups=self.in_c if self.depthwise else 1)
+            with _fp32_exact():
+                y = F.conv2d(xc, self.weight, None, (self.sh, self.sw), (self.ph, self.pw),
+                             groups=self.in_c if self.depthwise else 1)
             return y.permute(0, 2, 3, 1).contiguous()
         # lazy clip init: clip = max(max_abs(t), 1e-12) (layers.cpp:106-107); under data
         # parallelism the max is over the global batch, so every rank quantises with one scale
@@ -493,10 +501,11 @@ class Conv2d(Layer):
             xc = self._x.permute(0, 3, 1, 2)
             gc = gz.permute(0, 3, 1, 2)
             groups = self.in_c if self.depthwise else 1
-            gi = torch.nn.grad.conv2d_input(xc.shape, self.weight, gc, (self.sh, self.sw), (self.ph, self.pw),
-                                            groups=groups)
-            self.grad_weight.copy_(torch.nn.grad.conv2d_weight(xc, self.weight.shape, gc, (self.sh, self.sw),
-                                                               (self.ph, self.pw), groups=groups))
+            with _fp32_exact():
+                gi = torch.nn.grad.conv2d_input(xc.shape, self.weight, gc, (self.sh, self.sw), (self.ph, self.pw),
+                                                groups=groups)
+                self.grad_weight.copy_(torch.nn.grad.conv2d_weight(xc, self.weight.shape, gc, (self.sh, self.sw),
+                                                                   (self.ph, self.pw), groups=groups))
             return gi.permute(0, 2, 3, 1).contiguous()
         h = ops.ctx()
         stream_in = ctx.grad_stream.clone() if TRACE is not None else None

@@ -178,7 +178,25 @@ def _gpu_step(tr, x, y, it, rec):
 
 
 # ------------------------------------------------------------------ the teacher-forced step
-def test_resnet20_b128_step_teacher_forced_matches_oracle():
+def _calibrate_both(tr, otr, m):
+    """Trainer::calibrate + finish_calibration on both sides (train.cpp:29-46).
+    The FP32 forward differs in the last bits (cuDNN fp32 vs the reference's
+    double-accumulated conv2d_f32), so the activation clips agree to 1e-5; the
+    oracle then adopts the device's clips so the INT8 steps stay teacher-forced."""
+    from paper_1912_12607_b200.trainer import synthetic_batch
+    xc, _ = synthetic_batch(m, BATCH, 99)
+    tr.calibrate(xc)
+    otr.calibrate(_nchw(xc))
+    tr.finish_calibration()
+    otr.finish_calibration()
+    for (path, gl), (_, ol) in zip(tr.quant_layers, otr.quant_layers):
+        assert float(gl.qs.clip_w.item()) == float(ol.qs.clip_w), path
+        assert float(gl.qs.clip_a.item()) == pytest.approx(float(ol.qs.clip_a), rel=1e-5), path
+        ol.qs.clip_a = np.float32(gl.qs.clip_a.item())
+
+
+@pytest.mark.parametrize("calibrate", [False, True])
+def test_resnet20_b128_step_teacher_forced_matches_oracle(calibrate):
     from paper_1912_12607_b200 import layers as L
     old = L.BN_IMPL
     L.BN_IMPL = "eager"
@@ -189,7 +207,9 @@ def test_resnet20_b128_step_teacher_forced_matches_oracle():
         olayers = [layer for _, layer in otr.quant_layers]
         assert len(gconvs) == len(olayers) == 22  # 21 convs + fc
         oidx = {id(l): i for i, l in enumerate(olayers)}
-        batches = _batches(m)
+        if calibrate:
+            _calibrate_both(tr, otr, m)
+        batches = _batches(m)[:2 if calibrate else STEPS]
         report = {"config": "resnet20 b128 int8, 1 GPU vs CPU oracle (teacher-forced)", "steps": []}
         for it, (x, y) in enumerate(batches):
             rec = Recorder(gconvs)
@@ -299,23 +319,30 @@ def test_resnet20_b128_step_teacher_forced_matches_oracle():
             _adopt(tr, net)
             report["steps"].append(srep)
         path = os.environ.get("I8T_PARITY_REPORT")
-        if path:
+        if path and not calibrate:
             with open(path, "w") as f:
                 json.dump(report, f, indent=1)
     finally:
         L.BN_IMPL = old
 
 
-def test_resnet20_b128_fused_equals_eager():
+@pytest.mark.parametrize("calibrate", [False, True])
+def test_resnet20_b128_fused_equals_eager(calibrate):
     """The teacher-forced test runs the eager (materialised) BN path; the
-    default fused path is bit-identical to it at this batch size."""
+    default fused path is bit-identical to it at this batch size (with lazy
+    clips the fused block-input quantisers join from step 1 on, with
+    calibrated clips from step 0)."""
     from paper_1912_12607_b200 import layers as L
+    from paper_1912_12607_b200.trainer import synthetic_batch
     res = {}
     for impl in ("eager", "fused"):
         old = L.BN_IMPL
         L.BN_IMPL = impl
         try:
             m, tr = _gpu_model()
+            if calibrate:
+                tr.calibrate(synthetic_batch(m, BATCH, 99)[0])
+                tr.finish_calibration()
             reps = [tr.train_step(x, y, it, 100) for it, (x, y) in enumerate(_batches(m))]
             res[impl] = (reps, tr.pflat.clone(), int(tr.grad_stream.item()))
         finally:
