@@ -167,6 +167,137 @@ def cpu_reference_sample(threads=None):
     return t_ref + t_port, kind, {"ref_layers": n_ref, "port_layers": n_port, "ref_s": t_ref, "port_s": t_port}
 
 
+C1 = (32, 64, 56, 64, 3, 1, 1)  # configs[0]: 3x3 conv 64->64 @56x56, batch 32
+
+
+def _c1_inputs():
+    import numpy as np
+    from oracle import lib as O
+    n, c, h, k, kk, s, p = C1
+    x = O.gaussian((n, c, h, h), 11, 1.0, True)                       # a = ReLU(N(0,1))
+    w = O.gaussian((k, c, kk, kk), 12, float(np.sqrt(2.0 / (c * kk * kk))))  # Kaiming
+    g = O.gradient_like((n, k, h, h), 13, 1e-4, 0.01)                 # Laplace(1e-4), 1 % x40 outliers
+    return x, w, g
+
+
+def host_info():
+    """nproc, usable CPUs, CPU model and the cgroup CPU quota of this host."""
+    info = {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+            else None}
+    try:
+        with open("/proc/cpuinfo") as f:
+            info["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        info["cpu_model"] = None
+    for path in ("/sys/fs/cgroup/cpu.max", "/sys/fs/cgroup/cpu/cpu.cfs_quota_us"):
+        try:
+            with open(path) as f:
+                info["cgroup_cpu_quota"] = f.read().strip()
+            break
+        except OSError:
+            continue
+    return info
+
+
+def c1_cpu_ops(reps=5):
+    """the reference's own operators (oracle/_ref, compiled
+    unmodified) on the config-1 tensors, median of `reps` runs each, at
+    threads = 1 and threads = nproc where the operator takes a thread count
+    (quantize / maybe_update are single-threaded in the reference)."""
+    import statistics
+    import numpy as np
+    from oracle import lib as O
+    from oracle import ref as R
+    if not R.available():
+        return None
+    x, w, g = _c1_inputs()
+    n, c, h, k, kk, s, p = C1
+    gv = R.gvec(n, c, h, h, k, kk, kk, s, p)
+    ca, cw = float(O.max_abs(x)), float(O.max_abs(w))
+    qa, _ = R.quantize(x, ca)
+    qw, _ = R.quantize(w, cw)
+    st0 = O.new_clip_state(100)
+    R.maybe_update(st0, g, 0)
+    qg, _ = R.quantize(g, st0.clip, True, 1)
+
+    def med(fn):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts) * 1e3
+    nproc = os.cpu_count() or 1
+    out = {"quantize_nearest_a_ms": med(lambda: R.quantize(x, ca)),
+           "quantize_stochastic_g_ms": med(lambda: R.quantize(g, st0.clip, True, 1))}
+    for t in (1, nproc):
+        out[f"conv2d_q_t{t}_ms"] = med(lambda: R.conv2d_q(qa, ca, qw, cw, gv, t))
+        out[f"conv2d_backward_q_t{t}_ms"] = med(lambda: R.conv2d_backward_q(qg, st0.clip, qa, ca, qw, cw, gv, t))
+
+    def upd(search):
+        st = O.ClipState(st0.clip, st0.last_dc, -1 if search else 0, 100)
+        R.maybe_update(st, g, 1)
+    out["maybe_update_search_ms"] = med(lambda: upd(True))
+    out["maybe_update_nonsearch_ms"] = med(lambda: upd(False))
+    out["threads"] = [1, nproc]
+    out["reps"] = reps
+    out["host"] = host_info()
+    return out
+
+
+def c1_gpu_ops(reps=20):
+    """The same config-1 operators on the device through the ops mirror
+    (device-resident tensors, CUDA events on the launching stream, median)."""
+    import statistics
+    import torch
+    from oracle import lib as O
+    from paper_1912_12607_b200 import ops
+    x, w, g = _c1_inputs()
+    n, c, h, k, kk, s, p = C1
+    pg = ops.geom(n, c, h, h, k, kk, kk, s, p)
+    xd = torch.from_numpy(x).cuda().permute(0, 2, 3, 1).contiguous()  # NHWC on the device
+    gd = torch.from_numpy(g).cuda().permute(0, 2, 3, 1).contiguous()
+    wd = torch.from_numpy(w).cuda()
+    ca, cw = float(O.max_abs(x)), float(O.max_abs(w))
+    c_pad, k_pad = ops.pad4(c), ops.pad4(k)
+    qa = torch.empty((n, h, h, c_pad), dtype=torch.int8, device="cuda")
+    qw, ld = ops.kcrs_to_krsc_i8(ops.quantize(wd, cw), c_pad)
+    qwt, ldt = ops.kcrs_to_crsk_i8(ops.quantize(wd, cw), k_pad)
+    dca, dcw = ops._dev_f32(ca), ops._dev_f32(cw)
+    st = ops.DsgcState(period=100)
+    lcg = ops.new_lcg_state(1)
+    qg = ops.quantize_gradient(st, gd, 0, lcg, nhwc=True)
+    v = st.sync()
+    dcg = ops._dev_f32(v.clip_q)
+
+    def med(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+    it = {False: 1, True: 100}  # last search at 0: iterations 1..99 measure, multiples of 100 search
+
+    def qgrad(search):
+        ops.quantize_gradient(st, gd, it[search], lcg, nhwc=True)
+        it[search] += 100 if search else 1
+    return {
+        "quantize_nearest_a_ms": med(lambda: ops.call("i8t_quantize_nearest_rows", ops.ctx(), xd, n * h * h, c, dca, qa,
+                                                      c_pad, None, 0)),
+        "conv2d_q_ms": med(lambda: ops.conv_fwd_nhwc(pg, qa, c_pad, qw, ld, ca, cw)),
+        "quantize_gradient_nonsearch_ms": med(lambda: qgrad(False)),
+        "quantize_gradient_search_ms": med(lambda: qgrad(True)),
+        "conv2d_backward_q_ms": med(lambda: (ops.conv_dgrad_nhwc(pg, qg, k_pad, qwt, ldt, v.clip_q, cw),
+                                             ops.conv_wgrad_nhwc(pg, qg, k_pad, qa, c_pad, v.clip_q, ca))),
+        "reps": reps}
+
+
 def run_reference_arm(a, rank, world):
     if rank != 0:
         return
@@ -363,7 +494,10 @@ def main():
     if rank == 0 and not a.no_cpu_baseline:
         t, kind, detail = cpu_reference_sample(os.cpu_count())
         line["cpu_baseline"] = {"value": 1.0 / t, "unit": "imgs/s", "cores": os.cpu_count(), "kind": kind,
-                                "sample": f"1 image through all 53 ResNet-50 conv layer steps ({detail})"}
+                                "sample": f"1 image through all 53 ResNet-50 conv layer steps ({detail})",
+                                # config 1 operator by operator: the reference on the host, the device beside it
+                                "c1_ops_reference": c1_cpu_ops(), "c1_ops_gpu": c1_gpu_ops(),
+                                "c1_config": "3x3 conv 64->64 @56x56 batch 32 (configs[0])"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
