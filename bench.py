@@ -539,6 +539,9 @@ def instrumented_conv_time(tr, x, y, it, total, model, batch):
     import paper_1912_12607_b200.layers as L
     L.call = wrapped
     try:
+        # the step has no host sync: with the GPU held in a sleep while the host
+        # queues it, no host launch gap falls between a conv's two events
+        torch.cuda._sleep(200_000_000)
         tr.train_step(x, y, it + 1, total, read_stats=False)
         torch.cuda.synchronize()
     finally:

@@ -83,6 +83,14 @@ int i8t_ctx_set_stream(i8t_ctx* ctx, void* stream);
 int i8t_ctx_destroy(i8t_ctx* ctx);
 /* Synchronise the stream; report and clear any latched device error. */
 int i8t_ctx_check(i8t_ctx* ctx);
+/* Device address of the context's latched error word (int32), so a caller can
+ * snapshot / restore it on the stream (the trainer does, around the backward of
+ * a step whose divergence is only known on the device). */
+int i8t_ctx_error_word(i8t_ctx* ctx, int32_t** out);
+/* dst <- src (bytes, 16-byte aligned pointers) iff the device int32 *flag != 0,
+ * stream-ordered: restores the pre-backward DSGC / LCG state of a diverged step
+ * (train.cpp:73-77 returns before the backward) without a host round trip. */
+int i8t_copy_if(i8t_ctx* ctx, const int32_t* flag, void* dst, const void* src, int64_t bytes);
 const char* i8t_last_error(void);
 /* Device memory for hosts that do not link a CUDA runtime (the C++ shim):
  * synchronous on the context's stream.  kind: 0 host->device, 1 device->host,

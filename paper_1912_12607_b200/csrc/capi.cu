@@ -1,6 +1,7 @@
 // capi.cu -- context, error reporting and scratch management behind i8t_cuda.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -197,6 +198,38 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_tickets) cudaFree(c->d_tickets);
   delete c;
+  return I8T_OK;
+}
+
+// dst <- src (bytes) iff *flag != 0, on the stream (no host round trip): the
+// trainer's restore of the pre-backward device state on a diverged step.
+static __global__ void k_copy_if(const int32_t* flag, uint4* dst, const uint4* src, int64_t n16, uint8_t* dtail,
+                                 const uint8_t* stail, int tail) {
+  pdl_entry();
+  if (!*flag) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n16; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < tail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
+int i8t_copy_if(i8t_ctx* ctx, const int32_t* flag, void* dst, const void* src, int64_t bytes) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !flag || !dst || !src || bytes < 0) return set_error(I8T_EINVAL, "copy_if: bad arguments");
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u)
+    return set_error(I8T_EUNSUPPORTED, "copy_if: 16-byte alignment");
+  const int64_t n16 = bytes / 16;
+  const int tail = static_cast<int>(bytes - n16 * 16);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>((n16 + 255) / 256, 1), 148 * 4));
+  launch_k(k_copy_if, blocks, 256, 0, c->stream, flag, static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+           static_cast<uint8_t*>(dst) + n16 * 16, static_cast<const uint8_t*>(src) + n16 * 16, tail);
+  count_launch(1);
+  return cuda_check("k_copy_if");
+}
+
+int i8t_ctx_error_word(i8t_ctx* ctx, int32_t** out) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !out) return set_error(I8T_EINVAL, "ctx_error_word: bad arguments");
+  *out = reinterpret_cast<int32_t*>(c->d_err);
   return I8T_OK;
 }
 

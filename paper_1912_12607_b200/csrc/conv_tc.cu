@@ -854,7 +854,8 @@ static int make_out_map(CUtensorMap* map, void* base, int64_t cols, int64_t rows
 }
 
 static bool tma_out_ok(const void* p, int64_t ld) {
-  return p && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+  static const bool off = getenv("I8T_NO_TMA_OUT") != nullptr;  // tuning experiments: direct epilogue stores
+  return !off && p && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
 static int num_sms() {

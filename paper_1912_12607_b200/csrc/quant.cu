@@ -85,28 +85,86 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
 // K2 over every quantised layer of a model in one launch (blockIdx.y = layer):
 // the per-layer launches cost more than their ~150 MB of traffic.  Padding
 // bytes of the outputs are never written (zeroed once at allocation).
-__global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* __restrict__ descs, int* err) {
+// All layers' weights in one launch (blockIdx.y = layer).  Each block
+// quantises a [32 k x TC c x RS] tile into shared memory from contiguous
+// source rows, then writes both device layouts from it in 32-byte runs:
+// KRSC (c fastest) and CRSK (k fastest) -- a per-element transpose would
+// scatter single bytes across the two outputs.
+constexpr int WQ_TK = 32, WQ_TILE = 32 * 32 * 9;
+__global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* __restrict__ descs, int n_layers,
+                                                             int* err) {
   pdl_entry();
-  const i8t_wq_desc d = descs[blockIdx.y];
-  const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
-  const uint32_t K = d.k, C = d.c, RS = d.rs, tot = K * C * RS;
+  __shared__ int8_t tq[WQ_TILE];
   bool bad = false;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
-    uint32_t k, c, rs;
-    if (d.src_krsc) {
-      c = i % C;
-      rs = (i / C) % RS;
-      k = i / (C * RS);
-    } else {
-      rs = i % RS;
-      c = (i / RS) % C;
-      k = i / (RS * C);
+  // one flat list of tiles over all layers (a per-layer grid would run the
+  // layers one after another, each at the latency of a single tile)
+  int layer = 0, first = 0;  // tiles of layers [0, layer) come before `first`
+  for (int t = blockIdx.x;; t += gridDim.x) {
+    int K = 0, C = 0, RS = 0, TK = 0, TC = 0, ktiles = 0, ctiles = 0;
+    for (; layer < n_layers; ++layer) {
+      const i8t_wq_desc& dl = descs[layer];
+      K = dl.k; C = dl.c; RS = dl.rs;
+      TK = min(WQ_TK, max(1, WQ_TILE / RS));
+      TC = min(256, max(1, WQ_TILE / (TK * RS)));  // TK*TC*RS <= tile (1x1 layers: 32 x 256)
+      ktiles = (K + TK - 1) / TK;
+      ctiles = (C + TC - 1) / TC;
+      if (t < first + ktiles * ctiles) break;
+      first += ktiles * ctiles;
     }
-    const float v = __ldg(d.w + i);
-    bad |= !isfinite(v);
-    const int8_t qv = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
-    if (d.q_krsc) d.q_krsc[static_cast<size_t>(k) * d.ld_krsc + rs * d.c_pad + c] = qv;
-    if (d.q_crsk) d.q_crsk[static_cast<size_t>(c) * d.ld_crsk + rs * d.k_pad + k] = qv;
+    if (layer >= n_layers) break;
+    const i8t_wq_desc d = descs[layer];
+    const float clip = *d.clip, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
+    const int tl = t - first;
+    const int k0 = (tl / ctiles) * TK, c0 = (tl % ctiles) * TC;
+    const int nk = min(TK, K - k0), nc = min(TC, C - c0), row = nc * RS;  // row: (c, rs) of one k
+    __syncthreads();  // the previous tile's writes have read tq
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (!d.src_krsc) {
+      // KCRS rows: (c, rs) contiguous; each warp streams four k rows at once so
+      // four independent loads per lane are in flight
+      const float* w0 = d.w + static_cast<size_t>(k0) * C * RS + static_cast<size_t>(c0) * RS;
+      for (int kb = warp; kb < nk; kb += 32)
+        for (int cr = lane; cr < row; cr += 32) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int kk = kb + 8 * u;
+            v[u] = kk < nk ? __ldg(w0 + static_cast<size_t>(kk) * C * RS + cr) : 0.0f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int kk = kb + 8 * u;
+            if (kk < nk) {
+              bad |= !isfinite(v[u]);
+              tq[kk * TC * RS + cr] = static_cast<int8_t>(quant_nearest_fast(v[u], clip, hs, s, inv_s));
+            }
+          }
+        }
+    } else {
+      for (int kk = warp; kk < nk; kk += 8) {  // KRSC rows
+        const float* wrow = d.w + static_cast<size_t>(k0 + kk) * RS * C + c0;
+        int8_t* trow = tq + kk * TC * RS;
+        for (int rs = 0; rs < RS; ++rs)
+          for (int cc = lane; cc < nc; cc += 32) {
+            const float v = __ldg(wrow + static_cast<size_t>(rs) * C + cc);
+            bad |= !isfinite(v);
+            trow[cc * RS + rs] = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
+          }
+      }
+    }
+    __syncthreads();
+    if (d.q_krsc)  // [k][rs][c]: c along the lanes
+      for (int pr = warp; pr < nk * RS; pr += 8) {
+        const int kk = pr / RS, rs = pr - kk * RS;
+        int8_t* dst = d.q_krsc + static_cast<size_t>(k0 + kk) * d.ld_krsc + rs * d.c_pad + c0;
+        for (int cc = lane; cc < nc; cc += 32) dst[cc] = tq[kk * TC * RS + cc * RS + rs];
+      }
+    if (d.q_crsk)  // [c][rs][k]: k along the lanes
+      for (int pr = warp; pr < nc * RS; pr += 8) {
+        const int cc = pr / RS, rs = pr - cc * RS;
+        int8_t* dst = d.q_crsk + static_cast<size_t>(c0 + cc) * d.ld_crsk + rs * d.k_pad + k0;
+        for (int kk = lane; kk < nk; kk += 32) dst[kk] = tq[kk * TC * RS + cc * RS + rs];
+      }
   }
   if (bad) atomicOr(err, ERR_NONFINITE);
 }
@@ -401,7 +459,7 @@ int i8t_quantize_weight(i8t_ctx* ctx, const float* w, int src_krsc, int64_t k, i
 int i8t_quantize_weights_multi(i8t_ctx* ctx, const i8t_wq_desc* dev_descs, int n_layers) {
   Ctx* cx = CTX(ctx);
   if (!cx || !dev_descs || n_layers < 1 || n_layers > 65535) return set_error(I8T_EINVAL, "quantize_weights_multi: bad arguments");
-  launch_k(k_quant_weight_multi, dim3(2 * 148, static_cast<unsigned>(n_layers)), 256, 0, cx->stream, dev_descs, cx->d_err);
+  launch_k(k_quant_weight_multi, 148 * 4, 256, 0, cx->stream, dev_descs, n_layers, cx->d_err);
   count_launch(1);
   return cuda_check("k_quant_weight_multi");
 }

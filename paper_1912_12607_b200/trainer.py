@@ -76,6 +76,12 @@ class _DistHook:
         self.cfn = self.FN(self._call)
 
     @staticmethod
+    def _view_i32(ptr):
+        class _A:
+            __cuda_array_interface__ = {"shape": (1,), "typestr": "<i4", "data": (int(ptr), False), "version": 3}
+        return torch.as_tensor(_A(), device="cuda")
+
+    @staticmethod
     def _view(ptr, count):
         class _A:
             __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
@@ -118,6 +124,17 @@ class Trainer:
         if hasattr(first, "need_input_grad"):
             first.need_input_grad = False
         self.skip = torch.zeros(1, dtype=torch.int32, device=device)
+        # divergence (train.cpp:73-77) is decided on the device: the backward runs
+        # regardless and a diverged step restores what it mutated (DSGC states,
+        # LCG stream, latched error word) from a pre-backward snapshot -- no host
+        # sync inside the step
+        self.div = torch.zeros(1, dtype=torch.int32, device=device)
+        self._snap_arena = torch.empty_like(self.arena.buf)
+        self._snap_lcg = torch.empty_like(self.grad_stream)
+        self._snap_err = torch.empty(4, dtype=torch.int32, device=device)
+        ptr = C.POINTER(C.c_int32)()
+        call("i8t_ctx_error_word", ops.ctx(), C.byref(ptr))
+        self._err = _DistHook._view_i32(C.cast(ptr, C.c_void_p).value)
         self._wq_buf, self._wq_n = None, 0  # device i8t_wq_desc array (built at the second step)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
         self.lr_dev = torch.zeros(1, dtype=torch.float64, device=device)
@@ -198,16 +215,14 @@ class Trainer:
         logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8, wq))
         # data parallel: the mean is over the GLOBAL batch (loss summed across ranks when read)
         loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels, logits.shape[0] * self.world)
-        bad = (~torch.isfinite(loss)) | (~torch.isfinite(logits).all())
+        bad = ((~torch.isfinite(loss)) | (~torch.isfinite(logits).all())).to(torch.int32).reshape(1)
         if self.world > 1:  # every rank takes the same branch
-            bad = bad.to(torch.int32)
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-            bad = bad.bool()
-        # divergence check before backward (train.cpp:73-77): one host sync per step
-        if bool(bad.item()):
-            rep.loss, rep.diverged = float(loss.item()), True
-            return rep
+        self.div.copy_(bad)
         self.loss_dev.copy_(loss.reshape(1))
+        self._snap_arena.copy_(self.arena.buf)
+        self._snap_lcg.copy_(self.grad_stream)
+        self._snap_err[:1].copy_(self._err)
         bctx = BackwardCtx(cfg.mode, it, self.grad_stream, cfg.grid_resolution, cfg.refine_rounds, cfg.clip_enabled,
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
                            self._wgrad_allreduce if self._hook is not None else None)
@@ -219,18 +234,26 @@ class Trainer:
         if self.world > 1:
             params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
             self._allreduce_fp32_grads(params)
-        # bad-gradient check (train.cpp:87-95) stays on the device and gates the update
+        # bad-gradient check (train.cpp:87-95) stays on the device and gates the update,
+        # as does the divergence flag
         h = ops.ctx()
         call("i8t_nonfinite_flag", h, ops._p(self.gflat), self.gflat.numel(), ops._p(self.skip))
+        self.skip.bitwise_or_(self.div)
         self.lr_dev.fill_(rep.base_lr_t)
         call("i8t_sgd_dclr_multi", h, ops._p(self.pflat), ops._p(self.gflat), self.nseg, ops._p(self.seg_off),
              ops._p(self.seg_state), C.c_double(rep.base_lr_t), self.lr_dev, ops._p(self.skip), self.mflat,
              C.c_double(cfg.momentum))
+        # a diverged step leaves the state as the reference's early return does
+        call("i8t_copy_if", h, self.div, self.arena.buf, self._snap_arena, self.arena.buf.numel())
+        call("i8t_copy_if", h, self.div, self.grad_stream, self._snap_lcg, 4)
+        call("i8t_copy_if", h, self.div, self._err, self._snap_err, 4)
         if read_stats:
             if self.world > 1:
                 dist.all_reduce(self.loss_dev, op=dist.ReduceOp.SUM)
             rep.loss = float(self.loss_dev.item())
             rep.diverged = bool(self.skip.item())
+            if bool(self.div.item()):  # the host mirrors of the restored DSGC states
+                self.sync_states()
             self._read_layer_stats(rep)
         return rep
 

@@ -373,3 +373,61 @@ def test_maxpool_matches_torch(ops, shape, with_bn):
     gx = torch.empty((n, h, w, c), device="cuda")
     ops.call("i8t_maxpool_bwd", ops.ctx(), ops._p(gy), ops._p(idx), n, h, w, c, k, s, p, ops._p(gx))
     torch.testing.assert_close(gx, ref_in.grad.permute(0, 2, 3, 1), rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("case", ["collide", "negative_gamma", "all_clamped", "nan"])
+def test_maxpool_bn_first_max_slot_exact(ops, case):
+    """The BN-fused max pool finds the window maximum from the raw extreme z
+    (act(bn(.)) is monotone per channel); its one-byte slot must still be the
+    reference's FIRST maximum of act(bn(z)) in window order (Pool2d's `>`,
+    layers.cpp:366-373) -- checked against a brute-force first-max over the
+    materialised act(bn(z)) on inputs built to collide after rounding: values
+    one ulp apart squeezed by a small BN slope, negative gammas (decreasing
+    map), all-clamped windows, NaN inputs."""
+    n, h, w, c, k, s, p = 2, 24, 20, 64, 3, 2, 1
+    rng = np.random.default_rng(["collide", "negative_gamma", "all_clamped", "nan"].index(case))
+    x = rng.standard_normal((n * h * w, c)).astype(np.float32)
+    gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    beta = rng.uniform(-.3, .3, c).astype(np.float32)
+    if case == "collide":  # a few distinct floats around 100 (one to three ulps apart), wide spread elsewhere
+        base = np.float32(100.0)
+        x[:, : c // 2] = base + (rng.integers(0, 4, (n * h * w, c // 2)) * np.spacing(base)).astype(np.float32)
+        x[rng.random(x.shape) < 0.3] *= np.float32(50.0)
+        gamma[: c // 2] = 1e-3
+    elif case == "negative_gamma":
+        gamma[::2] *= -1.0
+        x[rng.random(x.shape) < 0.2] = 0.0
+    elif case == "all_clamped":
+        beta[:] = -40.0
+    else:
+        x[rng.random(x.shape) < 0.1] = np.nan
+    xt = t(x)
+    bn = _stats(ops, t(np.nan_to_num(x)), c)  # statistics from finite data
+    gt, bt = t(gamma), t(beta)
+    act = torch.empty_like(xt)
+    ops.call("i8t_bn_act", ops.ctx(), ops._p(xt), n * h * w, c, ops._p(bn), ops._p(gt), ops._p(bt), 1, None, None, None,
+             None, None, ops._p(act))
+    P, Q = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    y = torch.empty((n, P, Q, c), device="cuda")
+    idx = torch.empty((n, P, Q, c), dtype=torch.uint8, device="cuda")
+    ops.call("i8t_maxpool_fwd", ops.ctx(), ops._p(xt), n, h, w, c, k, s, p, ops._p(bn), ops._p(gt), ops._p(bt), 1,
+             ops._p(y), ops._p(idx))
+    a = act.view(n, h, w, c).cpu().numpy()
+    want_y = np.empty((n, P, Q, c), np.float32)
+    want_i = np.empty((n, P, Q, c), np.uint8)
+    for pp in range(P):
+        for qq in range(Q):
+            best = np.full((n, c), -np.inf, np.float32)
+            arg = np.zeros((n, c), np.uint8)
+            for dy in range(k):
+                for dx in range(k):
+                    hh, ww = pp * s - p + dy, qq * s - p + dx
+                    if not (0 <= hh < h and 0 <= ww < w):
+                        continue
+                    v = a[:, hh, ww, :]
+                    upd = v > best
+                    best = np.where(upd, v, best)
+                    arg = np.where(upd, dy * k + dx, arg)
+            want_y[:, pp, qq, :], want_i[:, pp, qq, :] = best, arg
+    np.testing.assert_array_equal(y.cpu().numpy(), want_y)
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_i)

@@ -30,6 +30,7 @@ def timeit(fn, reps=10, warm=3):
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
+        torch.cuda._sleep(5_000_000)  # the GPU idles while the host queues flush + launch: no host gap inside s..e
         flush()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
