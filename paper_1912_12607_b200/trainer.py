@@ -207,7 +207,8 @@ class Trainer:
         return self.cfg.base_lr * 0.5 * (1.0 + math.cos(math.pi * it / total))
 
     # ---------------------------------------------------------------- step
-    def train_step(self, images, labels, it: int, total_iters: int, read_stats: bool = True) -> StepReport:
+    def train_step(self, images, labels, it: int, total_iters: int, read_stats: bool = True,
+                   _lr_preset: bool = False) -> StepReport:
         """Trainer::train_step (train.cpp:54-120).  images: NHWC float32 CUDA tensor."""
         cfg = self.cfg
         rep = StepReport(iter=it, base_lr_t=self.base_lr_at(it, total_iters))
@@ -239,7 +240,8 @@ class Trainer:
         h = ops.ctx()
         call("i8t_nonfinite_flag", h, ops._p(self.gflat), self.gflat.numel(), ops._p(self.skip))
         self.skip.bitwise_or_(self.div)
-        self.lr_dev.fill_(rep.base_lr_t)
+        if not _lr_preset:  # a graph replay sets the learning rate of its step before launching
+            self.lr_dev.fill_(rep.base_lr_t)
         call("i8t_sgd_dclr_multi", h, ops._p(self.pflat), ops._p(self.gflat), self.nseg, ops._p(self.seg_off),
              ops._p(self.seg_state), C.c_double(rep.base_lr_t), self.lr_dev, ops._p(self.skip), self.mflat,
              C.c_double(cfg.momentum))
@@ -253,6 +255,46 @@ class Trainer:
             rep.loss = float(self.loss_dev.item())
             rep.diverged = bool(self.skip.item())
             if bool(self.div.item()):  # the host mirrors of the restored DSGC states
+                self.sync_states()
+            self._read_layer_stats(rep)
+        return rep
+
+    # ---------------------------------------------------------------- CUDA graph replay
+    def graph_eligible(self, it: int) -> bool:
+        """A step can replay the captured graph when it launches exactly what the
+        captured step launched: INT8, single device, DSGC search enabled and
+        due on no layer (search steps and lazy-clip steps run eagerly), every
+        layer's buffers and clips in place (from the third step on)."""
+        cfg = self.cfg
+        if cfg.mode != Mode.INT8 or not cfg.clip_enabled or self.world > 1 or self._wq_buf is None:
+            return False
+        return not any(layer.qs.dsgc.due(it) or not (layer.qs.clip_w_set and layer.qs.clip_a_set)
+                       for _, layer in self.quant_layers)
+
+    def train_step_graphed(self, images, labels, it: int, total_iters: int, read_stats: bool = False) -> StepReport:
+        """train_step replayed from a CUDA graph captured on the first eligible
+        step (one graph per input buffer pair), eager otherwise.  The step has
+        no host sync, so the ~500 launches of ResNet-50 become one graph launch;
+        only the learning rate changes between replays and it is read from
+        device memory (lr_dev).  Bit-identical to train_step
+        (tests/test_gpu_graph.py)."""
+        if not self.graph_eligible(it):
+            return self.train_step(images, labels, it, total_iters, read_stats)
+        key = (images.data_ptr(), labels.data_ptr())
+        graphs = self.__dict__.setdefault("_graphs", {})
+        rep = StepReport(iter=it, base_lr_t=self.base_lr_at(it, total_iters))
+        self.lr_dev.fill_(rep.base_lr_t)
+        if key not in graphs:
+            pool = self.__dict__.setdefault("_graph_pool", torch.cuda.graph_pool_handle())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool):
+                self.train_step(images, labels, it, total_iters, read_stats=False, _lr_preset=True)
+            graphs[key] = g
+        graphs[key].replay()
+        if read_stats:
+            rep.loss = float(self.loss_dev.item())
+            rep.diverged = bool(self.skip.item())
+            if bool(self.div.item()):
                 self.sync_states()
             self._read_layer_stats(rep)
         return rep
