@@ -84,18 +84,34 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
   pdl_entry();
   constexpr int NV = 3 + 2 * NG;
   if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
-  __shared__ double dq_tab[NG * 256];
+  // NG <= 2 (memory-bound passes): dequantisation tables as separate high / low
+  // 32-bit words -- a lane's two 4-byte loads conflict only for entries 32
+  // apart, an 8-byte load from a double table for entries 16 apart (9.4 -> 6.8 ms
+  // for the single-candidate passes of a ResNet-50 search step).  NG = 8 is
+  // issue-bound: one 8-byte load per candidate beats two 4-byte loads there.
+  constexpr bool SPLIT = NG <= 2;
+  __shared__ uint32_t dq_w[NG * 512];  // SPLIT: [hi words | lo words] per candidate; else doubles
   const int j0 = blockIdx.y * NG;
   float hs[NG];
   bool tiny = false;  // a subnormal candidate scale: the exact function for every element
-  uint32_t tab_n[NG];  // dq_tab[j][q + 127] at the qn_bits pattern RMAGIC + q + 1 (32-bit wrap)
+  uint32_t tab_n[NG];  // table entry of q at the qn_bits pattern RMAGIC + q + 1 (32-bit wrap)
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(dq_w));
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
     const float cl = cands[min(j0 + j, nc - 1)];  // past nc: a duplicate, never scattered
     hs[j] = __fdiv_rn(0.5f, cl);
     tiny |= !(scale_of(cl) >= 0x1p-126f);
-    build_dequant_table(dq_tab + j * 256, scale_of(cl));
-    tab_n[j] = static_cast<uint32_t>(__cvta_generic_to_shared(dq_tab + j * 256)) + 8u * (126u - RMAGIC_BITS);
+    const float sc = scale_of(cl);
+    for (int i = threadIdx.x; i < 255; i += blockDim.x) {
+      const double d = __fmul_rn(static_cast<float>(i - 127), sc);
+      if (SPLIT) {
+        dq_w[j * 512 + i] = static_cast<uint32_t>(__double2hiint(d));
+        dq_w[j * 512 + 256 + i] = static_cast<uint32_t>(__double2loint(d));
+      } else {
+        reinterpret_cast<double*>(dq_w)[j * 256 + i] = d;
+      }
+    }
+    tab_n[j] = SPLIT ? base + 4u * (j * 512u + 126u - RMAGIC_BITS) : base + 8u * (j * 256u + 126u - RMAGIC_BITS);
   }
   __syncthreads();
   double acc[NV];
@@ -121,7 +137,13 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
     }
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      const double gh = lds_f64(tab_n[j] + 8u * kb[j]);
+      double gh;
+      if (SPLIT) {
+        const uint32_t a = tab_n[j] + 4u * kb[j];
+        gh = __hiloint2double(static_cast<int>(lds_u32(a)), static_cast<int>(lds_u32(a + 1024u)));
+      } else {
+        gh = lds_f64(tab_n[j] + 8u * kb[j]);
+      }
       acc[3 + 2 * j] = fma(vd, gh, acc[3 + 2 * j]);
       acc[4 + 2 * j] = fma(gh, gh, acc[4 + 2 * j]);
     }

@@ -116,6 +116,11 @@ __device__ __forceinline__ int quant_nearest_fast(float v, float clip, float hs,
   return static_cast<int>(kb) - (RMAGIC_BITS + 1);
 }
 // 8-byte shared load at a 32-bit shared-window address.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));

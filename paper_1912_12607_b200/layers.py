@@ -656,6 +656,9 @@ class Dense(Layer):
         if self.conv.quantize_enabled and ctx.mode == Mode.INT8:
             # sum_i s*q[i,o] in double == s * (integer sum) exactly (layers.cpp:214-220)
             sums = self.conv._qg.reshape(n, -1)[:, :self.out_f].sum(0, dtype=torch.int64)
+            if ctx.wgrad_allreduce is not None:  # data parallel: the integer sums across ranks (exact)
+                from . import dp
+                dp.allreduce_int64_(sums)
             scale = self.qs.dsgc.buf[_SCALE_OFF:_SCALE_OFF + 4].view(torch.float32)
             self.grad_bias.copy_((sums.double() * scale.double()).float())
             self.conv._qg = None

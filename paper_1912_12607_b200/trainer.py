@@ -146,12 +146,24 @@ class Trainer:
         """Every parameter / gradient becomes a view into one flat arena
         (segments padded to 4 floats) so the bad-gradient scan and the DCLR
         SGD step are one launch each."""
+        cfg = self.cfg
         segs, total = [], 0
-        for _, layer in self.leaves:
-            for owner, va, ga in layer.param_attrs():
-                v = getattr(owner, va)
-                segs.append((layer, owner, va, ga, total, v.numel(), v.shape))
-                total += (v.numel() + 3) // 4 * 4
+        # quantised layers' parameters first: their gradients are reduced as
+        # integer sums (int64 wgrad accumulators, the fc bias's int8 column
+        # sums), the rest (FP32 BN gradients) form one tail slice that a
+        # data-parallel step all-reduces in a single collective
+        attrs = [(layer, owner, va, ga) for _, layer in self.leaves for owner, va, ga in layer.param_attrs()]
+        exact = lambda t: t[0].quantized and (t[2] == "weight" or isinstance(t[0], Dense))  # noqa: E731
+        q = [t for t in attrs if exact(t)]  # int64-reduced under DP: conv / fc weights, fc bias (integer sums)
+        rest = [t for t in attrs if not exact(t)]
+        for layer, owner, va, ga in q + rest:
+            v = getattr(owner, va)
+            segs.append((layer, owner, va, ga, total, v.numel(), v.shape))
+            total += (v.numel() + 3) // 4 * 4
+            if (layer, owner, va, ga) == (q[-1] if q else None):
+                self.fp32_grad_off = total
+        if not q or cfg.mode != Mode.INT8:  # FP32 mode: every gradient is an FP32 sum
+            self.fp32_grad_off = 0
         self.pflat = torch.zeros(total, dtype=torch.float32, device=device)
         self.gflat = torch.zeros(total, dtype=torch.float32, device=device)
         offs, states = [], []
@@ -227,11 +239,14 @@ class Trainer:
         bctx = BackwardCtx(cfg.mode, it, self.grad_stream, cfg.grid_resolution, cfg.refine_rounds, cfg.clip_enabled,
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
                            self._wgrad_allreduce if self._hook is not None else None)
+        self._wgrad_step_begin()
         self.model.net.backward(g_logits, bctx)
         for work, finalize in bctx.deferred:  # int64 wgrad allreduces issued during the backward
             if work is not None:
                 work.wait()
             finalize()
+        if self._hook is not None:
+            self._wgrad_arena_build()
         if self.world > 1:
             params = [(layer, p) for _, layer in self.leaves for p in layer.params() if p.grad is not None]
             self._allreduce_fp32_grads(params)
@@ -330,18 +345,87 @@ class Trainer:
             layer.qs.dsgc.sync(v)
 
     # ---------------------------------------------------------------- data parallel
+    BUCKET_BYTES = 32 << 20  # int64 wgrad allreduce buckets (launch latency vs overlap)
+
     def _wgrad_allreduce(self, acc: torch.Tensor):
-        return dp.allreduce_int64_(acc, async_op=True)
+        """Exact int64 weight-gradient sum across ranks, bucketed.  The first
+        data-parallel step reduces layer by layer and records the order in
+        which the backward produces the accumulators; from then on every
+        layer's accumulator is a view into one int64 arena laid out in that
+        order, and a bucket (>= BUCKET_BYTES, or the last layer) is all-reduced
+        asynchronously as soon as its last layer is done, overlapping the rest
+        of the backward.  The returned handle's wait() covers the layer's bucket."""
+        st = self.__dict__.setdefault("_wg", {"order": [], "arena": None})
+        if st["arena"] is None:
+            st["order"].append(acc)
+            return dp.allreduce_int64_(acc, async_op=True)
+        i = st["next"]
+        st["next"] += 1
+        lo, hi = st["slices"][i]
+        if acc.data_ptr() != st["arena"][lo:hi].data_ptr():
+            raise RuntimeError("data parallel: the backward produced weight gradients in a new order")
+        h = st["handles"][i]
+        if i == st["bucket_end"][i]:  # last layer of its bucket: launch it
+            lo, hi = st["bucket_span"][i]
+            h.work = dp.allreduce_int64_(st["arena"][lo:hi], async_op=True)
+        return h
+
+    def _wgrad_arena_build(self):
+        """After the first data-parallel step: one int64 arena in backward order,
+        each layer's accumulator rebound to its slice, buckets fixed."""
+        st = self.__dict__.get("_wg")
+        if not st or st["arena"] is not None or not st["order"]:
+            return
+        accs = st["order"]
+        owners = {}
+        for _, layer in self.quant_layers:
+            conv = getattr(layer, "conv", layer)
+            if conv.wgrad_acc is not None:
+                owners[conv.wgrad_acc.data_ptr()] = conv
+        total = sum(a.numel() for a in accs)
+        arena = torch.zeros(total, dtype=torch.int64, device=accs[0].device)
+        off, spans, ends, b0, bbytes = 0, [], [], 0, 0
+        for i, a in enumerate(accs):
+            conv = owners[a.data_ptr()]
+            conv.wgrad_acc = arena[off: off + a.numel()].view(a.shape)
+            off += a.numel()
+            bbytes += a.numel() * 8
+            if bbytes >= self.BUCKET_BYTES or i == len(accs) - 1:
+                for j in range(b0, i + 1):
+                    spans.append(None)
+                    ends.append(i)
+                spans[i] = (sum(x.numel() for x in accs[:b0]), off)
+                b0, bbytes = i + 1, 0
+
+        class _Bucket:
+            work = None
+
+            def wait(self):
+                if self.work is not None:
+                    self.work.wait()
+        handles = []
+        for i in range(len(accs)):
+            handles.append(_Bucket() if ends[i] == i else None)
+        for i in range(len(accs)):  # layers share their bucket's handle
+            handles[i] = handles[ends[i]]
+        slices, o = [], 0
+        for a in accs:
+            slices.append((o, o + a.numel()))
+            o += a.numel()
+        st.update(arena=arena, bucket_end=ends, bucket_span=spans, handles=handles, slices=slices, next=0)
+
+    def _wgrad_step_begin(self):
+        st = self.__dict__.get("_wg")
+        if st and st["arena"] is not None:
+            st["next"] = 0
+            for h in st["handles"]:
+                h.work = None
 
     def _allreduce_fp32_grads(self, params):
-        flat = [p.grad for layer, p in params if not (layer.quantized and p.name == "weight")]
-        if flat:
-            buf = torch.cat([t.reshape(-1) for t in flat])
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
-            off = 0
-            for t in flat:
-                t.copy_(buf[off: off + t.numel()].view_as(t))
-                off += t.numel()
+        """FP32 parameter gradients (BN gamma / beta, fc bias): one contiguous
+        slice of the gradient arena (quantised weights are laid out first)."""
+        if self.fp32_grad_off < self.gflat.numel():
+            dist.all_reduce(self.gflat[self.fp32_grad_off:], op=dist.ReduceOp.SUM)
 
 
 def synthetic_batch(model, batch, seed, device="cuda"):
