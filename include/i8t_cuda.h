@@ -111,6 +111,14 @@ uint64_t i8t_launch_count(void);
 typedef int (*i8t_allreduce_fn)(void* user, void* dev_buf, int64_t count, int dtype, int op, void* stream);
 int i8t_ctx_set_allreduce(i8t_ctx* ctx, i8t_allreduce_fn fn, void* user);
 int i8t_ctx_set_shard(i8t_ctx* ctx, int rank, int world);
+/* Data parallelism without a host callback: the context owns an NCCL
+ * communicator (libnccl.so.2 resolved at run time) and combines the gradient
+ * quantiser's statistics with an all-gather + fixed-order fold on its stream
+ * (no host sync; graph-capturable).  Rank 0 makes the id, every rank passes
+ * the same bytes (>= 128) with its rank / world; this also sets the shard
+ * (i8t_ctx_set_shard).  id == NULL detaches. */
+int i8t_nccl_unique_id(uint8_t* out, int64_t bytes);
+int i8t_ctx_set_nccl(i8t_ctx* ctx, const uint8_t* id, int64_t bytes, int rank, int world);
 
 /* ------------------------------------------------------------ LCG stream */
 /* The gradient stream of LcgStream (quantize.hpp:32-50) lives in device memory

@@ -93,7 +93,9 @@ void* ensure_fold(Ctx* c, size_t bytes) {
 }
 
 int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op) {
-  if (!c->allreduce || count <= 0) return I8T_OK;
+  if (count <= 0) return I8T_OK;
+  if (c->nccl_comm) return ctx_allreduce_nccl(c, buf, count, op);
+  if (!c->allreduce) return I8T_OK;
   const int rc = c->allreduce(c->allreduce_user, buf, count, 0, op, c->stream);
   return rc ? set_error(I8T_ECUDA, "allreduce hook failed") : I8T_OK;
 }
@@ -189,6 +191,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (!ctx) return I8T_OK;
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   cudaStreamSynchronize(c->stream);
+  ctx_comm_destroy(c);
   if (c->d_err) cudaFree(c->d_err);
   if (c->d_partials) cudaFree(c->d_partials);
   if (c->d_scratch) cudaFree(c->d_scratch);

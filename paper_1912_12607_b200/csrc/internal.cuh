@@ -73,7 +73,15 @@ struct Ctx {
   i8t_allreduce_fn allreduce = nullptr;
   void* allreduce_user = nullptr;
   int rank = 0, world = 1;
+  // or an NCCL communicator owned by the context (comm.cu): the statistics are
+  // all-gathered on `stream` and folded in rank order
+  void* nccl_comm = nullptr;
+  double* d_gather = nullptr;  // [world][gather_cap]
+  int64_t gather_cap = 0;
 };
+
+int ctx_allreduce_nccl(Ctx* c, double* buf, int64_t count, int op);
+int ctx_comm_destroy(Ctx* c);
 
 // Runs the allreduce hook (if any) on `count` device doubles: op 0 = SUM, 1 = MAX.
 int ctx_allreduce(Ctx* c, double* buf, int64_t count, int op);

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -116,9 +117,22 @@ class Trainer:
         self.rank = dist.get_rank() if self.world > 1 else 0
         self._hook = None
         if self.world > 1 or force_dp_hook:  # force: exercise the data-parallel phases at world size 1
-            self._hook = _DistHook()
-            call("i8t_ctx_set_allreduce", ops.ctx(), C.cast(self._hook.cfn, C.c_void_p), None)
-            call("i8t_ctx_set_shard", ops.ctx(), self.rank, self.world)
+            if self.world > 1 and dist.get_backend() == "nccl" and os.environ.get("I8T_DP_COMM", "nccl") == "nccl":
+                # the library's own NCCL communicator combines the DSGC statistics
+                # on the compute stream (no host callback inside the backward)
+                self._hook = "nccl"
+                ident = torch.zeros(128, dtype=torch.uint8, device=device)
+                if self.rank == 0:
+                    raw = (C.c_uint8 * 128)()
+                    call("i8t_nccl_unique_id", C.cast(raw, C.c_void_p), 128)
+                    ident.copy_(torch.tensor(list(raw), dtype=torch.uint8))
+                dist.broadcast(ident, 0)
+                raw = (C.c_uint8 * 128)(*ident.cpu().tolist())
+                call("i8t_ctx_set_nccl", ops.ctx(), C.cast(raw, C.c_void_p), 128, self.rank, self.world)
+            else:  # gloo (tests) or I8T_DP_COMM=python: torch.distributed through a host callback
+                self._hook = _DistHook()
+                call("i8t_ctx_set_allreduce", ops.ctx(), C.cast(self._hook.cfn, C.c_void_p), None)
+                call("i8t_ctx_set_shard", ops.ctx(), self.rank, self.world)
         # the gradient w.r.t. the input images is discarded: the first conv skips backward-data
         first = self.leaves[0][1]
         if hasattr(first, "need_input_grad"):

@@ -99,3 +99,29 @@ def test_data_parallel_quantiser_equals_single_device(ops, tmp_path):
                         torch.from_numpy(a).cuda(), 64, one, one, acc=acc)
     for r in ranks:
         np.testing.assert_array_equal(r["acc"], acc.cpu().numpy())
+
+
+def test_nccl_communicator_in_the_context(ops):
+    """The library-owned NCCL communicator (comm.cu) on a world of one: the
+    statistics go through ncclAllGather + the fixed-order fold on the stream;
+    quantiser results must equal the communicator-free path bit for bit."""
+    import ctypes as C
+    g = torch.from_numpy(_grad(4, 64, 14, 9)).cuda()
+
+    def run():
+        st = ops.DsgcState(period=100)
+        lcg = ops.new_lcg_state(5)
+        q = [ops.quantize_gradient(st, g, it, lcg, nhwc=True).cpu().numpy() for it in range(2)]
+        v = st.view()
+        return q, (v.clip, v.last_dc, v.eps_norm, v.ghat_sqnorm), ops.lcg_value(lcg)
+    ref = run()
+    raw = (C.c_uint8 * 128)()
+    ops.call("i8t_nccl_unique_id", C.cast(raw, C.c_void_p), 128)
+    ops.call("i8t_ctx_set_nccl", ops.ctx(), C.cast(raw, C.c_void_p), 128, 0, 1)
+    try:
+        got = run()
+    finally:
+        ops.call("i8t_ctx_set_nccl", ops.ctx(), None, 0, 0, 1)
+    for a, b in zip(ref[0], got[0]):
+        np.testing.assert_array_equal(a, b)
+    assert ref[1:] == got[1:]
