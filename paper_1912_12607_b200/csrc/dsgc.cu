@@ -461,7 +461,7 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
   // data parallelism every rank takes the same branch (global totals), and a
   // skipped pass contributes a zero totals buffer to the hook.
   auto pass = [&](int nc) -> int {
-    if (c->allreduce) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * nc), c->stream);
+    if (ctx_dp(c)) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * nc), c->stream);
     int r = dc_pass_n(c, g, n, st->cand, &st->active, nc);
     if (r || (r = allreduce_totals(c, 3 + 2 * nc))) return r;
     launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, nc, R, rounds);

@@ -81,6 +81,8 @@ struct Ctx {
 };
 
 int ctx_allreduce_nccl(Ctx* c, double* buf, int64_t count, int op);
+// data parallelism active: statistics must be combined across ranks
+inline bool ctx_dp(const Ctx* c) { return c->allreduce != nullptr || c->nccl_comm != nullptr; }
 int ctx_comm_destroy(Ctx* c);
 
 // Runs the allreduce hook (if any) on `count` device doubles: op 0 = SUM, 1 = MAX.

@@ -204,7 +204,7 @@ inline int gcd_i(int64_t a, int64_t b) { return b == 0 ? static_cast<int>(a) : g
 // Global totals for data parallelism: totals[0] MAX, totals[1..nv) SUM.
 // One collective per phase: op 2 = MAX on element 0, SUM on the rest.
 inline int allreduce_totals(Ctx* c, int nv) {
-  if (!c->allreduce) return I8T_OK;
+  if (!ctx_dp(c)) return I8T_OK;
   return ctx_allreduce(c, c->d_totals, nv, 2);
 }
 
@@ -236,7 +236,7 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
     step_wrap = lcg_jump_map(static_cast<uint64_t>(C - 1) * static_cast<uint64_t>(HW));
   }
   fin.advance = static_cast<uint32_t>(static_cast<uint64_t>(c->world) * static_cast<uint64_t>(numel));
-  const bool fused = (c->allreduce == nullptr);
+  const bool fused = !ctx_dp(c);
   const uint32_t un = static_cast<uint32_t>(numel), uc = static_cast<uint32_t>(flat ? 1 : C),
                  uhw = static_cast<uint32_t>(flat ? numel : HW);
 #define LAUNCH(F, D, U)                                                                                  \

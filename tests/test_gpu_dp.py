@@ -114,14 +114,19 @@ def test_nccl_communicator_in_the_context(ops):
         q = [ops.quantize_gradient(st, g, it, lcg, nhwc=True).cpu().numpy() for it in range(2)]
         v = st.view()
         return q, (v.clip, v.last_dc, v.eps_norm, v.ghat_sqnorm), ops.lcg_value(lcg)
+    n0 = ops.launch_count()
     ref = run()
+    n_ref = ops.launch_count() - n0
     raw = (C.c_uint8 * 128)()
     ops.call("i8t_nccl_unique_id", C.cast(raw, C.c_void_p), 128)
     ops.call("i8t_ctx_set_nccl", ops.ctx(), C.cast(raw, C.c_void_p), 128, 0, 1)
     try:
+        n0 = ops.launch_count()
         got = run()
+        n_comm = ops.launch_count() - n0
     finally:
         ops.call("i8t_ctx_set_nccl", ops.ctx(), None, 0, 0, 1)
+    assert n_comm > n_ref  # the statistics really went through the communicator (one fold per phase)
     for a, b in zip(ref[0], got[0]):
         np.testing.assert_array_equal(a, b)
     assert ref[1:] == got[1:]
