@@ -437,7 +437,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         for (int kt = 0; kt < nk; ++kt, ++kc) {
           const int s = kc % C::STAGES;
           mbar_wait(&full[s], (kc / C::STAGES) & 1);
-          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma operand reads
+          // cp.async (generic proxy) writes -> tcgen05.mma operand reads; TMA-only
+          // stages were written by the async proxy and need no proxy fence
+          if (!args.tma_a) fence_proxy_async_smem();
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKB / 32; ++kk) {
