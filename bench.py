@@ -470,7 +470,7 @@ def main():
     att_ms = attainable_conv_ms(a.model, a.batch, peak)
     traffic = None  # DRAM bytes of all conv launches of one step, from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_conv_dram_step.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_conv_dram_step.json")) as f:
             traffic = json.load(f)["traffic_bytes_per_step"] if a.model == "resnet50" and a.batch == 256 else None
     except Exception:
         traffic = None
@@ -490,7 +490,7 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_note": "DRAM bytes per step summed over the conv launches (profiles/r1_conv_dram_step.json)",
+                     "traffic_note": "DRAM bytes per step summed over the conv launches (profiles/r2_conv_dram_step.json; ncu --cache-control none: dirty-line write-backs counted)",
                      "peak_source": peak_src,
                      "nominal_peak": 4500.0, "frac_nominal": achieved / 4500.0,
                      "kernel": "k_conv_tc + k_conv_sw (fwd+dgrad+wgrad, all ResNet-50 convs)",
