@@ -242,6 +242,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             continue;
           }
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
+          if (MODE == MODE_FWD && args.tma_a == 2) {
+            // implicit im2col by TMA: 128 consecutive output pixels of tap (r, s),
+            // 128 channels from cb; zero padding = out-of-box fill
+            const int pq = args.P * args.Q;
+            const int n = m0 / pq, rem = m0 - n * pq, p = rem / args.Q, q = rem - p * args.Q;
+            const int tap = kb / args.Cp, cb = kb - tap * args.Cp;
+            const int r = tap / args.S, sx = tap - r * args.S;
+            tma_load_im2col_4d(a_st, &tmap_a, &full[s], cb, q * args.sw - args.pw, p * args.sh - args.ph, n,
+                               static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+            tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
+            continue;
+          }
           if constexpr (MODE == MODE_WGRAD) {
             tma_load_2d(a_st, &tmap_a, &full[s], m0, kb);  // [128 npq rows][128 channels], MN-major
 #pragma unroll
@@ -825,6 +837,56 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+static EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
+// NHWC int8 activations [N][H][W][Cp] -> im2col TMA map: 128-pixel columns of
+// 128 channels (SWIZZLE_128B, the K-major A tile), the pixel box of the output
+// positions (lower = -pad, upper = pad - (k - 1)), traversal strides (sw, sh).
+static int make_im2col_map(CUtensorMap* map, const int8_t* a, const i8t_conv_geom* g, int64_t c_pad) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col unavailable");
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(g->w), static_cast<cuuint64_t>(g->h),
+                        static_cast<cuuint64_t>(g->n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(g->w * c_pad),
+                           static_cast<cuuint64_t>(g->h * g->w * c_pad)};
+  const int lower[2] = {static_cast<int>(-g->pad_w), static_cast<int>(-g->pad_h)};
+  const int upper[2] = {static_cast<int>(g->pad_w - (g->kw - 1)), static_cast<int>(g->pad_h - (g->kh - 1))};
+  cuuint32_t estr[4] = {1u, static_cast<cuuint32_t>(g->stride_w), static_cast<cuuint32_t>(g->stride_h), 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(a), dims, strides, lower, upper, 128u,
+                  static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
+  return I8T_OK;
+}
+
+// Forward convs whose A operand TMA im2col can load: 128-channel blocks, the
+// output grid exactly the pixel box (floor mode with an exact fit), offsets in
+// range.  I8T_NO_IM2COL=1 keeps the cp.async gather (A/B experiments).
+static bool im2col_ok(const i8t_conv_geom* g, int64_t c_pad, const void* a, int64_t P, int64_t Q) {
+  static const bool off = getenv("I8T_NO_IM2COL") != nullptr;
+  if (off || g->depthwise || c_pad % 128 != 0 || (reinterpret_cast<uintptr_t>(a) & 15u)) return false;
+  if (g->kh * g->kw == 1 && g->stride_h == 1 && g->stride_w == 1 && g->pad_h == 0 && g->pad_w == 0) return false;
+  if (g->stride_h > 8 || g->stride_w > 8 || g->kh > 8 || g->kw > 8 || g->pad_h >= g->kh || g->pad_w >= g->kw) return false;
+  // the box [-pad, W - 1 + pad - (k - 1)] traversed with stride s has exactly
+  // floor((W + 2 pad - k) / s) + 1 = Q positions per row (P per column)
+  return (g->w + 2 * g->pad_w - g->kw) / g->stride_w + 1 == Q && (g->h + 2 * g->pad_h - g->kh) / g->stride_h + 1 == P;
+}
+
 // 2-D int8 weight matrix [rows][ld] -> TMA map with box {128 B, box_rows}, SWIZZLE_128B.
 static int make_weight_map(CUtensorMap* map, const int8_t* w, int64_t rows, int64_t ld, int box_rows) {
   EncodeTiledFn fn = encode_fn();
@@ -1091,6 +1153,9 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   if (plain_1x1(g, a, c_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, a, x.M, c_pad, BM))) return rc;
+  } else if (im2col_ok(g, c_pad, a, P, Q)) {
+    x.tma_a = 2;
+    if ((rc = make_im2col_map(&amap, a, g, c_pad))) return rc;
   }
   x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;
