@@ -255,11 +255,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             continue;
           }
           if constexpr (MODE == MODE_WGRAD) {
-            tma_load_2d(a_st, &tmap_a, &full[s], m0, kb);  // [128 npq rows][128 channels], MN-major
+            if (args.tma_a == 2) {  // im2col rows npq = kb.. of tap (r, s), channels c0 of the m-tile
+              const int pq = args.P * args.Q;
+              const int n = kb / pq, rem = kb - n * pq, p = rem / args.Q, q = rem - p * args.Q;
+              const int tap = m0 / args.Cp, c0 = m0 - tap * args.Cp;
+              const int r = tap / args.S, sx = tap - r * args.S;
+              tma_load_im2col_4d(a_st, &tmap_a, &full[s], c0, q * args.sw - args.pw, p * args.sh - args.ph, n,
+                                 static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+            } else {
+              tma_load_2d(a_st, &tmap_a, &full[s], m0, kb);  // [128 npq rows][128 channels], MN-major
+            }
 #pragma unroll
             for (int sub = 0; sub < C::B_SUB; ++sub) tma_load_2d(b_st + sub * 16384, &tmap_b, &full[s], n0 + sub * 128, kb);
           } else {
-            tma_load_2d(a_st, &tmap_a, &full[s], kb, m0);  // [128 pixel rows][128 B of channels], K-major
+            if (MODE == MODE_DGRAD && args.tma_a == 2) {
+              // stride-1 backward-data as the im2col of g_z over the input grid:
+              // tap (r, s) reads g_z at (h + ph - r, w + pw - s) = base (h - (R-1-ph),
+              // w - (S-1-pw)) + mirrored offset (R-1-r, S-1-s)
+              const int hw = args.H * args.W;
+              const int n = m0 / hw, rem = m0 - n * hw, h = rem / args.W, w = rem - h * args.W;
+              const int tap = kb / args.Kp, kc = kb - tap * args.Kp;
+              const int r = tap / args.S, sx = tap - r * args.S;
+              tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, w - (args.S - 1 - args.pw), h - (args.R - 1 - args.ph), n,
+                                 static_cast<uint16_t>(args.S - 1 - sx), static_cast<uint16_t>(args.R - 1 - r));
+            } else {
+              tma_load_2d(a_st, &tmap_a, &full[s], kb, m0);  // [128 pixel rows][128 B of channels], K-major
+            }
             tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
           }
         }
@@ -854,24 +875,31 @@ static EncodeIm2colFn encode_im2col_fn() {
   return fn;
 }
 
-// NHWC int8 activations [N][H][W][Cp] -> im2col TMA map: 128-pixel columns of
-// 128 channels (SWIZZLE_128B, the K-major A tile), the pixel box of the output
-// positions (lower = -pad, upper = pad - (k - 1)), traversal strides (sw, sh).
-static int make_im2col_map(CUtensorMap* map, const int8_t* a, const i8t_conv_geom* g, int64_t c_pad) {
+// NHWC int8 tensor [N][H][W][C] -> im2col TMA map: 128-pixel columns of 128
+// channels (SWIZZLE_128B: the K-major A tile of FWD / DGRAD and the MN-major
+// A tile of WGRAD alike), traversing the pixel box [lower, dim - 1 + upper]
+// with strides (sw, sh); out-of-tensor taps are zero-filled.
+static int make_im2col_map(CUtensorMap* map, const int8_t* t, int64_t N, int64_t H, int64_t W, int64_t C, int lower_w,
+                           int lower_h, int upper_w, int upper_h, int sw, int sh) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col unavailable");
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(g->w), static_cast<cuuint64_t>(g->h),
-                        static_cast<cuuint64_t>(g->n)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(g->w * c_pad),
-                           static_cast<cuuint64_t>(g->h * g->w * c_pad)};
-  const int lower[2] = {static_cast<int>(-g->pad_w), static_cast<int>(-g->pad_h)};
-  const int upper[2] = {static_cast<int>(g->pad_w - (g->kw - 1)), static_cast<int>(g->pad_h - (g->kh - 1))};
-  cuuint32_t estr[4] = {1u, static_cast<cuuint32_t>(g->stride_w), static_cast<cuuint32_t>(g->stride_h), 1u};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(a), dims, strides, lower, upper, 128u,
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W * C), static_cast<cuuint64_t>(H * W * C)};
+  const int lower[2] = {lower_w, lower_h};
+  const int upper[2] = {upper_w, upper_h};
+  cuuint32_t estr[4] = {1u, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(sh), 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(t), dims, strides, lower, upper, 128u,
                   static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
   return I8T_OK;
+}
+// the forward / backward-weight activation map: box = the output positions
+static int make_im2col_map(CUtensorMap* map, const int8_t* a, const i8t_conv_geom* g, int64_t c_pad) {
+  return make_im2col_map(map, a, g->n, g->h, g->w, c_pad, static_cast<int>(-g->pad_w), static_cast<int>(-g->pad_h),
+                         static_cast<int>(g->pad_w - (g->kw - 1)), static_cast<int>(g->pad_h - (g->kh - 1)),
+                         static_cast<int>(g->stride_w), static_cast<int>(g->stride_h));
 }
 
 // Forward convs whose A operand TMA im2col can load: 128-channel blocks, the
@@ -1233,6 +1261,14 @@ static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   if (plain_1x1(g, gz, k_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, gz, x.M, k_pad, BM))) return rc;
+  } else if (g->stride_h == 1 && g->stride_w == 1 && im2col_ok(g, k_pad, gz, P, Q) && P + g->kh - 1 - 2 * g->pad_h == g->h &&
+             Q + g->kw - 1 - 2 * g->pad_w == g->w) {
+    // g_z [N][P][Q][k_pad] traversed over the input positions: box [-(S-1-pw), Q-1-pw]
+    x.tma_a = 2;
+    if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, static_cast<int>(-(g->kw - 1 - g->pad_w)),
+                              static_cast<int>(-(g->kh - 1 - g->pad_h)), static_cast<int>(-g->pad_w),
+                              static_cast<int>(-g->pad_h), 1, 1)))
+      return rc;
   }
   x.use_tma_out = tma_out_ok(ga, g->c) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, ga, g->c, x.M, g->c, false))) return rc;
@@ -1313,6 +1349,9 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   if (plain_1x1(g, a, c_pad, gz, k_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, a, x.Kd, c_pad, BKB))) return rc;   // [npq][c_pad], box {128 ch, 128 rows}
+  } else if (im2col_ok(g, c_pad, a, P, Q) && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
+    x.tma_a = 2;  // A = im2col of the activations (128 npq rows x 128 channels of one tap), B = g_z rows
+    if ((rc = make_im2col_map(&amap, a, g, c_pad))) return rc;
   }
   static const bool no_tma_b = getenv("I8T_NO_TMA_A") != nullptr;
   if (x.tma_a || (!no_tma_b && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0)) {
