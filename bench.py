@@ -401,7 +401,7 @@ def main():
         nonlocal it
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches0 = ops.launch_count()
+        launches0 = ops.launch_count() + tr.graph_replayed_launches
         comp = torch.cuda.current_stream()
         ev0.record()
         if e2e:
@@ -435,7 +435,7 @@ def main():
         barrier()
         if e2e:
             assert torch.isfinite(loss_host).all(), "non-finite loss in the e2e run"
-        return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() - launches0
+        return max_over_ranks(ev0.elapsed_time(ev1)), ops.launch_count() + tr.graph_replayed_launches - launches0
 
     if os.environ.get("I8T_PROFILE_STEP"):  # ncu --profile-from-start off: capture exactly one step
         if os.environ.get("I8T_PROFILE_STEP") == "search":  # ... the DSGC search step (Periodic Update)
@@ -453,7 +453,11 @@ def main():
     # e2e through the public API: pinned host batch -> device each step, loss read back each step
     host = (x.cpu().pin_memory(), y.cpu().pin_memory())
     ms_e2e, _ = timed(a.steps, e2e=True, host=host)
-    # one DSGC search step (Periodic Update, every clip_period iterations), amortised
+    # one DSGC search step (Periodic Update, every clip_period iterations), amortised;
+    # an untimed one first: the eager search path allocates its activations once
+    # (the graph replays live in their own memory pool)
+    it = ((it // cfg.clip_period) + 1) * cfg.clip_period
+    timed(1)
     it = ((it // cfg.clip_period) + 1) * cfg.clip_period
     ms_search, _ = timed(1)
     extra = max(ms_search - ms / a.steps, 0.0) / cfg.clip_period

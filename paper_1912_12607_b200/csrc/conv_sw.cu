@@ -378,7 +378,11 @@ int conv_sw_run(Ctx* c, bool dgrad, const i8t_conv_geom* g, const int8_t* in, in
 bool conv_sw_eligible(const i8t_conv_geom* g, int64_t Cred, int Ng, int OH, int OW, const void* in, const void* out,
                       int64_t ldw) {
   static const bool off = getenv("I8T_NO_CONV_SW") != nullptr;
-  if (off || g->depthwise || g->stride_h != 1 || g->stride_w != 1) return false;
+  static const int max_c = [] {  // tuning experiments: widest reduction channel count routed here
+    const char* e = getenv("I8T_CONV_SW_MAXC");
+    return e ? atoi(e) : 1 << 30;
+  }();
+  if (off || g->depthwise || g->stride_h != 1 || g->stride_w != 1 || Cred > max_c) return false;
   if (!((g->kh == 3 && g->kw == 3) || (g->kh == 1 && g->kw == 3) || (g->kh == 3 && g->kw == 1))) return false;
   if (Cred % sw::CC != 0 || Ng % 4 != 0 || ldw % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(in) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u) || !out) return false;

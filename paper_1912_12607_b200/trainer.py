@@ -151,6 +151,7 @@ class Trainer:
         self._err = _DistHook._view_i32(C.cast(ptr, C.c_void_p).value)
         self._wq_buf, self._wq_n = None, 0  # device i8t_wq_desc array (built at the second step)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=device)
+        self.graph_replayed_launches = 0
         self.lr_dev = torch.zeros(1, dtype=torch.float64, device=device)
         self._build_param_arenas(device)
         if self.world > 1:  # identical initial parameters on every rank (seeded alike; made certain)
@@ -316,10 +317,13 @@ class Trainer:
         if key not in graphs:
             pool = self.__dict__.setdefault("_graph_pool", torch.cuda.graph_pool_handle())
             g = torch.cuda.CUDAGraph()
+            n0 = ops.launch_count()
             with torch.cuda.graph(g, pool=pool):
                 self.train_step(images, labels, it, total_iters, read_stats=False, _lr_preset=True)
-            graphs[key] = g
-        graphs[key].replay()
+            graphs[key] = (g, ops.launch_count() - n0)
+        g, n = graphs[key]
+        g.replay()
+        self.graph_replayed_launches += n  # this library's kernels inside the replayed graph
         if read_stats:
             rep.loss = float(self.loss_dev.item())
             rep.diverged = bool(self.skip.item())

@@ -119,11 +119,9 @@ def test_momentum_step_matches_oracle():
         if it == 0:  # identical inputs: the buffers are the gradients (BN's last bits aside)
             segs = [p for _, layer in tr.leaves for p in layer.params()]
             om = [otr.mom[(i, j)] for i, (_, l) in enumerate(otr.leaves) for j in range(len(l.params()))]
-            off = 0
             mf = tr.mflat.cpu().numpy()
-            for p, ob in zip(segs, om):
-                n = p.value.numel()
-                got = mf[off:off + n].reshape(ob.shape)
+            for p, ob in zip(segs, om):  # a parameter's momentum sits at its offset in the parameter arena
+                off = (p.value.data_ptr() - tr.pflat.data_ptr()) // 4
+                got = mf[off:off + p.value.numel()].reshape(ob.shape)
                 np.testing.assert_allclose(got, ob, rtol=1e-4, atol=1e-6 * float(np.abs(ob).max()), err_msg=p.name)
-                off += (n + 3) // 4 * 4
         _adopt(tr, net)
