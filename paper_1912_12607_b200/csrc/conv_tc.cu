@@ -237,7 +237,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             // both CTAs' A and B halves complete on the leader's barrier
             if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_BYTES));
             const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
-            tma_load_2d_pair(a_st, &tmap_a, lbar, kb, m0);
+            if (MODE == MODE_FWD && args.tma_a == 2) {  // this CTA's 128 output pixels, im2col
+              const int pq = args.P * args.Q;
+              const int n = m0 / pq, rem = m0 - n * pq, p = rem / args.Q, q = rem - p * args.Q;
+              const int tap = kb / args.Cp, cb = kb - tap * args.Cp;
+              const int r = tap / args.S, sx = tap - r * args.S;
+              tma_load_im2col_4d_pair(a_st, &tmap_a, lbar, cb, q * args.sw - args.pw, p * args.sh - args.ph, n,
+                                      static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+            } else if (MODE == MODE_DGRAD && args.tma_a == 2) {
+              const int hw = args.H * args.W;
+              const int n = m0 / hw, rem = m0 - n * hw, h = rem / args.W, w = rem - h * args.W;
+              const int tap = kb / args.Kp, kc = kb - tap * args.Kp;
+              const int r = tap / args.S, sx = tap - r * args.S;
+              tma_load_im2col_4d_pair(a_st, &tmap_a, lbar, kc, w - (args.S - 1 - args.pw), h - (args.R - 1 - args.ph),
+                                      n, static_cast<uint16_t>(args.S - 1 - sx), static_cast<uint16_t>(args.R - 1 - r));
+            } else {
+              tma_load_2d_pair(a_st, &tmap_a, lbar, kb, m0);
+            }
             tma_load_2d_pair(b_st, &tmap_b, lbar, kb, n0 + static_cast<int>(crank) * (BN / 2));
             continue;
           }
@@ -1176,7 +1192,7 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   const int bn = pick_bn_balanced(g->k, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->k + bn - 1) / bn); x.splits = 1;
   CUtensorMap amap{}, map, omap{};
-  const bool pair = pair_enabled() && bn == 256 && plain_1x1(g, a, c_pad);
+  const bool pair = pair_enabled() && bn == 256 && (plain_1x1(g, a, c_pad) || im2col_ok(g, c_pad, a, P, Q));
   if ((rc = make_weight_map(&map, w, g->k, ld_w, pair ? bn / 2 : bn))) return rc;
   if (plain_1x1(g, a, c_pad)) {
     x.tma_a = 1;
@@ -1256,13 +1272,14 @@ static int dgrad_impl(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, in
   const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
   x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
   CUtensorMap amap{}, map, omap{};
-  const bool pair = pair_enabled() && bn == 256 && plain_1x1(g, gz, k_pad) && !add_g;
+  const bool dg_im2col = g->stride_h == 1 && g->stride_w == 1 && im2col_ok(g, k_pad, gz, P, Q) &&
+                         P + g->kh - 1 - 2 * g->pad_h == g->h && Q + g->kw - 1 - 2 * g->pad_w == g->w;
+  const bool pair = pair_enabled() && bn == 256 && (plain_1x1(g, gz, k_pad) || dg_im2col) && !add_g;
   if ((rc = make_weight_map(&map, wt, g->c, ld_wt, pair ? bn / 2 : bn))) return rc;
   if (plain_1x1(g, gz, k_pad)) {
     x.tma_a = 1;
     if ((rc = make_weight_map(&amap, gz, x.M, k_pad, BM))) return rc;
-  } else if (g->stride_h == 1 && g->stride_w == 1 && im2col_ok(g, k_pad, gz, P, Q) && P + g->kh - 1 - 2 * g->pad_h == g->h &&
-             Q + g->kw - 1 - 2 * g->pad_w == g->w) {
+  } else if (dg_im2col) {
     // g_z [N][P][Q][k_pad] traversed over the input positions: box [-(S-1-pw), Q-1-pw]
     x.tma_a = 2;
     if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, static_cast<int>(-(g->kw - 1 - g->pad_w)),
