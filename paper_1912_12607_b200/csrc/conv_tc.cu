@@ -58,6 +58,7 @@ struct ConvArgs {
   // q = ww + dw - is), every k-tile inside one tap (Kp % 128 == 0).
   int phase;
   int Hq, Wq, fh, fw, r0, s0, ns, dh, dw;
+  int nr;  // phase taps along r (with ns along s)
   // 1x1 / stride 1 / pad 0: the A operand rows are plain matrix rows, loaded
   // by TMA (tmap_a; WGRAD also takes its B = g_z rows from tmap_b) by one
   // thread -- no cp.async gather
@@ -284,6 +285,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
 #pragma unroll
             for (int sub = 0; sub < C::B_SUB; ++sub) tma_load_2d(b_st + sub * 16384, &tmap_b, &full[s], n0 + sub * 128, kb);
           } else {
+            if (MODE == MODE_DGRAD && args.tma_a == 2 && args.phase) {
+              // one stride phase: rows (n, hh, ww) of the phase grid, compact tap
+              // (ir, is) reads g_z at (hh + dh - ir, ww + dw - is) = base (hh + dh -
+              // (nr-1), ww + dw - (ns-1)) + mirrored offset (nr-1-ir, ns-1-is)
+              const int hwq = args.Hq * args.Wq;
+              const int n = m0 / hwq, rem = m0 - n * hwq, hh = rem / args.Wq, ww = rem - hh * args.Wq;
+              const int it = kb / args.Kp, kc = kb - it * args.Kp;
+              const int ir = it / args.ns, is = it - ir * args.ns;
+              tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, ww + args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n,
+                                 static_cast<uint16_t>(args.ns - 1 - is), static_cast<uint16_t>(args.nr - 1 - ir));
+              const int bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp + kc;
+              tma_load_2d(b_st, &tmap_b, &full[s], bx, n0);
+              continue;
+            }
             if (MODE == MODE_DGRAD && args.tma_a == 2) {
               // stride-1 backward-data as the im2col of g_z over the input grid:
               // tap (r, s) reads g_z at (h + ph - r, w + pw - s) = base (h - (R-1-ph),
@@ -1137,6 +1152,7 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
         continue;
       }
       x.Kd = (int64_t)nr * x.ns * k_pad;
+      x.nr = nr;
       x.k_tiles = (int)((x.Kd + BKB - 1) / BKB);
       x.m_tiles = (int)((x.M + BM - 1) / BM);
       const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
@@ -1144,6 +1160,14 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       CUtensorMap amap{}, map, omap{};
       int rc = make_weight_map(&map, wt, g->c, ld_wt, bn);
       if (rc) return rc;
+      static const bool no_im2col = getenv("I8T_NO_IM2COL") != nullptr;
+      if (!no_im2col && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
+        // the phase grid Hq x Wq as the pixel box over g_z [N][P][Q][k_pad]
+        const int lw = x.dw - (x.ns - 1), lh = x.dh - (nr - 1);
+        x.tma_a = 2;
+        if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, lw, lh, x.Wq - (int)Q + lw, x.Hq - (int)P + lh, 1, 1)))
+          return rc;
+      }
       if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16))) return rc;
     }
   }
