@@ -5,6 +5,8 @@
 // rescale epilogue identical to the dense path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace i8t_dev {
@@ -223,9 +225,9 @@ __global__ void __launch_bounds__(256) k_dw_dgrad4(const DwArgs d, const uint32_
 // a lane takes groups of 4 consecutive output pixels of one row for its channel
 // quad, transposes the 4 pixels x 4 channels byte blocks with PRMT and
 // accumulates each channel's 4-pixel dot product with one DP4A per tap.
-// block = 64 quads x 4 lanes over DW_GROUPS pixel groups (int32 partials stay
-// exact), the lanes folded in smem, one int64 atomic per (c, tap) per block.
-constexpr int DW_GROUPS = 512;
+// block = 64 quads x 4 lanes over a run of pixel groups (int32 partials stay
+// exact), the lanes folded in smem, one int32 partial row per block, summed in
+// int64 over the blocks by k_dw_wgrad_reduce.
 
 __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&c)[4]) {
   const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
@@ -238,7 +240,8 @@ __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t 
 
 template <int R, int S, int SH>
 __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_t* __restrict__ g,
-                                                   const uint32_t* __restrict__ a, unsigned long long* acc) {
+                                                   const uint32_t* __restrict__ a, int32_t* __restrict__ part,
+                                                   uint32_t groups_per_block) {
   pdl_entry();
   const uint32_t nq = d.C / 4;
   const uint32_t qd = blockIdx.x * 64 + (threadIdx.x & 63);
@@ -246,8 +249,8 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
   const uint32_t lane4 = threadIdx.x >> 6;
   const uint32_t qgs = (d.Q + 3) / 4;  // pixel groups per output row
   const uint32_t ngroups = static_cast<uint32_t>(d.N) * d.P * qgs;
-  const uint32_t lo = blockIdx.y * static_cast<uint32_t>(DW_GROUPS);
-  const uint32_t hi = min(lo + static_cast<uint32_t>(DW_GROUPS), ngroups);
+  const uint32_t lo = blockIdx.y * groups_per_block;
+  const uint32_t hi = min(lo + groups_per_block, ngroups);
   int sum[R * S][4];
 #pragma unroll
   for (int t = 0; t < R * S; ++t) sum[t][0] = sum[t][1] = sum[t][2] = sum[t][3] = 0;
@@ -293,14 +296,41 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
   }
   __syncthreads();
   if (lane4) return;
+  // this block's exact partial per (channel, tap): int32 (groups_per_block x 4 pixels x 127^2 < 2^31),
+  // one row per block -- summed in int64 by k_dw_wgrad_reduce (no contended atomics)
+  int32_t* prow = part + static_cast<size_t>(blockIdx.y) * d.C * (R * S);
 #pragma unroll
   for (int t = 0; t < R * S; ++t)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const long long v = static_cast<long long>(sum[t][k]) + red[0][threadIdx.x][t * 4 + k] +
-                          red[1][threadIdx.x][t * 4 + k] + red[2][threadIdx.x][t * 4 + k];
-      if (live && v) atomicAdd(acc + static_cast<int64_t>(4 * qd + k) * (R * S) + t, static_cast<unsigned long long>(v));
+      const int v = sum[t][k] + red[0][threadIdx.x][t * 4 + k] + red[1][threadIdx.x][t * 4 + k] +
+                    red[2][threadIdx.x][t * 4 + k];
+      if (live) prow[(4 * qd + k) * (R * S) + t] = v;
     }
+}
+
+// acc[i] = sum over the blocks' partial rows (int64, exact), and gw[i] =
+// float(s_g * s_a * acc[i]); P threads per output fold strided row subsets.
+constexpr int DWR_P = 32;
+__global__ void __launch_bounds__(256) k_dw_wgrad_reduce(const int32_t* __restrict__ part, int rows, int n,
+                                                         long long* __restrict__ acc, const float* clip_g,
+                                                         const float* clip_a, float* __restrict__ gw) {
+  pdl_entry();
+  constexpr int W = 256 / DWR_P;
+  __shared__ long long red[DWR_P][W];
+  const int lo = threadIdx.x % W, ph = threadIdx.x / W;
+  const int i = blockIdx.x * W + lo;
+  long long sum = 0;
+  if (i < n)
+    for (int r = ph; r < rows; r += DWR_P) sum += __ldg(part + static_cast<size_t>(r) * n + i);
+  red[ph][lo] = sum;
+  __syncthreads();
+  if (ph == 0 && i < n) {
+#pragma unroll
+    for (int p = 1; p < DWR_P; ++p) sum += red[p][lo];
+    if (acc) acc[i] = sum;
+    if (gw) gw[i] = static_cast<float>(dw_rescale(clip_g, clip_a) * static_cast<double>(sum));
+  }
 }
 
 static bool dw_quad_ok(const DwArgs& d, const void* p0, const void* p1) {
@@ -396,24 +426,30 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
   if (rc) return rc;
   if (!c || !gz || !a || !clip_g || !clip_a || !acc) return set_error(I8T_EINVAL, "conv_dw_wgrad: null argument");
   const int64_t RS = (int64_t)d.R * d.S, npq = (int64_t)d.N * d.P * d.Q;
-  cudaMemsetAsync(acc, 0, sizeof(int64_t) * d.C * RS, c->stream);
   if (dw_quad_ok(d, gz, a)) {
     const int nq = d.C / 4;
     const int64_t ngroups = static_cast<int64_t>(d.N) * d.P * ((d.Q + 3) / 4);
-    const dim3 grid((nq + 63) / 64, static_cast<unsigned>((ngroups + DW_GROUPS - 1) / DW_GROUPS));
+    // ~4 blocks per SM over the pixel groups; each block's partial stays an exact int32
+    const int64_t cblk = (nq + 63) / 64;
+    int64_t ysplit = std::max<int64_t>(1, (4 * 148 + cblk - 1) / cblk);
+    int64_t per = (ngroups + ysplit - 1) / ysplit;
+    per = std::min<int64_t>(std::max<int64_t>(per, 64), 8192);
+    ysplit = (ngroups + per - 1) / per;
+    const dim3 grid(static_cast<unsigned>(cblk), static_cast<unsigned>(ysplit));
     const uint32_t *g4 = reinterpret_cast<const uint32_t*>(gz), *a4 = reinterpret_cast<const uint32_t*>(a);
-    unsigned long long* acc_u = reinterpret_cast<unsigned long long*>(acc);
-    if (d.sh == 1) launch_k(k_dw_wgrad4<3, 3, 1>, grid, 256, 0, c->stream, d, g4, a4, acc_u);
-    else launch_k(k_dw_wgrad4<3, 3, 2>, grid, 256, 0, c->stream, d, g4, a4, acc_u);
+    int32_t* part = reinterpret_cast<int32_t*>(ensure_scratch(c, sizeof(int32_t) * static_cast<size_t>(ysplit * d.C * RS)));
+    if (!part) return set_error(I8T_ECUDA, "conv_dw_wgrad: scratch alloc failed");
+    if (d.sh == 1) launch_k(k_dw_wgrad4<3, 3, 1>, grid, 256, 0, c->stream, d, g4, a4, part, static_cast<uint32_t>(per));
+    else launch_k(k_dw_wgrad4<3, 3, 2>, grid, 256, 0, c->stream, d, g4, a4, part, static_cast<uint32_t>(per));
     count_launch(1);
     if ((rc = cuda_check("k_dw_wgrad4"))) return rc;
-    if (gw) {
-      launch_k(k_dw_wgrad_finalize, blocks_for(d.C * RS), 256, 0, c->stream, reinterpret_cast<const long long*>(acc), d.C * RS,
-                                                                     clip_g, clip_a, gw);
-      count_launch(1);
-    }
-    return cuda_check("k_dw_wgrad_finalize");
+    const int n = static_cast<int>(d.C * RS);
+    launch_k(k_dw_wgrad_reduce, (n + 256 / DWR_P - 1) / (256 / DWR_P), 256, 0, c->stream, part, static_cast<int>(ysplit), n,
+             reinterpret_cast<long long*>(acc), clip_g, clip_a, gw);
+    count_launch(1);
+    return cuda_check("k_dw_wgrad_reduce");
   }
+  cudaMemsetAsync(acc, 0, sizeof(int64_t) * d.C * RS, c->stream);
   const int cblk = (d.C + 63) / 64;
   int64_t ysplit = (4 * 148 + cblk - 1) / cblk;
   int64_t per = (npq + ysplit - 1) / ysplit;
