@@ -136,6 +136,34 @@ __device__ __forceinline__ void dw_load_wq(const int8_t* __restrict__ w, int c0,
             static_cast<uint32_t>(static_cast<uint8_t>(w[(c0 + 3) * R * S + t])) << 24;
 }
 
+// 3x3 taps with DP4A: the four channels' weights of taps 0-3 and 4-7 transposed
+// into per-channel words (byte t = tap), tap 8 kept per channel.
+struct DwW9 {
+  uint32_t t03[4], t47[4];
+  int t8[4];
+};
+__device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&c)[4]);
+__device__ __forceinline__ DwW9 dw_w9(const uint32_t (&wq)[9]) {
+  DwW9 r;
+  transpose4x4(wq[0], wq[1], wq[2], wq[3], r.t03);
+  transpose4x4(wq[4], wq[5], wq[6], wq[7], r.t47);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) r.t8[k] = sbyte(wq[8], k);
+  return r;
+}
+// s[k] += sum over the 9 taps of a[t] byte k * w[t] byte k (a[t]: the 4 channels of tap t)
+__device__ __forceinline__ void dw_dot9(int (&s)[4], const uint32_t (&av)[9], const DwW9& w) {
+  uint32_t c03[4], c47[4];
+  transpose4x4(av[0], av[1], av[2], av[3], c03);
+  transpose4x4(av[4], av[5], av[6], av[7], c47);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s[k] = __dp4a(static_cast<int>(c03[k]), static_cast<int>(w.t03[k]), s[k]);
+    s[k] = __dp4a(static_cast<int>(c47[k]), static_cast<int>(w.t47[k]), s[k]);
+    s[k] += sbyte(av[8], k) * w.t8[k];
+  }
+}
+
 __device__ __forceinline__ void dw_mac4(int (&s)[4], uint32_t a, uint32_t w) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) s[k] += sbyte(a, k) * sbyte(w, k);
@@ -162,6 +190,8 @@ __global__ void __launch_bounds__(256) k_dw_fwd4(const DwArgs d, const uint32_t*
   const uint32_t qd = tid % nq;
   uint32_t wq[R * S];
   dw_load_wq<R, S>(w, 4 * qd, wq);
+  DwW9 w9;
+  if constexpr (R == 3 && S == 3) w9 = dw_w9(wq);
   const uint32_t tot = static_cast<uint32_t>(d.N) * d.P * d.Q * nq;
   for (uint32_t i = tid; i < tot; i += T) {
     const uint32_t pix = i / nq;
@@ -169,15 +199,30 @@ __global__ void __launch_bounds__(256) k_dw_fwd4(const DwArgs d, const uint32_t*
     const int y0 = static_cast<int>(p) * SH - d.ph, x0 = static_cast<int>(q) * SH - d.pw;
     const uint32_t* img = a + static_cast<uint32_t>(n) * d.H * d.W * nq + qd;
     int s[4] = {0, 0, 0, 0};
+    if constexpr (R == 3 && S == 3) {  // every tap loaded (0 outside), four taps per DP4A
+      uint32_t av[9];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int ih = y0 + r;
-      if (ih < 0 || ih >= d.H) continue;
+      for (int r = 0; r < 3; ++r) {
+        const int ih = y0 + r;
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        const int iw = x0 + t;
-        if (iw < 0 || iw >= d.W) continue;
-        dw_mac4(s, __ldg(img + (static_cast<uint32_t>(ih) * d.W + iw) * nq), wq[r * S + t]);
+        for (int t = 0; t < 3; ++t) {
+          const int iw = x0 + t;
+          const bool ok = ih >= 0 && ih < d.H && iw >= 0 && iw < d.W;
+          av[r * 3 + t] = ok ? __ldg(img + (static_cast<uint32_t>(ih) * d.W + iw) * nq) : 0u;
+        }
+      }
+      dw_dot9(s, av, w9);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int ih = y0 + r;
+        if (ih < 0 || ih >= d.H) continue;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const int iw = x0 + t;
+          if (iw < 0 || iw >= d.W) continue;
+          dw_mac4(s, __ldg(img + (static_cast<uint32_t>(ih) * d.W + iw) * nq), wq[r * S + t]);
+        }
       }
     }
     dw_store4(s, rs, z, acc, i);
@@ -196,25 +241,45 @@ __global__ void __launch_bounds__(256) k_dw_dgrad4(const DwArgs d, const uint32_
   const uint32_t qd = tid % nq;
   uint32_t wq[R * S];
   dw_load_wq<R, S>(w, 4 * qd, wq);
+  DwW9 w9;
+  if constexpr (R == 3 && S == 3) w9 = dw_w9(wq);
   const uint32_t tot = static_cast<uint32_t>(d.N) * d.H * d.W * nq;
   for (uint32_t i = tid; i < tot; i += T) {
     const uint32_t pix = i / nq;
     const uint32_t x = pix % d.W, ny = pix / d.W, y = ny % d.H, n = ny / d.H;
     const uint32_t* img = g + static_cast<uint32_t>(n) * d.P * d.Q * nq + qd;
     int s[4] = {0, 0, 0, 0};
+    if constexpr (R == 3 && S == 3) {  // every tap loaded (0 where it does not reach), DP4A over 4 taps
+      uint32_t av[9];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int pn = static_cast<int>(y) + d.ph - r;
-      if (pn < 0 || (SH > 1 && pn % SH)) continue;
-      const int p = pn / SH;
-      if (p >= d.P) continue;
+      for (int r = 0; r < 3; ++r) {
+        const int pn = static_cast<int>(y) + d.ph - r;
+        const int p = pn / SH;
+        const bool rok = pn >= 0 && (SH == 1 || pn % SH == 0) && p < d.P;
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        const int qn = static_cast<int>(x) + d.pw - t;
-        if (qn < 0 || (SH > 1 && qn % SH)) continue;
-        const int qq = qn / SH;
-        if (qq >= d.Q) continue;
-        dw_mac4(s, __ldg(img + (static_cast<uint32_t>(p) * d.Q + qq) * nq), wq[r * S + t]);
+        for (int t = 0; t < 3; ++t) {
+          const int qn = static_cast<int>(x) + d.pw - t;
+          const int qq = qn / SH;
+          const bool ok = rok && qn >= 0 && (SH == 1 || qn % SH == 0) && qq < d.Q;
+          av[r * 3 + t] = ok ? __ldg(img + (static_cast<uint32_t>(p) * d.Q + qq) * nq) : 0u;
+        }
+      }
+      dw_dot9(s, av, w9);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int pn = static_cast<int>(y) + d.ph - r;
+        if (pn < 0 || (SH > 1 && pn % SH)) continue;
+        const int p = pn / SH;
+        if (p >= d.P) continue;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const int qn = static_cast<int>(x) + d.pw - t;
+          if (qn < 0 || (SH > 1 && qn % SH)) continue;
+          const int qq = qn / SH;
+          if (qq >= d.Q) continue;
+          dw_mac4(s, __ldg(img + (static_cast<uint32_t>(p) * d.Q + qq) * nq), wq[r * S + t]);
+        }
       }
     }
     dw_store4(s, rs, ga, acc, i);
