@@ -303,15 +303,16 @@ __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t 
   c[3] = __byte_perm(t2, t3, 0x7632);
 }
 
-template <int R, int S, int SH>
+template <int R, int S, int SH, int QB>
 __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_t* __restrict__ g,
                                                    const uint32_t* __restrict__ a, int32_t* __restrict__ part,
                                                    uint32_t groups_per_block) {
   pdl_entry();
+  constexpr int LANES = 256 / QB;  // QB channel quads per block, LANES pixel-group lanes per quad
   const uint32_t nq = d.C / 4;
-  const uint32_t qd = blockIdx.x * 64 + (threadIdx.x & 63);
+  const uint32_t qd = blockIdx.x * QB + (threadIdx.x % QB);
   const bool live = qd < nq;  // no early return: the block folds its lanes with a barrier
-  const uint32_t lane4 = threadIdx.x >> 6;
+  const uint32_t lane4 = threadIdx.x / QB;
   const uint32_t qgs = (d.Q + 3) / 4;  // pixel groups per output row
   const uint32_t ngroups = static_cast<uint32_t>(d.N) * d.P * qgs;
   const uint32_t lo = blockIdx.y * groups_per_block;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
   int sum[R * S][4];
 #pragma unroll
   for (int t = 0; t < R * S; ++t) sum[t][0] = sum[t][1] = sum[t][2] = sum[t][3] = 0;
-  for (uint32_t gi = lo + lane4; live && gi < hi; gi += 4) {
+  for (uint32_t gi = lo + lane4; live && gi < hi; gi += LANES) {
     const uint32_t qg = gi % qgs, np = gi / qgs, p = np % d.P, n = np / d.P;
     const uint32_t q0 = qg * 4;
     const uint32_t* grow = g + ((static_cast<uint32_t>(n) * d.P + p) * d.Q) * nq + qd;
@@ -336,6 +337,28 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
       const int ih = y0 + r;
       if (ih < 0 || ih >= d.H) continue;
       const uint32_t* arow = img + static_cast<uint32_t>(ih) * d.W * nq;
+      if constexpr (SH == 1 && S == 3) {
+        // sliding window: the 3 taps of 4 consecutive pixels span 6 input
+        // columns -- load each once, transpose two 4-column blocks, shift per tap
+        uint32_t aw[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int iw = x0 + j;
+          aw[j] = (iw >= 0 && iw < d.W) ? __ldg(arow + iw * nq) : 0u;
+        }
+        uint32_t c0[4], c1[4];
+        transpose4x4(aw[0], aw[1], aw[2], aw[3], c0);
+        transpose4x4(aw[4], aw[5], 0u, 0u, c1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sum[r * 3 + 0][k] = __dp4a(static_cast<int>(gc[k]), static_cast<int>(c0[k]), sum[r * 3 + 0][k]);
+          sum[r * 3 + 1][k] = __dp4a(static_cast<int>(gc[k]), static_cast<int>(__byte_perm(c0[k], c1[k], 0x4321)),
+                                     sum[r * 3 + 1][k]);
+          sum[r * 3 + 2][k] = __dp4a(static_cast<int>(gc[k]), static_cast<int>(__byte_perm(c0[k], c1[k], 0x5432)),
+                                     sum[r * 3 + 2][k]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < S; ++t) {
         uint32_t aw[4];
@@ -352,12 +375,12 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
       }
     }
   }
-  __shared__ int red[3][64][R * S * 4 + 1];  // lanes 1..3 (+1 pad: bank spread)
+  __shared__ int red[LANES - 1][QB][R * S * 4 + 1];  // lanes 1.. (+1 pad: bank spread)
   if (lane4) {
 #pragma unroll
     for (int t = 0; t < R * S; ++t)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) red[lane4 - 1][threadIdx.x & 63][t * 4 + k] = sum[t][k];
+      for (int k = 0; k < 4; ++k) red[lane4 - 1][threadIdx.x % QB][t * 4 + k] = sum[t][k];
   }
   __syncthreads();
   if (lane4) return;
@@ -368,8 +391,9 @@ __global__ void __launch_bounds__(256) k_dw_wgrad4(const DwArgs d, const uint32_
   for (int t = 0; t < R * S; ++t)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int v = sum[t][k] + red[0][threadIdx.x][t * 4 + k] + red[1][threadIdx.x][t * 4 + k] +
-                    red[2][threadIdx.x][t * 4 + k];
+      int v = sum[t][k];
+#pragma unroll
+      for (int l = 0; l < LANES - 1; ++l) v += red[l][threadIdx.x][t * 4 + k];
       if (live) prow[(4 * qd + k) * (R * S) + t] = v;
     }
 }
@@ -495,7 +519,13 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
     const int nq = d.C / 4;
     const int64_t ngroups = static_cast<int64_t>(d.N) * d.P * ((d.Q + 3) / 4);
     // ~4 blocks per SM over the pixel groups; each block's partial stays an exact int32
-    const int64_t cblk = (nq + 63) / 64;
+    // quads per block: the width that leaves the fewest threads without a channel
+    int qb = 64;
+    for (int cand : {64, 32, 16})
+      if (static_cast<int64_t>(nq) * 1000 / ((nq + cand - 1) / cand * cand) >
+          static_cast<int64_t>(nq) * 1000 / ((nq + qb - 1) / qb * qb))
+        qb = cand;
+    const int64_t cblk = (nq + qb - 1) / qb;
     int64_t ysplit = std::max<int64_t>(1, (4 * 148 + cblk - 1) / cblk);
     int64_t per = (ngroups + ysplit - 1) / ysplit;
     per = std::min<int64_t>(std::max<int64_t>(per, 64), 8192);
@@ -504,8 +534,13 @@ int i8t_conv_dw_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, co
     const uint32_t *g4 = reinterpret_cast<const uint32_t*>(gz), *a4 = reinterpret_cast<const uint32_t*>(a);
     int32_t* part = reinterpret_cast<int32_t*>(ensure_scratch(c, sizeof(int32_t) * static_cast<size_t>(ysplit * d.C * RS)));
     if (!part) return set_error(I8T_ECUDA, "conv_dw_wgrad: scratch alloc failed");
-    if (d.sh == 1) launch_k(k_dw_wgrad4<3, 3, 1>, grid, 256, 0, c->stream, d, g4, a4, part, static_cast<uint32_t>(per));
-    else launch_k(k_dw_wgrad4<3, 3, 2>, grid, 256, 0, c->stream, d, g4, a4, part, static_cast<uint32_t>(per));
+#define DW_WG(SH_, QB_) launch_k(k_dw_wgrad4<3, 3, SH_, QB_>, grid, 256, 0, c->stream, d, g4, a4, part, static_cast<uint32_t>(per))
+    if (d.sh == 1) {
+      if (qb == 64) DW_WG(1, 64); else if (qb == 32) DW_WG(1, 32); else DW_WG(1, 16);
+    } else {
+      if (qb == 64) DW_WG(2, 64); else if (qb == 32) DW_WG(2, 32); else DW_WG(2, 16);
+    }
+#undef DW_WG
     count_launch(1);
     if ((rc = cuda_check("k_dw_wgrad4"))) return rc;
     const int n = static_cast<int>(d.C * RS);
