@@ -198,6 +198,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_totals) cudaFree(c->d_totals);
   if (c->d_wgrad) cudaFree(c->d_wgrad);
   if (c->d_fold) cudaFree(c->d_fold);
+  if (c->d_hist) cudaFree(c->d_hist);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_tickets) cudaFree(c->d_tickets);
   delete c;

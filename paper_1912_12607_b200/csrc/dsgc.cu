@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "qcore.cuh"
@@ -419,6 +420,311 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
   }
 }
 
+// ---- K4H: the grid pass of search_clip (clip.cpp:45-46) as one histogram pass.
+//
+// For the R <= 32 grid candidates c_i = m * (i/R), quantize_value kNearest
+// (quantize.cpp:16-31) is a step function of |g|: q_i(x) >= q + 1 exactly
+// when x >= b_{i,q}, the smallest float with that property (monotone: the
+// exact round-half-away of x/s_i).  The R*127 boundaries, sorted, cut |g| into
+// fine bins; every element of fine bin F (F boundaries <= x) has the same q_i
+// for every candidate, so
+//   sum g*g_hat_i = sum_F tab_i(q_i(F)) * (sum of |g| over F),
+//   sum g_hat_i^2 = sum_F tab_i(q_i(F))^2 * count(F)
+// (g_hat keeps g's sign).  One pass over g bins the elements (count and an
+// exact fixed-point sum of |g| per bin: integer adds, order-independent);
+// a one-block finaliser walks the bins per candidate.  The sums are the
+// reference's double sums up to their rounding (the reference's own
+// accumulation error), like the per-candidate passes they replace.
+//
+// Bin lookup: cell(x) = min(floor(x*K + 1/2), tmax) with K = 254 R / m puts
+// every boundary (~ (2q+1) i / K) mid-cell; lut[t] = first boundary with
+// cell >= t.  cell() is monotone, so only the boundaries of x's own cell are
+// compared with x (usually 0-2).
+constexpr int HR_MAX = 32;
+constexpr int HNB_PAD = 4096;                    // >= HR_MAX * 127, power of two (bitonic sort)
+constexpr int HCELLS = 2 * 127 * HR_MAX + 4;     // cells 0..tmax = 2*127*R + 1, plus lut[tmax + 1]
+constexpr int HIST_THREADS = 512;
+
+struct HistBuf {
+  int fail;  // a boundary search gave up (never observed): per-candidate passes; cleared by k_hist_final
+  float K;
+  int nb;    // R * 127 boundaries
+  int e0;    // biased exponent of the smallest boundary: |g| >= B[0] is a multiple of 2^(e0 - 150)
+  int tmax;
+  float s[HR_MAX];
+  float B[HNB_PAD];
+  alignas(16) uint32_t Bu[HNB_PAD];  // b_{i,q} bits at (i-1)*127 + q, unsorted
+  uint16_t pos[HNB_PAD];  // sorted position of b_{i,q} at (i-1)*127 + q
+  uint8_t tag[HNB_PAD];   // candidate (i-1) of the boundary at each sorted position
+  uint16_t lut[HCELLS];
+  unsigned long long cnt[HNB_PAD + 1];
+  unsigned long long sum[3][HNB_PAD + 1];  // fixed-point |g| sums of the digits at bits 0, 14, 28
+};
+
+__device__ __forceinline__ int hist_cell(float x, float K, int tmax) {
+  return min(__float2int_rz(__fmaf_rn(x, K, 0.5f)), tmax);
+}
+
+// Setup, part 1 (R blocks of 128 threads, thread q of block i-1): the exact
+// boundary b_{i,q}, the smallest float with quantize_value(x, c_i) >= q + 1,
+// found by stepping from (q + 1/2) s_i (within an ulp or two); the blocks also
+// clear the global bins.
+__device__ __forceinline__ bool hist_ok(const DsgcState* st, int R) {
+  // below 2^-100 the candidate scales approach the float-subnormal range: per-candidate passes
+  const float m = st->m;
+  return st->active != 0 && R >= 1 && R <= HR_MAX && m >= 0x1p-100f && m <= 3.4e38f;
+}
+__device__ __forceinline__ float hist_cand(float m, int i, int R) {  // ds_grid_chunk, i = 1..R
+  return __fmul_rn(m, __fdiv_rn(static_cast<float>(i), static_cast<float>(R)));
+}
+__global__ void __launch_bounds__(128) k_hist_bounds(const DsgcState* st, int R, HistBuf* hb) {
+  pdl_entry();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= HNB_PAD; i += gridDim.x * blockDim.x) {
+    hb->cnt[i] = 0ull;
+    hb->sum[0][i] = 0ull;
+    hb->sum[1][i] = 0ull;
+    hb->sum[2][i] = 0ull;
+  }
+  if (!hist_ok(st, R)) return;
+  const int i = blockIdx.x, q = threadIdx.x;
+  const float cl = hist_cand(st->m, i + 1, R);
+  const float sc = scale_of(cl), isc = 1.0f / sc;
+  if (q == 0) hb->s[i] = sc;
+  if (q >= 127) return;
+  const int target = q + 1;
+  uint32_t b;
+  if (quant_nearest(cl, cl, sc, isc) < target) {
+    b = 0x7F800000u;  // never reached (x <= m): +inf
+  } else {
+    b = __float_as_uint(__fmul_rn(static_cast<float>(q) + 0.5f, sc));
+    int steps = 0;
+    if (quant_nearest(__uint_as_float(b), cl, sc, isc) >= target) {
+      while (b > 0u && quant_nearest(__uint_as_float(b - 1u), cl, sc, isc) >= target && ++steps < 4096) --b;
+    } else {
+      while (quant_nearest(__uint_as_float(b), cl, sc, isc) < target && ++steps < 4096) ++b;
+    }
+    if (steps >= 4096) atomicOr(&hb->fail, 1);
+  }
+  hb->Bu[i * 127 + q] = b;
+}
+
+// Setup, part 2 (R blocks of 128): boundary (i, q)'s position in the sorted
+// order (key: bits, then candidate, then q -- each candidate's list is already
+// sorted) by binary searches in the other candidates' lists, and its share of
+// the lookup table, lut[t] = first position p with cell(B[p]) >= t: the cells
+// (cell(predecessor), cell(own)], and for the last boundary the cells after it.
+__global__ void __launch_bounds__(128) k_hist_rank(DsgcState* st, int R, HistBuf* hb) {
+  pdl_entry();
+  __shared__ uint32_t sbu[HNB_PAD];
+  const bool ok = hist_ok(st, R);
+  if (!ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->hist = 0;
+      st->grid_active = st->active;
+    }
+    return;
+  }
+  const int nb = R * 127;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(hb->Bu);
+    uint4* dst = reinterpret_cast<uint4*>(sbu);
+#pragma unroll 8
+    for (int k = threadIdx.x; k < (nb + 3) / 4; k += blockDim.x) dst[k] = src[k];
+  }
+  __syncthreads();
+  const float m = st->m;
+  const float K = __fdiv_rn(static_cast<float>(2 * 127 * R), m);
+  const int tmax = 2 * 127 * R + 1;
+  const int i = blockIdx.x, q = threadIdx.x;
+  if (q < 127) {
+    const uint32_t b = sbu[i * 127 + q];
+    int rank = q;
+    uint64_t pred = q > 0 ? (static_cast<uint64_t>(sbu[i * 127 + q - 1]) << 32) | static_cast<uint32_t>(i * 127 + q - 1) : 0ull;
+    bool has_pred = q > 0;
+    for (int j = 0; j < R; ++j) {
+      if (j == i) continue;
+      const uint32_t* L = sbu + j * 127;
+      int lo = 0, hi = 127;  // count of list-j keys below (b, i): bits first, then candidate order
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (L[mid] < b || (L[mid] == b && j < i)) lo = mid + 1;
+        else hi = mid;
+      }
+      rank += lo;
+      if (lo > 0) {
+        const uint64_t kp = (static_cast<uint64_t>(L[lo - 1]) << 32) | static_cast<uint32_t>(j * 127 + lo - 1);
+        if (!has_pred || kp > pred) pred = kp;
+        has_pred = true;
+      }
+    }
+    const float bf = __uint_as_float(b);
+    hb->B[rank] = bf;
+    hb->tag[rank] = static_cast<uint8_t>(i);
+    hb->pos[i * 127 + q] = static_cast<uint16_t>(rank);
+    const int c_own = hist_cell(bf, K, tmax);
+    const int t0 = has_pred ? hist_cell(__uint_as_float(static_cast<uint32_t>(pred >> 32)), K, tmax) + 1 : 0;
+    for (int t = t0; t <= c_own; ++t) hb->lut[t] = static_cast<uint16_t>(rank);
+    if (rank == nb - 1)
+      for (int t = c_own + 1; t <= tmax + 1; ++t) hb->lut[t] = static_cast<uint16_t>(nb);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t b0 = sbu[0];
+    for (int j = 1; j < R; ++j) b0 = min(b0, sbu[j * 127]);
+    const int e0 = static_cast<int>(b0 >> 23);
+    const bool good = hb->fail == 0 && e0 >= 1 && e0 < 255;
+    hb->K = K;
+    hb->nb = nb;
+    hb->e0 = e0;
+    hb->tmax = tmax;
+    st->hist = good ? 1 : 0;
+    st->grid_active = good ? 0 : st->active;
+  }
+}
+
+// The pass over g: per-block bins in shared memory -- a count and the sums of
+// the 14-, 14- and 10-bit digits of |g| in units of 2^(e0 - 150) (< 2^38), all with
+// native 32-bit shared atomics (a 64-bit shared add is a CAS loop, which
+// serialises on the few bins where gradients pile up).  A block flushes its
+// bins to the global 64-bit totals every HIST_ROUND elements, before any
+// 32-bit digit sum can wrap.
+constexpr int HIST_ITERS = 64;  // iterations of 2 float4 per thread per round: 2^18 elements per block
+__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist_pass(const float* __restrict__ g, uint32_t n,
+                                                             const DsgcState* st, HistBuf* hb) {
+  pdl_entry();
+  if (!st->hist) return;
+  extern __shared__ __align__(16) unsigned char hsm[];
+  const int nb = hb->nb, tmax = hb->tmax, e0 = hb->e0;
+  const float K = hb->K;
+  uint4* sbin = reinterpret_cast<uint4*>(hsm);                 // [nb + 1] {count, digit 0, 1, 2}
+  float* sB = reinterpret_cast<float*>(sbin + (nb + 1));      // [nb]
+  uint32_t* slut = reinterpret_cast<uint32_t*>(sB + nb);      // [tmax + 1] {lut[t], lut[t + 1]}
+  for (int i = threadIdx.x; i <= nb; i += blockDim.x) sbin[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sB[i] = hb->B[i];
+  for (int i = threadIdx.x; i <= tmax; i += blockDim.x) slut[i] = hb->lut[i] | (static_cast<uint32_t>(hb->lut[i + 1]) << 16);
+  __syncthreads();
+  unsigned* sw = reinterpret_cast<unsigned*>(sbin);
+  auto body = [&](float v) {
+    const float x = fabsf(v);
+    const int t = hist_cell(x, K, tmax);
+    const uint32_t lp = slut[t];
+    int p = static_cast<int>(lp & 0xFFFFu);
+    const int pe = static_cast<int>(lp >> 16);
+    // a cell's boundaries sit within rounding of one value: x is past all of
+    // them or before all of them but for a few ulps around it
+    if (p < pe) {
+      if (sB[pe - 1] <= x) {
+        p = pe;
+      } else if (sB[p] <= x) {
+        ++p;
+        while (sB[p] <= x) ++p;  // stops before pe - 1
+      }
+    }
+    if (p) {
+      const uint32_t b = __float_as_uint(x);
+      const unsigned long long fx = static_cast<unsigned long long>((b & 0x7FFFFFu) | 0x800000u)
+                                    << ((b >> 23) - static_cast<uint32_t>(e0));
+      unsigned* w = sw + 4 * p;
+      atomicAdd(w, 1u);
+      atomicAdd(w + 1, static_cast<unsigned>(fx) & 0x3FFFu);
+      atomicAdd(w + 2, static_cast<unsigned>(fx >> 14) & 0x3FFFu);
+      const unsigned d2 = static_cast<unsigned>(fx >> 28);  // 0 for all but the top 4 binades above B[0]
+      if (d2) atomicAdd(w + 3, d2);
+    }
+  };
+  auto flush = [&]() {
+    __syncthreads();
+    for (int p = threadIdx.x + 1; p <= nb; p += blockDim.x) {
+      const uint4 c = sbin[p];
+      if (!c.x) continue;
+      atomicAdd(hb->cnt + p, static_cast<unsigned long long>(c.x));
+      atomicAdd(hb->sum[0] + p, static_cast<unsigned long long>(c.y));
+      atomicAdd(hb->sum[1] + p, static_cast<unsigned long long>(c.z));
+      atomicAdd(hb->sum[2] + p, static_cast<unsigned long long>(c.w));
+      sbin[p] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+  };
+  const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  // rounds of HIST_ITERS block-wide iterations; the loop bounds are block-uniform
+  // (every thread reaches the flush barriers)
+  const uint32_t base0 = blockIdx.x * blockDim.x;
+  uint32_t fb = base0;  // block's first float4 of the iteration
+  while (fb < n4) {
+    for (int it = 0; it < HIST_ITERS && fb < n4; ++it, fb += 2 * stride) {
+      const uint32_t f = fb + threadIdx.x;
+      if (f + stride < n4) {
+        const float4 a = __ldg(g4 + f), c = __ldg(g4 + f + stride);
+        body(a.x); body(a.y); body(a.z); body(a.w);
+        body(c.x); body(c.y); body(c.z); body(c.w);
+      } else if (f < n4) {
+        const float4 a = __ldg(g4 + f);
+        body(a.x); body(a.y); body(a.z); body(a.w);
+      }
+    }
+    flush();
+  }
+  for (uint32_t i = n4 * 4 + base0 + threadIdx.x; i < n; i += stride) body(g[i]);
+  flush();
+}
+
+// Finaliser (one block of 32 warps): the bins are staged in shared memory as
+// doubles (count, sum of |g|), then warp w walks a slice of them with lane j
+// tracking candidate j's q; fixed-order combination into totals[3 + 2j], [4 + 2j].
+__global__ void __launch_bounds__(1024) k_hist_final(const DsgcState* st, HistBuf* hb, int R, double* totals) {
+  pdl_entry();
+  if (threadIdx.x == 0 && hb->fail) hb->fail = 0;
+  if (!st->hist) return;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ double part[32][HR_MAX][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = hb->nb;
+  double2* sbin = reinterpret_cast<double2*>(fsm);                 // [nb + 1] {count, sum}
+  uint8_t* stag = reinterpret_cast<uint8_t*>(sbin + (nb + 1));     // [nb]
+  for (int F = threadIdx.x; F <= nb; F += blockDim.x) {
+    const double S = static_cast<double>(hb->sum[2][F]) * 268435456.0 + static_cast<double>(hb->sum[1][F]) * 16384.0 +
+                     static_cast<double>(hb->sum[0][F]);
+    sbin[F] = make_double2(static_cast<double>(hb->cnt[F]), S);
+  }
+  for (int F = threadIdx.x; F < nb; F += blockDim.x) stag[F] = hb->tag[F];
+  __syncthreads();
+  const int per = (nb + 32) / 32;  // bins 1..nb
+  const int F0 = 1 + w * per, F1 = min(nb + 1, F0 + per);
+  double num = 0.0, sqh = 0.0;
+  if (lane < R && F0 < F1) {
+    const float s = hb->s[lane];
+    // q at F0 = boundaries of candidate `lane` at sorted positions < F0
+    int lo = 0, hi = 127;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (hb->pos[lane * 127 + mid] < F0) lo = mid + 1;
+      else hi = mid;
+    }
+    int q = lo;
+    for (int F = F0; F < F1; ++F) {
+      const double2 b = sbin[F];
+      if (b.x != 0.0) {
+        const double td = __fmul_rn(static_cast<float>(q), s);
+        num = fma(td, b.y, num);
+        sqh = fma(b.x, td * td, sqh);
+      }
+      if (F < nb && stag[F] == lane) ++q;
+    }
+  }
+  part[w][lane][0] = num;
+  part[w][lane][1] = sqh;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < 32; ++k) {
+      a += part[k][threadIdx.x][0];
+      b += part[k][threadIdx.x][1];
+    }
+    totals[3 + 2 * threadIdx.x] = ldexp(a, hb->e0 - 150);
+    totals[4 + 2 * threadIdx.x] = b;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 static int stats_pass0(Ctx* c, const float* x, int64_t n) {
@@ -451,6 +757,42 @@ static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, cons
   return cuda_check("k_dc_stats");
 }
 
+static bool hist_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("I8T_DSGC_HIST");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static size_t hist_smem(int R) {
+  const size_t nb = static_cast<size_t>(R) * 127, tmax = 2 * 127 * static_cast<size_t>(R) + 1;
+  return (nb + 1) * 16 + nb * 4 + (tmax + 1) * 4;
+}
+
+static size_t hist_final_smem(int R) {
+  const size_t nb = static_cast<size_t>(R) * 127;
+  return (nb + 1) * 16 + nb;
+}
+
+static HistBuf* ensure_hist(Ctx* c) {
+  if (c->d_hist) return reinterpret_cast<HistBuf*>(c->d_hist);
+  static const bool attr = [] {
+    return cudaFuncSetAttribute(k_hist_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(hist_smem(HR_MAX))) == cudaSuccess &&
+           cudaFuncSetAttribute(k_hist_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(hist_final_smem(HR_MAX))) == cudaSuccess;
+  }();
+  if (!attr) return nullptr;
+  cudaStreamSynchronize(c->stream);
+  if (cudaMalloc(&c->d_hist, sizeof(HistBuf)) != cudaSuccess) {
+    c->d_hist = nullptr;
+    return nullptr;
+  }
+  cudaMemset(c->d_hist, 0, sizeof(HistBuf));
+  return reinterpret_cast<HistBuf*>(c->d_hist);
+}
+
 static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, int rounds, float prev_clip,
                       int prev_from_state) {
   int rc = stats_pass0(c, g, n);
@@ -468,8 +810,32 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
     count_launch(1);
     return cuda_check("k_search_step");
   };
-  for (int done = 0; done < R; done += 32)
-    if ((rc = pass((R - done) < 32 ? (R - done) : 32))) return rc;
+  if (R <= HR_MAX && hist_enabled()) {
+    // the grid as one histogram pass; the per-candidate pass stays queued for
+    // the inputs the histogram declines (st->grid_active), e.g. tiny max|g|
+    HistBuf* hb = ensure_hist(c);
+    if (!hb) return set_error(I8T_ECUDA, "histogram buffer alloc failed");
+    if (ctx_dp(c)) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * R), c->stream);
+    launch_k(k_hist_bounds, R, 128, 0, c->stream, static_cast<const DsgcState*>(st), R, hb);
+    launch_k(k_hist_rank, R, 128, 0, c->stream, st, R, hb);
+    const size_t smem = hist_smem(R);
+    const int64_t want = (n + HIST_THREADS * 16 - 1) / (HIST_THREADS * 16);
+    const int nbk = static_cast<int>(want < 1 ? 1 : want > 2 * 148 ? 2 * 148 : want);
+    launch_k(k_hist_pass, nbk, HIST_THREADS, smem, c->stream, g, static_cast<uint32_t>(n),
+             static_cast<const DsgcState*>(st), hb);
+    launch_k(k_hist_final, 1, 1024, hist_final_smem(R), c->stream, static_cast<const DsgcState*>(st), hb, R,
+             c->d_totals);
+    count_launch(4);
+    if ((rc = cuda_check("k_hist"))) return rc;
+    if ((rc = dc_pass_n(c, g, n, st->cand, &st->grid_active, R))) return rc;
+    if ((rc = allreduce_totals(c, 3 + 2 * R))) return rc;
+    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, R, R, rounds);
+    count_launch(1);
+    if ((rc = cuda_check("k_search_step"))) return rc;
+  } else {
+    for (int done = 0; done < R; done += 32)
+      if ((rc = pass((R - done) < 32 ? (R - done) : 32))) return rc;
+  }
   if (rounds > 0) {
     if ((rc = pass(2))) return rc;
     for (int r = 0; r < rounds; ++r)

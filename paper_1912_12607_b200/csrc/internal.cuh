@@ -51,6 +51,8 @@ struct DsgcState {
   float cand[32];
   float prev_clip;
   int32_t pad_;
+  int32_t hist;         // the grid pass runs on the boundary histogram (dsgc.cu)
+  int32_t grid_active;  // active && !hist: the per-candidate grid pass runs instead
 };
 
 // Context: stream, error word, scratch, data-parallel hooks.
@@ -68,6 +70,7 @@ struct Ctx {
   size_t wgrad_cap = 0;
   void* d_fold = nullptr;              // tap-folded activations / weights (narrow-channel convs)
   size_t fold_cap = 0;
+  void* d_hist = nullptr;              // DSGC grid-search boundary histogram (dsgc.cu)
   // data parallel: the gradient of this rank is shard `rank` of `world` equal
   // shards of the global batch; statistics are combined through `allreduce`.
   i8t_allreduce_fn allreduce = nullptr;

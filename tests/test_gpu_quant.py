@@ -201,6 +201,50 @@ def test_search_clip_grid_only_exact(seed, ops):
     assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
 
 
+@pytest.mark.parametrize("R,seed", [(32, 0), (32, 1), (32, 2), (8, 3), (17, 4), (31, 5), (32, 6), (32, 7)])
+def test_search_clip_grid_histogram_exact(R, seed, ops):
+    """R <= 32: the grid runs as one boundary-histogram pass (dsgc.cu K4H);
+    same clip as the reference's 32 measure_dc calls, d_c within the sums'
+    rounding.  Sizes straddle the one-block and many-block grids."""
+    n = [20_000, 300_000, 2_000_003, 50_000, 123_457, 1_000, 4_000_000, 77_777][seed]
+    g = O.gradient_like((n,), 300 + seed, 1e-3, 0.01)
+    ref = O.search_clip(g, R, 0)
+    got = ops.search_clip(t(g), R, 0)
+    assert got[0] == ref[0]
+    assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
+
+
+def test_search_clip_grid_histogram_adversarial(ops):
+    """Elements exactly on (and one ulp either side of) quantisation
+    boundaries of every grid candidate, duplicates of max|g|, signed zeros,
+    and a constant tensor (every element in the top bin)."""
+    rng = np.random.default_rng(11)
+    m = np.float32(0.37)
+    R = 32
+    vals = [m]
+    for i in range(1, R + 1):
+        c = np.float32(m * np.float32(np.float32(i) / np.float32(R)))
+        s = np.float32(c / np.float32(127))
+        for q in range(0, 127, 3):
+            b = np.float32((q + 0.5) * s)
+            vals += [b, np.nextafter(b, np.float32(0)), np.nextafter(b, np.float32(1))]
+    v = np.array(vals, np.float32)
+    g = np.concatenate([v, -v, rng.choice(v, 200_000), np.full(1000, m, np.float32),
+                        np.zeros(100, np.float32), -np.zeros(100, np.float32)]).astype(np.float32)
+    rng.shuffle(g)
+    for rounds in (0, 2):
+        ref = O.search_clip(g, R, rounds)
+        got = ops.search_clip(t(g), R, rounds)
+        assert got[0] == ref[0] or O.measure_dc(g, got[0]) <= ref[1] + DC_ABS
+        assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
+    # constant tensor: every candidate's d_c is 0 up to rounding (the pick is a
+    # rounding tie-break), so only the objective is compared
+    c = np.full(100_000, np.float32(-2.5), np.float32)
+    got, ref = ops.search_clip(t(c), R, 0), O.search_clip(c, R, 0)
+    assert got[1] == pytest.approx(ref[1], abs=DC_ABS)
+    assert O.measure_dc(c, got[0]) <= ref[1] + DC_ABS
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_search_clip_refined(seed, ops):
     g = O.gradient_like((30_000,), 100 + seed, 1e-4, 0.02)
