@@ -77,11 +77,16 @@ __global__ void __launch_bounds__(RED_THREADS) k_dc_stats0(const float* __restri
 // lookups and 2*NG FMAs, in registers small enough for three blocks per SM.
 // Group y reduces over blockIdx.x into its own partials / ticket, and its last
 // block scatters the candidate sums (and, for y == 0, [0..2]) into totals.
-template <int NG>
+__device__ __noinline__ void search_step_dev(DsgcState* st, const double* tot, int nc, int R, int rounds);
+
+// STATS = false (the search passes after k_search_begin): max|g|, the
+// non-finite flag and sum g^2 are already known; only the candidate sums run.
+template <int NG, bool STATS>
 __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __restrict__ g, uint32_t n,
                                                           const float* __restrict__ cands, int nc,
                                                           const int32_t* active, double* partials, double* gtot,
-                                                          double* totals, unsigned* tickets) {
+                                                          double* totals, unsigned* tickets, DsgcState* step_st,
+                                                          int R, int rounds) {
   pdl_entry();
   constexpr int NV = 3 + 2 * NG;
   if (active && *active == 0) return;  // uniform across the grid: nobody takes a ticket
@@ -121,10 +126,12 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
   float m = 0.0f;
   bool bad = false;
   auto body = [&](float v) {
-    bad |= !isfinite(v);
-    m = fmaxf(m, fabsf(v));
+    if (STATS) {
+      bad |= !isfinite(v);
+      m = fmaxf(m, fabsf(v));
+    }
     const double vd = v;
-    acc[2] = fma(vd, vd, acc[2]);
+    if (STATS) acc[2] = fma(vd, vd, acc[2]);
     uint32_t kb[NG];
     bool slow = tiny;
 #pragma unroll
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
   };
   const uint32_t stride = gridDim.x * blockDim.x, n4 = n / 4;
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  constexpr int U = NG <= 2 ? 4 : 1;  // float4 loads in flight per thread (HBM-bound passes)
+  constexpr int U = NG <= 4 ? 4 : 1;  // float4 loads in flight per thread (HBM-bound passes)
   uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if constexpr (U > 1)
   for (; f + (U - 1) * stride < n4; f += U * stride) {
@@ -182,7 +189,11 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_dc_stats(const float* __rest
     return;
   const int ncg = min(NG, nc - j0);
   for (int t = threadIdx.x; t < 2 * ncg; t += blockDim.x) totals[3 + 2 * j0 + t] = __ldcg(gt + 3 + t);
-  if (blockIdx.y == 0 && threadIdx.x < 3) totals[threadIdx.x] = __ldcg(gt + threadIdx.x);
+  if (STATS && blockIdx.y == 0 && threadIdx.x < 3) totals[threadIdx.x] = __ldcg(gt + threadIdx.x);
+  if (step_st) {  // one group, no allreduce: the last block runs the search step itself
+    __syncthreads();
+    if (threadIdx.x == 0) search_step_dev(step_st, totals, nc, R, rounds);
+  }
 }
 
 // ---- DSGC search state machine (clip.cpp:30-78), one thread, on totals.
@@ -235,9 +246,8 @@ __global__ void k_search_begin(DsgcState* st, const double* tot, int R, float pr
 }
 
 // After a k_dc_stats<nc> pass over st->cand.
-__global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, int rounds) {
-  pdl_entry();
-  if (threadIdx.x || st->active == 0) return;
+__device__ __noinline__ void search_step_dev(DsgcState* st, const double* tot, int nc, int R, int rounds) {
+  if (st->active == 0) return;
   double dcs[32];
   for (int j = 0; j < nc; ++j) dcs[j] = cosine_from(tot[3 + 2 * j], st->sq_g, tot[4 + 2 * j]);
   if (st->phase == 0) {  // grid
@@ -261,17 +271,39 @@ __global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, i
     // x1 = hi - (hi-lo)*kInvPhi, x2 = lo + (hi-lo)*kInvPhi, FMA-contracted like the reference build
     st->x1 = __fma_rn(-(hi - lo), kInvPhi, hi);
     st->x2 = __fma_rn(hi - lo, kInvPhi, lo);
+    // the first golden-section round's two possible probes ride along with
+    // x1 and x2 in the same pass: f1 < f2 probes A, else B
+    const double A = __fma_rn(-(st->x2 - lo), kInvPhi, st->x2);
+    const double B = __fma_rn(hi - st->x1, kInvPhi, st->x1);
     st->cand[0] = static_cast<float>(st->x1);
     st->cand[1] = static_cast<float>(st->x2);
-    st->ncand = 2;
+    st->cand[2] = static_cast<float>(A);
+    st->cand[3] = static_cast<float>(B);
+    st->ncand = 4;
     st->phase = 1;
     return;
   }
-  if (st->phase == 1) {
+  if (st->phase == 1) {  // x1, x2 and round 1 (clip.cpp:57-75)
     st->f1 = dcs[0];
     st->f2 = dcs[1];
     ds_track(st, st->x1, st->f1);
     ds_track(st, st->x2, st->f2);
+    if (st->f1 < st->f2) {
+      st->hi = st->x2;
+      st->x2 = st->x1;
+      st->f2 = st->f1;
+      st->x1 = __fma_rn(-(st->hi - st->lo), kInvPhi, st->hi);
+      st->f1 = dcs[2];
+      ds_track(st, st->x1, st->f1);
+    } else {
+      st->lo = st->x1;
+      st->x1 = st->x2;
+      st->f1 = st->f2;
+      st->x2 = __fma_rn(st->hi - st->lo, kInvPhi, st->lo);
+      st->f2 = dcs[3];
+      ds_track(st, st->x2, st->f2);
+    }
+    st->phase = 2;
   } else if (st->pad_ == 0) {
     st->f1 = dcs[0];
     ds_track(st, st->x1, st->f1);
@@ -300,6 +332,15 @@ __global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, i
   }
   st->ncand = 1;
   st->phase += 1;
+}
+
+// The state machine as its own one-thread launch: after an allreduce of the
+// totals (data parallel) or after the per-candidate grid pass; skipped when
+// *only_if == 0 (the histogram finaliser already ran it).
+__global__ void k_search_step(DsgcState* st, const double* tot, int nc, int R, int rounds, const int32_t* only_if) {
+  pdl_entry();
+  if (threadIdx.x || (only_if && *only_if == 0)) return;
+  search_step_dev(st, tot, nc, R, rounds);
 }
 
 // End of maybe_update's search branch (clip.cpp:84-88) or a raw search_clip.
@@ -597,18 +638,17 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist_pass(const float* __re
   const float K = hb->K;
   uint4* sbin = reinterpret_cast<uint4*>(hsm);                 // [nb + 1] {count, digit 0, 1, 2}
   float* sB = reinterpret_cast<float*>(sbin + (nb + 1));      // [nb]
-  uint32_t* slut = reinterpret_cast<uint32_t*>(sB + nb);      // [tmax + 1] {lut[t], lut[t + 1]}
+  uint16_t* slut = reinterpret_cast<uint16_t*>(sB + nb);      // [tmax + 2]
   for (int i = threadIdx.x; i <= nb; i += blockDim.x) sbin[i] = make_uint4(0u, 0u, 0u, 0u);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) sB[i] = hb->B[i];
-  for (int i = threadIdx.x; i <= tmax; i += blockDim.x) slut[i] = hb->lut[i] | (static_cast<uint32_t>(hb->lut[i + 1]) << 16);
+  for (int i = threadIdx.x; i <= tmax + 1; i += blockDim.x) slut[i] = hb->lut[i];
   __syncthreads();
   unsigned* sw = reinterpret_cast<unsigned*>(sbin);
   auto body = [&](float v) {
     const float x = fabsf(v);
     const int t = hist_cell(x, K, tmax);
-    const uint32_t lp = slut[t];
-    int p = static_cast<int>(lp & 0xFFFFu);
-    const int pe = static_cast<int>(lp >> 16);
+    int p = slut[t];
+    const int pe = slut[t + 1];
     // a cell's boundaries sit within rounding of one value: x is past all of
     // them or before all of them but for a few ulps around it
     if (p < pe) {
@@ -671,7 +711,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist_pass(const float* __re
 // Finaliser (one block of 32 warps): the bins are staged in shared memory as
 // doubles (count, sum of |g|), then warp w walks a slice of them with lane j
 // tracking candidate j's q; fixed-order combination into totals[3 + 2j], [4 + 2j].
-__global__ void __launch_bounds__(1024) k_hist_final(const DsgcState* st, HistBuf* hb, int R, double* totals) {
+__global__ void __launch_bounds__(1024) k_hist_final(DsgcState* st, HistBuf* hb, int R, double* totals, int rounds,
+                                                     int fuse_step) {
   pdl_entry();
   if (threadIdx.x == 0 && hb->fail) hb->fail = 0;
   if (!st->hist) return;
@@ -723,6 +764,10 @@ __global__ void __launch_bounds__(1024) k_hist_final(const DsgcState* st, HistBu
     totals[3 + 2 * threadIdx.x] = ldexp(a, hb->e0 - 150);
     totals[4 + 2 * threadIdx.x] = b;
   }
+  if (fuse_step) {
+    __syncthreads();
+    if (threadIdx.x == 0) search_step_dev(st, totals, R, R, rounds);
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -738,9 +783,12 @@ static int stats_pass0(Ctx* c, const float* x, int64_t n) {
 
 // K4 over nc <= 32 candidates: groups of 8 (or one group of 1 / 2 for the
 // golden-section rounds).
-static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nc) {
+// step_st: run the search state machine in the pass's last block (one
+// candidate group only; *fused reports whether it did).
+static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, const int32_t* active, int nc,
+                     bool stats, DsgcState* step_st = nullptr, int R = 0, int rounds = 0, bool* fused = nullptr) {
   if (nc < 1 || nc > 32) return set_error(I8T_EINVAL, "dc pass: bad candidate count");
-  const int ng = nc <= 1 ? 1 : nc <= 2 ? 2 : 8;
+  const int ng = nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : 8;
   const int groups = (nc + ng - 1) / ng;
   const int nb = nblocks(n, 1, 3 * 148);
   const int nv = 3 + 2 * ng;
@@ -750,9 +798,20 @@ static int dc_pass_n(Ctx* c, const float* g, int64_t n, const float* cands, cons
   double* gt = p + static_cast<size_t>(nb) * groups * nv;
   const dim3 grid(nb, groups);
   const uint32_t un = static_cast<uint32_t>(n);
-  if (ng == 1) launch_k(k_dc_stats<1>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
-  else if (ng == 2) launch_k(k_dc_stats<2>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
-  else launch_k(k_dc_stats<8>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32);
+  DsgcState* sst = groups == 1 ? step_st : nullptr;
+  if (fused) *fused = sst != nullptr;
+#define DCS(NG, ST) launch_k(k_dc_stats<NG, ST>, grid, RED_THREADS, 0, c->stream, g, un, cands, nc, active, p, gt, c->d_totals, t + 32, sst, R, rounds)
+  if (stats) {
+    if (ng == 1) DCS(1, true);
+    else if (ng == 2) DCS(2, true);
+    else DCS(8, true);
+  } else {
+    if (ng == 1) DCS(1, false);
+    else if (ng == 2) DCS(2, false);
+    else if (ng == 4) DCS(4, false);
+    else DCS(8, false);
+  }
+#undef DCS
   count_launch(1);
   return cuda_check("k_dc_stats");
 }
@@ -767,7 +826,7 @@ static bool hist_enabled() {
 
 static size_t hist_smem(int R) {
   const size_t nb = static_cast<size_t>(R) * 127, tmax = 2 * 127 * static_cast<size_t>(R) + 1;
-  return (nb + 1) * 16 + nb * 4 + (tmax + 1) * 4;
+  return (nb + 1) * 16 + nb * 4 + (tmax + 2) * 2;
 }
 
 static size_t hist_final_smem(int R) {
@@ -804,9 +863,11 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
   // skipped pass contributes a zero totals buffer to the hook.
   auto pass = [&](int nc) -> int {
     if (ctx_dp(c)) cudaMemsetAsync(c->d_totals, 0, sizeof(double) * (3 + 2 * nc), c->stream);
-    int r = dc_pass_n(c, g, n, st->cand, &st->active, nc);
-    if (r || (r = allreduce_totals(c, 3 + 2 * nc))) return r;
-    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, nc, R, rounds);
+    bool fused = false;
+    int r = dc_pass_n(c, g, n, st->cand, &st->active, nc, false, ctx_dp(c) ? nullptr : st, R, rounds, &fused);
+    if (r || fused) return r;
+    if ((r = allreduce_totals(c, 3 + 2 * nc))) return r;
+    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, nc, R, rounds, static_cast<const int32_t*>(nullptr));
     count_launch(1);
     return cuda_check("k_search_step");
   };
@@ -823,13 +884,15 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
     const int nbk = static_cast<int>(want < 1 ? 1 : want > 2 * 148 ? 2 * 148 : want);
     launch_k(k_hist_pass, nbk, HIST_THREADS, smem, c->stream, g, static_cast<uint32_t>(n),
              static_cast<const DsgcState*>(st), hb);
-    launch_k(k_hist_final, 1, 1024, hist_final_smem(R), c->stream, static_cast<const DsgcState*>(st), hb, R,
-             c->d_totals);
+    const bool fuse = !ctx_dp(c);
+    launch_k(k_hist_final, 1, 1024, hist_final_smem(R), c->stream, st, hb, R, c->d_totals, rounds, fuse ? 1 : 0);
     count_launch(4);
     if ((rc = cuda_check("k_hist"))) return rc;
-    if ((rc = dc_pass_n(c, g, n, st->cand, &st->grid_active, R))) return rc;
+    if ((rc = dc_pass_n(c, g, n, st->cand, &st->grid_active, R, false))) return rc;
     if ((rc = allreduce_totals(c, 3 + 2 * R))) return rc;
-    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, R, R, rounds);
+    // the state machine already ran in k_hist_final unless the fallback pass did the work
+    launch_k(k_search_step, 1, 32, 0, c->stream, st, c->d_totals, R, R, rounds,
+             fuse ? static_cast<const int32_t*>(&st->grid_active) : static_cast<const int32_t*>(nullptr));
     count_launch(1);
     if ((rc = cuda_check("k_search_step"))) return rc;
   } else {
@@ -837,8 +900,8 @@ static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, i
       if ((rc = pass((R - done) < 32 ? (R - done) : 32))) return rc;
   }
   if (rounds > 0) {
-    if ((rc = pass(2))) return rc;
-    for (int r = 0; r < rounds; ++r)
+    if ((rc = pass(4))) return rc;  // x1, x2 and both possible probes of round 1
+    for (int r = 1; r < rounds; ++r)
       if ((rc = pass(1))) return rc;
   }
   return I8T_OK;
@@ -942,7 +1005,7 @@ int i8t_measure_dc(i8t_ctx* ctx, const float* g, int64_t n, float clip, double* 
   float* dclip = reinterpret_cast<float*>(ensure_scratch(c, 256));
   if (!dclip) return set_error(I8T_ECUDA, "scratch alloc failed");
   cudaMemcpyAsync(dclip, &clip, sizeof(float), cudaMemcpyHostToDevice, c->stream);
-  int rc = dc_pass_n(c, g, n, dclip, nullptr, 1);
+  int rc = dc_pass_n(c, g, n, dclip, nullptr, 1, true);
   if (rc) return rc;
   launch_k(k_fin_measure_dc, 1, 32, 0, c->stream, c->d_totals, out, c->d_err);
   count_launch(1);
@@ -1006,7 +1069,7 @@ int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64
     count_launch(1);
     return cuda_check("maybe_update");
   }
-  if ((rc = dc_pass_n(c, g, n, &st->v.clip, nullptr, 1)) || (rc = allreduce_totals(c, 5))) return rc;
+  if ((rc = dc_pass_n(c, g, n, &st->v.clip, nullptr, 1, true)) || (rc = allreduce_totals(c, 5))) return rc;
   launch_k(k_fin_maybe_dc, 1, 32, 0, c->stream, st, c->d_totals, c->d_err);
   count_launch(1);
   return cuda_check("maybe_update");
