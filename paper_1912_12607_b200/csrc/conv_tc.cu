@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -272,7 +273,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             continue;
           }
           if constexpr (MODE == MODE_WGRAD) {
-            if (args.tma_a == 2) {  // im2col rows npq = kb.. of tap (r, s), channels c0 of the m-tile
+            if (args.tma_a == 3) {
+              // 64-channel taps: the m-tile's two 64-row halves are two im2col boxes
+              // [128 npq rows][64 channels] (SWIZZLE_64B) of their own (tap, c0);
+              // a half past M repeats the last valid rows (its output rows are dropped)
+              const int pq = args.P * args.Q;
+              const int n = kb / pq, rem = kb - n * pq, p = rem / args.Q, q = rem - p * args.Q;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                int mh = static_cast<int>(m0) + 64 * h;
+                if (mh >= args.M) mh = args.M - 64;
+                const int tap = mh / args.Cp, c0 = mh - tap * args.Cp;
+                const int r = tap / args.S, sx = tap - r * args.S;
+                tma_load_im2col_4d(a_st + h * 8192, &tmap_a, &full[s], c0, q * args.sw - args.pw, p * args.sh - args.ph,
+                                   n, static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+              }
+            } else if (args.tma_a == 2) {  // im2col rows npq = kb.. of tap (r, s), channels c0 of the m-tile
               const int pq = args.P * args.Q;
               const int n = kb / pq, rem = kb - n * pq, p = rem / args.Q, q = rem - p * args.Q;
               const int tap = m0 / args.Cp, c0 = m0 - tap * args.Cp;
@@ -334,6 +350,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       const int nk = tile_nk(args, tc.split);
       int rowA_n[PASSES_A], rowA_y[PASSES_A], rowA_x[PASSES_A];
       bool rowA_ok[PASSES_A];
+      int runR = 0, runS = 0, runC = 0;  // WGRAD run path: (r, s, c) of this thread's column run
+      bool runOk = false;
       if constexpr (MODE != MODE_WGRAD) {
 #pragma unroll
         for (int i = 0; i < PASSES_A; ++i) {
@@ -416,6 +434,59 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           }
         } else {
           // ---- WGRAD: smem rows = npq (reduction), columns = M bytes (A) / N bytes (B), MN-major
+          // Channel strides that are multiples of 32 / 64 bytes: a thread copies a
+          // whole run of 32 / 64 contiguous bytes of one (pixel, tap) -- one
+          // address per run instead of per 16-byte piece, tap decoded once per tile
+          // (the 64-channel 3x3 layers and the stem's 32-byte folded taps).
+          if constexpr (VA == 16) {
+            if (args.Cp % 32 == 0) {
+              auto runs = [&](auto run_c) {
+                constexpr int RUN = decltype(run_c)::value;
+                constexpr int TPR = BKB / RUN, RPP = NPROD / TPR, PASSES = BM / RPP;
+                static_assert(PASSES <= PASSES_A, "row state");
+                const int jr = tid % TPR, r0 = tid / TPR;
+                if (kt == 0) {
+                  const int64_t mR = m0 + jr * RUN;
+                  runOk = mR < args.M;
+                  const int tapR = runOk ? static_cast<int>(mR / args.Cp) : 0;
+                  runC = runOk ? static_cast<int>(mR - static_cast<int64_t>(tapR) * args.Cp) : 0;
+                  runR = tapR / args.S;
+                  runS = tapR - runR * args.S;
+#pragma unroll
+                  for (int i = 0; i < PASSES; ++i) {
+                    const int kdi = static_cast<int>(kbase) + r0 + i * RPP;
+                    const int pq = args.P * args.Q;
+                    const int n = kdi / pq, rem = kdi - n * pq;
+                    rowA_n[i] = n;
+                    rowA_y[i] = rem / args.Q;
+                    rowA_x[i] = rem - rowA_y[i] * args.Q;
+                  }
+                }
+#pragma unroll
+                for (int i = 0; i < PASSES; ++i) {
+                  const int row = r0 + i * RPP;
+                  const int64_t kd = kbase + row;
+                  bool ok = runOk && kd < args.Kd;
+                  const int ih = rowA_y[i] * args.sh - args.ph + runR, iw = rowA_x[i] * args.sw - args.pw + runS;
+                  ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
+                  const int8_t* src =
+                      ok ? args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + runC
+                         : args.act;
+#pragma unroll
+                  for (int u = 0; u < RUN / 16; ++u)
+                    cp_async_vec<16>(a_st + sw128_offset(row, jr * RUN + u * 16), ok ? src + u * 16 : src, ok);
+                  int q = rowA_x[i] + adv_q, p = rowA_y[i] + adv_p, n = rowA_n[i];
+                  if (q >= args.Q) { q -= args.Q; ++p; }
+                  while (p >= args.P) { p -= args.P; ++n; }
+                  rowA_x[i] = q; rowA_y[i] = p; rowA_n[i] = n;
+                }
+              };
+              if (args.Cp % 64 == 0) runs(std::integral_constant<int, 64>{});
+              else runs(std::integral_constant<int, 32>{});
+            }
+          }
+          const bool run_path = VA == 16 && args.Cp % 32 == 0;
+          if (!run_path) {
           const int64_t mA = m0 + ja * VA;
           const bool mok = mA < args.M;
           const int tapA = mok ? static_cast<int>(mA / args.Cp) : 0;
@@ -448,6 +519,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             while (p >= args.P) { p -= args.P; ++n; }
             rowA_x[i] = q; rowA_y[i] = p; rowA_n[i] = n;
           }
+          }  // !run_path
           if (args.tma_b) {  // g_z rows by TMA (thread 0; same barrier protocol as the FWD weights)
             if (tid == 0) {
               mbar_expect_tx(&full[s], C::B_BYTES);
@@ -510,7 +582,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             uint64_t ad, bd;
             if constexpr (MN) {
               // MN-major: 32 reduction rows per MMA = 4096 B; SBO = 8-row atom stride, LBO = 128-col sub-tile
-              ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 4096, 16384, 1024);
+              ad = args.tma_a == 3 ? make_sdesc_sw64_mn(a0 + s * C::A_BYTES + kk * 2048, 8192, 512)
+                                   : make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 4096, 16384, 1024);
               bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 4096, 16384, 1024);
             } else {
               // K-major: 32 B of reduction per MMA inside the 128 B swizzled row; SBO = 8 rows x 128 B
@@ -911,7 +984,8 @@ static EncodeIm2colFn encode_im2col_fn() {
 // A tile of WGRAD alike), traversing the pixel box [lower, dim - 1 + upper]
 // with strides (sw, sh); out-of-tensor taps are zero-filled.
 static int make_im2col_map(CUtensorMap* map, const int8_t* t, int64_t N, int64_t H, int64_t W, int64_t C, int lower_w,
-                           int lower_h, int upper_w, int upper_h, int sw, int sh) {
+                           int lower_h, int upper_w, int upper_h, int sw, int sh, uint32_t cbox = 128u,
+                           CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col unavailable");
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
@@ -920,30 +994,37 @@ static int make_im2col_map(CUtensorMap* map, const int8_t* t, int64_t N, int64_t
   const int lower[2] = {lower_w, lower_h};
   const int upper[2] = {upper_w, upper_h};
   cuuint32_t estr[4] = {1u, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(sh), 1u};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(t), dims, strides, lower, upper, 128u,
-                  static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(t), dims, strides, lower, upper, cbox,
+                  static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
   return I8T_OK;
 }
 // the forward / backward-weight activation map: box = the output positions
-static int make_im2col_map(CUtensorMap* map, const int8_t* a, const i8t_conv_geom* g, int64_t c_pad) {
+static int make_im2col_map(CUtensorMap* map, const int8_t* a, const i8t_conv_geom* g, int64_t c_pad,
+                           uint32_t cbox = 128u, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   return make_im2col_map(map, a, g->n, g->h, g->w, c_pad, static_cast<int>(-g->pad_w), static_cast<int>(-g->pad_h),
                          static_cast<int>(g->pad_w - (g->kw - 1)), static_cast<int>(g->pad_h - (g->kh - 1)),
-                         static_cast<int>(g->stride_w), static_cast<int>(g->stride_h));
+                         static_cast<int>(g->stride_w), static_cast<int>(g->stride_h), cbox, swz);
 }
 
 // Forward convs whose A operand TMA im2col can load: 128-channel blocks, the
 // output grid exactly the pixel box (floor mode with an exact fit), offsets in
 // range.  I8T_NO_IM2COL=1 keeps the cp.async gather (A/B experiments).
-static bool im2col_ok(const i8t_conv_geom* g, int64_t c_pad, const void* a, int64_t P, int64_t Q) {
+static bool im2col_ok(const i8t_conv_geom* g, int64_t c_pad, const void* a, int64_t P, int64_t Q, int64_t cblk = 128) {
   static const bool off = getenv("I8T_NO_IM2COL") != nullptr;
-  if (off || g->depthwise || c_pad % 128 != 0 || (reinterpret_cast<uintptr_t>(a) & 15u)) return false;
+  if (off || g->depthwise || c_pad % cblk != 0 || (reinterpret_cast<uintptr_t>(a) & 15u)) return false;
   if (g->kh * g->kw == 1 && g->stride_h == 1 && g->stride_w == 1 && g->pad_h == 0 && g->pad_w == 0) return false;
   if (g->stride_h > 8 || g->stride_w > 8 || g->kh > 8 || g->kw > 8 || g->pad_h >= g->kh || g->pad_w >= g->kw) return false;
   // the box [-pad, W - 1 + pad - (k - 1)] traversed with stride s has exactly
   // floor((W + 2 pad - k) / s) + 1 = Q positions per row (P per column)
   return (g->w + 2 * g->pad_w - g->kw) / g->stride_w + 1 == Q && (g->h + 2 * g->pad_h - g->kh) / g->stride_h + 1 == P;
+}
+
+// I8T_NO_WG64=1 keeps the cp.async gather for 64-channel-block wgrads (A/B experiments).
+static bool wg64_off() {
+  static const bool off = getenv("I8T_NO_WG64") != nullptr;
+  return off;
 }
 
 // 2-D int8 weight matrix [rows][ld] -> TMA map with box {128 B, box_rows}, SWIZZLE_128B.
@@ -1393,6 +1474,10 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   } else if (im2col_ok(g, c_pad, a, P, Q) && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
     x.tma_a = 2;  // A = im2col of the activations (128 npq rows x 128 channels of one tap), B = g_z rows
     if ((rc = make_im2col_map(&amap, a, g, c_pad))) return rc;
+  } else if (!wg64_off() && im2col_ok(g, c_pad, a, P, Q, 64) && x.M >= 64 && k_pad % 16 == 0 &&
+             (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
+    x.tma_a = 3;  // 64-channel blocks: two im2col boxes per m-tile (SWIZZLE_64B, MN-major SW64 descriptor)
+    if ((rc = make_im2col_map(&amap, a, g, c_pad, 64u, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   }
   static const bool no_tma_b = getenv("I8T_NO_TMA_A") != nullptr;
   if (x.tma_a || (!no_tma_b && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0)) {

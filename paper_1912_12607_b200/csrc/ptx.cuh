@@ -320,6 +320,18 @@ __device__ __forceinline__ uint64_t make_sdesc_sw64(uint32_t saddr, uint32_t sbo
   d |= 4ull << 61;
   return d;
 }
+// MN-major SWIZZLE_64B: 64-element (64-byte) MN chunks at LBO, 8-row K groups
+// (8 x 64 B) at SBO -- two separately loaded 64-byte-wide boxes form one
+// 128-row operand.
+__device__ __forceinline__ uint64_t make_sdesc_sw64_mn(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= 4ull << 61;
+  return d;
+}
 __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
          ((static_cast<uint32_t>(N) >> 3) << 17) | ((static_cast<uint32_t>(M) >> 4) << 24);

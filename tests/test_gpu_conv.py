@@ -44,6 +44,8 @@ GEOMS = [
     (1, 32, 9, 11, 40, 1, 7, 1, 0, 1, 3, False),         # 1x7 asym pad
     (1, 32, 11, 9, 40, 7, 1, 1, 3, 1, 0, False),         # 7x1 asym pad
     (1, 256, 7, 7, 300, 3, 3, 1, 1, None, None, False),  # N > 256 tile
+    (2, 192, 9, 9, 64, 3, 3, 2, 1, None, None, False),   # wgrad: 64-channel im2col halves straddling taps
+    (1, 320, 7, 7, 32, 3, 3, 1, 1, None, None, False),   # wgrad: 64-channel halves, last half past M
     # strided dgrad through the stride-phase decomposition (k % 128 == 0)
     (2, 40, 11, 11, 128, 1, 1, 2, 0, None, None, False),  # 1x1 s2, zero phases, odd H
     (2, 64, 10, 10, 256, 3, 3, 2, 1, None, None, False),  # 3x3 s2, four phases
