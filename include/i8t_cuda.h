@@ -247,7 +247,9 @@ int i8t_conv_dgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
  *   ga = dgrad + add_g                 (add_y == NULL: projection shortcut)
  *   ga = dgrad + add_g * (add_y > 0)   (identity shortcut through the block ReLU)
  * add_g / add_y: NHWC fp32 [N*H*W][C], 16-byte aligned, C % 4 == 0.  One float
- * add per element, so ga equals i8t_conv_dgrad followed by the join bit for bit. */
+ * add per element, so ga equals i8t_conv_dgrad followed by the join bit for bit.
+ * ga may alias add_g when add_y == NULL (in-place join): the pixels a strided
+ * dgrad gives no taps then keep add_g as is (0 + x, except that -0 stays -0). */
 int i8t_conv_dgrad_join(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64_t k_pad, const int8_t* wt,
                         int64_t ld_wt, const float* clip_g, const float* clip_w, float* ga, const float* add_g,
                         const float* add_y);

@@ -1225,6 +1225,11 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.add_g = add_g; x.add_y = add_y; x.add_bits = add_bits;
       x.use_tma_out = 0;
       if (nr == 0 || x.ns == 0) {
+        // in-place join (out is the addend, no mask): the phase already holds
+        // 0 + addend (up to the sign of a zero addend)
+        if (x.add_g && static_cast<const void*>(x.add_g) == static_cast<const void*>(x.out) && !x.add_y &&
+            !x.add_bits && !x.acc32)
+          continue;
         const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
         launch_k(k_zero_phase, blocks, 256, 0, c->stream, x);
         count_launch(1);

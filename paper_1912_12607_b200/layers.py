@@ -537,6 +537,10 @@ class Conv2d(Layer):
             join, self.dgrad_join, self.join_done = self.dgrad_join, None, False
             if self.need_input_grad and join is not None and g.c % 4 == 0:
                 add_g, add_y, add_bits = join
+                if add_y is None and add_bits is None and add_g.is_contiguous() and add_g.shape == ga.shape:
+                    # plain join (projection shortcut): accumulate into the addend in
+                    # place -- a strided dgrad's tap-less phases then write nothing
+                    ga = add_g
                 if add_bits is not None:  # identity shortcut through the block ReLU, mask as packed bits
                     call("i8t_conv_dgrad_join_bits", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qwt),
                          self.ld_wt, ops._p(clip_g), ops._p(self.qs.clip_w), ops._p(ga), ops._p(add_g.contiguous()),

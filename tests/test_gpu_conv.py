@@ -170,3 +170,30 @@ def test_resnet50_layer_shapes(shape, ops):
     np.testing.assert_array_equal(dacc.cpu().numpy().astype(np.int64), dacc_ref)
     wacc_ref, _ = O.conv_wgrad(qg, qa, og, 1.0, 1.0)
     np.testing.assert_array_equal(wacc.cpu().numpy(), wacc_ref)
+
+
+@pytest.mark.parametrize("shape", [(2, 40, 11, 128, 1, 2, 0), (2, 64, 10, 256, 3, 2, 1), (2, 64, 14, 64, 3, 1, 1)])
+def test_dgrad_join_in_place_matches_dgrad_plus_add(shape, ops):
+    """i8t_conv_dgrad_join with ga aliasing add_g (the projection-shortcut join
+    accumulating into the main-branch gradient): equal to dgrad + add_g, the
+    tap-less stride phases included (they are skipped, keeping add_g)."""
+    import ctypes as C
+    n, c, h, k, kk, s, p = shape
+    g = ops.geom(n, c, h, h, k, kk, kk, s, p)
+    P, Q = g.out_hw()
+    cp, kp = ops.pad4(c), ops.pad4(k)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    qg = torch.randint(-127, 128, (n, P, Q, kp), dtype=torch.int8, device="cuda", generator=gen)
+    w = torch.randn(k, c, kk, kk, device="cuda", generator=gen)
+    _, qwt = ops.quantize_weight(w, float(w.abs().max()), c_pad=cp, k_pad=kp)
+    cg = torch.tensor([0.02], device="cuda")
+    cw = torch.tensor([float(w.abs().max())], device="cuda")
+    add = torch.randn((n * h * h, c), device="cuda", generator=gen)
+    add[add.abs() < 0.01] = 0.0  # +0 addends: -0 would stay -0 in place
+    ref, _ = ops.conv_dgrad_nhwc(g, qg, kp, qwt, qwt.shape[1], cg, cw)
+    ref = ref + add
+    buf = add.clone()
+    ops.call("i8t_conv_dgrad_join", ops.ctx(), C.byref(g), ops._p(qg), kp, ops._p(qwt), qwt.shape[1], ops._p(cg),
+             ops._p(cw), ops._p(buf), ops._p(buf), None)
+    torch.cuda.synchronize()
+    assert torch.equal(buf.view(torch.int32), ref.view(torch.int32))
