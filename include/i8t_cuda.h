@@ -344,6 +344,14 @@ int i8t_bn_act_q(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const doubl
 int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, double* bn,
                       const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* grad_gamma,
                       float* grad_beta);
+/* i8t_bn_bwd_reduce (mask_mode 3, mask_bits) of g_out = a_add + g * join_bit,
+ * with g_out also written (bit for bit i8t_add_masked_bits(a_add, g,
+ * join_bits) followed by i8t_bn_bwd_reduce): the identity-shortcut join of a
+ * residual block's backward fused with the preceding BN's column sums
+ * (layers.cpp:458-464 then 285-300). */
+int i8t_bn_bwd_reduce_join(i8t_ctx* ctx, const float* a_add, const float* g, const uint32_t* join_bits,
+                           const float* z, int64_t m, int64_t c, double* bn, const float* gamma, const float* beta,
+                           const uint32_t* mask_bits, float* grad_gamma, float* grad_beta, float* g_out);
 /* gz = BN backward (materialised fp32). */
 int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
                      const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz);

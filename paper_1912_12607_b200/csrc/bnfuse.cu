@@ -46,10 +46,18 @@ struct ColArgs {
   float* running_var;
   float* grad_gamma;    // MODE 1
   float* grad_beta;
+  // MODE 2 (MODE 1 after an identity-shortcut join): g_out = ja + g * jbit is
+  // materialised into gout (k_add_masked_bits, bit for bit) and reduced as g
+  const float* ja;
+  const uint32_t* jbits;
+  float* gout;
 };
 
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
 // MODE 0: sum z, sum z^2.  MODE 1: sum g_m, sum g_m * x_hat (g_m = masked g).
+// MODE 2: MODE 1 on g = ja + g * jbit, which is also written to gout (the
+// residual join of the next block's backward and this BN's reduction in one
+// pass: g is read once instead of written, then read).
 template <int MODE, int MASK = 0>
 __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets,
                                                    unsigned* set_tickets) {
@@ -65,7 +73,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
   double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0};
   float lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
-  if (MODE == 1 && MASK == 1) {
+  if (MODE >= 1 && MASK == 1) {
     // ReLU-mask bounds of this block's channel group, bisected in the prologue
     // (redundantly per block: cheaper than a launch); block x == 0 stores them
     // in bn[5c..6c) for the gradient quantiser.
@@ -85,7 +93,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
       }
     }
   }
-  if (MODE == 1 && active) {
+  if (MODE >= 1 && active) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       mean[j] = a.bn[ch + j];
@@ -94,28 +102,31 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   }
   if (active) {
     // U rows per thread per trip: all loads of a trip are issued before any math
-    constexpr int U = MODE == 0 ? 10 : 4;
+    constexpr int U = MODE == 0 ? 10 : MODE == 1 ? 4 : 2;
     const uint32_t row_step = gridDim.x * 8 * rpw;
     uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub;
     // software pipeline: the U rows of the next trip are loaded before the
     // current trip's math, so U (x tensors) 16-byte loads are always in flight
     float4 zv[U], gv[U], yv[U], zn[U], gn[U], yn[U];
     uint32_t bv[U], bn_[U];  // MASK 3: raw mask words (the nibble is extracted at use: keeps the loads in flight)
-    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd, uint32_t* bd) {
+    uint32_t jv[U], jn[U];   // MODE 2: join mask words (yv / yn carry the join addend)
+    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd, uint32_t* bd, uint32_t* jd) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t ru = rr + u * row_step;
         const size_t off = static_cast<size_t>(ru < a.m ? ru : r) * a.c + ch;
         zd[u] = ldg_stream(a.z + off);
-        if (MODE == 1) gd[u] = ldg_stream(a.g + off);
+        if (MODE >= 1) gd[u] = ldg_stream(a.g + off);
         if (MODE == 1 && MASK == 2) yd[u] = ldg_stream(a.mask_y + off);
-        if (MODE == 1 && MASK == 3) bd[u] = __ldg(reinterpret_cast<const uint32_t*>(a.mask_y) + (off >> 5));
+        if (MODE == 2) yd[u] = ldg_stream(a.ja + off);
+        if (MODE == 2) jd[u] = __ldg(a.jbits + (off >> 5));
+        if (MODE >= 1 && MASK == 3) bd[u] = __ldg(reinterpret_cast<const uint32_t*>(a.mask_y) + (off >> 5));
       }
     };
-    if (r < a.m) fetch(r, zv, gv, yv, bv);
+    if (r < a.m) fetch(r, zv, gv, yv, bv, jv);
     for (; r < a.m; r += U * row_step) {
       const uint32_t rn = r + U * row_step;
-      if (rn < a.m) fetch(rn, zn, gn, yn, bn_);
+      if (rn < a.m) fetch(rn, zn, gn, yn, bn_, jn);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool valid = r + u * row_step < a.m;  // rows past the end re-read row r: not accumulated
@@ -128,8 +139,16 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
             acc1[j] = fma(zd, zd, acc1[j]);
           }
         } else {
-          const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+          float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
           const float yy[4] = {yv[u].x, yv[u].y, yv[u].z, yv[u].w};
+          if (MODE == 2) {  // the join, exactly as k_add_masked_bits
+            const uint32_t row = r + u * row_step;
+            const uint32_t jb = jv[u] >> ((row * a.c + ch) & 31u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) gg[j] = __fadd_rn(yy[j], ((jb >> j) & 1u) ? gg[j] : 0.0f);
+            if (valid)
+              *reinterpret_cast<float4*>(a.gout + static_cast<size_t>(row) * a.c + ch) = make_float4(gg[0], gg[1], gg[2], gg[3]);
+          }
           double xh[4], gm[4];
           // MASK 3: this row's nibble (ch % 4 == 0, so the 4 bits share a word)
           const uint32_t w = (MASK == 3 && valid) ? bv[u] >> (((r + u * row_step) * a.c + ch) & 31u) : 0u;
@@ -138,7 +157,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
             const double xv = (static_cast<double>(zz[j]) - mean[j]) * invstd[j];
             bool mk = valid;
             if (MASK == 1) mk = mk && zz[j] >= lo[j] && zz[j] <= hi[j];
-            else if (MASK == 2) mk = mk && yy[j] > 0.0f;
+            else if (MODE == 1 && MASK == 2) mk = mk && yy[j] > 0.0f;
             else if (MASK == 3) mk = (w >> j) & 1u;
             float gmf;  // masked g as a float select, converted once
             asm("{.reg .pred p; setp.ne.u32 p, %1, 0; selp.f32 %0, %2, 0f00000000, p;}"
@@ -156,9 +175,10 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         zv[u] = zn[u];
-        if (MODE == 1) gv[u] = gn[u];
-        if (MODE == 1 && MASK == 2) yv[u] = yn[u];
-        if (MODE == 1 && MASK == 3) bv[u] = bn_[u];
+        if (MODE >= 1) gv[u] = gn[u];
+        if ((MODE == 1 && MASK == 2) || MODE == 2) yv[u] = yn[u];
+        if (MODE == 2) jv[u] = jn[u];
+        if (MODE >= 1 && MASK == 3) bv[u] = bn_[u];
       }
     }
   }
@@ -604,6 +624,7 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   if (!p || !t || !st) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
   if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t, st);
+  else if (mode == 2) launch_k(k_bn_colsum<2, 3>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 1) launch_k(k_bn_colsum<1, 1>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 2) launch_k(k_bn_colsum<1, 2>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 3) launch_k(k_bn_colsum<1, 3>, grid, 256, 0, c->stream, a, p, t, st);
@@ -695,6 +716,24 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
   // mask_mode 1: the column-sum kernel bisects the ReLU-mask bounds in its
   // prologue and stores them in bn[5c..6c)
   return colsum(cx, a, 1);
+}
+
+int i8t_bn_bwd_reduce_join(i8t_ctx* ctx, const float* a_add, const float* g, const uint32_t* join_bits,
+                           const float* z, int64_t m, int64_t c, double* bn, const float* gamma, const float* beta,
+                           const uint32_t* mask_bits, float* grad_gamma, float* grad_beta, float* g_out) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !a_add || !g || !join_bits || !bn || !gamma || !beta || !mask_bits || !grad_gamma || !grad_beta || !g_out)
+    return set_error(I8T_EINVAL, "bn_bwd_reduce_join: bad arguments");
+  if ((reinterpret_cast<uintptr_t>(a_add) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(g_out)) & 15u)
+    return set_error(I8T_EUNSUPPORTED, "bn_bwd_reduce_join: 16-byte alignment");
+  ColArgs a{};
+  a.z = z; a.g = g; a.mask_y = reinterpret_cast<const float*>(mask_bits); a.gamma = gamma; a.beta = beta; a.bn = bn;
+  a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = 3;
+  a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
+  a.ja = a_add; a.jbits = join_bits; a.gout = g_out;
+  return colsum(cx, a, 2);
 }
 
 int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,

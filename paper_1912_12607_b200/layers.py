@@ -88,6 +88,11 @@ JOIN_FUSION = os.environ.get("I8T_JOIN", "0") == "1"
 # main-branch gradient; 4 ResNet-50 blocks) pays off: 35.01 -> 34.90 ms per
 # step.  I8T_JOIN_PROJ=0 turns it off.
 JOIN_PROJ = os.environ.get("I8T_JOIN_PROJ", "1") == "1" or JOIN_FUSION
+# The identity-shortcut join (gm + g * mask) materialised inside the preceding
+# BatchNorm's backward column-sum pass instead of its own elementwise pass
+# (JoinGrad; g_out is written once and never re-read by the reduction).
+# I8T_JOIN_REDUCE=0 keeps the separate i8t_add_masked_bits.
+JOIN_REDUCE = os.environ.get("I8T_JOIN_REDUCE", "1") == "1"
 # Test instrumentation: when set, TRACE(conv, event, **tensors) is called at the
 # end of every INT8 Conv2d forward ("fwd") and backward ("bwd") -- the step-level
 # parity test (tests/test_gpu_step_parity.py) teacher-forces the CPU oracle with
@@ -158,13 +163,13 @@ class MaskedGrad:
         return self.g.numel()
 
     def materialize(self):
+        g = dense_grad(self.g)
         if self.mode == 2:
-            return torch.where(self.mask_y > 0, self.g, torch.zeros((), device=self.g.device))
+            return torch.where(self.mask_y > 0, g, torch.zeros((), device=g.device))
         if self.mode == 3:
-            return torch.where(unpack_mask(self.mask_y, self.g.numel()).view_as(self.g), self.g,
-                               torch.zeros((), device=self.g.device))
+            return torch.where(unpack_mask(self.mask_y, g.numel()).view_as(g), g, torch.zeros((), device=g.device))
         y = LazyAct(self.bn._z, self.bn, relu=True).materialize()
-        return torch.where(y > 0, self.g, torch.zeros((), device=self.g.device))
+        return torch.where(y > 0, g, torch.zeros((), device=g.device))
 
 
 class BnGrad:
@@ -192,6 +197,37 @@ class BnGrad:
         return out
 
 
+class JoinGrad:
+    """gm + g * bit: the identity-shortcut join of a residual block's backward
+    (layers.cpp:458-464) not yet materialised.  The preceding BatchNorm's
+    backward materialises it inside its column-sum pass
+    (i8t_bn_bwd_reduce_join); anything else calls materialize()."""
+
+    def __init__(self, gm, g, bits):
+        self.gm, self.g, self.bits = gm, g, bits
+        self.out = None
+
+    @property
+    def shape(self):
+        return self.g.shape
+
+    @property
+    def device(self):
+        return self.g.device
+
+    def numel(self):
+        return self.g.numel()
+
+    def materialize(self):
+        if self.out is None:
+            out = torch.empty_like(self.gm)
+            call("i8t_add_masked_bits", ops.ctx(), ops._p(self.gm), ops._p(self.g), ops._p(self.bits), self.gm.numel(),
+                 ops._p(out))
+            self.out = out
+            self.gm = self.g = self.bits = None
+        return self.out
+
+
 def unpack_mask(bits: torch.Tensor, n: int) -> torch.Tensor:
     """Packed ReLU mask (int32 words, bit e%32 of word e/32) -> bool [n]."""
     sh = torch.arange(32, device=bits.device, dtype=torch.int32)
@@ -203,7 +239,7 @@ def dense(x):
 
 
 def dense_grad(g):
-    return g.materialize() if isinstance(g, (MaskedGrad, BnGrad)) else g
+    return g.materialize() if isinstance(g, (MaskedGrad, BnGrad, JoinGrad)) else g
 
 
 # ------------------------------------------------------------------ state arena
@@ -730,6 +766,15 @@ class BatchNorm2d(Layer):
                     g = g.materialize()
                 else:
                     mode, mask_y, g = g.mode, g.mask_y, g.g
+            if isinstance(g, JoinGrad) and g.out is None and mode == 3 and JOIN_REDUCE:
+                n, h, w, c = g.shape
+                out = torch.empty_like(g.gm)
+                call("i8t_bn_bwd_reduce_join", ops.ctx(), ops._p(g.gm), ops._p(g.g), ops._p(g.bits), ops._p(self._z),
+                     n * h * w, c, ops._p(self.stats), ops._p(self.gamma), ops._p(self.beta), ops._p(mask_y),
+                     ops._p(self.grad_gamma), ops._p(self.grad_beta), ops._p(out))
+                g.out, g.gm, g.g, g.bits = out, None, None, None
+                gb = BnGrad(out, self, mode, mask_y)
+                return gb.materialize() if BN_IMPL == "eager" else gb
             g = dense_grad(g).contiguous()
             n, h, w, c = g.shape
             call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(self._z), n * h * w, c, ops._p(self.stats),
@@ -940,7 +985,8 @@ class ResidualBlock(Layer):
         return self.relu.forward(dense(y) + dense(sc), ctx)
 
     def backward(self, g, ctx):
-        g = dense_grad(g)
+        jg = g if isinstance(g, JoinGrad) and self._fused and self._bits is not None else None
+        g = jg if jg is not None else dense_grad(g)
         if self._fused:
             gl = MaskedGrad(g, 3, mask_y=self._bits) if self._bits is not None else MaskedGrad(g, 2, mask_y=self._y)
             first = self.main.children[0][1] if self.main.children else None
@@ -948,6 +994,8 @@ class ResidualBlock(Layer):
             if joinable and not self.shortcut:  # identity: conv1's dgrad adds g * (y > 0)
                 first.dgrad_join = (g, self._y, self._bits)
             gm = dense_grad(self.main.backward(gl, ctx))
+            if jg is not None:  # the main branch's last BN materialised the incoming join (or does it now)
+                g = jg.materialize()
             if joinable and not self.shortcut and first.join_done:
                 return gm
             if self.shortcut:
@@ -959,6 +1007,10 @@ class ResidualBlock(Layer):
                 if sc_join and sc.join_done:
                     return gs
                 return gm + gs
+            if self._bits is not None and JOIN_REDUCE and BN_IMPL == "fused":
+                jout = JoinGrad(gm, g, self._bits)
+                self._bits = self._y = None
+                return jout
             out = torch.empty_like(gm)
             if self._bits is not None:
                 call("i8t_add_masked_bits", ops.ctx(), ops._p(gm), ops._p(g), ops._p(self._bits), gm.numel(),

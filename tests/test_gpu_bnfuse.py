@@ -257,6 +257,33 @@ def test_packed_mask_mode3_equals_mode2(ops):
     assert torch.equal(o2, o3)
 
 
+@pytest.mark.parametrize("m,c", [(3136, 64), (1000, 256), (49 * 8, 2048)])
+def test_bn_bwd_reduce_join_equals_join_then_reduce(ops, m, c):
+    """i8t_bn_bwd_reduce_join (identity-shortcut join materialised inside the
+    BN backward column sums) == i8t_add_masked_bits then i8t_bn_bwd_reduce with
+    mask mode 3: the joined gradient, grad_gamma / grad_beta and the BN
+    coefficients bit for bit."""
+    z, gamma, beta, g = _data(m, c, 31)
+    rng = np.random.default_rng(32)
+    zt, gt, bt, g_t = t(z), t(gamma), t(beta), t(g)
+    a = t(rng.standard_normal((m, c)).astype(np.float32))
+    jbits = t(_pack_bits(rng.random(m * c) < 0.6))
+    mbits = t(_pack_bits(rng.random(m * c) < 0.5))
+    bn = _stats(ops, zt, c)
+    ref_g = torch.empty_like(zt)
+    ops.call("i8t_add_masked_bits", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(jbits), m * c, ops._p(ref_g))
+    bn_r, bn_f = bn.clone(), bn.clone()
+    gg_r, gb_r = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+    ops.call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(ref_g), ops._p(zt), m, c, ops._p(bn_r), ops._p(gt), ops._p(bt), 3,
+             ops._p(mbits), ops._p(gg_r), ops._p(gb_r))
+    out = torch.empty_like(zt)
+    gg_f, gb_f = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+    ops.call("i8t_bn_bwd_reduce_join", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(jbits), ops._p(zt), m, c,
+             ops._p(bn_f), ops._p(gt), ops._p(bt), ops._p(mbits), ops._p(gg_f), ops._p(gb_f), ops._p(out))
+    assert torch.equal(out.view(torch.int32), ref_g.view(torch.int32))
+    assert torch.equal(gg_f, gg_r) and torch.equal(gb_f, gb_r) and torch.equal(bn_f, bn_r)
+
+
 def test_bn_rejects_bad_shapes(ops):
     z = torch.zeros(10, 6, device="cuda")
     bn = torch.zeros(30, dtype=torch.float64, device="cuda")
