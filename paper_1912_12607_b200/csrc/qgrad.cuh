@@ -26,6 +26,11 @@ struct PlainSrc {
 // totals layout of K3 (QG_NV doubles): max|g|, nonfinite, sum g^2, sum g*gn,
 // sum gn^2, sum (g-gs)^2, sum gs^2, 0.
 constexpr int QG_NV = 8;
+// resident blocks per SM of K3 (register budget 65536 / (256 * QG_BLOCKS))
+#ifndef I8T_QG_BLOCKS
+#define I8T_QG_BLOCKS 2
+#endif
+constexpr int QG_BLOCKS = I8T_QG_BLOCKS;
 
 struct QgFin {
   int mode;  // bit0: d_c from the sums (non-search), bit1: lr scaling, bit2: plain quantize (no DSGC state)
@@ -70,7 +75,7 @@ static __device__ void fin_quant_grad(DsgcState* st, const double* tot, const Qg
 // dequantised values come from a per-block table (no conversions on the XU pipe
 // except double(g)).
 template <class Src, bool FLAT, bool DC_SUMS, bool FUSED>
-__global__ void __launch_bounds__(RED_THREADS, 2) k_quant_grad(Src src, uint32_t numel, uint32_t C,
+__global__ void __launch_bounds__(RED_THREADS, QG_BLOCKS) k_quant_grad(Src src, uint32_t numel, uint32_t C,
                                                             uint32_t HW, uint32_t draw_offset, Affine step_iter,
                                                             Affine step_elem, Affine step_wrap, uint32_t dpix,
                                                             const float* clip_override, DsgcState* st,
@@ -219,7 +224,7 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
   if (numel >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "quantize_gradient: tensor >= 2^31 elements");
   // grid: threads*4 must be a multiple of C (each thread keeps its channel quad)
   const int64_t mult = flat ? 1 : C / gcd_i(C, RED_THREADS * 4);
-  int nb = nblocks(numel, mult, 2 * 148);  // one resident wave (__launch_bounds__(256, 2))
+  int nb = nblocks(numel, mult, QG_BLOCKS * 148);  // one resident wave (__launch_bounds__(256, QG_BLOCKS))
   double* p = ensure_partials(c, static_cast<size_t>(nb) * QG_NV);
   if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
   const uint32_t T4 = static_cast<uint32_t>(nb) * RED_THREADS * 4u;
