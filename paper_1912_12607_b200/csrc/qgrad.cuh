@@ -84,6 +84,29 @@ __global__ void __launch_bounds__(RED_THREADS, QG_BLOCKS) k_quant_grad(Src src, 
                                                             int* err) {
   pdl_entry();
   __shared__ double tab[256];
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  const bool live = e < numel;
+  // the first two data fetches and the per-channel coefficients go out before
+  // the chain of dependent scalar loads (clip -> table, LCG state -> jump)
+  uint32_t hw = 0, draw0 = 0;
+  typename Src::Raw ra{}, rb{}, rc{};
+  if (live) {
+    if (FLAT) {
+      draw0 = e;
+      src.init(0u);
+    } else {
+      const uint32_t pix = e / C, c = e - pix * C;
+      const uint32_t n = pix / HW;
+      hw = pix - n * HW;
+      draw0 = (n * C + c) * HW + hw;
+      src.init(c);
+    }
+    ra = src.fetch(e / 4);
+    rb = ra;
+    rc = ra;
+    if (e + T4 < numel) rb = src.fetch((e + T4) / 4);
+  }
   float clip = clip_override ? *clip_override : st->v.clip;
   if (!(clip > 0.0f)) clip = 1.0f;  // only with an all-zero g (q == 0 either way)
   const float s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
@@ -94,22 +117,10 @@ __global__ void __launch_bounds__(RED_THREADS, QG_BLOCKS) k_quant_grad(Src src, 
   const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 8u * (127u - RMAGIC_BITS);
   const uint32_t tab_n = tab_s - 8u;
   const uint32_t X0 = *lcg_state;
-  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
-  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
   double a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0, a6 = 0.0;
   float m = 0.0f;
-  if (e < numel) {
-    uint32_t X, hw = 0;
-    if (FLAT) {
-      X = apply(lcg_jump_map(static_cast<uint64_t>(e) + draw_offset + 1u), X0);
-      src.init(0u);
-    } else {
-      const uint32_t pix = e / C, c = e - pix * C;
-      const uint32_t n = pix / HW;
-      hw = pix - n * HW;
-      X = apply(lcg_jump_map(static_cast<uint64_t>((n * C + c) * HW + hw) + draw_offset + 1u), X0);
-      src.init(c);
-    }
+  if (live) {
+    uint32_t X = apply(lcg_jump_map(static_cast<uint64_t>(draw0) + draw_offset + 1u), X0);
     // one float4: fast path; any element within QK of a rounding boundary (or
     // with a float-subnormal BN x_hat) sends the float4 to the exact functions
     auto process = [&](const typename Src::Raw& r) {
@@ -155,19 +166,18 @@ __global__ void __launch_bounds__(RED_THREADS, QG_BLOCKS) k_quant_grad(Src src, 
     };
     auto advance = [&]() {
       e += T4;
-      X = apply(step_iter, X);
+      X = apply(step_iter, X);  // NHWC: includes the dpix / HW whole image wraps
       if (!FLAT) {
-        hw += dpix;
-        while (hw >= HW) {
+        hw += dpix;  // dpix % HW
+        if (hw >= HW) {
           hw -= HW;
           X = apply(step_wrap, X);
         }
       }
     };
     // three-slot ring, two float4 fetches in flight ahead of the one being
-    // quantised; unrolled so the slots never move between registers
-    typename Src::Raw ra = src.fetch(e / 4), rb = ra, rc = ra;
-    if (e + T4 < numel) rb = src.fetch((e + T4) / 4);
+    // quantised (the first two issued above); unrolled so the slots never move
+    // between registers
     while (true) {  // e + 2*T4 < 2^31 + 2*T4: no wrap
       if (e + 2 * T4 < numel) rc = src.fetch((e + 2 * T4) / 4);
       process(ra);
@@ -235,8 +245,13 @@ int launch_quant_grad_src(Ctx* c, DsgcState* st, const float* clip_override, Src
     step_iter = lcg_jump_map(T4);
     step_elem = lcg_jump_map(1);
   } else {
-    dpix = T4 / static_cast<uint32_t>(C);
-    step_iter = lcg_jump_map(dpix);
+    // a thread steps dpix pixels: q = dpix / HW whole images (each adds
+    // (C-1)*HW draws beyond the pixels) folded into step_iter, and at most one
+    // more image wrap from the remainder (small-HW layers would otherwise loop)
+    const uint32_t dp = T4 / static_cast<uint32_t>(C);
+    const uint64_t q = dp / static_cast<uint64_t>(HW);
+    dpix = static_cast<uint32_t>(dp - q * static_cast<uint64_t>(HW));
+    step_iter = lcg_jump_map(static_cast<uint64_t>(dp) + q * static_cast<uint64_t>(C - 1) * static_cast<uint64_t>(HW));
     step_elem = lcg_jump_map(static_cast<uint64_t>(HW));
     step_wrap = lcg_jump_map(static_cast<uint64_t>(C - 1) * static_cast<uint64_t>(HW));
   }
