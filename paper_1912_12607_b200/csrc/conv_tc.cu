@@ -35,6 +35,25 @@ namespace i8t_dev {
 
 enum ConvMode { MODE_FWD = 0, MODE_DGRAD = 1, MODE_WGRAD = 2 };
 
+// Division of a non-negative int32 by a kernel-invariant divisor d >= 1 as a
+// multiply-high: q = (umulhi(x, m) + x) >> s with s = ceil(log2 d),
+// m = floor(2^32 (2^s - d) / d) + 1 (exact for 0 <= x < 2^31).  The conv
+// producers decode (n, p, q) / (tap, channel) per row and per k-block; a
+// runtime integer division is ~20 dependent instructions (a 64-bit one a call).
+struct FDiv {
+  uint32_t m, s;
+};
+inline FDiv fdiv_of(int d) {
+  uint32_t sh = 0;
+  while ((1ull << sh) < static_cast<uint64_t>(d)) ++sh;
+  const uint64_t m = ((1ull << 32) * ((1ull << sh) - static_cast<uint64_t>(d))) / static_cast<uint64_t>(d) + 1;
+  return FDiv{d > 1 ? static_cast<uint32_t>(m) : 0u, sh};
+}
+__device__ __forceinline__ int fdiv(int64_t x, FDiv f) {
+  const uint32_t u = static_cast<uint32_t>(x);
+  return static_cast<int>((__umulhi(u, f.m) + u) >> f.s);
+}
+
 struct ConvArgs {
   const int8_t* act;  // NHWC [N][H][W][Cp]
   const int8_t* gz;   // NHWC [N][P][Q][Kp]
@@ -71,7 +90,22 @@ struct ConvArgs {
   const float* add_g;
   const float* add_y;
   const uint32_t* add_bits;  // instead of add_y: packed mask (bit e of word e/32 for flat NHWC index e)
+  // fast divisions by the invariant extents (set_divs, before every launch)
+  FDiv dCp, dKp, dS, dQ, dW, dWq, dns, dpq, dhw, dhwq;
 };
+
+inline void set_divs(ConvArgs& a) {
+  a.dCp = fdiv_of(a.Cp > 0 ? a.Cp : 1);
+  a.dKp = fdiv_of(a.Kp > 0 ? a.Kp : 1);
+  a.dS = fdiv_of(a.S > 0 ? a.S : 1);
+  a.dQ = fdiv_of(a.Q > 0 ? a.Q : 1);
+  a.dW = fdiv_of(a.W > 0 ? a.W : 1);
+  a.dWq = fdiv_of(a.Wq > 0 ? a.Wq : 1);
+  a.dns = fdiv_of(a.ns > 0 ? a.ns : 1);
+  a.dpq = fdiv_of(a.P * a.Q > 0 ? a.P * a.Q : 1);
+  a.dhw = fdiv_of(a.H * a.W > 0 ? a.H * a.W : 1);
+  a.dhwq = fdiv_of(a.Hq * a.Wq > 0 ? a.Hq * a.Wq : 1);
+}
 
 // residual addend of output row `orow`, columns c0..c0+3
 __device__ __forceinline__ float4 join_addend(const ConvArgs& a, int64_t orow, int c0) {
@@ -107,8 +141,8 @@ __device__ __forceinline__ float dequant_acc(double rescale, uint32_t v) {
 __device__ __forceinline__ int64_t out_row_of(const ConvArgs& a, int64_t m) {
   if (!a.phase) return m;
   const int hwq = a.Hq * a.Wq;
-  const int n = static_cast<int>(m / hwq), rem = static_cast<int>(m - static_cast<int64_t>(n) * hwq);
-  const int hh = rem / a.Wq, ww = rem - hh * a.Wq;
+  const int n = fdiv(m, a.dhwq), rem = static_cast<int>(m - static_cast<int64_t>(n) * hwq);
+  const int hh = fdiv(rem, a.dWq), ww = rem - hh * a.Wq;
   return (static_cast<int64_t>(n) * a.H + hh * a.sh + a.fh) * a.W + ww * a.sw + a.fw;
 }
 
@@ -241,16 +275,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
             if (MODE == MODE_FWD && args.tma_a == 2) {  // this CTA's 128 output pixels, im2col
               const int pq = args.P * args.Q;
-              const int n = m0 / pq, rem = m0 - n * pq, p = rem / args.Q, q = rem - p * args.Q;
-              const int tap = kb / args.Cp, cb = kb - tap * args.Cp;
-              const int r = tap / args.S, sx = tap - r * args.S;
+              const int n = fdiv(m0, args.dpq), rem = m0 - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
+              const int tap = fdiv(kb, args.dCp), cb = kb - tap * args.Cp;
+              const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
               tma_load_im2col_4d_pair(a_st, &tmap_a, lbar, cb, q * args.sw - args.pw, p * args.sh - args.ph, n,
                                       static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
             } else if (MODE == MODE_DGRAD && args.tma_a == 2) {
               const int hw = args.H * args.W;
-              const int n = m0 / hw, rem = m0 - n * hw, h = rem / args.W, w = rem - h * args.W;
-              const int tap = kb / args.Kp, kc = kb - tap * args.Kp;
-              const int r = tap / args.S, sx = tap - r * args.S;
+              const int n = fdiv(m0, args.dhw), rem = m0 - n * hw, h = fdiv(rem, args.dW), w = rem - h * args.W;
+              const int tap = fdiv(kb, args.dKp), kc = kb - tap * args.Kp;
+              const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
               tma_load_im2col_4d_pair(a_st, &tmap_a, lbar, kc, w - (args.S - 1 - args.pw), h - (args.R - 1 - args.ph),
                                       n, static_cast<uint16_t>(args.S - 1 - sx), static_cast<uint16_t>(args.R - 1 - r));
             } else {
@@ -264,9 +298,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             // implicit im2col by TMA: 128 consecutive output pixels of tap (r, s),
             // 128 channels from cb; zero padding = out-of-box fill
             const int pq = args.P * args.Q;
-            const int n = m0 / pq, rem = m0 - n * pq, p = rem / args.Q, q = rem - p * args.Q;
-            const int tap = kb / args.Cp, cb = kb - tap * args.Cp;
-            const int r = tap / args.S, sx = tap - r * args.S;
+            const int n = fdiv(m0, args.dpq), rem = m0 - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
+            const int tap = fdiv(kb, args.dCp), cb = kb - tap * args.Cp;
+            const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
             tma_load_im2col_4d(a_st, &tmap_a, &full[s], cb, q * args.sw - args.pw, p * args.sh - args.ph, n,
                                static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
             tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
@@ -278,21 +312,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               // [128 npq rows][64 channels] (SWIZZLE_64B) of their own (tap, c0);
               // a half past M repeats the last valid rows (its output rows are dropped)
               const int pq = args.P * args.Q;
-              const int n = kb / pq, rem = kb - n * pq, p = rem / args.Q, q = rem - p * args.Q;
+              const int n = fdiv(kb, args.dpq), rem = kb - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 int mh = static_cast<int>(m0) + 64 * h;
                 if (mh >= args.M) mh = args.M - 64;
-                const int tap = mh / args.Cp, c0 = mh - tap * args.Cp;
-                const int r = tap / args.S, sx = tap - r * args.S;
+                const int tap = fdiv(mh, args.dCp), c0 = mh - tap * args.Cp;
+                const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
                 tma_load_im2col_4d(a_st + h * 8192, &tmap_a, &full[s], c0, q * args.sw - args.pw, p * args.sh - args.ph,
                                    n, static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
               }
             } else if (args.tma_a == 2) {  // im2col rows npq = kb.. of tap (r, s), channels c0 of the m-tile
               const int pq = args.P * args.Q;
-              const int n = kb / pq, rem = kb - n * pq, p = rem / args.Q, q = rem - p * args.Q;
-              const int tap = m0 / args.Cp, c0 = m0 - tap * args.Cp;
-              const int r = tap / args.S, sx = tap - r * args.S;
+              const int n = fdiv(kb, args.dpq), rem = kb - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
+              const int tap = fdiv(m0, args.dCp), c0 = m0 - tap * args.Cp;
+              const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
               tma_load_im2col_4d(a_st, &tmap_a, &full[s], c0, q * args.sw - args.pw, p * args.sh - args.ph, n,
                                  static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
             } else {
@@ -306,9 +340,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               // (ir, is) reads g_z at (hh + dh - ir, ww + dw - is) = base (hh + dh -
               // (nr-1), ww + dw - (ns-1)) + mirrored offset (nr-1-ir, ns-1-is)
               const int hwq = args.Hq * args.Wq;
-              const int n = m0 / hwq, rem = m0 - n * hwq, hh = rem / args.Wq, ww = rem - hh * args.Wq;
-              const int it = kb / args.Kp, kc = kb - it * args.Kp;
-              const int ir = it / args.ns, is = it - ir * args.ns;
+              const int n = fdiv(m0, args.dhwq), rem = m0 - n * hwq, hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
+              const int it = fdiv(kb, args.dKp), kc = kb - it * args.Kp;
+              const int ir = fdiv(it, args.dns), is = it - ir * args.ns;
               tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, ww + args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n,
                                  static_cast<uint16_t>(args.ns - 1 - is), static_cast<uint16_t>(args.nr - 1 - ir));
               const int bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp + kc;
@@ -320,9 +354,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               // tap (r, s) reads g_z at (h + ph - r, w + pw - s) = base (h - (R-1-ph),
               // w - (S-1-pw)) + mirrored offset (R-1-r, S-1-s)
               const int hw = args.H * args.W;
-              const int n = m0 / hw, rem = m0 - n * hw, h = rem / args.W, w = rem - h * args.W;
-              const int tap = kb / args.Kp, kc = kb - tap * args.Kp;
-              const int r = tap / args.S, sx = tap - r * args.S;
+              const int n = fdiv(m0, args.dhw), rem = m0 - n * hw, h = fdiv(rem, args.dW), w = rem - h * args.W;
+              const int tap = fdiv(kb, args.dKp), kc = kb - tap * args.Kp;
+              const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
               tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, w - (args.S - 1 - args.pw), h - (args.R - 1 - args.ph), n,
                                  static_cast<uint16_t>(args.S - 1 - sx), static_cast<uint16_t>(args.R - 1 - r));
             } else {
@@ -360,22 +394,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           const int mm = rowA_ok[i] ? static_cast<int>(m) : 0;
           if constexpr (MODE == MODE_FWD) {
             const int pq = args.P * args.Q;
-            const int n = mm / pq, rem = mm - n * pq;
-            const int p = rem / args.Q, q = rem - p * args.Q;
+            const int n = fdiv(mm, args.dpq), rem = mm - n * pq;
+            const int p = fdiv(rem, args.dQ), q = rem - p * args.Q;
             rowA_n[i] = n;
             rowA_y[i] = p * args.sh - args.ph;
             rowA_x[i] = q * args.sw - args.pw;
           } else if (args.phase) {
             const int hwq = args.Hq * args.Wq;
-            const int n = mm / hwq, rem = mm - n * hwq;
-            const int hh = rem / args.Wq, ww = rem - hh * args.Wq;
+            const int n = fdiv(mm, args.dhwq), rem = mm - n * hwq;
+            const int hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
             rowA_n[i] = n;
             rowA_y[i] = hh + args.dh;
             rowA_x[i] = ww + args.dw;
           } else {
             const int hw = args.H * args.W;
-            const int n = mm / hw, rem = mm - n * hw;
-            const int h = rem / args.W, w = rem - h * args.W;
+            const int n = fdiv(mm, args.dhw), rem = mm - n * hw;
+            const int h = fdiv(rem, args.dW), w = rem - h * args.W;
             rowA_n[i] = n;
             rowA_y[i] = h + args.ph;
             rowA_x[i] = w + args.pw;
@@ -393,8 +427,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             mbar_expect_tx(&full[s], C::B_BYTES);
             int bx = static_cast<int>(kbase);
             if (MODE == MODE_DGRAD && args.phase) {  // compact tap index -> CRSK column of (r, s)
-              const int it = static_cast<int>(kbase / args.Kp);
-              const int ir = it / args.ns, is = it - ir * args.ns;
+              const int it = fdiv(kbase, args.dKp);
+              const int ir = fdiv(it, args.dns), is = it - ir * args.ns;
               bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp +
                    static_cast<int>(kbase - static_cast<int64_t>(it) * args.Kp);
             }
@@ -403,10 +437,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           const int64_t kk = kbase + ja * VA;
           const bool kok = kk < args.Kd;
           const int CH = (MODE == MODE_FWD) ? args.Cp : args.Kp;
-          const int tap = kok ? static_cast<int>(kk / CH) : 0;
+          const int tap = kok ? fdiv(kk, (MODE == MODE_FWD) ? args.dCp : args.dKp) : 0;
           const int ch = kok ? static_cast<int>(kk - static_cast<int64_t>(tap) * CH) : 0;
           const int tS = (MODE == MODE_DGRAD && args.phase) ? args.ns : args.S;
-          const int r = tap / tS, sx = tap - r * tS;
+          const int r = fdiv(tap, (MODE == MODE_DGRAD && args.phase) ? args.dns : args.dS), sx = tap - r * tS;
 #pragma unroll
           for (int i = 0; i < PASSES_A; ++i) {
             const int row = ra0 + i * ROWS_PER_PASS_A;
@@ -448,17 +482,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                 if (kt == 0) {
                   const int64_t mR = m0 + jr * RUN;
                   runOk = mR < args.M;
-                  const int tapR = runOk ? static_cast<int>(mR / args.Cp) : 0;
+                  const int tapR = runOk ? fdiv(mR, args.dCp) : 0;
                   runC = runOk ? static_cast<int>(mR - static_cast<int64_t>(tapR) * args.Cp) : 0;
-                  runR = tapR / args.S;
+                  runR = fdiv(tapR, args.dS);
                   runS = tapR - runR * args.S;
 #pragma unroll
                   for (int i = 0; i < PASSES; ++i) {
                     const int kdi = static_cast<int>(kbase) + r0 + i * RPP;
                     const int pq = args.P * args.Q;
-                    const int n = kdi / pq, rem = kdi - n * pq;
+                    const int n = fdiv(kdi, args.dpq), rem = kdi - n * pq;
                     rowA_n[i] = n;
-                    rowA_y[i] = rem / args.Q;
+                    rowA_y[i] = fdiv(rem, args.dQ);
                     rowA_x[i] = rem - rowA_y[i] * args.Q;
                   }
                 }
@@ -489,17 +523,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           if (!run_path) {
           const int64_t mA = m0 + ja * VA;
           const bool mok = mA < args.M;
-          const int tapA = mok ? static_cast<int>(mA / args.Cp) : 0;
+          const int tapA = mok ? fdiv(mA, args.dCp) : 0;
           const int cA = mok ? static_cast<int>(mA - static_cast<int64_t>(tapA) * args.Cp) : 0;
-          const int rA = tapA / args.S, sA_ = tapA - rA * args.S;
+          const int rA = fdiv(tapA, args.dS), sA_ = tapA - rA * args.S;
           if (kt == 0) {  // decode this thread's rows once per tile, then advance 128 pixels per k-tile
 #pragma unroll
             for (int i = 0; i < PASSES_A; ++i) {
               const int kdi = static_cast<int>(kbase) + ra0 + i * ROWS_PER_PASS_A;
               const int pq = args.P * args.Q;
-              const int n = kdi / pq, rem = kdi - n * pq;
+              const int n = fdiv(kdi, args.dpq), rem = kdi - n * pq;
               rowA_n[i] = n;
-              rowA_y[i] = rem / args.Q;
+              rowA_y[i] = fdiv(rem, args.dQ);
               rowA_x[i] = rem - rowA_y[i] * args.Q;
             }
           }
@@ -1075,8 +1109,10 @@ static int num_sms() {
 
 // CTA-pair launch (TMA-operand path, 256-row tiles): a.m_tiles counts 256-row tiles.
 template <int MODE, int BN>
-static int launch_pair(cudaStream_t st, const ConvArgs& a, const CUtensorMap& amap, const CUtensorMap& map,
+static int launch_pair(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& amap, const CUtensorMap& map,
                        const CUtensorMap& omap) {
+  ConvArgs a = a0;
+  set_divs(a);
   using C = Cfg<MODE, BN, 2>;
   static bool configured = false;
   if (!configured) {
@@ -1103,8 +1139,10 @@ static bool pair_enabled() {
 }
 
 template <int MODE, int BN, int VA, int VB>
-static int launch_one(cudaStream_t st, const ConvArgs& a, const CUtensorMap& amap, const CUtensorMap& map,
+static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& amap, const CUtensorMap& map,
                       const CUtensorMap& omap) {
+  ConvArgs a = a0;
+  set_divs(a);
   using C = Cfg<MODE, BN>;
   static bool configured = false;
   if (!configured) {
@@ -1231,6 +1269,7 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
             !x.add_bits && !x.acc32)
           continue;
         const int blocks = (int)std::min<int64_t>((x.M + 7) / 8, 148 * 16);
+        set_divs(x);
         launch_k(k_zero_phase, blocks, 256, 0, c->stream, x);
         count_launch(1);
         int rc = cuda_check("k_zero_phase");
