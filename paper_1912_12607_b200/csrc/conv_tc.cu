@@ -84,6 +84,7 @@ struct ConvArgs {
   // thread -- no cp.async gather
   int tma_a;
   int tma_b;  // WGRAD with a gathered A: B = g_z rows still come by TMA (tmap_b)
+  int wg_cb;  // WGRAD tma_a == 3: channel block of the im2col boxes (64 or 32 bytes), 128 / wg_cb boxes per m-tile
   // DGRAD residual join fused into the epilogue: out = dgrad + add_g, or
   // dgrad + add_g * (add_y > 0) when add_y is set (a single float add, so the
   // result equals the separate join bit for bit)
@@ -308,20 +309,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           }
           if constexpr (MODE == MODE_WGRAD) {
             if (args.tma_a == 3) {
-              // 64-channel taps: the m-tile's two 64-row halves are two im2col boxes
-              // [128 npq rows][64 channels] (SWIZZLE_64B) of their own (tap, c0);
-              // a half past M repeats the last valid rows (its output rows are dropped)
+              // 64- / 32-channel taps: the m-tile's 128 rows are 128 / cb im2col boxes
+              // [128 npq rows][cb channels] (SWIZZLE_64B / 32B) of their own (tap, c0);
+              // a box past M repeats the last valid rows (its output rows are dropped)
               const int pq = args.P * args.Q;
               const int n = fdiv(kb, args.dpq), rem = kb - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
+              auto boxes = [&](auto cb_c) {
+                constexpr int CB = decltype(cb_c)::value;
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                int mh = static_cast<int>(m0) + 64 * h;
-                if (mh >= args.M) mh = args.M - 64;
-                const int tap = fdiv(mh, args.dCp), c0 = mh - tap * args.Cp;
-                const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
-                tma_load_im2col_4d(a_st + h * 8192, &tmap_a, &full[s], c0, q * args.sw - args.pw, p * args.sh - args.ph,
-                                   n, static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
-              }
+                for (int h = 0; h < 128 / CB; ++h) {
+                  int mh = static_cast<int>(m0) + CB * h;
+                  if (mh >= args.M) mh = static_cast<int>(args.M) - CB;
+                  const int tap = fdiv(mh, args.dCp), c0 = mh - tap * args.Cp;
+                  const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
+                  tma_load_im2col_4d(a_st + h * 128 * CB, &tmap_a, &full[s], c0, q * args.sw - args.pw,
+                                     p * args.sh - args.ph, n, static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+                }
+              };
+              if (args.wg_cb == 64) boxes(std::integral_constant<int, 64>{});
+              else boxes(std::integral_constant<int, 32>{});
             } else if (args.tma_a == 2) {  // im2col rows npq = kb.. of tap (r, s), channels c0 of the m-tile
               const int pq = args.P * args.Q;
               const int n = fdiv(kb, args.dpq), rem = kb - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
@@ -596,6 +602,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
       constexpr bool MN = (MODE == MODE_WGRAD);
       constexpr uint32_t idesc = make_idesc_i8(TM, BN, MN, MN);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      // A descriptor of stage 0, kk 0 and its per-kk start-address step (the
+      // start field holds addr >> 4 in the low 14 bits: plain adds stay in it)
+      uint64_t a_desc0;
+      uint32_t a_kstep;
+      if constexpr (MN) {
+        const int cb = args.tma_a == 3 ? args.wg_cb : 128;
+        a_desc0 = cb == 128 ? make_sdesc_sw128(a0, 16384, 1024)
+                  : cb == 64 ? make_sdesc_sw64_mn(a0, 8192, 512) : make_sdesc_sw32_mn(a0, 4096, 256);
+        a_kstep = (32u * static_cast<uint32_t>(cb)) >> 4;
+      } else {
+        a_desc0 = make_sdesc_sw128(a0, 16, 1024);
+        a_kstep = 32u >> 4;
+      }
       int kc = 0, it = 0;
       for (int t = cta0; t < total_tiles; t += ncta, ++it) {
         const TileCoord tc = tile_of(args, t);
@@ -614,14 +633,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
 #pragma unroll
           for (int kk = 0; kk < BKB / 32; ++kk) {
             uint64_t ad, bd;
+            // A: the stage-0 / kk-0 descriptor advanced in its start-address field
+            ad = a_desc0 + static_cast<uint64_t>((static_cast<uint32_t>(s) * C::A_BYTES >> 4) + kk * a_kstep);
             if constexpr (MN) {
               // MN-major: 32 reduction rows per MMA = 4096 B; SBO = 8-row atom stride, LBO = 128-col sub-tile
-              ad = args.tma_a == 3 ? make_sdesc_sw64_mn(a0 + s * C::A_BYTES + kk * 2048, 8192, 512)
-                                   : make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 4096, 16384, 1024);
               bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 4096, 16384, 1024);
             } else {
               // K-major: 32 B of reduction per MMA inside the 128 B swizzled row; SBO = 8 rows x 128 B
-              ad = make_sdesc_sw128(a0 + s * C::A_BYTES + kk * 32, 16, 1024);
               bd = make_sdesc_sw128(b0 + s * C::B_BYTES + kk * 32, 16, 1024);
             }
             if constexpr (PAIR) mma_i8_pair(d_tmem, ad, bd, idesc, (kt | kk) != 0 ? 1u : 0u);
@@ -1055,7 +1073,7 @@ static bool im2col_ok(const i8t_conv_geom* g, int64_t c_pad, const void* a, int6
   return (g->w + 2 * g->pad_w - g->kw) / g->stride_w + 1 == Q && (g->h + 2 * g->pad_h - g->kh) / g->stride_h + 1 == P;
 }
 
-// I8T_NO_WG64=1 keeps the cp.async gather for 64-channel-block wgrads (A/B experiments).
+// I8T_NO_WG64=1 keeps the cp.async gather for 64 / 32-channel-block wgrads (A/B experiments).
 static bool wg64_off() {
   static const bool off = getenv("I8T_NO_WG64") != nullptr;
   return off;
@@ -1518,10 +1536,15 @@ int i8t_conv_wgrad(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* gz, int64
   } else if (im2col_ok(g, c_pad, a, P, Q) && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
     x.tma_a = 2;  // A = im2col of the activations (128 npq rows x 128 channels of one tap), B = g_z rows
     if ((rc = make_im2col_map(&amap, a, g, c_pad))) return rc;
-  } else if (!wg64_off() && im2col_ok(g, c_pad, a, P, Q, 64) && x.M >= 64 && k_pad % 16 == 0 &&
-             (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
-    x.tma_a = 3;  // 64-channel blocks: two im2col boxes per m-tile (SWIZZLE_64B, MN-major SW64 descriptor)
-    if ((rc = make_im2col_map(&amap, a, g, c_pad, 64u, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  } else if (!wg64_off() && im2col_ok(g, c_pad, a, P, Q, 32) && k_pad % 16 == 0 &&
+             (reinterpret_cast<uintptr_t>(gz) & 15u) == 0 && x.M >= (c_pad % 64 == 0 ? 64 : 32)) {
+    // 64 / 32-channel blocks: 2 / 4 im2col boxes per m-tile (SWIZZLE_64B / 32B,
+    // MN-major SW64 / SW32 descriptor) -- the 64-channel layers, the stem's folded taps
+    x.tma_a = 3;
+    x.wg_cb = c_pad % 64 == 0 ? 64 : 32;
+    if ((rc = make_im2col_map(&amap, a, g, c_pad, static_cast<uint32_t>(x.wg_cb),
+                              x.wg_cb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)))
+      return rc;
   }
   static const bool no_tma_b = getenv("I8T_NO_TMA_A") != nullptr;
   if (x.tma_a || (!no_tma_b && k_pad % 16 == 0 && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0)) {

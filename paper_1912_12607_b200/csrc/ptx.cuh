@@ -332,6 +332,17 @@ __device__ __forceinline__ uint64_t make_sdesc_sw64_mn(uint32_t saddr, uint32_t 
   d |= 4ull << 61;
   return d;
 }
+// The same with SWIZZLE_32B (layout type 6): 32-byte MN chunks at LBO, 8-row K
+// groups (8 x 32 B) at SBO.
+__device__ __forceinline__ uint64_t make_sdesc_sw32_mn(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= 6ull << 61;
+  return d;
+}
 __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
          ((static_cast<uint32_t>(N) >> 3) << 17) | ((static_cast<uint32_t>(M) >> 4) << 24);
