@@ -295,6 +295,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             continue;
           }
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
+          if (MODE == MODE_FWD && args.tma_a == 3) {
+            // 32-channel taps (the stem's folded taps): the k-block's four 32-byte K
+            // chunks are four im2col boxes [128 output pixels][32 channels]
+            // (SWIZZLE_32B), one per MMA; a chunk past Kd repeats a valid tap (its
+            // weights are the zero fill of the weight box)
+            const int pq = args.P * args.Q;
+            const int n = fdiv(m0, args.dpq), rem = m0 - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              int kh = kb + 32 * h;
+              if (kh >= args.Kd) kh = static_cast<int>(args.Kd) - 32;
+              const int tap = fdiv(kh, args.dCp), cb = kh - tap * args.Cp;
+              const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
+              tma_load_im2col_4d(a_st + h * 4096, &tmap_a, &full[s], cb, q * args.sw - args.pw, p * args.sh - args.ph,
+                                 n, static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+            }
+            tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
+            continue;
+          }
           if (MODE == MODE_FWD && args.tma_a == 2) {
             // implicit im2col by TMA: 128 consecutive output pixels of tap (r, s),
             // 128 channels from cb; zero padding = out-of-box fill
@@ -611,6 +630,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         a_desc0 = cb == 128 ? make_sdesc_sw128(a0, 16384, 1024)
                   : cb == 64 ? make_sdesc_sw64_mn(a0, 8192, 512) : make_sdesc_sw32_mn(a0, 4096, 256);
         a_kstep = (32u * static_cast<uint32_t>(cb)) >> 4;
+      } else if (MODE == MODE_FWD && args.tma_a == 3) {
+        a_desc0 = make_sdesc_sw32_k(a0, 256);  // MMA kk reads box kk: [128 rows][32 B]
+        a_kstep = 4096u >> 4;
       } else {
         a_desc0 = make_sdesc_sw128(a0, 16, 1024);
         a_kstep = 32u >> 4;
@@ -1367,6 +1389,9 @@ int i8t_conv_fwd(i8t_ctx* ctx, const i8t_conv_geom* g, const int8_t* a, int64_t 
   } else if (im2col_ok(g, c_pad, a, P, Q)) {
     x.tma_a = 2;
     if ((rc = make_im2col_map(&amap, a, g, c_pad))) return rc;
+  } else if (!pair && !wg64_off() && c_pad == 32 && im2col_ok(g, c_pad, a, P, Q, 32)) {
+    x.tma_a = 3;  // 32-channel taps: four SWIZZLE_32B im2col boxes per k-block (K-major SW32 descriptor)
+    if ((rc = make_im2col_map(&amap, a, g, c_pad, 32u, CU_TENSOR_MAP_SWIZZLE_32B))) return rc;
   }
   x.use_tma_out = tma_out_ok(z, g->k) ? 1 : 0;
   if (x.use_tma_out && (rc = make_out_map(&omap, z, g->k, x.M, g->k, false))) return rc;

@@ -332,6 +332,16 @@ __device__ __forceinline__ uint64_t make_sdesc_sw64_mn(uint32_t saddr, uint32_t 
   d |= 4ull << 61;
   return d;
 }
+// K-major SWIZZLE_32B: 32-byte rows (one MMA's K = 32 int8), 8-row groups at SBO.
+__device__ __forceinline__ uint64_t make_sdesc_sw32_k(uint32_t saddr, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;  // LBO unused for swizzled K-major
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= 6ull << 61;
+  return d;
+}
 // The same with SWIZZLE_32B (layout type 6): 32-byte MN chunks at LBO, 8-row K
 // groups (8 x 32 B) at SBO.
 __device__ __forceinline__ uint64_t make_sdesc_sw32_mn(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
