@@ -134,6 +134,14 @@ int i8t_quantize_nearest(i8t_ctx* ctx, const float* x, int64_t n, const float* c
                          int accumulate_amax);
 /* Same quantiser, writing rows of `cols` values into a padded row stride
  * ld_q >= cols (zero pad).  x is [rows, cols] contiguous (NHWC activations). */
+/* The activation quantiser of a second consumer of the same tensor x (the
+ * projection-shortcut conv beside the block's first conv, both quantising x
+ * with their own clip, layers.cpp:101-109): when *clip equals *ref_clip bit for
+ * bit the result is ref_q (copied) and *amax takes max(*amax, *ref_amax);
+ * otherwise q = quantize_nearest(x, *clip) with the running max|x| into *amax
+ * (accumulated).  n elements, 16-byte aligned x / q / ref_q. */
+int i8t_quantize_nearest_shared(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, const float* ref_clip,
+                                const int8_t* ref_q, const float* ref_amax, int8_t* q, float* amax);
 int i8t_quantize_nearest_rows(i8t_ctx* ctx, const float* x, int64_t rows, int64_t cols, const float* clip,
                               int8_t* q, int64_t ld_q, float* amax, int accumulate_amax);
 /* NCHW float -> NHWC int8 with padded channel stride c_pad (drop-in path). */

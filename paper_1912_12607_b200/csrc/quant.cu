@@ -57,6 +57,55 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_flat(const float*
   if (amax) block_amax(m, amax);
 }
 
+// K1 of a second consumer of the same activations (the projection shortcut
+// conv beside the block's first conv): when its clip equals the first
+// consumer's bit for bit, the int8 tensor is the same -- copy it (2 B per
+// element instead of 5) and take over the first consumer's running max;
+// otherwise quantise as k_quant_nearest_flat.
+__global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_share(const float* __restrict__ x, uint32_t n,
+                                                                     const float* __restrict__ clip_p,
+                                                                     const float* __restrict__ ref_clip,
+                                                                     const int8_t* __restrict__ ref_q,
+                                                                     const float* ref_amax, int8_t* __restrict__ q,
+                                                                     float* amax, int* err) {
+  pdl_entry();
+  const float clip = *clip_p;
+  if (__float_as_uint(clip) == __float_as_uint(*ref_clip)) {
+    const uint32_t n16 = n / 16, stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+      reinterpret_cast<uint4*>(q)[i] = __ldg(reinterpret_cast<const uint4*>(ref_q) + i);
+    for (uint32_t i = n16 * 16 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) q[i] = ref_q[i];
+    if (amax && ref_amax && blockIdx.x == 0 && threadIdx.x == 0) {
+      const float r = *ref_amax;
+      if (r > 0.0f) atomicMax(reinterpret_cast<int*>(amax), __float_as_int(r));
+    }
+    return;
+  }
+  const float s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
+  float m = 0.0f;
+  bool bad = false;
+  const uint32_t n4 = n / 4, stride = gridDim.x * blockDim.x;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  char4* q4 = reinterpret_cast<char4*>(q);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = __ldg(x4 + i);
+    bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    q4[i] = make_char4(static_cast<signed char>(quant_nearest_fast(v.x, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.y, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.z, clip, hs, s, inv_s)),
+                       static_cast<signed char>(quant_nearest_fast(v.w, clip, hs, s, inv_s)));
+  }
+  for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = x[i];
+    bad |= !isfinite(v);
+    m = fmaxf(m, fabsf(v));
+    q[i] = static_cast<int8_t>(quant_nearest_fast(v, clip, hs, s, inv_s));
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+  if (amax) block_amax(m, amax);
+}
+
 // K1 rows: x [rows][cols] -> q [rows][ld_q], zero pad (e.g. the C=3 stem -> 4).
 __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float* __restrict__ x, uint32_t rows,
                                                                     uint32_t cols, const float* __restrict__ clip_p,
@@ -400,6 +449,20 @@ using namespace i8t_dev;
 #define CTX(c) reinterpret_cast<Ctx*>(c)
 
 extern "C" {
+
+int i8t_quantize_nearest_shared(i8t_ctx* ctx, const float* x, int64_t n, const float* clip, const float* ref_clip,
+                                const int8_t* ref_q, const float* ref_amax, int8_t* q, float* amax) {
+  Ctx* c = CTX(ctx);
+  if (!c || !x || !clip || !ref_clip || !ref_q || !q || n < 0) return set_error(I8T_EINVAL, "quantize: bad arguments");
+  if (n == 0) return I8T_OK;
+  if (too_big(n)) return set_error(I8T_EUNSUPPORTED, "quantize: tensor >= 2^31 elements");
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(ref_q)) & 15u))
+    return set_error(I8T_EUNSUPPORTED, "quantize_nearest_shared: 16-byte alignment");
+  launch_k(k_quant_nearest_share, grid_for(n / 4 + 1), RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), clip,
+           ref_clip, ref_q, ref_amax, q, amax, c->d_err);
+  count_launch(1);
+  return cuda_check("k_quant_nearest_share");
+}
 
 int i8t_quantize_nearest_rows(i8t_ctx* ctx, const float* x, int64_t rows, int64_t cols, const float* clip, int8_t* q,
                               int64_t ld_q, float* amax, int accumulate_amax) {

@@ -93,6 +93,10 @@ JOIN_PROJ = os.environ.get("I8T_JOIN_PROJ", "1") == "1" or JOIN_FUSION
 # (JoinGrad; g_out is written once and never re-read by the reduction).
 # I8T_JOIN_REDUCE=0 keeps the separate i8t_add_masked_bits.
 JOIN_REDUCE = os.environ.get("I8T_JOIN_REDUCE", "1") == "1"
+# The projection shortcut conv reuses the block's first conv's int8 input when
+# their activation clips agree (i8t_quantize_nearest_shared).  I8T_SHARE_ACT=0
+# quantises twice.
+SHARE_ACT = os.environ.get("I8T_SHARE_ACT", "1") == "1"
 # Test instrumentation: when set, TRACE(conv, event, **tensors) is called at the
 # end of every INT8 Conv2d forward ("fwd") and backward ("bwd") -- the step-level
 # parity test (tests/test_gpu_step_parity.py) teacher-forces the CPU oracle with
@@ -411,6 +415,9 @@ class Conv2d(Layer):
         # dgrad epilogue returns dgrad + add_g [* (add_y > 0)]; join_done reports it
         self.dgrad_join = None
         self.join_done = False
+        self.act_twin = None  # a conv quantising the same input first (ResidualBlock: the shortcut's twin)
+        self.keep_qa_src = False  # this conv is someone's act_twin: remember which tensor _qa quantised
+        self._qa_src = None
 
     @property
     def quantized(self):
@@ -505,6 +512,14 @@ class Conv2d(Layer):
         pre = getattr(x, "_i8t_q", None) if not fuse_in else None
         if pre is not None and pre[0] is self:  # quantised by the producing block (i8t_bn_act_q)
             qa = pre[1]
+        elif (not fuse_in and self.act_twin is not None and self.act_twin._qa_src is x and self.c_pad == c
+              and self.act_twin._qa is not None and self.act_twin._qa.shape == qa.shape):
+            # same input as the block's first conv (projection shortcut): its int8
+            # tensor when the clips agree (they track the same tensor), else quantise
+            tw = self.act_twin
+            call("i8t_quantize_nearest_shared", h, ops._p(x), x.numel(), ops._p(qs.clip_a), ops._p(tw.qs.clip_a),
+                 ops._p(tw._qa), ops._p(tw.qs.pending_amax) if ctx.track_amax else None, ops._p(qa),
+                 ops._p(qs.pending_amax) if ctx.track_amax else None)
         elif fuse_in:  # BN-apply + ReLU + nearest quantise + amax in one pass over z
             bn = x.bn
             call("i8t_bn_act_quant", h, ops._p(x.z), n * hh * ww, c, ops._p(bn.stats), ops._p(bn.gamma),
@@ -514,6 +529,7 @@ class Conv2d(Layer):
             call("i8t_quantize_nearest_rows", h, ops._p(x), n * hh * ww, c, ops._p(qs.clip_a), ops._p(qa),
                  self.c_pad, ops._p(qs.pending_amax) if ctx.track_amax else None, 1)
         self._qa = qa
+        self._qa_src = x if (self.keep_qa_src and not fuse_in) else None
         z = torch.empty((n, p, q, self.out_c), dtype=torch.float32, device=dev)
         if self.depthwise:
             call("i8t_conv_dw_fwd", h, C.byref(g), ops._p(qa), self.c_pad, ops._p(self._qw), ops._p(qs.clip_a),
@@ -967,11 +983,19 @@ class ResidualBlock(Layer):
     def __init__(self, main: Sequential, shortcut: Sequential | None):
         self.main, self.shortcut, self.relu = main, shortcut, ReLU()
         self.next_conv = None  # first conv of the next block: its int8 input is written with the block output
+        first = main.children[0][1] if main.children else None
+        sc = shortcut.children[0][1] if shortcut and shortcut.children else None
+        if isinstance(first, Conv2d) and isinstance(sc, Conv2d) and SHARE_ACT:
+            sc.act_twin = first  # both quantise the block input x
+            first.keep_qa_src = True
 
     def forward(self, x, ctx):
         x = dense(x)
         y = self.main.forward(x, ctx)
         sc = self.shortcut.forward(x, ctx) if self.shortcut else x
+        first = self.main.children[0][1] if self.main.children else None
+        if isinstance(first, Conv2d):
+            first._qa_src = None  # the shortcut has taken its int8 input (or not): drop the reference
         if isinstance(y, LazyAct) and not y.relu:  # relu(bn3(z3) + shortcut) in one pass
             bits = None
             if ctx.training and y.z.numel() % 4 == 0:  # the backward keeps one bit of y per element

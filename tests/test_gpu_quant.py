@@ -391,3 +391,27 @@ def test_sgd_dclr_matches_oracle(ops):
     wt = t(w)
     ops.sgd_dclr_(wt, t(gr), 0.05, st)
     np.testing.assert_array_equal(wt.cpu().numpy(), O.sgd_update(w, gr, 0.05 * 0.37))
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_quantize_nearest_shared(same, ops):
+    """i8t_quantize_nearest_shared: with the reference clip bit-equal the result
+    is the reference int8 tensor and the running max is taken over; otherwise
+    the plain nearest quantiser of x (payload and running max)."""
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal(4096 * 3).astype(np.float32)
+    xt = t(x)
+    ref_clip = torch.tensor([2.5], device="cuda")
+    ref_amax = torch.tensor([3.25], device="cuda")
+    ref_q = torch.randint(-127, 128, (x.size,), dtype=torch.int8, device="cuda")
+    clip = torch.tensor([2.5 if same else 1.75], device="cuda")
+    q = torch.empty_like(ref_q)
+    amax = torch.tensor([0.5], device="cuda")
+    ops.call("i8t_quantize_nearest_shared", ops.ctx(), ops._p(xt), x.size, ops._p(clip), ops._p(ref_clip),
+             ops._p(ref_q), ops._p(ref_amax), ops._p(q), ops._p(amax))
+    torch.cuda.synchronize()
+    if same:
+        assert torch.equal(q, ref_q) and float(amax) == 3.25
+    else:
+        assert np.array_equal(q.cpu().numpy(), O.quantize(x, 1.75)[0])
+        assert float(amax) == max(0.5, float(np.abs(x).max()))
