@@ -22,7 +22,13 @@
 #include "qgrad.cuh"
 #include "bncore.cuh"
 
+#ifndef I8T_BNQ_BLOCKS
+#define I8T_BNQ_BLOCKS 3
+#endif
 namespace i8t_dev {
+
+// resident blocks per SM of k_bn_act_quant: its grid is one such wave
+constexpr int BNQ_BLOCKS = I8T_BNQ_BLOCKS;
 
 constexpr int BN_GROUP = 128;  // channels per column-reduction block group
 
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
 }
 
 // Forward: q = quantize_nearest(act(bn(z))), running max|act| (layers.cpp:101, 108-109).
-__global__ void __launch_bounds__(256) k_bn_act_quant(const float* __restrict__ z, uint32_t n, uint32_t c,
+__global__ void __launch_bounds__(256, BNQ_BLOCKS) k_bn_act_quant(const float* __restrict__ z, uint32_t n, uint32_t c,
                                                       const double* bn, const float* gamma, const float* beta, int relu,
                                                       const float* clip_p, int8_t* __restrict__ q, float* amax,
                                                       int* err) {
@@ -557,11 +563,11 @@ __global__ void __launch_bounds__(256) k_add_masked_bits(const float* __restrict
 }
 
 // ---------------------------------------------------------------- host
-static int ew_blocks(int64_t n, int64_t c) {
+static int ew_blocks(int64_t n, int64_t c, int64_t cap = 148 * 8) {
   // grid such that blocks*256*4 % c == 0 (fixed channel quad per thread)
   const int64_t mult = c / gcd_i(c, 1024);
   int64_t b = (n / 4 + 255) / 256;
-  if (b > 148 * 8) b = 148 * 8;
+  if (b > cap) b = cap;
   if (b < 1) b = 1;
   b = (b + mult - 1) / mult * mult;
   return static_cast<int>(b);
@@ -573,7 +579,8 @@ static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const d
                           const float* res_gamma, const float* res_beta, float* y, const float* clip, int8_t* q,
                           uint32_t* mbits, float* amax) {
   const uint32_t n = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
-  const int nb = ew_blocks(m * c, c);
+  // one resident wave (k_bn_act's __launch_bounds__: 2 blocks per SM with a lazy residual BN, else 3)
+  const int nb = ew_blocks(m * c, c, 148 * (res_z ? 2 : 3));
   if (res_z)
     launch_k(k_bn_act<QOUT, 2>, nb, 256, 0, cx->stream, z, n, uc, bn, gamma, beta, relu, nullptr, res_z, res_bn, res_gamma,
                                                   res_beta, y, clip, q, mbits, amax, cx->d_err);
@@ -665,7 +672,7 @@ int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const d
   int rc = bn_check(m, c, z);
   if (rc) return rc;
   if (!cx || !bn || !gamma || !beta || !clip || !q) return set_error(I8T_EINVAL, "bn_act_quant: bad arguments");
-  launch_k(k_bn_act_quant, ew_blocks(m * c, c), 256, 0, cx->stream, z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c),
+  launch_k(k_bn_act_quant, ew_blocks(m * c, c, 148 * BNQ_BLOCKS), 256, 0, cx->stream, z, static_cast<uint32_t>(m * c), static_cast<uint32_t>(c),
                                                                bn, gamma, beta, relu, clip, q, amax, cx->d_err);
   count_launch(1);
   return cuda_check("k_bn_act_quant");
