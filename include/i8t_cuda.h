@@ -330,6 +330,12 @@ int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t 
 /* gx [n,h,w,c] = sum of gy over the windows whose argmax (idx) is (h, w). */
 int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n, int64_t h, int64_t w, int64_t c,
                     int64_t k, int64_t s, int64_t pad, float* gx);
+/* Global average pool, NHWC [n][hw][c] -> [n][c]: float(double sum / hw) per
+ * (n, c), summed in the reference's order (Pool2d kAvg over the whole map,
+ * layers.cpp:383-388); backward gx[n][p][c] = g[n][c] / float(hw)
+ * (layers.cpp:392-414; c % 4 == 0, 16-byte aligned). */
+int i8t_global_avgpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t hw, int64_t c, float* y);
+int i8t_global_avgpool_bwd(i8t_ctx* ctx, const float* g, int64_t n, int64_t hw, int64_t c, float* gx);
 /* q = quantize_nearest(act(bn(z)), clip) with running max|act| -> *amax: the
  * next conv's input quantiser (layers.cpp:101, 109) fused with BN + ReLU. */
 int i8t_bn_act_quant(i8t_ctx* ctx, const float* z, int64_t m, int64_t c, const double* bn, const float* gamma,

@@ -169,6 +169,39 @@ static int grid_of(int64_t tot) {
 
 using namespace i8t_dev;
 
+// Global average pool over NHWC [n][hw][c] (Pool2d kAvg with the window the
+// whole map, layers.cpp:383-388): one thread per (n, c) sums its hw values in
+// double in the reference's order, then float(acc / hw).
+__global__ void __launch_bounds__(256) k_gap_fwd(const float* __restrict__ x, int n, int hw, int c,
+                                                 float* __restrict__ y) {
+  pdl_entry();
+  const int64_t tot = static_cast<int64_t>(n) * c;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / c, ch = i - b * c;
+    const float* p = x + b * hw * c + ch;
+    double acc = 0.0;
+    for (int k = 0; k < hw; ++k) acc += __ldg(p + static_cast<int64_t>(k) * c);
+    y[i] = static_cast<float>(acc / hw);
+  }
+}
+
+// Its backward (layers.cpp:392-414): every position of (n, c) gets
+// g[n][c] / float(hw).
+__global__ void __launch_bounds__(256) k_gap_bwd(const float* __restrict__ g, int n, int hw, int c,
+                                                 float* __restrict__ gx) {
+  pdl_entry();
+  const float inv = static_cast<float>(hw);
+  const int64_t c4 = c / 4, tot = static_cast<int64_t>(n) * hw * c4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / c4, q = i - row * c4, b = row / hw;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(g + b * c) + q);
+    reinterpret_cast<float4*>(gx)[i] = make_float4(__fdiv_rn(v.x, inv), __fdiv_rn(v.y, inv), __fdiv_rn(v.z, inv),
+                                                   __fdiv_rn(v.w, inv));
+  }
+}
+
 extern "C" {
 
 int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t w, int64_t c, int64_t k, int64_t s,
@@ -203,6 +236,28 @@ int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n
   launch_k(k_maxpool_bwd, grid_of(tot), 256, 0, cx->stream, gy, idx, g, gx);
   count_launch(1);
   return cuda_check("k_maxpool_bwd");
+}
+
+int i8t_global_avgpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t hw, int64_t c, float* y) {
+  Ctx* cx = reinterpret_cast<Ctx*>(ctx);
+  if (!cx || !x || !y || n < 1 || hw < 1 || c < 1) return set_error(I8T_EINVAL, "global_avgpool_fwd: bad arguments");
+  if (n * hw * c >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "global_avgpool: tensor >= 2^31 elements");
+  launch_k(k_gap_fwd, grid_of(n * c), 256, 0, cx->stream, x, static_cast<int>(n), static_cast<int>(hw),
+           static_cast<int>(c), y);
+  count_launch(1);
+  return cuda_check("k_gap_fwd");
+}
+
+int i8t_global_avgpool_bwd(i8t_ctx* ctx, const float* g, int64_t n, int64_t hw, int64_t c, float* gx) {
+  Ctx* cx = reinterpret_cast<Ctx*>(ctx);
+  if (!cx || !g || !gx || n < 1 || hw < 1 || c < 4 || c % 4 ||
+      ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gx)) & 15u))
+    return set_error(I8T_EINVAL, "global_avgpool_bwd: bad arguments (c % 4, 16-byte alignment)");
+  if (n * hw * c >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "global_avgpool: tensor >= 2^31 elements");
+  launch_k(k_gap_bwd, grid_of(n * hw * (c / 4)), 256, 0, cx->stream, g, static_cast<int>(n), static_cast<int>(hw),
+           static_cast<int>(c), gx);
+  count_launch(1);
+  return cuda_check("k_gap_bwd");
 }
 
 }  // extern "C"

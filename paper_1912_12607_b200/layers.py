@@ -938,14 +938,22 @@ class GlobalAvgPool(Layer):
     kind = "avgpool"
 
     def forward(self, x, ctx):
-        x = dense(x)
+        x = dense(x).contiguous()
         self._shape = x.shape
         n, h, w, c = x.shape
+        if x.is_cuda:
+            y = torch.empty((n, c), dtype=torch.float32, device=x.device)
+            call("i8t_global_avgpool_fwd", ops.ctx(), ops._p(x), n, h * w, c, ops._p(y))
+            return y
         return (torch.sum(x, dim=(1, 2), dtype=torch.float64) / (h * w)).float()
 
     def backward(self, g, ctx):
-        g = dense_grad(g)
+        g = dense_grad(g).contiguous()
         n, h, w, c = self._shape
+        if g.is_cuda and c % 4 == 0:
+            gx = torch.empty((n, h, w, c), dtype=torch.float32, device=g.device)
+            call("i8t_global_avgpool_bwd", ops.ctx(), ops._p(g), n, h * w, c, ops._p(gx))
+            return gx
         return (g / (h * w)).reshape(n, 1, 1, c).expand(n, h, w, c).contiguous()
 
 

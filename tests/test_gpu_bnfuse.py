@@ -458,3 +458,23 @@ def test_maxpool_bn_first_max_slot_exact(ops, case):
             want_y[:, pp, qq, :], want_i[:, pp, qq, :] = best, arg
     np.testing.assert_array_equal(y.cpu().numpy(), want_y)
     np.testing.assert_array_equal(idx.cpu().numpy(), want_i)
+
+
+def test_global_avgpool_matches_reference_order(ops):
+    """i8t_global_avgpool_fwd / _bwd (Pool2d kAvg over the whole map,
+    layers.cpp:383-414): the window summed in double in the reference's
+    sequential order then float(acc / hw); backward g / float(hw) everywhere."""
+    rng = np.random.default_rng(51)
+    n, h, w, c = 4, 7, 7, 96
+    x = rng.standard_normal((n, h, w, c)).astype(np.float32) * np.float32(3.0)
+    y = torch.empty((n, c), device="cuda")
+    ops.call("i8t_global_avgpool_fwd", ops.ctx(), ops._p(t(x)), n, h * w, c, ops._p(y))
+    acc = np.zeros((n, c), np.float64)
+    for k in range(h * w):  # reference order: row-major over the window
+        acc += x.reshape(n, h * w, c)[:, k, :].astype(np.float64)
+    np.testing.assert_array_equal(y.cpu().numpy(), (acc / (h * w)).astype(np.float32))
+    g = rng.standard_normal((n, c)).astype(np.float32)
+    gx = torch.empty((n, h, w, c), device="cuda")
+    ops.call("i8t_global_avgpool_bwd", ops.ctx(), ops._p(t(g)), n, h * w, c, ops._p(gx))
+    ref = np.broadcast_to((g / np.float32(h * w))[:, None, None, :], (n, h, w, c))
+    np.testing.assert_array_equal(gx.cpu().numpy(), ref)
