@@ -330,6 +330,13 @@ int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t 
 /* gx [n,h,w,c] = sum of gy over the windows whose argmax (idx) is (h, w). */
 int i8t_maxpool_bwd(i8t_ctx* ctx, const float* gy, const uint8_t* idx, int64_t n, int64_t h, int64_t w, int64_t c,
                     int64_t k, int64_t s, int64_t pad, float* gx);
+/* SoftmaxCrossEntropy::loss_and_grad (layers.cpp:507-529) on the device:
+ * logits [n][classes] fp32, labels [n] int64; g_logits = float((p - y) / n_total),
+ * *loss = sum of the row losses / n_total (double; n_total = the global batch
+ * under data parallelism), *bad = 1 when the loss or any logit is non-finite
+ * (the divergence check of train.cpp:73-77), else 0. */
+int i8t_softmax_ce(i8t_ctx* ctx, const float* logits, const int64_t* labels, int64_t n, int64_t classes,
+                   int64_t n_total, float* g_logits, double* loss, int32_t* bad);
 /* Global average pool, NHWC [n][hw][c] -> [n][c]: float(double sum / hw) per
  * (n, c), summed in the reference's order (Pool2d kAvg over the whole map,
  * layers.cpp:383-388); backward gx[n][p][c] = g[n][c] / float(hw)

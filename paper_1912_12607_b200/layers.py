@@ -1091,14 +1091,28 @@ class SoftmaxCrossEntropy:
     loss as a 0-d CUDA double tensor and g_logits = float((p - y) / N)."""
 
     @staticmethod
-    def loss_and_grad(logits: torch.Tensor, labels: torch.Tensor, total_n: int | None = None):
-        """total_n: the global batch under data parallelism (default: local)."""
+    def loss_and_grad(logits: torch.Tensor, labels: torch.Tensor, total_n: int | None = None, bad=None):
+        """total_n: the global batch under data parallelism (default: local).
+        bad: optional int32 [1] device tensor that receives the divergence flag
+        (non-finite loss or logits) of the same pass."""
         n = logits.shape[0] if total_n is None else total_n
+        if logits.is_cuda and labels.dtype == torch.int64:
+            logits = logits.contiguous()
+            g = torch.empty_like(logits)
+            loss = torch.empty((), dtype=torch.float64, device=logits.device)
+            flag = bad if bad is not None else torch.empty(1, dtype=torch.int32, device=logits.device)
+            call("i8t_softmax_ce", ops.ctx(), ops._p(logits), ops._p(labels.contiguous()), logits.shape[0],
+                 logits.shape[1], n, ops._p(g), ops._p(loss), ops._p(flag))
+            return loss, g
+        if bad is not None:
+            bad.copy_(((~torch.isfinite(logits).all())).to(torch.int32).reshape(1))
         ld = logits.double()
         logz = torch.logsumexp(ld, dim=1)
         loss = (logz - ld.gather(1, labels.view(-1, 1)).squeeze(1)).sum() / n
         p = torch.exp(ld - logz.view(-1, 1))
         p[torch.arange(logits.shape[0], device=logits.device), labels] -= 1.0
+        if bad is not None:
+            bad.bitwise_or_((~torch.isfinite(loss)).to(torch.int32).reshape(1))
         return loss, (p / n).float()
 
 

@@ -242,11 +242,10 @@ class Trainer:
         wq = cfg.mode == Mode.INT8 and self._quantize_weights_at_once()
         logits = self.model.net.forward(images, ForwardCtx(cfg.mode, True, cfg.mode == Mode.INT8, wq))
         # data parallel: the mean is over the GLOBAL batch (loss summed across ranks when read)
-        loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels, logits.shape[0] * self.world)
-        bad = ((~torch.isfinite(loss)) | (~torch.isfinite(logits).all())).to(torch.int32).reshape(1)
+        # the divergence flag (non-finite loss or logits, train.cpp:73-77) comes out of the same pass
+        loss, g_logits = SoftmaxCrossEntropy.loss_and_grad(logits, labels, logits.shape[0] * self.world, bad=self.div)
         if self.world > 1:  # every rank takes the same branch
-            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-        self.div.copy_(bad)
+            dist.all_reduce(self.div, op=dist.ReduceOp.MAX)
         self.loss_dev.copy_(loss.reshape(1))
         self._snap_arena.copy_(self.arena.buf)
         self._snap_lcg.copy_(self.grad_stream)

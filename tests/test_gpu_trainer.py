@@ -132,3 +132,32 @@ def test_resnet20_trains_with_exact_stream_accounting():
     after = ops.lcg_value(tr.grad_stream)
     assert len(sizes) == 22
     assert after == O.lcg_jump(before, sum(sizes))
+
+
+def test_softmax_ce_device_matches_reference_formula():
+    """i8t_softmax_ce (SoftmaxCrossEntropy::loss_and_grad, layers.cpp:507-529):
+    loss and g_logits against a float64 numpy restatement, plus the divergence
+    flag on a non-finite logit."""
+    import numpy as np
+    import torch
+    from paper_1912_12607_b200.layers import SoftmaxCrossEntropy
+    rng = np.random.default_rng(61)
+    n, k = 37, 1000
+    x = (rng.standard_normal((n, k)) * 4).astype(np.float32)
+    lab = rng.integers(0, k, n)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    loss, g = SoftmaxCrossEntropy.loss_and_grad(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(), 2 * n,
+                                                bad=bad)
+    xd = x.astype(np.float64)
+    mx = xd.max(1, keepdims=True)
+    logz = mx + np.log(np.exp(xd - mx).sum(1, keepdims=True))
+    ref_loss = float((logz[:, 0] - xd[np.arange(n), lab]).sum() / (2 * n))
+    p = np.exp(xd - logz)
+    p[np.arange(n), lab] -= 1.0
+    ref_g = (p / (2 * n)).astype(np.float32)
+    assert float(loss) == pytest.approx(ref_loss, rel=1e-13)
+    np.testing.assert_allclose(g.cpu().numpy(), ref_g, rtol=2e-7, atol=1e-12)
+    assert int(bad) == 0
+    x[3, 17] = np.inf
+    SoftmaxCrossEntropy.loss_and_grad(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(), n, bad=bad)
+    assert int(bad) == 1
