@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(256) k_gap_fwd(const float* __restrict__ x, in
     const int64_t b = i / c, ch = i - b * c;
     const float* p = x + b * hw * c + ch;
     double acc = 0.0;
+#pragma unroll 8
     for (int k = 0; k < hw; ++k) acc += __ldg(p + static_cast<int64_t>(k) * c);
     y[i] = static_cast<float>(acc / hw);
   }
@@ -192,13 +193,15 @@ __global__ void __launch_bounds__(256) k_gap_bwd(const float* __restrict__ g, in
                                                  float* __restrict__ gx) {
   pdl_entry();
   const float inv = static_cast<float>(hw);
-  const int64_t c4 = c / 4, tot = static_cast<int64_t>(n) * hw * c4;
+  const int64_t c4 = c / 4, tot = static_cast<int64_t>(n) * c4;
+  // thread per (n, channel quad): the four shares once, then the hw positions
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = i / c4, q = i - row * c4, b = row / hw;
-    const float4 v = __ldg(reinterpret_cast<const float4*>(g + b * c) + q);
-    reinterpret_cast<float4*>(gx)[i] = make_float4(__fdiv_rn(v.x, inv), __fdiv_rn(v.y, inv), __fdiv_rn(v.z, inv),
-                                                   __fdiv_rn(v.w, inv));
+    const int64_t b = i / c4, q = i - b * c4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(g) + i);
+    const float4 o = make_float4(__fdiv_rn(v.x, inv), __fdiv_rn(v.y, inv), __fdiv_rn(v.z, inv), __fdiv_rn(v.w, inv));
+    float4* dst = reinterpret_cast<float4*>(gx) + b * hw * c4 + q;
+    for (int k = 0; k < hw; ++k) dst[static_cast<int64_t>(k) * c4] = o;
   }
 }
 
@@ -254,7 +257,7 @@ int i8t_global_avgpool_bwd(i8t_ctx* ctx, const float* g, int64_t n, int64_t hw, 
       ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gx)) & 15u))
     return set_error(I8T_EINVAL, "global_avgpool_bwd: bad arguments (c % 4, 16-byte alignment)");
   if (n * hw * c >= (int64_t(1) << 31)) return set_error(I8T_EUNSUPPORTED, "global_avgpool: tensor >= 2^31 elements");
-  launch_k(k_gap_bwd, grid_of(n * hw * (c / 4)), 256, 0, cx->stream, g, static_cast<int>(n), static_cast<int>(hw),
+  launch_k(k_gap_bwd, grid_of(n * (c / 4)), 256, 0, cx->stream, g, static_cast<int>(n), static_cast<int>(hw),
            static_cast<int>(c), gx);
   count_launch(1);
   return cuda_check("k_gap_bwd");
