@@ -156,14 +156,18 @@ constexpr int EPI_WARP0 = 9;
 constexpr int NEPI = 256;                    // 8 epilogue warps: 2 per TMEM lane quadrant
 constexpr int NTHREADS = NPROD + 32 + NEPI;  // 544
 
-template <int MODE, int BN, int CG = 1>
+// EDB = 1: two staging buffers per epilogue warp (a chunk's TMA store can still
+// be reading one while the next chunk is written to the other) at the price of
+// pipeline stages -- for the short-reduction convs whose fp32 epilogue is the
+// bottleneck (a tile of 1-4 k-blocks).
+template <int MODE, int BN, int CG = 1, int EDB = 0>
 struct Cfg {
   static constexpr int A_BYTES = BM * BKB;  // 16 KB
   static constexpr int B_SUB = (BN + 127) / 128;
   // CG == 2 (CTA pair): each CTA holds half of the B tile's N rows
   static constexpr int B_BYTES = (MODE == MODE_WGRAD) ? 128 * 128 * B_SUB : (BN / CG) * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = 8 * 32 * 128;  // per epilogue warp: one [32 rows x 128 B] staging tile
+  static constexpr int EPI_BYTES = (EDB ? 2 : 1) * 8 * 32 * 128;  // per epilogue warp: [32 rows x 128 B] staging tile(s)
   static constexpr int BUDGET = 232448 - EPI_BYTES - 1024 - 256;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -196,11 +200,11 @@ __device__ __forceinline__ int tile_nk(const ConvArgs& a, int split) {
 // tcgen05.mma.cta_group::2 -- each CTA loads its 128 A rows and half of the B
 // rows (TMA, completion counted on the leader's barrier), the leader issues
 // the M = 256 MMAs and multicasts their commits; TMA-operand path only.
-template <int MODE, int BN, int VA, int VB, int CG = 1>
+template <int MODE, int BN, int VA, int VB, int CG = 1, int EDB = 0>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
                                                           const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
-  using C = Cfg<MODE, BN, CG>;
+  using C = Cfg<MODE, BN, CG, EDB>;
   constexpr bool PAIR = CG == 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
     const int row = quad * 32 + lane;
     const double rescale =
         static_cast<double>(__fdiv_rn(*args.clip_x, 127.0f)) * static_cast<double>(__fdiv_rn(*args.clip_y, 127.0f));
-    const uint32_t stage_s = smem_u32(sEpi + (warp - EPI_WARP0) * (32 * 128));
+    const uint32_t stage_s = smem_u32(sEpi + (warp - EPI_WARP0) * ((EDB ? 2 : 1) * 32 * 128));
     int it = 0, nst = 0;
     constexpr int HALF = BN / 2 < 32 ? 32 : BN / 2;
     constexpr int NCH = HALF / 32;  // 32-column chunks per epilogue warp per tile
@@ -720,8 +724,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
         const int gc0 = n0 + col;
         if (args.use_tma_out) {
           // 32x32 sub-tile -> swizzled smem staging -> one TMA bulk store
-          const uint32_t buf_s = stage_s;
-          if (lane == 0) bulk_wait_read<0>();  // the previous store has finished reading the buffer
+          const uint32_t buf_s = stage_s + (EDB ? static_cast<uint32_t>(nst & 1) * (32 * 128) : 0u);
+          if (lane == 0) {  // the store that last used this buffer has finished reading it
+            if constexpr (EDB) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -1178,15 +1185,25 @@ static bool pair_enabled() {
   return on;
 }
 
-template <int MODE, int BN, int VA, int VB>
+// k-blocks per tile up to which FWD / DGRAD take the double-buffered epilogue
+// staging (I8T_EDB_KT; 0 turns it off)
+static int edb_max_ktiles() {
+  static const int v = [] {
+    const char* e = getenv("I8T_EDB_KT");
+    return e ? atoi(e) : 4;
+  }();
+  return v;
+}
+
+template <int MODE, int BN, int VA, int VB, int EDB = 0>
 static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& amap, const CUtensorMap& map,
                       const CUtensorMap& omap) {
   ConvArgs a = a0;
   set_divs(a);
-  using C = Cfg<MODE, BN>;
+  using C = Cfg<MODE, BN, 1, EDB>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_conv_tc<MODE, BN, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_conv_tc<MODE, BN, VA, VB, 1, EDB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
   const int tiles = a.m_tiles * a.n_tiles * a.splits;
@@ -1196,7 +1213,7 @@ static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& am
   }();
   const int sms = cap > 0 && cap < num_sms() ? cap : num_sms();
   const int grid = tiles < sms ? tiles : sms;
-  launch_k(k_conv_tc<MODE, BN, VA, VB>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
+  launch_k(k_conv_tc<MODE, BN, VA, VB, 1, EDB>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
 }
@@ -1204,7 +1221,14 @@ static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& am
 template <int MODE, int BN>
 static int dispatch_vec(cudaStream_t st, const ConvArgs& a, const CUtensorMap& am, const CUtensorMap& m,
                         const CUtensorMap& o, int va, int vb) {
-  if (a.tma_a) return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);  // no gather: vector widths unused
+  if (a.tma_a) {  // no gather: vector widths unused
+    if constexpr (MODE != MODE_WGRAD)
+      // (with BN = 256 only on small grids: the fourth pipeline stage it costs
+      // matters more than the staging once every SM runs tens of tiles)
+      if (a.use_tma_out && a.k_tiles <= edb_max_ktiles() && (BN <= 128 || a.M < 131072))
+        return launch_one<MODE, BN, 16, 16, 1>(st, a, am, m, o);
+    return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);
+  }
   if constexpr (MODE == MODE_WGRAD) {
     if (vb == 16) {
       if (va == 16) return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);
