@@ -202,18 +202,44 @@ __global__ void __launch_bounds__(256) k_quant_weight_multi(const i8t_wq_desc* _
       }
     }
     __syncthreads();
-    if (d.q_krsc)  // [k][rs][c]: c along the lanes
-      for (int pr = warp; pr < nk * RS; pr += 8) {
-        const int kk = pr / RS, rs = pr - kk * RS;
-        int8_t* dst = d.q_krsc + static_cast<size_t>(k0 + kk) * d.ld_krsc + rs * d.c_pad + c0;
-        for (int cc = lane; cc < nc; cc += 32) dst[cc] = tq[kk * TC * RS + cc * RS + rs];
+    // write-out, four bytes per lane (one 32-bit store): the lanes of a warp
+    // cover several rows when a row has fewer than 32 quads
+    auto put4 = [](int8_t* dst, int n4, const int8_t* src, int stride) {  // n4 = valid bytes (1..4)
+      const uint32_t b0 = static_cast<uint8_t>(src[0]);
+      const uint32_t b1 = n4 > 1 ? static_cast<uint8_t>(src[stride]) : 0u;
+      const uint32_t b2 = n4 > 2 ? static_cast<uint8_t>(src[2 * stride]) : 0u;
+      const uint32_t b3 = n4 > 3 ? static_cast<uint8_t>(src[3 * stride]) : 0u;
+      if (n4 == 4 && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) {
+        *reinterpret_cast<uint32_t*>(dst) = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+      } else {
+        dst[0] = static_cast<int8_t>(b0);
+        if (n4 > 1) dst[1] = static_cast<int8_t>(b1);
+        if (n4 > 2) dst[2] = static_cast<int8_t>(b2);
+        if (n4 > 3) dst[3] = static_cast<int8_t>(b3);
       }
-    if (d.q_crsk)  // [c][rs][k]: k along the lanes
-      for (int pr = warp; pr < nc * RS; pr += 8) {
-        const int cc = pr / RS, rs = pr - cc * RS;
-        int8_t* dst = d.q_crsk + static_cast<size_t>(c0 + cc) * d.ld_crsk + rs * d.k_pad + k0;
-        for (int kk = lane; kk < nk; kk += 32) dst[kk] = tq[kk * TC * RS + cc * RS + rs];
-      }
+    };
+    if (d.q_krsc) {  // [k][rs][c]: c along the lanes
+      const int q4 = (nc + 3) / 4, lpr = q4 < 32 ? q4 : 32, rpw = 32 / lpr;
+      const int sub = lane / lpr, l = lane - sub * lpr;
+      if (sub < rpw)
+        for (int pr = warp * rpw + sub; pr < nk * RS; pr += 8 * rpw) {
+          const int kk = pr / RS, rs = pr - kk * RS;
+          int8_t* dst = d.q_krsc + static_cast<size_t>(k0 + kk) * d.ld_krsc + rs * d.c_pad + c0;
+          for (int c4 = l; c4 < q4; c4 += lpr)
+            put4(dst + 4 * c4, min(4, nc - 4 * c4), tq + kk * TC * RS + 4 * c4 * RS + rs, RS);
+        }
+    }
+    if (d.q_crsk) {  // [c][rs][k]: k along the lanes
+      const int q4 = (nk + 3) / 4, lpr = q4 < 32 ? q4 : 32, rpw = 32 / lpr;
+      const int sub = lane / lpr, l = lane - sub * lpr;
+      if (sub < rpw)
+        for (int pr = warp * rpw + sub; pr < nc * RS; pr += 8 * rpw) {
+          const int cc = pr / RS, rs = pr - cc * RS;
+          int8_t* dst = d.q_crsk + static_cast<size_t>(c0 + cc) * d.ld_crsk + rs * d.k_pad + k0;
+          for (int k4 = l; k4 < q4; k4 += lpr)
+            put4(dst + 4 * k4, min(4, nk - 4 * k4), tq + 4 * k4 * TC * RS + cc * RS + rs, TC * RS);
+        }
+    }
   }
   if (bad) atomicOr(err, ERR_NONFINITE);
 }
