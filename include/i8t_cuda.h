@@ -235,6 +235,12 @@ int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64
 int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t c, int64_t hw,
                           int64_t iter, int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled,
                           double alpha, double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q);
+/* i8t_quantize_gradient with the search's first-pass statistics of g already
+ * reduced (i8t_bn_bwd_apply_stats): a due search skips its pass over g. */
+int i8t_quantize_gradient_stats(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW,
+                                int64_t iter, int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled,
+                                double alpha, double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q,
+                                const double* stats);
 /* scale_factor (lr_scale.cpp:8-20), host scalar helper. */
 int i8t_scale_factor(double dc, double alpha, double beta, int form, double* out);
 
@@ -373,6 +379,13 @@ int i8t_bn_bwd_reduce(i8t_ctx* ctx, const float* g, const float* z, int64_t m, i
 int i8t_bn_bwd_reduce_join(i8t_ctx* ctx, const float* a_add, const float* g, const uint32_t* join_bits,
                            const float* z, int64_t m, int64_t c, double* bn, const float* gamma, const float* beta,
                            const uint32_t* mask_bits, float* grad_gamma, float* grad_beta, float* g_out);
+/* i8t_bn_bwd_apply that also reduces the statistics of the value it writes:
+ * stats[0] = max|gz|, stats[1] = non-finite count, stats[2] = sum gz^2 (3 device
+ * doubles, fixed-order reduction) -- the first pass of a DSGC search over gz
+ * (clip.cpp:32-34), handed to i8t_quantize_gradient_stats. */
+int i8t_bn_bwd_apply_stats(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
+                           const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz,
+                           double* stats);
 /* gz = BN backward (materialised fp32). */
 int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
                      const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz);

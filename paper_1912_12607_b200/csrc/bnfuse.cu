@@ -529,6 +529,37 @@ __global__ void __launch_bounds__(256) k_bn_bwd_apply(BnBwdSrc<MASK> src, uint32
   for (; e < n; e += T4) reinterpret_cast<float4*>(out)[e / 4] = src.load(e / 4);
 }
 
+// The same with the statistics of the first DSGC search pass (clip.cpp:32-34)
+// of the value it writes: stats[0] = max|g|, [1] = non-finite count, [2] =
+// sum g^2 (fixed-order grid reduction) -- the search then skips that pass.
+template <int MASK>
+__global__ void __launch_bounds__(256) k_bn_bwd_apply_stats(BnBwdSrc<MASK> src, uint32_t n, float* __restrict__ out,
+                                                            double* partials, double* stats, unsigned* ticket) {
+  pdl_entry();
+  const uint32_t T4 = gridDim.x * blockDim.x * 4u;
+  uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+  float m = 0.0f;
+  bool bad = false;
+  double sq = 0.0;
+  if (e < n) {
+    src.init(e % src.c);
+    for (; e < n; e += T4) {
+      const float4 v = src.load(e / 4);
+      reinterpret_cast<float4*>(out)[e / 4] = v;
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bad |= !isfinite(vv[j]);
+        m = fmaxf(m, fabsf(vv[j]));
+        const double d = vv[j];
+        sq = fma(d, d, sq);
+      }
+    }
+  }
+  double acc[3] = {m, bad ? 1.0 : 0.0, sq};
+  grid_reduce<3>(acc, 1u, partials, stats, ticket);
+}
+
 // out = a + g * (y > 0): identity-shortcut gradient joined with the main branch.
 __global__ void __launch_bounds__(256) k_add_masked(const float* __restrict__ a, const float* __restrict__ g,
                                                     const float* __restrict__ y, uint32_t n4, float* __restrict__ out) {
@@ -758,6 +789,29 @@ int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, in
   else launch_k(k_bn_bwd_apply<0>, nb, 256, 0, cx->stream, BnBwdSrc<0>{g, z, mask_y, bn, gamma, beta, uc}, un, gz);
   count_launch(1);
   return cuda_check("k_bn_bwd_apply");
+}
+
+int i8t_bn_bwd_apply_stats(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
+                           const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz,
+                           double* stats) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc) return rc;
+  if (!cx || !g || !bn || !gz || !stats || mask_mode < 0 || mask_mode > 3 || (mask_mode >= 2 && !mask_y))
+    return set_error(I8T_EINVAL, "bn_bwd_apply_stats: bad arguments");
+  const uint32_t un = static_cast<uint32_t>(m * c), uc = static_cast<uint32_t>(c);
+  const int nb = ew_blocks(m * c, c);
+  double* p = ensure_partials(cx, static_cast<size_t>(nb) * 3);
+  if (!p) return set_error(I8T_ECUDA, "partials alloc failed");
+#define BNS(M) launch_k(k_bn_bwd_apply_stats<M>, nb, 256, 0, cx->stream, BnBwdSrc<M>{g, z, mask_y, bn, gamma, beta, uc}, \
+                        un, gz, p, stats, cx->d_ticket)
+  if (mask_mode == 1) BNS(1);
+  else if (mask_mode == 2) BNS(2);
+  else if (mask_mode == 3) BNS(3);
+  else BNS(0);
+#undef BNS
+  count_launch(1);
+  return cuda_check("k_bn_bwd_apply_stats");
 }
 
 int i8t_quantize_gradient_bn(i8t_ctx* ctx, void* state, const float* g, const float* z, int64_t n_img, int64_t c,

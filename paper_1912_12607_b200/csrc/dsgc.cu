@@ -853,8 +853,12 @@ static HistBuf* ensure_hist(Ctx* c) {
 }
 
 static int run_search(Ctx* c, DsgcState* st, const float* g, int64_t n, int R, int rounds, float prev_clip,
-                      int prev_from_state) {
-  int rc = stats_pass0(c, g, n);
+                      int prev_from_state, const double* stats = nullptr) {
+  // stats: max|g|, non-finite, sum g^2 of g already reduced by its producer
+  // (i8t_bn_bwd_apply_stats): the first pass over g is skipped
+  int rc = stats ? (cudaMemcpyAsync(c->d_totals, stats, 3 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream),
+                    cuda_check("stats copy"))
+                 : stats_pass0(c, g, n);
   if (rc || (rc = allreduce_totals(c, 3))) return rc;
   launch_k(k_search_begin, 1, 32, 0, c->stream, st, c->d_totals, R, prev_clip, prev_from_state, c->d_err);
   count_launch(1);
@@ -1075,9 +1079,31 @@ int i8t_maybe_update(i8t_ctx* ctx, void* state, const float* g, int64_t n, int64
   return cuda_check("maybe_update");
 }
 
+static int quantize_gradient_impl(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW,
+                                  int64_t iter, int grid, int rounds, int search_enabled, int due,
+                                  int lr_scaling_enabled, double alpha, double beta, int form, uint32_t* lcg_state,
+                                  int8_t* q, int64_t ld_q, const double* stats);
+
 int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW, int64_t iter,
                           int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled, double alpha,
                           double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q) {
+  return quantize_gradient_impl(ctx, state, g, n_img, C, HW, iter, grid, rounds, search_enabled, due,
+                                lr_scaling_enabled, alpha, beta, form, lcg_state, q, ld_q, nullptr);
+}
+
+int i8t_quantize_gradient_stats(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW,
+                                int64_t iter, int grid, int rounds, int search_enabled, int due, int lr_scaling_enabled,
+                                double alpha, double beta, int form, uint32_t* lcg_state, int8_t* q, int64_t ld_q,
+                                const double* stats) {
+  if (!stats) return set_error(I8T_EINVAL, "quantize_gradient_stats: null stats");
+  return quantize_gradient_impl(ctx, state, g, n_img, C, HW, iter, grid, rounds, search_enabled, due,
+                                lr_scaling_enabled, alpha, beta, form, lcg_state, q, ld_q, stats);
+}
+
+static int quantize_gradient_impl(i8t_ctx* ctx, void* state, const float* g, int64_t n_img, int64_t C, int64_t HW,
+                                  int64_t iter, int grid, int rounds, int search_enabled, int due,
+                                  int lr_scaling_enabled, double alpha, double beta, int form, uint32_t* lcg_state,
+                                  int8_t* q, int64_t ld_q, const double* stats) {
   Ctx* c = CTX(ctx);
   DsgcState* st = reinterpret_cast<DsgcState*>(state);
   if (!c || !st || !g || !lcg_state || !q || n_img < 1 || C < 1 || HW < 1)
@@ -1093,7 +1119,7 @@ int i8t_quantize_gradient(i8t_ctx* ctx, void* state, const float* g, int64_t n_i
   if (search_enabled) {
     if (grid < 8) return set_error(I8T_EINVAL, "search_clip: grid resolution must be >= 8");
     if (due) {
-      if ((rc = run_search(c, st, g, numel, grid, rounds, 0.0f, 1))) return rc;
+      if ((rc = run_search(c, st, g, numel, grid, rounds, 0.0f, 1, stats))) return rc;
       launch_k(k_search_end, 1, 32, 0, c->stream, st, iter, 1, nullptr, nullptr);
       count_launch(1);
       dc_sums = false;

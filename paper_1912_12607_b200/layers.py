@@ -193,9 +193,14 @@ class BnGrad:
     def numel(self):
         return self.g.numel()
 
-    def materialize(self):
+    def materialize(self, stats=None):
         n, h, w, c = self.g.shape
         out = torch.empty_like(self.g)
+        if stats is not None:  # + max|g|, non-finite count, sum g^2 of the result (a DSGC search's first pass)
+            call("i8t_bn_bwd_apply_stats", ops.ctx(), ops._p(self.g), ops._p(self.bn._z), n * h * w, c,
+                 ops._p(self.bn.stats), ops._p(self.bn.gamma), ops._p(self.bn.beta), self.mode, ops._p(self.mask_y),
+                 ops._p(out), ops._p(stats))
+            return out
         call("i8t_bn_bwd_apply", ops.ctx(), ops._p(self.g), ops._p(self.bn._z), n * h * w, c, ops._p(self.bn.stats),
              ops._p(self.bn.gamma), ops._p(self.bn.beta), self.mode, ops._p(self.mask_y), ops._p(out))
         return out
@@ -547,8 +552,17 @@ class Conv2d(Layer):
         use_int8 = self.quantize_enabled and ctx.mode == Mode.INT8
         fuse_g = (isinstance(gz, BnGrad) and use_int8 and ctx.clip_search_enabled
                   and not self.qs.dsgc.due(ctx.iter) and gz.shape[-1] % 4 == 0)
-        if not fuse_g:
+        g_stats = None
+        if (not fuse_g and isinstance(gz, BnGrad) and use_int8 and ctx.clip_search_enabled
+                and self.qs.dsgc.due(ctx.iter) and gz.shape[-1] % 4 == 0 and BN_IMPL == "fused"):
+            # a search step: the materialising BN backward also reduces the
+            # search's first-pass statistics (max|g|, non-finite, sum g^2)
+            g_stats = torch.empty(3, dtype=torch.float64, device=gz.g.device)
+            gz = gz.materialize(stats=g_stats)
+        elif not fuse_g:
             gz = dense_grad(gz)
+            if use_int8 and ctx.clip_search_enabled and self.qs.dsgc.due(ctx.iter):
+                g_stats = getattr(gz, "_i8t_stats", None)  # eager BN: reduced by its materialising pass
         if not use_int8:
             xc = self._x.permute(0, 3, 1, 2)
             gc = gz.permute(0, 3, 1, 2)
@@ -565,7 +579,7 @@ class Conv2d(Layer):
             qg = quantize_gradient_bn_layer(self.qs, gz, ctx)
         else:
             gz = gz.contiguous()
-            qg = quantize_gradient_layer(self.qs, gz, ctx)
+            qg = quantize_gradient_layer(self.qs, gz, ctx, stats=g_stats)
         clip_g = self.qs.dsgc.clip_q_ptr()
         gdev = qg.device
         ga = torch.empty((g.n, g.h, g.w, g.c), dtype=torch.float32, device=gdev) if self.need_input_grad else None
@@ -626,8 +640,10 @@ class Conv2d(Layer):
         return ga
 
 
-def quantize_gradient_layer(qs: QuantState, gz: torch.Tensor, ctx: BackwardCtx) -> torch.Tensor:
-    """quantize_gradient (layers.cpp:19-59) for an NHWC gradient [N,P,Q,K]."""
+def quantize_gradient_layer(qs: QuantState, gz: torch.Tensor, ctx: BackwardCtx, stats=None) -> torch.Tensor:
+    """quantize_gradient (layers.cpp:19-59) for an NHWC gradient [N,P,Q,K].
+    stats: the search's first-pass statistics of gz when its producer reduced
+    them (i8t_bn_bwd_apply_stats)."""
     n, p, q, k = gz.shape
     st = qs.dsgc
     st.period = ctx.clip_period
@@ -639,9 +655,13 @@ def quantize_gradient_layer(qs: QuantState, gz: torch.Tensor, ctx: BackwardCtx) 
         n_img, ch, hw = 1, 1, n * k
     else:
         raise ValueError("quantize_gradient: conv output channels must be a multiple of 4")
-    call("i8t_quantize_gradient", ops.ctx(), st.ptr, ops._p(gz), n_img, ch, hw, ctx.iter, ctx.grid_resolution,
-         ctx.refine_rounds, int(ctx.clip_search_enabled), int(due), int(ctx.lr_scaling_enabled),
-         C.c_double(ctx.alpha), C.c_double(ctx.beta), ops.FORMS[ctx.form], ops._p(ctx.grad_stream), ops._p(qg), ch)
+    args = (ops.ctx(), st.ptr, ops._p(gz), n_img, ch, hw, ctx.iter, ctx.grid_resolution, ctx.refine_rounds,
+            int(ctx.clip_search_enabled), int(due), int(ctx.lr_scaling_enabled), C.c_double(ctx.alpha),
+            C.c_double(ctx.beta), ops.FORMS[ctx.form], ops._p(ctx.grad_stream), ops._p(qg), ch)
+    if stats is not None and due:
+        call("i8t_quantize_gradient_stats", *args, ops._p(stats))
+    else:
+        call("i8t_quantize_gradient", *args)
     if due or not ctx.clip_search_enabled:
         st.mark_searched(ctx.iter)
         st.clip_valid = True  # refreshed from the device view at step end (zero-gradient edge case)
@@ -790,14 +810,24 @@ class BatchNorm2d(Layer):
                      ops._p(self.grad_gamma), ops._p(self.grad_beta), ops._p(out))
                 g.out, g.gm, g.g, g.bits = out, None, None, None
                 gb = BnGrad(out, self, mode, mask_y)
-                return gb.materialize() if BN_IMPL == "eager" else gb
+                if BN_IMPL == "eager":
+                    stats = torch.empty(3, dtype=torch.float64, device=out.device)
+                    res = gb.materialize(stats=stats)
+                    res._i8t_stats = stats
+                    return res
+                return gb
             g = dense_grad(g).contiguous()
             n, h, w, c = g.shape
             call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(self._z), n * h * w, c, ops._p(self.stats),
                  ops._p(self.gamma), ops._p(self.beta), mode, ops._p(mask_y), ops._p(self.grad_gamma),
                  ops._p(self.grad_beta))
             gb = BnGrad(g, self, mode, mask_y)
-            return gb.materialize() if BN_IMPL == "eager" else gb
+            if BN_IMPL == "eager":  # the same kernel the fused path's search steps use, stats attached
+                stats = torch.empty(3, dtype=torch.float64, device=g.device)
+                out = gb.materialize(stats=stats)
+                out._i8t_stats = stats
+                return out
+            return gb
         gc = dense_grad(g).contiguous().permute(0, 3, 1, 2)
         gi, gg, gb = torch.ops.aten.native_batch_norm_backward(gc, self._x, self.gamma, self.running_mean,
                                                                self.running_var, self._mean, self._invstd, True,

@@ -478,3 +478,40 @@ def test_global_avgpool_matches_reference_order(ops):
     ops.call("i8t_global_avgpool_bwd", ops.ctx(), ops._p(t(g)), n, h * w, c, ops._p(gx))
     ref = np.broadcast_to((g / np.float32(h * w))[:, None, None, :], (n, h, w, c))
     np.testing.assert_array_equal(gx.cpu().numpy(), ref)
+
+
+def test_bn_bwd_apply_stats_feeds_the_search(ops):
+    """i8t_bn_bwd_apply_stats writes the same gz as i8t_bn_bwd_apply plus the
+    DSGC search's first-pass statistics (max|g|, non-finite, sum g^2), and a
+    due i8t_quantize_gradient_stats search on them picks the clip the plain
+    search picks."""
+    n, hw, c = 8, 14 * 14, 64
+    m = n * hw
+    z, gamma, beta, g = _data(m, c, 71)
+    zt, gt, bt, g_t = t(z), t(gamma), t(beta), t(g)
+    bn = _stats(ops, zt, c)
+    gg, gb = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+    ops.call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bn), ops._p(gt), ops._p(bt), 1,
+             None, ops._p(gg), ops._p(gb))
+    ref = torch.empty_like(zt)
+    ops.call("i8t_bn_bwd_apply", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bn), ops._p(gt), ops._p(bt), 1,
+             None, ops._p(ref))
+    out = torch.empty_like(zt)
+    st3 = torch.zeros(3, dtype=torch.float64, device="cuda")
+    ops.call("i8t_bn_bwd_apply_stats", ops.ctx(), ops._p(g_t), ops._p(zt), m, c, ops._p(bn), ops._p(gt), ops._p(bt),
+             1, None, ops._p(out), ops._p(st3))
+    assert torch.equal(out, ref)
+    s = st3.cpu().numpy()
+    o = out.cpu().numpy().astype(np.float64)
+    assert s[0] == np.abs(o).max() and s[1] == 0.0
+    assert s[2] == pytest.approx((o * o).sum(), rel=1e-12)
+    g4 = out.view(n, 14, 14, c)
+    sa, sb = ops.DsgcState(period=4), ops.DsgcState(period=4)
+    la, lb = ops.new_lcg_state(5), ops.new_lcg_state(5)
+    qa = ops.quantize_gradient(sa, g4, 0, la, nhwc=True)
+    qb = torch.empty_like(qa)
+    ops.call("i8t_quantize_gradient_stats", ops.ctx(), sb.ptr, ops._p(g4), n, c, hw, 0, 32, 2, 1, 1, 1,
+             C.c_double(20.0), C.c_double(0.1), ops.FORMS["exp"], ops._p(lb), ops._p(qb), c, ops._p(st3))
+    va, vb = sa.view(), sb.view()
+    assert va.clip == vb.clip and torch.equal(qa, qb)
+    assert vb.last_dc == pytest.approx(va.last_dc, abs=1e-12)
