@@ -131,6 +131,37 @@ __global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rows(const float*
   if (amax) block_amax(m, amax);
 }
 
+// K1 rows for 3-channel pixels padded to 4 (the stem's RGB input): four pixels
+// per thread, three float4 loads in, one 16-byte store out.
+__global__ void __launch_bounds__(RED_THREADS) k_quant_nearest_rgb(const float4* __restrict__ x, uint32_t rows4,
+                                                                   const float* __restrict__ clip_p,
+                                                                   uint4* __restrict__ q, float* amax, int* err) {
+  pdl_entry();
+  const float clip = *clip_p, s = scale_of(clip), inv_s = 1.0f / s, hs = __fdiv_rn(0.5f, clip);
+  float m = 0.0f;
+  bool bad = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows4; i += gridDim.x * blockDim.x) {
+    const float4 a = __ldg(x + 3 * i), b = __ldg(x + 3 * i + 1), c = __ldg(x + 3 * i + 2);
+    const float v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const float f = v[3 * p + ch];
+        bad |= !isfinite(f);
+        m = fmaxf(m, fabsf(f));
+        word |= static_cast<uint32_t>(static_cast<uint8_t>(quant_nearest_fast(f, clip, hs, s, inv_s))) << (8 * ch);
+      }
+      w[p] = word;  // channel 3 = 0 (padding)
+    }
+    q[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+  if (amax) block_amax(m, amax);
+}
+
 // K2 over every quantised layer of a model in one launch (blockIdx.y = layer):
 // the per-layer launches cost more than their ~150 MB of traffic.  Padding
 // bytes of the outputs are never written (zeroed once at allocation).
@@ -501,6 +532,10 @@ int i8t_quantize_nearest_rows(i8t_ctx* ctx, const float* x, int64_t rows, int64_
     const int64_t n = rows * cols;
     launch_k(k_quant_nearest_flat, grid_for(n / 4 + 1), RED_THREADS, 0, c->stream, x, static_cast<uint32_t>(n), clip, q, amax,
                                                                               c->d_err);
+  } else if (cols == 3 && ld_q == 4 && rows % 4 == 0 &&
+             ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0) {
+    launch_k(k_quant_nearest_rgb, grid_for(rows / 4), RED_THREADS, 0, c->stream, reinterpret_cast<const float4*>(x),
+             static_cast<uint32_t>(rows / 4), clip, reinterpret_cast<uint4*>(q), amax, c->d_err);
   } else {
     launch_k(k_quant_nearest_rows, grid_for(rows * ld_q), RED_THREADS, 0, c->stream, 
         x, static_cast<uint32_t>(rows), static_cast<uint32_t>(cols), clip, q, static_cast<uint32_t>(ld_q), amax, c->d_err);

@@ -415,3 +415,20 @@ def test_quantize_nearest_shared(same, ops):
     else:
         assert np.array_equal(q.cpu().numpy(), O.quantize(x, 1.75)[0])
         assert float(amax) == max(0.5, float(np.abs(x).max()))
+
+
+@pytest.mark.parametrize("rows", [4096, 4097])
+def test_quantize_nearest_rows_rgb_padding(rows, ops):
+    """i8t_quantize_nearest_rows for 3-channel pixels padded to 4 (the stem
+    input; rows % 4 == 0 takes the four-pixels-per-thread kernel): payload
+    equal to the reference quantiser, pad byte 0, running max|x|."""
+    rng = np.random.default_rng(81)
+    x = (rng.standard_normal((rows, 3)) * 2).astype(np.float32)
+    q = torch.full((rows, 4), 77, dtype=torch.int8, device="cuda")
+    amax = torch.zeros(1, device="cuda")
+    clip = torch.tensor([3.5], device="cuda")
+    ops.call("i8t_quantize_nearest_rows", ops.ctx(), ops._p(t(x)), rows, 3, ops._p(clip), ops._p(q), 4, ops._p(amax), 0)
+    ref, _ = O.quantize(x, 3.5)
+    qn = q.cpu().numpy()
+    assert np.array_equal(qn[:, :3], ref.reshape(rows, 3)) and (qn[:, 3] == 0).all()
+    assert float(amax) == float(np.abs(x).max())
