@@ -386,6 +386,15 @@ int i8t_bn_bwd_reduce_join(i8t_ctx* ctx, const float* a_add, const float* g, con
 int i8t_bn_bwd_apply_stats(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
                            const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz,
                            double* stats);
+/* i8t_bn_bwd_reduce_join plus a second BatchNorm reduced on the same masked
+ * g_out in the same pass (z2 / bn2 / gamma2 -> grad_gamma2, grad_beta2 =
+ * grad_beta): the projection block's shortcut BN beside the main branch's last
+ * BN (ResidualBlock::backward, layers.cpp:458-464).  Bit for bit the two
+ * separate reductions. */
+int i8t_bn_bwd_reduce_join2(i8t_ctx* ctx, const float* a_add, const float* g, const uint32_t* join_bits,
+                            const float* z, int64_t m, int64_t c, double* bn, const float* gamma, const float* beta,
+                            const uint32_t* mask_bits, float* grad_gamma, float* grad_beta, const float* z2,
+                            double* bn2, const float* gamma2, float* grad_gamma2, float* grad_beta2, float* g_out);
 /* gz = BN backward (materialised fp32). */
 int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,
                      const float* gamma, const float* beta, int mask_mode, const float* mask_y, float* gz);

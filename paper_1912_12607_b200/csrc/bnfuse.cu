@@ -57,6 +57,14 @@ struct ColArgs {
   const float* ja;
   const uint32_t* jbits;
   float* gout;
+  // MODE 3 (MODE 2 + a second BN on the same masked g: the projection block's
+  // shortcut BN beside the main branch's last BN): z2 / bn2 / gamma2, sums
+  // sum g_m * x_hat2 into grad_gamma2; grad_beta2 = grad_beta
+  const float* z2;
+  double* bn2;
+  const float* gamma2;
+  float* grad_gamma2;
+  float* grad_beta2;
 };
 
 // Column sums over the m rows for one 128-channel group per blockIdx.y.
@@ -76,8 +84,9 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   const bool active = lane < rpw * lpr;
   const uint32_t quad = lane % lpr, sub = lane / lpr;
   const uint32_t ch = c0 + quad * 4;
-  double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
-  double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0};
+  constexpr int NS = MODE == 3 ? 3 : 2;  // column sums per channel
+  double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
+  double mean[4] = {0, 0, 0, 0}, invstd[4] = {0, 0, 0, 0}, mean2[4] = {0, 0, 0, 0}, invstd2[4] = {0, 0, 0, 0};
   float lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
   if (MODE >= 1 && MASK == 1) {
     // ReLU-mask bounds of this block's channel group, bisected in the prologue
@@ -104,11 +113,16 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     for (int j = 0; j < 4; ++j) {
       mean[j] = a.bn[ch + j];
       invstd[j] = a.bn[a.c + ch + j];
+      if (MODE == 3) {
+        mean2[j] = a.bn2[ch + j];
+        invstd2[j] = a.bn2[a.c + ch + j];
+      }
     }
   }
   if (active) {
     // U rows per thread per trip: all loads of a trip are issued before any math
     constexpr int U = MODE == 0 ? 10 : MODE == 1 ? 4 : 2;
+    constexpr int U2 = MODE == 3 ? U : 1;  // second z (MODE 3)
     const uint32_t row_step = gridDim.x * 8 * rpw;
     uint32_t r = (blockIdx.x * 8 + warp) * rpw + sub;
     // software pipeline: the U rows of the next trip are loaded before the
@@ -116,7 +130,8 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
     float4 zv[U], gv[U], yv[U], zn[U], gn[U], yn[U];
     uint32_t bv[U], bn_[U];  // MASK 3: raw mask words (the nibble is extracted at use: keeps the loads in flight)
     uint32_t jv[U], jn[U];   // MODE 2: join mask words (yv / yn carry the join addend)
-    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd, uint32_t* bd, uint32_t* jd) {
+    float4 z2v[U2], z2n[U2];
+    auto fetch = [&](uint32_t rr, float4* zd, float4* gd, float4* yd, uint32_t* bd, uint32_t* jd, float4* z2d) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t ru = rr + u * row_step;
@@ -124,15 +139,16 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
         zd[u] = ldg_stream(a.z + off);
         if (MODE >= 1) gd[u] = ldg_stream(a.g + off);
         if (MODE == 1 && MASK == 2) yd[u] = ldg_stream(a.mask_y + off);
-        if (MODE == 2) yd[u] = ldg_stream(a.ja + off);
-        if (MODE == 2) jd[u] = __ldg(a.jbits + (off >> 5));
+        if (MODE >= 2) yd[u] = ldg_stream(a.ja + off);
+        if (MODE >= 2) jd[u] = __ldg(a.jbits + (off >> 5));
+        if (MODE == 3) z2d[u] = ldg_stream(a.z2 + off);
         if (MODE >= 1 && MASK == 3) bd[u] = __ldg(reinterpret_cast<const uint32_t*>(a.mask_y) + (off >> 5));
       }
     };
-    if (r < a.m) fetch(r, zv, gv, yv, bv, jv);
+    if (r < a.m) fetch(r, zv, gv, yv, bv, jv, z2v);
     for (; r < a.m; r += U * row_step) {
       const uint32_t rn = r + U * row_step;
-      if (rn < a.m) fetch(rn, zn, gn, yn, bn_, jn);
+      if (rn < a.m) fetch(rn, zn, gn, yn, bn_, jn, z2n);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool valid = r + u * row_step < a.m;  // rows past the end re-read row r: not accumulated
@@ -147,7 +163,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
         } else {
           float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
           const float yy[4] = {yv[u].x, yv[u].y, yv[u].z, yv[u].w};
-          if (MODE == 2) {  // the join, exactly as k_add_masked_bits
+          if (MODE >= 2) {  // the join, exactly as k_add_masked_bits
             const uint32_t row = r + u * row_step;
             const uint32_t jb = jv[u] >> ((row * a.c + ch) & 31u);
 #pragma unroll
@@ -155,7 +171,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
             if (valid)
               *reinterpret_cast<float4*>(a.gout + static_cast<size_t>(row) * a.c + ch) = make_float4(gg[0], gg[1], gg[2], gg[3]);
           }
-          double xh[4], gm[4];
+          double xh[4], gm[4], xh2[4];
           // MASK 3: this row's nibble (ch % 4 == 0, so the 4 bits share a word)
           const uint32_t w = (MASK == 3 && valid) ? bv[u] >> (((r + u * row_step) * a.c + ch) & 31u) : 0u;
 #pragma unroll
@@ -170,11 +186,16 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
                 : "=f"(gmf) : "r"(mk ? 1u : 0u), "f"(gg[j]));
             gm[j] = static_cast<double>(gmf);
             xh[j] = rn24(xv);  // x_hat as in BnBwdSrc::elem
+            if (MODE == 3) {
+              const float z2 = j == 0 ? z2v[u].x : j == 1 ? z2v[u].y : j == 2 ? z2v[u].z : z2v[u].w;
+              xh2[j] = rn24((static_cast<double>(z2) - mean2[j]) * invstd2[j]);
+            }
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             acc0[j] += gm[j];
             acc1[j] = fma(gm[j], xh[j], acc1[j]);
+            if (MODE == 3) acc2[j] = fma(gm[j], xh2[j], acc2[j]);
           }
         }
       }
@@ -182,31 +203,35 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
       for (int u = 0; u < U; ++u) {
         zv[u] = zn[u];
         if (MODE >= 1) gv[u] = gn[u];
-        if ((MODE == 1 && MASK == 2) || MODE == 2) yv[u] = yn[u];
-        if (MODE == 2) jv[u] = jn[u];
+        if ((MODE == 1 && MASK == 2) || MODE >= 2) yv[u] = yn[u];
+        if (MODE >= 2) jv[u] = jn[u];
+        if (MODE == 3) z2v[u] = z2n[u];
         if (MODE >= 1 && MASK == 3) bv[u] = bn_[u];
       }
     }
   }
   // block reduction in a fixed order: warps, then sub-rows
-  __shared__ double red[8][32][8];
+  __shared__ double red[8][32][4 * NS];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     red[warp][lane][j] = acc0[j];
     red[warp][lane][4 + j] = acc1[j];
+    if (NS == 3) red[warp][lane][8 + j] = acc2[j];
   }
   __syncthreads();
   if (threadIdx.x < gw) {
     const uint32_t q = threadIdx.x / 4, j = threadIdx.x % 4;
-    double s0 = 0.0, s1 = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int w = 0; w < 8; ++w)
       for (uint32_t sr = 0; sr < rpw; ++sr) {
         s0 += red[w][sr * lpr + q][j];
         s1 += red[w][sr * lpr + q][4 + j];
+        if (NS == 3) s2 += red[w][sr * lpr + q][8 + j];
       }
-    double* p = partials + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (2 * BN_GROUP);
+    double* p = partials + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (NS * BN_GROUP);
     p[threadIdx.x] = s0;
     p[BN_GROUP + threadIdx.x] = s1;
+    if (NS == 3) p[2 * BN_GROUP + threadIdx.x] = s2;
   }
   // two-level fixed-order reduction of the per-block partials: the last block
   // of each set of COL_SET blocks folds its set (in block order), the last set
@@ -215,7 +240,7 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   constexpr uint32_t COL_SET = 16;
   const uint32_t gx = gridDim.x, set = blockIdx.x / COL_SET, nsets = (gx + COL_SET - 1) / COL_SET;
   const uint32_t set_lo = set * COL_SET, set_n = min(COL_SET, gx - set_lo);
-  double* const level2 = partials + static_cast<size_t>(gridDim.y) * gx * (2 * BN_GROUP);
+  double* const level2 = partials + static_cast<size_t>(gridDim.y) * gx * (NS * BN_GROUP);
   __threadfence();
   __syncthreads();
   __shared__ bool last;
@@ -223,17 +248,17 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < 2 * gw) {  // thread t: column t % gw, sum t / gw
-    const uint32_t col = threadIdx.x % gw, which = threadIdx.x / gw;
-    const double* base = partials + (static_cast<size_t>(blockIdx.y) * gx + set_lo) * (2 * BN_GROUP) +
+  for (uint32_t t = threadIdx.x; t < NS * gw; t += blockDim.x) {  // thread t: column t % gw, sum t / gw
+    const uint32_t col = t % gw, which = t / gw;
+    const double* base = partials + (static_cast<size_t>(blockIdx.y) * gx + set_lo) * (NS * BN_GROUP) +
                          which * BN_GROUP + col;
     double v[COL_SET];
 #pragma unroll
-    for (uint32_t k = 0; k < COL_SET; ++k) v[k] = k < set_n ? __ldcg(base + static_cast<size_t>(k) * (2 * BN_GROUP)) : 0.0;
+    for (uint32_t k = 0; k < COL_SET; ++k) v[k] = k < set_n ? __ldcg(base + static_cast<size_t>(k) * (NS * BN_GROUP)) : 0.0;
     double sum = 0.0;
 #pragma unroll
     for (uint32_t k = 0; k < COL_SET; ++k) sum += v[k];
-    level2[(static_cast<size_t>(blockIdx.y) * nsets + set) * (2 * BN_GROUP) + which * BN_GROUP + col] = sum;
+    level2[(static_cast<size_t>(blockIdx.y) * nsets + set) * (NS * BN_GROUP) + which * BN_GROUP + col] = sum;
   }
   if (threadIdx.x == 0) set_tickets[blockIdx.y * 32 + set] = 0u;
   __threadfence();
@@ -242,27 +267,23 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double s0 = 0.0, s1 = 0.0;
-  if (threadIdx.x < 2 * gw) {
-    const uint32_t col = threadIdx.x % gw, which = threadIdx.x / gw;
-    const double* base = level2 + static_cast<size_t>(blockIdx.y) * nsets * (2 * BN_GROUP) + which * BN_GROUP + col;
+  __shared__ double fold[NS][BN_GROUP];
+  for (uint32_t tt = threadIdx.x; tt < NS * gw; tt += blockDim.x) {
+    const uint32_t col = tt % gw, which = tt / gw;
+    const double* base = level2 + static_cast<size_t>(blockIdx.y) * nsets * (NS * BN_GROUP) + which * BN_GROUP + col;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains, combined in a fixed order
     uint32_t k = 0;
     for (; k + 3 < nsets; k += 4) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] += __ldcg(base + static_cast<size_t>(k + j) * (2 * BN_GROUP));
+      for (int j = 0; j < 4; ++j) acc[j] += __ldcg(base + static_cast<size_t>(k + j) * (NS * BN_GROUP));
     }
-    for (int j = 0; k < nsets; ++k, ++j) acc[j] += __ldcg(base + static_cast<size_t>(k) * (2 * BN_GROUP));
-    const double t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    if (which == 0) s0 = t; else s1 = t;
+    for (int j = 0; k < nsets; ++k, ++j) acc[j] += __ldcg(base + static_cast<size_t>(k) * (NS * BN_GROUP));
+    fold[which][col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
-  __shared__ double fold[2][BN_GROUP];
-  if (threadIdx.x < gw) fold[0][threadIdx.x] = s0;
-  else if (threadIdx.x < 2 * gw) fold[1][threadIdx.x - gw] = s1;
   __syncthreads();
   if (threadIdx.x < gw) {
-    s0 = fold[0][threadIdx.x];
-    s1 = fold[1][threadIdx.x];
+    double s0 = fold[0][threadIdx.x];
+    double s1 = fold[1][threadIdx.x];
     const uint32_t cc = c0 + threadIdx.x;
     const double m = static_cast<double>(a.m);
     if (MODE == 0) {  // layers.cpp:260-268
@@ -282,6 +303,15 @@ __global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* part
       a.bn[2 * a.c + cc] = k * (s0 / m);
       a.bn[3 * a.c + cc] = k * (s1 / m);
       a.bn[4 * a.c + cc] = k;
+      if (MODE == 3) {  // the second BN on the same masked g
+        const double s2 = fold[NS - 1][threadIdx.x];
+        a.grad_beta2[cc] = static_cast<float>(s0);
+        a.grad_gamma2[cc] = static_cast<float>(s2);
+        const double k2 = static_cast<double>(a.gamma2[cc]) * a.bn2[a.c + cc];
+        a.bn2[2 * a.c + cc] = k2 * (s0 / m);
+        a.bn2[3 * a.c + cc] = k2 * (s2 / m);
+        a.bn2[4 * a.c + cc] = k2;
+      }
     }
   }
   __syncthreads();
@@ -656,13 +686,14 @@ static int colsum(Ctx* c, const ColArgs& a, int mode) {
   if (bx < 1) bx = 1;
   if (bx > 32 * 16) bx = 32 * 16;  // <= 32 sets of 16 blocks per group
   const int nsets = (bx + 15) / 16;
-  double* p = ensure_partials(c, static_cast<size_t>(bx + nsets) * groups * 2 * BN_GROUP);
+  double* p = ensure_partials(c, static_cast<size_t>(bx + nsets) * groups * 3 * BN_GROUP);
   unsigned* t = group_tickets(c);
   unsigned* st = set_tickets(c);
   if (!p || !t || !st) return set_error(I8T_ECUDA, "bn: scratch alloc failed");
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(groups));
   if (mode == 0) launch_k(k_bn_colsum<0>, grid, 256, 0, c->stream, a, p, t, st);
   else if (mode == 2) launch_k(k_bn_colsum<2, 3>, grid, 256, 0, c->stream, a, p, t, st);
+  else if (mode == 3) launch_k(k_bn_colsum<3, 3>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 1) launch_k(k_bn_colsum<1, 1>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 2) launch_k(k_bn_colsum<1, 2>, grid, 256, 0, c->stream, a, p, t, st);
   else if (a.mask_mode == 3) launch_k(k_bn_colsum<1, 3>, grid, 256, 0, c->stream, a, p, t, st);
@@ -772,6 +803,27 @@ int i8t_bn_bwd_reduce_join(i8t_ctx* ctx, const float* a_add, const float* g, con
   a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
   a.ja = a_add; a.jbits = join_bits; a.gout = g_out;
   return colsum(cx, a, 2);
+}
+
+int i8t_bn_bwd_reduce_join2(i8t_ctx* ctx, const float* a_add, const float* g, const uint32_t* join_bits,
+                            const float* z, int64_t m, int64_t c, double* bn, const float* gamma, const float* beta,
+                            const uint32_t* mask_bits, float* grad_gamma, float* grad_beta, const float* z2,
+                            double* bn2, const float* gamma2, float* grad_gamma2, float* grad_beta2, float* g_out) {
+  Ctx* cx = CTX(ctx);
+  int rc = bn_check(m, c, z);
+  if (rc || (rc = bn_check(m, c, z2))) return rc;
+  if (!cx || !a_add || !g || !join_bits || !bn || !gamma || !beta || !mask_bits || !grad_gamma || !grad_beta ||
+      !g_out || !bn2 || !gamma2 || !grad_gamma2 || !grad_beta2)
+    return set_error(I8T_EINVAL, "bn_bwd_reduce_join2: bad arguments");
+  if ((reinterpret_cast<uintptr_t>(a_add) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(g_out)) & 15u)
+    return set_error(I8T_EUNSUPPORTED, "bn_bwd_reduce_join2: 16-byte alignment");
+  ColArgs a{};
+  a.z = z; a.g = g; a.mask_y = reinterpret_cast<const float*>(mask_bits); a.gamma = gamma; a.beta = beta; a.bn = bn;
+  a.m = static_cast<uint32_t>(m); a.c = static_cast<uint32_t>(c); a.mask_mode = 3;
+  a.grad_gamma = grad_gamma; a.grad_beta = grad_beta;
+  a.ja = a_add; a.jbits = join_bits; a.gout = g_out;
+  a.z2 = z2; a.bn2 = bn2; a.gamma2 = gamma2; a.grad_gamma2 = grad_gamma2; a.grad_beta2 = grad_beta2;
+  return colsum(cx, a, 3);
 }
 
 int i8t_bn_bwd_apply(i8t_ctx* ctx, const float* g, const float* z, int64_t m, int64_t c, const double* bn,

@@ -93,6 +93,9 @@ JOIN_PROJ = os.environ.get("I8T_JOIN_PROJ", "1") == "1" or JOIN_FUSION
 # (JoinGrad; g_out is written once and never re-read by the reduction).
 # I8T_JOIN_REDUCE=0 keeps the separate i8t_add_masked_bits.
 JOIN_REDUCE = os.environ.get("I8T_JOIN_REDUCE", "1") == "1"
+# The projection block's shortcut BN reduces its backward sums in the main
+# branch's last-BN pass over the same joined gradient (i8t_bn_bwd_reduce_join2).
+JOIN_REDUCE2 = os.environ.get("I8T_JOIN_REDUCE2", "1") == "1"
 # The projection shortcut conv reuses the block's first conv's int8 input when
 # their activation clips agree (i8t_quantize_nearest_shared).  I8T_SHARE_ACT=0
 # quantises twice.
@@ -215,6 +218,7 @@ class JoinGrad:
     def __init__(self, gm, g, bits):
         self.gm, self.g, self.bits = gm, g, bits
         self.out = None
+        self.co_bn = None  # a second BN reduced on the same masked gradient in the same pass (projection shortcut)
 
     @property
     def shape(self):
@@ -802,6 +806,26 @@ class BatchNorm2d(Layer):
                     g = g.materialize()
                 else:
                     mode, mask_y, g = g.mode, g.mask_y, g.g
+            if (isinstance(g, JoinGrad) and g.out is None and mode == 3 and JOIN_REDUCE and g.co_bn is not None
+                    and g.co_bn is not self and not g.co_bn._torch and g.co_bn._z is not None
+                    and g.co_bn._z.shape == self._z.shape):
+                # the projection shortcut's BN on the same masked gradient, in the same pass
+                n, h, w, c = g.shape
+                co = g.co_bn
+                out = torch.empty_like(g.gm)
+                call("i8t_bn_bwd_reduce_join2", ops.ctx(), ops._p(g.gm), ops._p(g.g), ops._p(g.bits), ops._p(self._z),
+                     n * h * w, c, ops._p(self.stats), ops._p(self.gamma), ops._p(self.beta), ops._p(mask_y),
+                     ops._p(self.grad_gamma), ops._p(self.grad_beta), ops._p(co._z), ops._p(co.stats),
+                     ops._p(co.gamma), ops._p(co.grad_gamma), ops._p(co.grad_beta), ops._p(out))
+                co._reduced_for = out  # its own backward finds its sums done for this gradient
+                g.out, g.gm, g.g, g.bits = out, None, None, None
+                gb = BnGrad(out, self, mode, mask_y)
+                if BN_IMPL == "eager":
+                    stats = torch.empty(3, dtype=torch.float64, device=out.device)
+                    res = gb.materialize(stats=stats)
+                    res._i8t_stats = stats
+                    return res
+                return gb
             if isinstance(g, JoinGrad) and g.out is None and mode == 3 and JOIN_REDUCE:
                 n, h, w, c = g.shape
                 out = torch.empty_like(g.gm)
@@ -818,9 +842,13 @@ class BatchNorm2d(Layer):
                 return gb
             g = dense_grad(g).contiguous()
             n, h, w, c = g.shape
-            call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(self._z), n * h * w, c, ops._p(self.stats),
-                 ops._p(self.gamma), ops._p(self.beta), mode, ops._p(mask_y), ops._p(self.grad_gamma),
-                 ops._p(self.grad_beta))
+            if getattr(self, "_reduced_for", None) is g and mode == 3:
+                self._reduced_for = None  # sums done in the main branch BN's pass (i8t_bn_bwd_reduce_join2)
+            else:
+                self._reduced_for = None
+                call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(g), ops._p(self._z), n * h * w, c, ops._p(self.stats),
+                     ops._p(self.gamma), ops._p(self.beta), mode, ops._p(mask_y), ops._p(self.grad_gamma),
+                     ops._p(self.grad_beta))
             gb = BnGrad(g, self, mode, mask_y)
             if BN_IMPL == "eager":  # the same kernel the fused path's search steps use, stats attached
                 stats = torch.empty(3, dtype=torch.float64, device=g.device)
@@ -1049,6 +1077,10 @@ class ResidualBlock(Layer):
     def backward(self, g, ctx):
         jg = g if isinstance(g, JoinGrad) and self._fused and self._bits is not None else None
         g = jg if jg is not None else dense_grad(g)
+        if jg is not None and self.shortcut and self.shortcut.children and JOIN_REDUCE2:
+            last = self.shortcut.children[-1][1]
+            if isinstance(last, BatchNorm2d):
+                jg.co_bn = last  # the shortcut BN's sums ride along with the main branch's last BN
         if self._fused:
             gl = MaskedGrad(g, 3, mask_y=self._bits) if self._bits is not None else MaskedGrad(g, 2, mask_y=self._y)
             first = self.main.children[0][1] if self.main.children else None

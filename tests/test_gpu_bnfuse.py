@@ -515,3 +515,34 @@ def test_bn_bwd_apply_stats_feeds_the_search(ops):
     va, vb = sa.view(), sb.view()
     assert va.clip == vb.clip and torch.equal(qa, qb)
     assert vb.last_dc == pytest.approx(va.last_dc, abs=1e-12)
+
+
+@pytest.mark.parametrize("m,c", [(3136, 64), (49 * 8, 2048)])
+def test_bn_bwd_reduce_join2_equals_two_reductions(ops, m, c):
+    """i8t_bn_bwd_reduce_join2 (the projection block's two BNs reduced on the
+    same joined, masked gradient in one pass) == i8t_bn_bwd_reduce_join for the
+    first BN and i8t_bn_bwd_reduce for the second, bit for bit."""
+    z, gamma, beta, g = _data(m, c, 91)
+    z2, gamma2, beta2, _ = _data(m, c, 92)
+    rng = np.random.default_rng(93)
+    zt, gt, bt, g_t, z2t, g2t, b2t = t(z), t(gamma), t(beta), t(g), t(z2), t(gamma2), t(beta2)
+    a = t(rng.standard_normal((m, c)).astype(np.float32))
+    jbits = t(_pack_bits(rng.random(m * c) < 0.6))
+    mbits = t(_pack_bits(rng.random(m * c) < 0.5))
+    bn, bn2 = _stats(ops, zt, c), _stats(ops, z2t, c)
+    out_r = torch.empty_like(zt)
+    bn_r, bn2_r = bn.clone(), bn2.clone()
+    gg_r, gb_r, gg2_r, gb2_r = (torch.zeros(c, device="cuda") for _ in range(4))
+    ops.call("i8t_bn_bwd_reduce_join", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(jbits), ops._p(zt), m, c,
+             ops._p(bn_r), ops._p(gt), ops._p(bt), ops._p(mbits), ops._p(gg_r), ops._p(gb_r), ops._p(out_r))
+    ops.call("i8t_bn_bwd_reduce", ops.ctx(), ops._p(out_r), ops._p(z2t), m, c, ops._p(bn2_r), ops._p(g2t), ops._p(b2t),
+             3, ops._p(mbits), ops._p(gg2_r), ops._p(gb2_r))
+    out = torch.empty_like(zt)
+    bn_f, bn2_f = bn.clone(), bn2.clone()
+    gg_f, gb_f, gg2_f, gb2_f = (torch.zeros(c, device="cuda") for _ in range(4))
+    ops.call("i8t_bn_bwd_reduce_join2", ops.ctx(), ops._p(a), ops._p(g_t), ops._p(jbits), ops._p(zt), m, c,
+             ops._p(bn_f), ops._p(gt), ops._p(bt), ops._p(mbits), ops._p(gg_f), ops._p(gb_f), ops._p(z2t),
+             ops._p(bn2_f), ops._p(g2t), ops._p(gg2_f), ops._p(gb2_f), ops._p(out))
+    assert torch.equal(out.view(torch.int32), out_r.view(torch.int32))
+    for x, y in ((gg_f, gg_r), (gb_f, gb_r), (bn_f, bn_r), (gg2_f, gg2_r), (gb2_f, gb2_r), (bn2_f, bn2_r)):
+        assert torch.equal(x, y)
