@@ -73,7 +73,7 @@ struct ColArgs {
 // residual join of the next block's backward and this BN's reduction in one
 // pass: g is read once instead of written, then read).
 template <int MODE, int MASK = 0>
-__global__ void __launch_bounds__(256) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets,
+__global__ void __launch_bounds__(256, 2) k_bn_colsum(const ColArgs a, double* partials, unsigned* tickets,
                                                    unsigned* set_tickets) {
   pdl_entry();
   const uint32_t c0 = blockIdx.y * BN_GROUP;
