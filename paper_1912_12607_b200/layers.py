@@ -60,6 +60,9 @@ class BackwardCtx:
     # (work, finalize) pairs: the int64 weight-gradient allreduces run while the
     # backward continues; the trainer waits on each and rescales before the update
     deferred: list = field(default_factory=list)
+    # single device: weight gradients on this side stream (their own i8t_ctx),
+    # overlapping the backward-data chain; the trainer joins it before the update
+    wgrad_stream: object = None
 
 
 @dataclass
@@ -626,7 +629,16 @@ class Conv2d(Layer):
             if self.wgrad_acc is None and ctx.wgrad_allreduce is not None:
                 self.wgrad_acc = torch.empty((self.kh * self.kw * self.c_pad, self.out_c), dtype=torch.int64,
                                              device=gdev)
-            if ctx.wgrad_allreduce is None:  # single device: weights straight from the partials, no int64 copy
+            if ctx.wgrad_allreduce is None and ctx.wgrad_stream is not None:
+                # the weight gradient on the side stream, after this layer's gradient quantiser
+                side = ctx.wgrad_stream
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    call("i8t_conv_wgrad", ops.side_ctx(side), C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa),
+                         self.c_pad, ops._p(clip_g), ops._p(self.qs.clip_a), None, ops._p(self.grad_weight), 1)
+                qg.record_stream(side)
+                self._qa.record_stream(side)
+            elif ctx.wgrad_allreduce is None:  # single device: weights straight from the partials, no int64 copy
                 call("i8t_conv_wgrad", h, C.byref(g), ops._p(qg), self.k_pad, ops._p(self._qa), self.c_pad,
                      ops._p(clip_g), ops._p(self.qs.clip_a), None, ops._p(self.grad_weight), 1)
             else:  # data parallel: exact int64 sum across ranks (async, overlapping the backward), then rescale
@@ -639,6 +651,8 @@ class Conv2d(Layer):
         self._qa = None
         self._qg = qg if self.keep_qg else None
         if TRACE is not None:
+            if ctx.wgrad_stream is not None:  # the instrumentation reads gw: wait for the side stream
+                torch.cuda.current_stream().wait_stream(ctx.wgrad_stream)
             TRACE(self, "bwd", g=None if fuse_g else gz, qg=qg, stream_in=stream_in, stream_out=ctx.grad_stream,
                   ga=ga, gw=self.grad_weight if ctx.wgrad_allreduce is None else None)
         return ga

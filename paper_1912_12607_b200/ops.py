@@ -43,6 +43,23 @@ def ctx(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
     return h
 
 
+_side_ctx: dict = {}
+
+
+def side_ctx(stream: torch.cuda.Stream) -> C.c_void_p:
+    """A second i8t_ctx per device (its own scratch) for work on a side stream
+    that overlaps the main context's (the weight gradients)."""
+    dev = torch.cuda.current_device()
+    h = _side_ctx.get(dev)
+    if h is None:
+        h = C.c_void_p()
+        call("i8t_ctx_create", C.c_void_p(stream.cuda_stream), C.byref(h))
+        _side_ctx[dev] = h
+    else:
+        call("i8t_ctx_set_stream", h, C.c_void_p(stream.cuda_stream))
+    return h
+
+
 def check():
     """Synchronise and raise the latched device error (reference exceptions)."""
     call("i8t_ctx_check", ctx())

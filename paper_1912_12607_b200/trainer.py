@@ -101,6 +101,11 @@ class _DistHook:
             return 1
 
 
+# Weight gradients on a side stream overlapping the backward-data chain
+# (single device; I8T_WGRAD_STREAM=0 keeps them in line).
+WGRAD_STREAM = os.environ.get("I8T_WGRAD_STREAM", "1") == "1"
+
+
 class Trainer:
     def __init__(self, model, cfg: TrainConfig, device="cuda", force_dp_hook: bool = False):
         self.model, self.cfg = model, cfg
@@ -116,6 +121,8 @@ class Trainer:
         self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank() if self.world > 1 else 0
         self._hook = None
+        self._wgrad_side = None  # side stream of the weight gradients (single device)
+        self.device = device
         if self.world > 1 or force_dp_hook:  # force: exercise the data-parallel phases at world size 1
             if self.world > 1 and dist.get_backend() == "nccl" and os.environ.get("I8T_DP_COMM", "nccl") == "nccl":
                 # the library's own NCCL communicator combines the DSGC statistics
@@ -253,12 +260,18 @@ class Trainer:
         bctx = BackwardCtx(cfg.mode, it, self.grad_stream, cfg.grid_resolution, cfg.refine_rounds, cfg.clip_enabled,
                            cfg.clip_period, cfg.alpha, cfg.beta, cfg.form, cfg.lr_scaling_enabled,
                            self._wgrad_allreduce if self._hook is not None else None)
+        if self._hook is None and WGRAD_STREAM and cfg.mode == Mode.INT8:
+            if self._wgrad_side is None:
+                self._wgrad_side = torch.cuda.Stream(device=self.device)
+            bctx.wgrad_stream = self._wgrad_side
         self._wgrad_step_begin()
         self.model.net.backward(g_logits, bctx)
         for work, finalize in bctx.deferred:  # int64 wgrad allreduces issued during the backward
             if work is not None:
                 work.wait()
             finalize()
+        if bctx.wgrad_stream is not None:  # join the side-stream weight gradients before the update
+            torch.cuda.current_stream().wait_stream(bctx.wgrad_stream)
         if self._hook is not None:
             self._wgrad_arena_build()
         if self.world > 1:

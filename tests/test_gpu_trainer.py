@@ -161,3 +161,37 @@ def test_softmax_ce_device_matches_reference_formula():
     x[3, 17] = np.inf
     SoftmaxCrossEntropy.loss_and_grad(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(), n, bad=bad)
     assert int(bad) == 1
+
+
+def test_side_stream_weight_gradients_bit_identical():
+    """Weight gradients on the side stream (trainer.WGRAD_STREAM) train
+    bit-identically to the in-line weight gradients: parameters, losses, DSGC
+    measurements and the LCG stream after three ResNet-20 steps (one a search
+    step)."""
+    import torch
+    from paper_1912_12607_b200 import trainer as T
+    from paper_1912_12607_b200.models import build_model
+    from paper_1912_12607_b200.layers import int8_replace
+
+    def run(flag):
+        old = T.WGRAD_STREAM
+        T.WGRAD_STREAM = flag
+        try:
+            torch.manual_seed(0)
+            m = build_model("resnet20", num_classes=10)
+            int8_replace(m.net)
+            tr = T.Trainer(m, T.TrainConfig(base_lr=0.05, clip_period=2, seed=3))
+            x, y = T.synthetic_batch(m, 16, 5)
+            reps = [tr.train_step(x, y, it, 10) for it in range(3)]
+            return tr, reps
+        finally:
+            T.WGRAD_STREAM = old
+
+    ta, ra = run(True)
+    tb, rb = run(False)
+    for a, b in zip(ra, rb):
+        assert a.loss == b.loss
+        for la, lb in zip(a.layers, b.layers):
+            assert (la.clip, la.dc) == (lb.clip, lb.dc)
+    assert torch.equal(ta.pflat, tb.pflat)
+    assert int(ta.grad_stream.item()) == int(tb.grad_stream.item())
