@@ -654,15 +654,13 @@ static void launch_bn_act(Ctx* cx, const float* z, int64_t m, int64_t c, const d
 }
 
 // per-(group, set) tickets of the two-level column-sum reduction: 64 groups x 32 sets
-// (self-resetting; one array per process: column sums of one stream run in order)
-static unsigned* set_tickets(Ctx*) {
-  static unsigned* t = [] {
-    unsigned* p = nullptr;
-    if (cudaMalloc(&p, 64 * 32 * sizeof(unsigned)) != cudaSuccess) return static_cast<unsigned*>(nullptr);
-    cudaMemset(p, 0, 64 * 32 * sizeof(unsigned));
-    return p;
-  }();
-  return t;
+// (self-resetting; one array per context: the column sums of one stream run in order)
+static unsigned* set_tickets(Ctx* c) {
+  if (!c->d_set_tickets) {
+    if (cudaMalloc(&c->d_set_tickets, 64 * 32 * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    cudaMemset(c->d_set_tickets, 0, 64 * 32 * sizeof(unsigned));
+  }
+  return c->d_set_tickets;
 }
 
 unsigned* group_tickets(Ctx* c) {

@@ -201,6 +201,7 @@ int i8t_ctx_destroy(i8t_ctx* ctx) {
   if (c->d_hist) cudaFree(c->d_hist);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_tickets) cudaFree(c->d_tickets);
+  if (c->d_set_tickets) cudaFree(c->d_set_tickets);
   delete c;
   return I8T_OK;
 }

@@ -64,6 +64,7 @@ struct Ctx {
   double* d_totals = nullptr;          // grid-reduced totals (128 doubles)
   unsigned* d_ticket = nullptr;        // last-block ticket (self-resetting)
   unsigned* d_tickets = nullptr;       // per-group tickets of the BN column reductions
+  unsigned* d_set_tickets = nullptr;   // per-(group, set) tickets of their two-level reduction
   void* d_scratch = nullptr;           // misc scratch (temp states, small buffers)
   size_t scratch_cap = 0;
   void* d_wgrad = nullptr;             // per-split int32 wgrad partial tiles
