@@ -458,8 +458,12 @@ def main():
     # (the graph replays live in their own memory pool)
     it = ((it // cfg.clip_period) + 1) * cfg.clip_period
     timed(1)
-    it = ((it // cfg.clip_period) + 1) * cfg.clip_period
-    ms_search, _ = timed(1)
+    # (median of three search steps: one sample occasionally caught a stall)
+    ms_s = []
+    for _ in range(3):
+        it = ((it // cfg.clip_period) + 1) * cfg.clip_period
+        ms_s.append(timed(1)[0])
+    ms_search = sorted(ms_s)[1]
     extra = max(ms_search - ms / a.steps, 0.0) / cfg.clip_period
 
     imgs = a.batch * world

@@ -79,6 +79,12 @@ struct ConvArgs {
   int phase;
   int Hq, Wq, fh, fw, r0, s0, ns, dh, dw;
   int nr;  // phase taps along r (with ns along s)
+  // phase rows padded to 2^prow_lg (> 0: on): GEMM row m = gr * 2^prow_lg + ww
+  // with gr = n * Hq + hh, rows ww >= Wq computed and dropped, so every
+  // 32-row quadrant is whole phase-grid rows -- one 3-D TMA box of the output
+  // ([C][Wq][N*Hq], strides sw*C and sh*W*C floats; needs H == sh*Hq) -- and
+  // the A tile is 128 / 2^prow_lg im2col boxes of one row each
+  int prow_lg;
   // 1x1 / stride 1 / pad 0: the A operand rows are plain matrix rows, loaded
   // by TMA (tmap_a; WGRAD also takes its B = g_z rows from tmap_b) by one
   // thread -- no cp.async gather
@@ -92,7 +98,7 @@ struct ConvArgs {
   const float* add_y;
   const uint32_t* add_bits;  // instead of add_y: packed mask (bit e of word e/32 for flat NHWC index e)
   // fast divisions by the invariant extents (set_divs, before every launch)
-  FDiv dCp, dKp, dS, dQ, dW, dWq, dns, dpq, dhw, dhwq;
+  FDiv dCp, dKp, dS, dQ, dW, dWq, dns, dpq, dhw, dhwq, dHq;
 };
 
 inline void set_divs(ConvArgs& a) {
@@ -106,6 +112,7 @@ inline void set_divs(ConvArgs& a) {
   a.dpq = fdiv_of(a.P * a.Q > 0 ? a.P * a.Q : 1);
   a.dhw = fdiv_of(a.H * a.W > 0 ? a.H * a.W : 1);
   a.dhwq = fdiv_of(a.Hq * a.Wq > 0 ? a.Hq * a.Wq : 1);
+  a.dHq = fdiv_of(a.Hq > 0 ? a.Hq : 1);
 }
 
 // residual addend of output row `orow`, columns c0..c0+3
@@ -141,10 +148,19 @@ __device__ __forceinline__ float dequant_acc(double rescale, uint32_t v) {
 // output row of GEMM row m (identity except in DGRAD phase mode)
 __device__ __forceinline__ int64_t out_row_of(const ConvArgs& a, int64_t m) {
   if (!a.phase) return m;
+  if (a.prow_lg) {
+    const int gr = static_cast<int>(m >> a.prow_lg), ww = static_cast<int>(m & ((1 << a.prow_lg) - 1));
+    const int n = fdiv(gr, a.dHq), hh = gr - n * a.Hq;
+    return (static_cast<int64_t>(n) * a.H + hh * a.sh + a.fh) * a.W + ww * a.sw + a.fw;
+  }
   const int hwq = a.Hq * a.Wq;
   const int n = fdiv(m, a.dhwq), rem = static_cast<int>(m - static_cast<int64_t>(n) * hwq);
   const int hh = fdiv(rem, a.dWq), ww = rem - hh * a.Wq;
   return (static_cast<int64_t>(n) * a.H + hh * a.sh + a.fh) * a.W + ww * a.sw + a.fw;
+}
+// GEMM row m maps to an output row (not a padding row of the phase mode)
+__device__ __forceinline__ bool row_ok(const ConvArgs& a, int64_t m) {
+  return m < a.M && (!a.prow_lg || static_cast<int>(m & ((1 << a.prow_lg) - 1)) < a.Wq);
 }
 
 
@@ -368,12 +384,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               // one stride phase: rows (n, hh, ww) of the phase grid, compact tap
               // (ir, is) reads g_z at (hh + dh - ir, ww + dw - is) = base (hh + dh -
               // (nr-1), ww + dw - (ns-1)) + mirrored offset (nr-1-ir, ns-1-is)
-              const int hwq = args.Hq * args.Wq;
-              const int n = fdiv(m0, args.dhwq), rem = m0 - n * hwq, hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
               const int it = fdiv(kb, args.dKp), kc = kb - it * args.Kp;
               const int ir = fdiv(it, args.dns), is = it - ir * args.ns;
-              tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, ww + args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n,
-                                 static_cast<uint16_t>(args.ns - 1 - is), static_cast<uint16_t>(args.nr - 1 - ir));
+              const uint16_t ow = static_cast<uint16_t>(args.ns - 1 - is), oh = static_cast<uint16_t>(args.nr - 1 - ir);
+              if (args.prow_lg) {
+                // one box of 2^prow_lg pixels per phase-grid row (its tail past Wq
+                // wraps into the next row: padding rows, dropped by the store);
+                // rows past the grid repeat the last one
+                const int ghq = args.N * args.Hq, nb = BM >> args.prow_lg;
+                const int gr0 = m0 >> args.prow_lg;
+                for (int i = 0; i < nb; ++i) {
+                  const int gr = gr0 + i < ghq ? gr0 + i : ghq - 1;
+                  const int n = fdiv(gr, args.dHq), hh = gr - n * args.Hq;
+                  tma_load_im2col_4d(a_st + static_cast<uint32_t>(i << args.prow_lg) * 128u, &tmap_a, &full[s], kc,
+                                     args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n, ow, oh);
+                }
+              } else {
+                const int hwq = args.Hq * args.Wq;
+                const int n = fdiv(m0, args.dhwq), rem = m0 - n * hwq, hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
+                tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, ww + args.dw - (args.ns - 1),
+                                   hh + args.dh - (args.nr - 1), n, ow, oh);
+              }
               const int bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp + kc;
               tma_load_2d(b_st, &tmap_b, &full[s], bx, n0);
               continue;
@@ -738,7 +769,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             } else {
               float4 f = make_float4(dequant_acc(rescale, v[4 * j + 0]), dequant_acc(rescale, v[4 * j + 1]),
                                      dequant_acc(rescale, v[4 * j + 2]), dequant_acc(rescale, v[4 * j + 3]));
-              if (MODE == MODE_DGRAD && args.add_g && m < args.M && gc0 + 4 * j < args.Ng) {
+              if (MODE == MODE_DGRAD && args.add_g && row_ok(args, m) && gc0 + 4 * j < args.Ng) {
                 const float4 ad = join_addend(args, out_row_of(args, m), gc0 + 4 * j);
                 f.x = __fadd_rn(f.x, ad.x); f.y = __fadd_rn(f.y, ad.y); f.z = __fadd_rn(f.z, ad.z); f.w = __fadd_rn(f.w, ad.w);
               }
@@ -750,11 +781,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           __syncwarp();
           if (lane == 0) {
             const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * TM + row_base + quad * 32;
-            tma_store_2d(&tmap_out, buf_s, gc0, r0);
+            if (MODE == MODE_DGRAD && args.prow_lg) tma_store_3d(&tmap_out, buf_s, gc0, 0, r0 >> args.prow_lg);
+            else tma_store_2d(&tmap_out, buf_s, gc0, r0);
             bulk_commit();
           }
           ++nst;
-        } else if (m < args.M) {
+        } else if (row_ok(args, m)) {
           if constexpr (MODE != MODE_WGRAD) {
             if (args.out) {
               float* dst = args.out + out_row_of(args, m) * args.ldo + gc0;
@@ -789,7 +821,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             }
           }
         }
-        if (args.acc32 && m < args.M && MODE != MODE_WGRAD) {
+        if (args.acc32 && row_ok(args, m) && MODE != MODE_WGRAD) {
           int32_t* dst = args.acc32 + out_row_of(args, m) * args.Ng + gc0;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -1066,7 +1098,7 @@ static EncodeIm2colFn encode_im2col_fn() {
 // with strides (sw, sh); out-of-tensor taps are zero-filled.
 static int make_im2col_map(CUtensorMap* map, const int8_t* t, int64_t N, int64_t H, int64_t W, int64_t C, int lower_w,
                            int lower_h, int upper_w, int upper_h, int sw, int sh, uint32_t cbox = 128u,
-                           CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                           CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, uint32_t pix = BM) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col unavailable");
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
@@ -1076,7 +1108,7 @@ static int make_im2col_map(CUtensorMap* map, const int8_t* t, int64_t N, int64_t
   const int upper[2] = {upper_w, upper_h};
   cuuint32_t estr[4] = {1u, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(sh), 1u};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(t), dims, strides, lower, upper, cbox,
-                  static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  static_cast<cuuint32_t>(pix), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
   return I8T_OK;
@@ -1135,6 +1167,26 @@ static int make_out_map(CUtensorMap* map, void* base, int64_t cols, int64_t rows
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string(int(r)) + ")");
+  return I8T_OK;
+}
+
+// One stride phase (fh, fw) of an NHWC fp32 output [N][H][W][C] as a 3-D map
+// [C][Wq][N*Hq] (rows n*Hq + hh merge because H == sh*Hq), box {32 channels,
+// 2^lg pixels, 32 >> lg rows}, SWIZZLE_128B: a 32-row quadrant of the padded
+// phase rows (prow_lg) in one store, the padding columns ww >= Wq clipped.
+static int make_phase_out_map(CUtensorMap* map, float* out, const ConvArgs& x, int lg) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  float* base = out + (static_cast<int64_t>(x.fh) * x.W + x.fw) * x.ldo;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(x.Ng), static_cast<cuuint64_t>(x.Wq),
+                        static_cast<cuuint64_t>(x.N) * static_cast<cuuint64_t>(x.Hq)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(x.sw * x.ldo * 4),
+                           static_cast<cuuint64_t>(x.sh) * static_cast<cuuint64_t>(x.W) * x.ldo * 4};
+  cuuint32_t box[3] = {32u, 1u << lg, 32u >> lg};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(I8T_ECUDA, "cuTensorMapEncodeTiled(phase out) failed (" + std::to_string(int(r)) + ")");
   return I8T_OK;
 }
 
@@ -1343,18 +1395,34 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       x.Kd = (int64_t)nr * x.ns * k_pad;
       x.nr = nr;
       x.k_tiles = (int)((x.Kd + BKB - 1) / BKB);
+      static const bool no_im2col = getenv("I8T_NO_IM2COL") != nullptr;
+      static const bool no_prow = getenv("I8T_NO_PHASE_TMA") != nullptr;
+      const bool im2col = !no_im2col && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0;
+      // padded phase rows + TMA stores (im2col operand only) when a phase-grid
+      // row fits a quadrant (9 <= Wq <= 32: at Wq <= 8 the sixteen 8-pixel
+      // boxes per stage made the 7x7 phases slower, 100 -> 135 us on 3x3/s2
+      // 512@14) and the (n, hh) rows merge (H == sh*Hq)
+      int lg = 4;
+      while ((1 << lg) < x.Wq) ++lg;
+      if (im2col && !no_prow && x.Wq >= 9 && lg <= 5 && g->h == static_cast<int64_t>(sh) * x.Hq &&
+          tma_out_ok(ga, g->c) && (static_cast<int64_t>(x.N) * x.Hq << lg) < (int64_t(1) << 31)) {
+        x.prow_lg = lg;
+        x.M = static_cast<int64_t>(x.N) * x.Hq << lg;
+        x.use_tma_out = 1;
+      }
       x.m_tiles = (int)((x.M + BM - 1) / BM);
       const int bn = pick_bn_balanced(g->c, x.m_tiles, num_sms());
       x.n_tiles = (int)((g->c + bn - 1) / bn); x.splits = 1;
       CUtensorMap amap{}, map, omap{};
       int rc = make_weight_map(&map, wt, g->c, ld_wt, bn);
       if (rc) return rc;
-      static const bool no_im2col = getenv("I8T_NO_IM2COL") != nullptr;
-      if (!no_im2col && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0) {
+      if (x.prow_lg && (rc = make_phase_out_map(&omap, ga, x, x.prow_lg))) return rc;
+      if (im2col) {
         // the phase grid Hq x Wq as the pixel box over g_z [N][P][Q][k_pad]
         const int lw = x.dw - (x.ns - 1), lh = x.dh - (nr - 1);
         x.tma_a = 2;
-        if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, lw, lh, x.Wq - (int)Q + lw, x.Hq - (int)P + lh, 1, 1)))
+        if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, lw, lh, x.Wq - (int)Q + lw, x.Hq - (int)P + lh, 1, 1,
+                                  128u, CU_TENSOR_MAP_SWIZZLE_128B, x.prow_lg ? (1u << x.prow_lg) : BM)))
           return rc;
       }
       if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16))) return rc;

@@ -51,6 +51,11 @@ GEOMS = [
     (2, 64, 10, 10, 256, 3, 3, 2, 1, None, None, False),  # 3x3 s2, four phases
     (1, 24, 9, 10, 128, 3, 3, 2, 1, 1, 1, False),         # stride (2, 1)
     (1, 16, 13, 13, 128, 7, 7, 2, 3, None, None, False),  # 7x7 s2 p3
+    # padded phase rows + 3-D TMA stores (9 <= Wq <= 32, H == 2 Hq)
+    (1, 64, 18, 18, 128, 3, 3, 2, 1, None, None, False),  # Wq 9 -> 16-pixel rows, ragged last tile
+    (3, 40, 20, 22, 128, 3, 3, 2, 1, None, None, False),  # Wq 11, C = 40 (clipped channel box)
+    (2, 40, 60, 60, 128, 1, 1, 2, 0, None, None, False),  # 1x1 s2, Wq 30 -> 32-pixel rows
+    (1, 24, 36, 20, 128, 3, 3, 2, 1, 1, 1, False),        # stride (2, 1): Wq 20, W stride C
     (3, 8, 6, 6, 8, 3, 3, 1, 1, None, None, True),       # depthwise
     (2, 40, 9, 9, 40, 3, 3, 2, 1, None, None, True),     # depthwise stride 2
     (4, 96, 28, 28, 96, 3, 3, 1, 1, None, None, True),   # depthwise, channel-quad kernels
@@ -172,7 +177,8 @@ def test_resnet50_layer_shapes(shape, ops):
     np.testing.assert_array_equal(wacc.cpu().numpy(), wacc_ref)
 
 
-@pytest.mark.parametrize("shape", [(2, 40, 11, 128, 1, 2, 0), (2, 64, 10, 256, 3, 2, 1), (2, 64, 14, 64, 3, 1, 1)])
+@pytest.mark.parametrize("shape", [(2, 40, 11, 128, 1, 2, 0), (2, 64, 10, 256, 3, 2, 1), (2, 64, 14, 64, 3, 1, 1),
+                                   (2, 40, 36, 128, 1, 2, 0), (1, 64, 22, 256, 3, 2, 1)])
 def test_dgrad_join_in_place_matches_dgrad_plus_add(shape, ops):
     """i8t_conv_dgrad_join with ga aliasing add_g (the projection-shortcut join
     accumulating into the main-branch gradient): equal to dgrad + add_g, the
