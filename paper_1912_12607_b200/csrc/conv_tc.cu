@@ -83,7 +83,7 @@ struct ConvArgs {
   // with gr = n * Hq + hh, rows ww >= Wq computed and dropped, so every
   // 32-row quadrant is whole phase-grid rows -- one 3-D TMA box of the output
   // ([C][Wq][N*Hq], strides sw*C and sh*W*C floats; needs H == sh*Hq) -- and
-  // the A tile is 128 / 2^prow_lg im2col boxes of one row each
+  // the A tile stays one im2col box (its pixel box widened to 2^prow_lg)
   int prow_lg;
   // 1x1 / stride 1 / pad 0: the A operand rows are plain matrix rows, loaded
   // by TMA (tmap_a; WGRAD also takes its B = g_z rows from tmap_b) by one
@@ -388,17 +388,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               const int ir = fdiv(it, args.dns), is = it - ir * args.ns;
               const uint16_t ow = static_cast<uint16_t>(args.ns - 1 - is), oh = static_cast<uint16_t>(args.nr - 1 - ir);
               if (args.prow_lg) {
-                // one box of 2^prow_lg pixels per phase-grid row (its tail past Wq
-                // wraps into the next row: padding rows, dropped by the store);
-                // rows past the grid repeat the last one
-                const int ghq = args.N * args.Hq, nb = BM >> args.prow_lg;
+                // the pixel box is 2^prow_lg wide (its columns past Wq read padding
+                // rows: zero fill or neighbours, dropped by the store), so the
+                // traversal order is the padded row order: one box as usual
                 const int gr0 = m0 >> args.prow_lg;
-                for (int i = 0; i < nb; ++i) {
-                  const int gr = gr0 + i < ghq ? gr0 + i : ghq - 1;
-                  const int n = fdiv(gr, args.dHq), hh = gr - n * args.Hq;
-                  tma_load_im2col_4d(a_st + static_cast<uint32_t>(i << args.prow_lg) * 128u, &tmap_a, &full[s], kc,
-                                     args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n, ow, oh);
-                }
+                const int n = fdiv(gr0, args.dHq), hh = gr0 - n * args.Hq;
+                tma_load_im2col_4d(a_st, &tmap_a, &full[s], kc, args.dw - (args.ns - 1), hh + args.dh - (args.nr - 1), n,
+                                   ow, oh);
               } else {
                 const int hwq = args.Hq * args.Wq;
                 const int n = fdiv(m0, args.dhwq), rem = m0 - n * hwq, hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
@@ -1399,12 +1395,10 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
       static const bool no_prow = getenv("I8T_NO_PHASE_TMA") != nullptr;
       const bool im2col = !no_im2col && (reinterpret_cast<uintptr_t>(gz) & 15u) == 0;
       // padded phase rows + TMA stores (im2col operand only) when a phase-grid
-      // row fits a quadrant (9 <= Wq <= 32: at Wq <= 8 the sixteen 8-pixel
-      // boxes per stage made the 7x7 phases slower, 100 -> 135 us on 3x3/s2
-      // 512@14) and the (n, hh) rows merge (H == sh*Hq)
-      int lg = 4;
+      // row fits a quadrant (5 <= Wq <= 32) and the (n, hh) rows merge (H == sh*Hq)
+      int lg = 3;
       while ((1 << lg) < x.Wq) ++lg;
-      if (im2col && !no_prow && x.Wq >= 9 && lg <= 5 && g->h == static_cast<int64_t>(sh) * x.Hq &&
+      if (im2col && !no_prow && x.Wq >= 5 && lg <= 5 && g->h == static_cast<int64_t>(sh) * x.Hq &&
           tma_out_ok(ga, g->c) && (static_cast<int64_t>(x.N) * x.Hq << lg) < (int64_t(1) << 31)) {
         x.prow_lg = lg;
         x.M = static_cast<int64_t>(x.N) * x.Hq << lg;
@@ -1421,8 +1415,8 @@ static int dgrad_phases(Ctx* c, const i8t_conv_geom* g, int64_t P, int64_t Q, co
         // the phase grid Hq x Wq as the pixel box over g_z [N][P][Q][k_pad]
         const int lw = x.dw - (x.ns - 1), lh = x.dh - (nr - 1);
         x.tma_a = 2;
-        if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, lw, lh, x.Wq - (int)Q + lw, x.Hq - (int)P + lh, 1, 1,
-                                  128u, CU_TENSOR_MAP_SWIZZLE_128B, x.prow_lg ? (1u << x.prow_lg) : BM)))
+        const int bw = x.prow_lg ? (1 << x.prow_lg) : x.Wq;  // pixel-box width (padded rows)
+        if ((rc = make_im2col_map(&amap, gz, g->n, P, Q, k_pad, lw, lh, bw - (int)Q + lw, x.Hq - (int)P + lh, 1, 1)))
           return rc;
       }
       if ((rc = dispatch<MODE_DGRAD>(c->stream, x, bn, amap, map, omap, vec_of(k_pad), 16))) return rc;

@@ -56,6 +56,8 @@ GEOMS = [
     (3, 40, 20, 22, 128, 3, 3, 2, 1, None, None, False),  # Wq 11, C = 40 (clipped channel box)
     (2, 40, 60, 60, 128, 1, 1, 2, 0, None, None, False),  # 1x1 s2, Wq 30 -> 32-pixel rows
     (1, 24, 36, 20, 128, 3, 3, 2, 1, 1, 1, False),        # stride (2, 1): Wq 20, W stride C
+    (2, 64, 14, 14, 128, 3, 3, 2, 1, None, None, False),  # Wq 7 -> 8-pixel rows, one ragged tile
+    (1, 32, 12, 16, 128, 3, 3, 2, 1, None, None, False),  # Wq 8: no padding columns
     (3, 8, 6, 6, 8, 3, 3, 1, 1, None, None, True),       # depthwise
     (2, 40, 9, 9, 40, 3, 3, 2, 1, None, None, True),     # depthwise stride 2
     (4, 96, 28, 28, 96, 3, 3, 1, 1, None, None, True),   # depthwise, channel-quad kernels
