@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "bncore.cuh"
 #include "internal.cuh"
@@ -62,6 +63,102 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const float* __restrict__ x
     }
     reinterpret_cast<float4*>(y)[i] = make_float4(best[0], best[1], best[2], best[3]);
     reinterpret_cast<uchar4*>(idx)[i] = make_uchar4(arg[0], arg[1], arg[2], arg[3]);
+  }
+}
+
+// 3x3 / stride 2 / pad 1 with H == 2P, W == 2Q (the ResNet stem): a thread
+// walks a column of RUN windows (n, p0.., q, quad) downwards, so the window's
+// top row (2p-1) is the previous window's bottom row, already loaded and
+// normalised: 6 loads and 24 BN evaluations per window instead of 9 and 36.
+// The 9 slots are scanned in the same (dy, dx) order with the same update rule
+// as k_maxpool_fwd; only the top row (p = 0) and the left column (q = 0) pad.
+template <bool BN>
+__global__ void __launch_bounds__(256, 3) k_maxpool_fwd_s2k3(const float* __restrict__ x, PoolGeom g, const double* bn,
+                                                          const float* gamma, const float* beta, int relu, int run,
+                                                          float* __restrict__ y, uint8_t* __restrict__ idx) {
+  pdl_entry();
+  const uint32_t c4n = g.C / 4;
+  const uint32_t nrun = (g.P + run - 1) / run;
+  const uint32_t tot = static_cast<uint32_t>(g.N) * nrun * g.Q * c4n;  // < 2^31 (host check)
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    const uint32_t c4 = i % c4n, t = i / c4n;
+    const int q = static_cast<int>(t % g.Q);
+    const uint32_t t2 = t / g.Q;
+    const int pr = static_cast<int>(t2 % nrun), n = static_cast<int>(t2 / nrun);
+    BnQuad k;
+    if (BN) k.load(bn, gamma, beta, g.C, c4 * 4);
+    const bool lok = q > 0;  // the left column 2q-1 exists
+    const int wl = lok ? 2 * q - 1 : 2 * q;  // clamped (the value is then ignored)
+    const uint32_t rowp = static_cast<uint32_t>(g.W) * c4n;
+    const float4* xn = x4 + static_cast<uint32_t>(n) * g.H * rowp + c4;
+    auto act = [&](const float4 v4, float (&v)[4]) {
+      v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+      if (BN) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[j] = k.y(j, v[j]);
+          if (relu) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+        }
+      }
+    };
+    int p = pr * run;
+    const int pe = p + run < g.P ? p + run : g.P;
+    float top[3][4];
+    bool top_ok = p > 0;
+    if (top_ok) {
+      const float4* r = xn + static_cast<uint32_t>(2 * p - 1) * rowp;
+      const float4 a = __ldg(r + static_cast<uint32_t>(wl) * c4n), b = __ldg(r + static_cast<uint32_t>(2 * q) * c4n),
+                   c = __ldg(r + static_cast<uint32_t>(2 * q + 1) * c4n);
+      act(a, top[0]);
+      act(b, top[1]);
+      act(c, top[2]);
+    }
+    for (; p < pe; ++p) {
+      const float4* r1 = xn + static_cast<uint32_t>(2 * p) * rowp;
+      const float4* r2 = r1 + rowp;
+      float4 l[6];
+      l[0] = __ldg(r1 + static_cast<uint32_t>(wl) * c4n);
+      l[1] = __ldg(r1 + static_cast<uint32_t>(2 * q) * c4n);
+      l[2] = __ldg(r1 + static_cast<uint32_t>(2 * q + 1) * c4n);
+      l[3] = __ldg(r2 + static_cast<uint32_t>(wl) * c4n);
+      l[4] = __ldg(r2 + static_cast<uint32_t>(2 * q) * c4n);
+      l[5] = __ldg(r2 + static_cast<uint32_t>(2 * q + 1) * c4n);
+      float mid[3][4], bot[3][4];
+      act(l[0], mid[0]); act(l[1], mid[1]); act(l[2], mid[2]);
+      act(l[3], bot[0]); act(l[4], bot[1]); act(l[5], bot[2]);
+      float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int arg[4] = {0, 0, 0, 0};
+      bool any[4] = {false, false, false, false};
+      auto take = [&](const float (&v)[4], int slot) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (!any[j] || v[j] > best[j] || isnan(v[j])) {  // torch's max_pool2d update rule
+            best[j] = v[j];
+            arg[j] = slot;
+            any[j] = true;
+          }
+      };
+      if (top_ok) {
+        if (lok) take(top[0], 0);
+        take(top[1], 1);
+        take(top[2], 2);
+      }
+      if (lok) take(mid[0], 3);
+      take(mid[1], 4);
+      take(mid[2], 5);
+      if (lok) take(bot[0], 6);
+      take(bot[1], 7);
+      take(bot[2], 8);
+      const uint32_t o = ((static_cast<uint32_t>(n) * g.P + p) * g.Q + q) * c4n + c4;
+      reinterpret_cast<float4*>(y)[o] = make_float4(best[0], best[1], best[2], best[3]);
+      reinterpret_cast<uchar4*>(idx)[o] = make_uchar4(arg[0], arg[1], arg[2], arg[3]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) top[c][j] = bot[c][j];
+      top_ok = true;
+    }
   }
 }
 
@@ -215,6 +312,18 @@ int i8t_maxpool_fwd(i8t_ctx* ctx, const float* x, int64_t n, int64_t h, int64_t 
   int rc = pool_geom(n, h, w, c, k, s, pad, &g);
   if (rc) return rc;
   if (!cx || !x || !y || !idx || (bn && (!gamma || !beta))) return set_error(I8T_EINVAL, "maxpool_fwd: bad arguments");
+  static const bool no_run = getenv("I8T_NO_POOL_RUN") != nullptr;  // A/B: the per-window kernel
+  if (!no_run && g.k == 3 && g.s == 2 && g.pad == 1 && g.H == 2 * g.P && g.W == 2 * g.Q) {
+    const int run = 7;
+    const int64_t tr = static_cast<int64_t>(g.N) * ((g.P + run - 1) / run) * g.Q * (g.C / 4);
+    if (bn)
+      launch_k(k_maxpool_fwd_s2k3<true>, grid_of(tr), 256, 0, cx->stream, x, g, bn, gamma, beta, relu, run, y, idx);
+    else
+      launch_k(k_maxpool_fwd_s2k3<false>, grid_of(tr), 256, 0, cx->stream, x, g, nullptr, nullptr, nullptr, 0, run, y,
+               idx);
+    count_launch(1);
+    return cuda_check("k_maxpool_fwd_s2k3");
+  }
   const int64_t tot = static_cast<int64_t>(g.N) * g.P * g.Q * (g.C / 4);
   if (bn) launch_k(k_maxpool_fwd<true>, grid_of(tot), 256, 0, cx->stream, x, g, bn, gamma, beta, relu, y, idx);
   else launch_k(k_maxpool_fwd<false>, grid_of(tot), 256, 0, cx->stream, x, g, nullptr, nullptr, nullptr, 0, y, idx);

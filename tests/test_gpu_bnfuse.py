@@ -369,7 +369,7 @@ def test_fused_int8_tracks_torch_bn():
 
 
 @pytest.mark.parametrize("shape", [(2, 112, 112, 64, 3, 2, 1), (2, 15, 13, 32, 3, 2, 1), (3, 17, 15, 8, 3, 2, 0),
-                                   (2, 9, 9, 12, 2, 2, 1)])
+                                   (2, 9, 9, 12, 2, 2, 1), (1, 18, 22, 8, 3, 2, 1)])
 @pytest.mark.parametrize("with_bn", [False, True])
 def test_maxpool_matches_torch(ops, shape, with_bn):
     """csrc/pool.cu vs torch max_pool2d (+ its backward) on act(bn(z)) / x."""
