@@ -757,22 +757,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             else bulk_wait_read<0>();
           }
           __syncwarp();
+          // the residual join decided once per chunk (a per-float4 test of the
+          // kernel arguments cost the dgrad epilogue ~15 % more instructions)
+          auto stage = [&](auto join_c) {
+            constexpr bool JOIN = decltype(join_c)::value;
+            const int64_t orow = JOIN ? out_row_of(args, m) : 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint4 w;
-            if constexpr (MODE == MODE_WGRAD) {
-              w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            } else {
-              float4 f = make_float4(dequant_acc(rescale, v[4 * j + 0]), dequant_acc(rescale, v[4 * j + 1]),
-                                     dequant_acc(rescale, v[4 * j + 2]), dequant_acc(rescale, v[4 * j + 3]));
-              if (MODE == MODE_DGRAD && args.add_g && row_ok(args, m) && gc0 + 4 * j < args.Ng) {
-                const float4 ad = join_addend(args, out_row_of(args, m), gc0 + 4 * j);
-                f.x = __fadd_rn(f.x, ad.x); f.y = __fadd_rn(f.y, ad.y); f.z = __fadd_rn(f.z, ad.z); f.w = __fadd_rn(f.w, ad.w);
+            for (int j = 0; j < 8; ++j) {
+              uint4 w;
+              if constexpr (MODE == MODE_WGRAD) {
+                w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              } else {
+                float4 f = make_float4(dequant_acc(rescale, v[4 * j + 0]), dequant_acc(rescale, v[4 * j + 1]),
+                                       dequant_acc(rescale, v[4 * j + 2]), dequant_acc(rescale, v[4 * j + 3]));
+                if (JOIN && gc0 + 4 * j < args.Ng) {
+                  const float4 ad = join_addend(args, orow, gc0 + 4 * j);
+                  f.x = __fadd_rn(f.x, ad.x); f.y = __fadd_rn(f.y, ad.y); f.z = __fadd_rn(f.z, ad.z); f.w = __fadd_rn(f.w, ad.w);
+                }
+                w = make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), __float_as_uint(f.w));
               }
-              w = make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), __float_as_uint(f.w));
+              sts128(buf_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
             }
-            sts128(buf_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
-          }
+          };
+          if (MODE == MODE_DGRAD && args.add_g && row_ok(args, m)) stage(std::true_type{});
+          else stage(std::false_type{});
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
