@@ -216,12 +216,16 @@ __device__ __forceinline__ int tile_nk(const ConvArgs& a, int split) {
 // tcgen05.mma.cta_group::2 -- each CTA loads its 128 A rows and half of the B
 // rows (TMA, completion counted on the leader's barrier), the leader issues
 // the M = 256 MMAs and multicasts their commits; TMA-operand path only.
-template <int MODE, int BN, int VA, int VB, int CG = 1, int EDB = 0>
+// DGX = false: a DGRAD without stride phases or residual join (the common
+// case) compiled without those paths -- the same epilogue as FWD (the extra
+// code and its per-chunk argument loads cost the plain dgrads ~10 %).
+template <int MODE, int BN, int VA, int VB, int CG = 1, int EDB = 0, bool DGX = true>
 __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, const __grid_constant__ CUtensorMap tmap_a,
                                                           const __grid_constant__ CUtensorMap tmap_b,
                                                           const __grid_constant__ CUtensorMap tmap_out) {
   using C = Cfg<MODE, BN, CG, EDB>;
   constexpr bool PAIR = CG == 2;
+  constexpr bool DX = MODE == MODE_DGRAD && DGX;  // stride phases / residual join compiled in
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
 #pragma unroll
             for (int sub = 0; sub < C::B_SUB; ++sub) tma_load_2d(b_st + sub * 16384, &tmap_b, &full[s], n0 + sub * 128, kb);
           } else {
-            if (MODE == MODE_DGRAD && args.tma_a == 2 && args.phase) {
+            if (DX && args.tma_a == 2 && args.phase) {
               // one stride phase: rows (n, hh, ww) of the phase grid, compact tap
               // (ir, is) reads g_z at (hh + dh - ir, ww + dw - is) = base (hh + dh -
               // (nr-1), ww + dw - (ns-1)) + mirrored offset (nr-1-ir, ns-1-is)
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             rowA_n[i] = n;
             rowA_y[i] = p * args.sh - args.ph;
             rowA_x[i] = q * args.sw - args.pw;
-          } else if (args.phase) {
+          } else if (DX && args.phase) {
             const int hwq = args.Hq * args.Wq;
             const int n = fdiv(mm, args.dhwq), rem = mm - n * hwq;
             const int hh = fdiv(rem, args.dWq), ww = rem - hh * args.Wq;
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           if (tid == 0) {  // weight tile [BN rows][128 B] by TMA (OOB rows / columns zero-filled)
             mbar_expect_tx(&full[s], C::B_BYTES);
             int bx = static_cast<int>(kbase);
-            if (MODE == MODE_DGRAD && args.phase) {  // compact tap index -> CRSK column of (r, s)
+            if (DX && args.phase) {  // compact tap index -> CRSK column of (r, s)
               const int it = fdiv(kbase, args.dKp);
               const int ir = fdiv(it, args.dns), is = it - ir * args.ns;
               bx = ((args.r0 + ir * args.sh) * args.S + args.s0 + is * args.sw) * args.Kp +
@@ -495,8 +499,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
           const int CH = (MODE == MODE_FWD) ? args.Cp : args.Kp;
           const int tap = kok ? fdiv(kk, (MODE == MODE_FWD) ? args.dCp : args.dKp) : 0;
           const int ch = kok ? static_cast<int>(kk - static_cast<int64_t>(tap) * CH) : 0;
-          const int tS = (MODE == MODE_DGRAD && args.phase) ? args.ns : args.S;
-          const int r = fdiv(tap, (MODE == MODE_DGRAD && args.phase) ? args.dns : args.dS), sx = tap - r * tS;
+          const int tS = (DX && args.phase) ? args.ns : args.S;
+          const int r = fdiv(tap, (DX && args.phase) ? args.dns : args.dS), sx = tap - r * tS;
 #pragma unroll
           for (int i = 0; i < PASSES_A; ++i) {
             const int row = ra0 + i * ROWS_PER_PASS_A;
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               const int ih = rowA_y[i] + r, iw = rowA_x[i] + sx;
               ok = ok && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
               if (ok) src = args.act + ((static_cast<int64_t>(rowA_n[i]) * args.H + ih) * args.W + iw) * args.Cp + ch;
-            } else if (args.phase) {
+            } else if (DX && args.phase) {
               const int p = rowA_y[i] - r, q = rowA_x[i] - sx;  // r, sx = compact (ir, is)
               ok = ok && p >= 0 && p < args.P && q >= 0 && q < args.Q;
               src = args.gz;
@@ -779,21 +783,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
               sts128(buf_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
             }
           };
-          if (MODE == MODE_DGRAD && args.add_g && row_ok(args, m)) stage(std::true_type{});
+          if (DX && args.add_g && row_ok(args, m)) stage(std::true_type{});
           else stage(std::false_type{});
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             const int r0 = (MODE == MODE_WGRAD ? tc.split * args.m_pad : 0) + tc.m_tile * TM + row_base + quad * 32;
-            if (MODE == MODE_DGRAD && args.prow_lg) tma_store_3d(&tmap_out, buf_s, gc0, 0, r0 >> args.prow_lg);
+            if (DX && args.prow_lg) tma_store_3d(&tmap_out, buf_s, gc0, 0, r0 >> args.prow_lg);
             else tma_store_2d(&tmap_out, buf_s, gc0, r0);
             bulk_commit();
           }
           ++nst;
-        } else if (row_ok(args, m)) {
+        } else if (DX ? row_ok(args, m) : m < args.M) {
           if constexpr (MODE != MODE_WGRAD) {
             if (args.out) {
-              float* dst = args.out + out_row_of(args, m) * args.ldo + gc0;
+              float* dst = args.out + (DX ? out_row_of(args, m) : m) * args.ldo + gc0;
               if (gc0 + 32 <= args.Ng && (args.ldo % 4) == 0) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -802,7 +806,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                   w.y = dequant_acc(rescale, v[4 * j + 1]);
                   w.z = dequant_acc(rescale, v[4 * j + 2]);
                   w.w = dequant_acc(rescale, v[4 * j + 3]);
-                  if (MODE == MODE_DGRAD && args.add_g) {
+                  if (DX && args.add_g) {
                     const float4 ad = join_addend(args, out_row_of(args, m), gc0 + 4 * j);
                     w.x = __fadd_rn(w.x, ad.x); w.y = __fadd_rn(w.y, ad.y); w.z = __fadd_rn(w.z, ad.z); w.w = __fadd_rn(w.w, ad.w);
                   }
@@ -813,7 +817,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
                 for (int i = 0; i < 32; ++i)
                   if (gc0 + i < args.Ng) {
                     float o = dequant_acc(rescale, v[i]);
-                    if (MODE == MODE_DGRAD && args.add_g) {
+                    if (DX && args.add_g) {
                       const int64_t ai = out_row_of(args, m) * args.ldo + gc0 + i;
                       const bool mk = args.add_y ? args.add_y[ai] > 0.0f
                                                  : !args.add_bits || ((args.add_bits[ai >> 5] >> (ai & 31)) & 1u);
@@ -825,8 +829,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             }
           }
         }
-        if (args.acc32 && row_ok(args, m) && MODE != MODE_WGRAD) {
-          int32_t* dst = args.acc32 + out_row_of(args, m) * args.Ng + gc0;
+        if (args.acc32 && (DX ? row_ok(args, m) : m < args.M) && MODE != MODE_WGRAD) {
+          int32_t* dst = args.acc32 + (DX ? out_row_of(args, m) : m) * args.Ng + gc0;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (gc0 + i < args.Ng) dst[i] = static_cast<int32_t>(v[i]);
@@ -1251,7 +1255,7 @@ static int edb_max_ktiles() {
   return v;
 }
 
-template <int MODE, int BN, int VA, int VB, int EDB = 0>
+template <int MODE, int BN, int VA, int VB, int EDB = 0, bool DGX = true>
 static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& amap, const CUtensorMap& map,
                       const CUtensorMap& omap) {
   ConvArgs a = a0;
@@ -1259,7 +1263,7 @@ static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& am
   using C = Cfg<MODE, BN, 1, EDB>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_conv_tc<MODE, BN, VA, VB, 1, EDB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_conv_tc<MODE, BN, VA, VB, 1, EDB, DGX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
   const int tiles = a.m_tiles * a.n_tiles * a.splits;
@@ -1269,7 +1273,7 @@ static int launch_one(cudaStream_t st, const ConvArgs& a0, const CUtensorMap& am
   }();
   const int sms = cap > 0 && cap < num_sms() ? cap : num_sms();
   const int grid = tiles < sms ? tiles : sms;
-  launch_k(k_conv_tc<MODE, BN, VA, VB, 1, EDB>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
+  launch_k(k_conv_tc<MODE, BN, VA, VB, 1, EDB, DGX>, grid, NTHREADS, C::SMEM, st, a, amap, map, omap);
   count_launch(1);
   return cuda_check("k_conv_tc");
 }
@@ -1278,11 +1282,15 @@ template <int MODE, int BN>
 static int dispatch_vec(cudaStream_t st, const ConvArgs& a, const CUtensorMap& am, const CUtensorMap& m,
                         const CUtensorMap& o, int va, int vb) {
   if (a.tma_a) {  // no gather: vector widths unused
-    if constexpr (MODE != MODE_WGRAD)
+    if constexpr (MODE != MODE_WGRAD) {
+      const bool plain = MODE == MODE_DGRAD && !a.phase && !a.add_g;  // DGX = false
       // (with BN = 256 only on small grids: the fourth pipeline stage it costs
       // matters more than the staging once every SM runs tens of tiles)
       if (a.use_tma_out && a.k_tiles <= edb_max_ktiles() && (BN <= 128 || a.M < 131072))
-        return launch_one<MODE, BN, 16, 16, 1>(st, a, am, m, o);
+        return plain ? launch_one<MODE, BN, 16, 16, 1, false>(st, a, am, m, o)
+                     : launch_one<MODE, BN, 16, 16, 1>(st, a, am, m, o);
+      if (plain) return launch_one<MODE, BN, 16, 16, 0, false>(st, a, am, m, o);
+    }
     return launch_one<MODE, BN, 16, 16>(st, a, am, m, o);
   }
   if constexpr (MODE == MODE_WGRAD) {
