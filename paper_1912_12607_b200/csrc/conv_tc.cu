@@ -318,18 +318,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             tma_load_2d_pair(b_st, &tmap_b, lbar, kb, n0 + static_cast<int>(crank) * (BN / 2));
             continue;
           }
-          mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
           if (MODE == MODE_FWD && args.tma_a == 3) {
             // 32-channel taps (the stem's folded taps): the k-block's four 32-byte K
             // chunks are four im2col boxes [128 output pixels][32 channels]
-            // (SWIZZLE_32B), one per MMA; a chunk past Kd repeats a valid tap (its
-            // weights are the zero fill of the weight box)
+            // (SWIZZLE_32B), one per MMA; a chunk past Kd is not loaded -- its
+            // weights are the zero fill of the weight box, so whatever int8 the
+            // stage's A slot still holds contributes 0
+            const int nbox = static_cast<int>(args.Kd - kb) / 32 < 4 ? static_cast<int>(args.Kd - kb) / 32 : 4;
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nbox) * 4096u + C::B_BYTES);
             const int pq = args.P * args.Q;
             const int n = fdiv(m0, args.dpq), rem = m0 - n * pq, p = fdiv(rem, args.dQ), q = rem - p * args.Q;
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-              int kh = kb + 32 * h;
-              if (kh >= args.Kd) kh = static_cast<int>(args.Kd) - 32;
+              if (h >= nbox) break;
+              const int kh = kb + 32 * h;
               const int tap = fdiv(kh, args.dCp), cb = kh - tap * args.Cp;
               const int r = fdiv(tap, args.dS), sx = tap - r * args.S;
               tma_load_im2col_4d(a_st + h * 4096, &tmap_a, &full[s], cb, q * args.sw - args.pw, p * args.sh - args.ph,
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_tc(const ConvArgs args, co
             tma_load_2d(b_st, &tmap_b, &full[s], kb, n0);
             continue;
           }
+          mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // the stage's single arrival
           if (MODE == MODE_FWD && args.tma_a == 2) {
             // implicit im2col by TMA: 128 consecutive output pixels of tap (r, s),
             // 128 channels from cb; zero padding = out-of-box fill
