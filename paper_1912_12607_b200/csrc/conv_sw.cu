@@ -212,17 +212,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_conv_sw(const Args a, const __g
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
+        // rescale into registers first, then wait for the previous chunk's
+        // store to release the (single) staging tile: the FP64 rescale
+        // overlaps the TMA store's read instead of following it
+        uint32_t f[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = __float_as_uint(static_cast<float>(rescale * i32_to_f64(v[i])));
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint4 w;
-          w.x = __float_as_uint(static_cast<float>(rescale * i32_to_f64(v[4 * j + 0])));
-          w.y = __float_as_uint(static_cast<float>(rescale * i32_to_f64(v[4 * j + 1])));
-          w.z = __float_as_uint(static_cast<float>(rescale * i32_to_f64(v[4 * j + 2])));
-          w.w = __float_as_uint(static_cast<float>(rescale * i32_to_f64(v[4 * j + 3])));
-          sts128(stage_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)), w);
-        }
+        for (int j = 0; j < 8; ++j)
+          sts128(stage_s + sw128_offset(static_cast<uint32_t>(lane), static_cast<uint32_t>(j * 16)),
+                 make_uint4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]));
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
